@@ -1,0 +1,373 @@
+"""Benchmark: batched Alg. 1 AM/AL trajectory optimization (trajectory-iterations / s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c2|c1] [--dtype f64|f32]
+    python bench.py --impl reference ...      # reference CPU path (oracle port) on host cores
+    torchrun --nproc-per-node N bench.py --gpus N   # one process per GPU, NCCL
+
+A step = one full solve (cold init + max_iter fused AM iterations) of the
+configuration's member batch; value = members x AM iterations / step time
+(device time, CUDA events, max over ranks).  Members are sharded contiguously
+across ranks with no data-path collective; one NCCL all-gather of per-shard
+summaries closes each step.  The per-element state (C5: 94 GB fp64) is far
+larger than L2, so no explicit L2 flush is needed between iterations.
+
+e2e: the same solve through the public batched API with the step's member
+inputs (boundary values + linear cost terms) copied from pinned host memory
+and the results (xi, residual max/norm, converged) copied back, inside the
+timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n_obs, members, n_iter, description)
+    "c5": (100, 131072, 200, "C5: 131072 traj x 100 dyn. ellipsoids x n_p 100, 200 AM its (3-D)"),
+    "c2": (50, 1024, 200, "C2: 1024 traj x 50 dyn. ellipsoids x n_p 100, 200 AM its (3-D)"),
+    "c1": (10, 1, 100, "C1: 1 quadrotor x 10 static ellipsoids x n_p 100, 100 AM its (3-D)"),
+}
+WORDS_3D = 9  # persistent words per (member, obstacle, sample): alpha beta lx ly lz lca lsa lcb lsb
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--groups", type=int, default=0)
+    ap.add_argument("--members", type=int, default=0, help="override the member count (testing)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------- clocks sampling
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[3 + k] and r[3 + k] != "Not Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU reference arm (oracle port)
+def _oracle_member_solve(args):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    n_o, member, n_iter = args
+    from oracle import alg1 as O
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200.basis import build_basis
+
+    bs = build_basis(0.0, 10.0, 100, 10)
+    batch = scenarios.flow3d_batch(n_o, [member], basis=bs) if n_o != 10 else None
+    if batch is None:
+        prob = scenarios.c1_problem()
+        tracks = np.stack([o.centers for o in prob.obstacles])
+        bvals = np.stack([bc.values() for bc in prob.boundary])[None]
+        desired = prob.desired[None]
+        a = np.array([o.shape.a for o in prob.obstacles])
+        b = np.array([o.shape.b for o in prob.obstacles])
+    else:
+        tracks = np.stack([o.centers for o in batch.obstacles])
+        bvals = batch.bvals
+        s = np.linspace(0, 1, 100)
+        desired = bvals[:, :, 0][:, None, :] + s[None, :, None] * (bvals[:, :, 3] - bvals[:, :, 0])[:, None, :]
+        a = np.array([o.shape.a for o in batch.obstacles])
+        b = np.array([o.shape.b for o in batch.obstacles])
+    prob = O.Problem(P=bs.P, Pd=bs.Pdot, Pdd=bs.Pddot, bvals=bvals, desired=desired, tracks=tracks, a=a, b=b)
+    t0 = time.perf_counter()
+    O.solve(prob, O.Params(max_iter=n_iter, tol=0.0))
+    return time.perf_counter() - t0
+
+
+def cpu_reference(cfg_name: str, members: int, procs: int | None = None):
+    """Reference CPU path: the oracle port of solver_single (bit-exact with the reference on C1),
+    one member per task, 1 BLAS thread per process, all host cores.  Returns (traj-it/s, info)."""
+    import multiprocessing as mp
+
+    n_o, _, n_iter, _ = CONFIGS[cfg_name]
+    procs = procs or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    tasks = [(n_o, i, n_iter) for i in range(members)]
+    with ctx.Pool(procs) as pool:
+        pool.map(_oracle_member_solve, [(n_o, 0, 2)] * procs)  # import warm-up
+        t0 = time.perf_counter()
+        pool.map(_oracle_member_solve, tasks, chunksize=1)
+        wall = time.perf_counter() - t0
+    return members * n_iter / wall, {"cores": procs, "wall_s": wall, "members": members, "iterations": n_iter}
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200.basis import build_basis
+    from paper_2408_10731_b200.solver_single import SingleParams, make_batch_engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n_o, members_total, n_iter, desc = CONFIGS[args.config]
+    if args.members:
+        members_total = args.members
+    lo = members_total * rank // world
+    hi = members_total * (rank + 1) // world
+    B = hi - lo
+    dtype = torch.float64 if args.dtype == "f64" else torch.float32
+    s_bytes = 8 if args.dtype == "f64" else 4
+
+    basis = build_basis(0.0, 10.0, 100, 10)
+    if args.config == "c1":
+        from paper_2408_10731_b200.solver_single import SingleBatch
+
+        batch = SingleBatch.from_problems([scenarios.c1_problem()])
+    else:
+        batch = scenarios.flow3d_batch(n_o, range(lo, hi), basis=basis)
+    params = SingleParams(max_iter=n_iter, tol=0.0)
+    eng = make_batch_engine(batch, params, dtype=dtype, groups=args.groups)
+    stream = torch.cuda.current_stream()
+
+    def solve_device():
+        eng.reset_schedule()
+        eng.level.copy_(eng.level0)
+        eng.cold_init()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.run(n_iter, use_graph=True)
+        e1.record(stream)
+        return e0, e1
+
+    def summary():
+        # per-shard end-of-solve summary: (best residual, its global member index, converged count)
+        rm = eng.res_max
+        k = torch.argmin(rm)
+        return torch.stack([rm[k], (k + lo).to(torch.float64), (rm <= 1e-3).sum().to(torch.float64)])
+
+    for _ in range(args.warmup):
+        solve_device()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    iter_ms = []
+    start.record(stream)
+    for _ in range(args.steps):
+        e0, e1 = solve_device()
+        if world > 1:
+            summ = summary()
+            out = [torch.empty_like(summ) for _ in range(world)]
+            dist.all_gather(out, summ)
+        iter_ms.append((e0, e1))
+    stop.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed = start.elapsed_time(stop) / 1e3
+    run_ms = [a.elapsed_time(b) for a, b in iter_ms]
+    t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    value = members_total * n_iter * args.steps / elapsed
+
+    # roofline of the dominant kernel (tro_alg1_iterate): algorithmic bytes per launch / avg launch time
+    alg_bytes = 2 * WORDS_3D * n_o * 100 * s_bytes * B
+    avg_launch_s = statistics.mean(run_ms) / 1e3 / n_iter
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / avg_launch_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_alg1_{args.config}_{args.dtype}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            prof = json.load(fh)
+        traffic = prof.get("dram_bytes_per_member_launch", 0) * B or None
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        bv_host = torch.as_tensor(batch.bvals, dtype=torch.float64).pin_memory()
+        q_host = torch.as_tensor(batch.linear_terms(), dtype=torch.float64).pin_memory()
+        xi_host = torch.empty(eng.xi.shape, dtype=torch.float64).pin_memory()
+        res_host = torch.empty((3, B), dtype=torch.float64).pin_memory()
+        h2d = (bv_host.numel() + q_host.numel()) * 8
+        d2h = (xi_host.numel() + res_host.numel()) * 8
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            eng.bvals.copy_(bv_host, non_blocking=True)
+            eng.q.copy_(q_host, non_blocking=True)
+            solve_device()
+            xi_host.copy_(eng.xi, non_blocking=True)
+            res_host[0].copy_(eng.res_max, non_blocking=True)
+            res_host[1].copy_(eng.res_norm, non_blocking=True)
+            res_host[2].copy_(eng.status, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": members_total * n_iter * args.steps / float(te.item()), "unit": "traj-it/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    line = {
+        "metric": "trajectory-iterations/sec (batch x AM iters)",
+        "value": value,
+        "unit": "traj-it/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic (seeded scenario recipe, SURVEY.md §8(d))",
+        "config": {"workload": desc, "members": members_total, "n_obs": n_o, "n_p": 100, "am_iters": n_iter,
+                   "state_dtype": args.dtype, "qp_step": "f64", "parallelism": f"member-shard x{world}",
+                   "l2": "state >> L2 (no flush needed)" if alg_bytes > 126e6 else "state fits L2"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_s * 1e3,
+                     "kernel": "tro_alg1_iterate (alg1_kernel<3,T>)"},
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": args.steps * (1 + n_iter),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = min(2 * (os.cpu_count() or 1), 64) if args.config != "c1" else 4
+        v, info = cpu_reference(args.config, sample)
+        line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port",
+                                "sample": f"{sample} members x {info['iterations']} AM its of the same recipe, "
+                                          f"oracle port of solver_single (1 BLAS thread/process), "
+                                          f"wall {info['wall_s']:.1f}s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_o, members_total, n_iter, desc = CONFIGS[args.config]
+    procs = os.cpu_count() or 1
+    sample = procs if args.config != "c1" else 1
+    vals = []
+    info = None
+    for k in range(args.warmup + args.steps):
+        v, info = cpu_reference(args.config, sample, procs)
+        if k >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference",
+        "metric": "trajectory-iterations/sec (batch x AM iters)",
+        "value": value,
+        "unit": "traj-it/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": info["wall_s"] * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded scenario recipe, SURVEY.md §8(d))",
+        "config": {"workload": desc, "members": members_total, "n_obs": n_o, "n_p": 100, "am_iters": n_iter},
+        "cpu_baseline": {"value": value, "unit": "traj-it/s", "cores": procs, "kind": "port",
+                         "sample": f"{sample} members x {n_iter} AM its per step (bounded sample of the workload)"},
+        "e2e": {"value": value, "unit": "traj-it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

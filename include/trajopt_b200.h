@@ -1,0 +1,141 @@
+/*
+ * trajopt_b200.h — C-ABI of the B200-native batched AM/AL trajectory-optimizer
+ * kernels (libtrajopt_b200.so).  Plain pointers and sizes only; no torch types.
+ *
+ * Conventions:
+ *  - every pointer in the structs below is a DEVICE pointer owned by the caller
+ *    (torch tensors in the Python host layer); nothing here allocates;
+ *  - every entry point only ENQUEUES work on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) and returns a cudaError_t value
+ *    (0 = success) or TRO_EINVAL for a host-side argument error;
+ *  - one solver instance per stream (the reference's single-owner state rule,
+ *    SPEC.md:298).
+ *
+ * Reference interfaces replaced (file:line into arxiv/paper_2408_10731's
+ * `trajopt` package, pkg/src/trajopt/):
+ *  - tro_kkt_apply_f64    <- qpcore.solve_batch           (qpcore.py:130-143)
+ *  - tro_alg1_prime       <- solver_single.init_state tail + the target/
+ *                            multiplier sums _position_step needs
+ *                            (solver_single.py:115-166, :177-189, :204-207)
+ *  - tro_alg1_iterate     <- solver_single.am_iteration + _residual_extremes +
+ *                            _maybe_grow_penalties, i.e. one trip of the loop
+ *                            body of solve_single (solver_single.py:373-427)
+ *  - tro_topk_stable      <- np.argsort(kind="stable")[:k] (solver_priest.py:358,
+ *                            :440) and sorted(key=aug_cost) (:362)
+ */
+#ifndef TRAJOPT_B200_H
+#define TRAJOPT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TRO_EINVAL (-1)
+
+/* storage type of the per-element state */
+#define TRO_F64 0
+#define TRO_F32 1
+
+/* status bits per member */
+#define TRO_CONVERGED 1
+#define TRO_FACTOR_FAILED 2
+
+typedef struct tro_alg1_dims {
+    int32_t n_members; /* B: members (independent problems) in this launch */
+    int32_t n_obs;     /* n_o: obstacles shared by every member */
+    int32_t n_p;       /* horizon samples */
+    int32_t m;         /* basis columns = degree + 1 (<= 16) */
+    int32_t dim;       /* 2 or 3 */
+    int32_t n_eq;      /* boundary rows per axis (6: p,v,a at both ends) */
+    int32_t n_levels;  /* entries of the K^-1 table */
+    int32_t groups;    /* obstacle groups per CTA; 0 = automatic */
+} tro_alg1_dims;
+
+typedef struct tro_alg1_consts {
+    const double* P;         /* n_p x m, row-major (basis.py:143-177) */
+    const double* tracks;    /* dim x n_o x n_p, obstacle centres (SoA) */
+    const double* shape_a;   /* n_o semi-axis a (x,y) */
+    const double* shape_b;   /* n_o semi-axis b (z; y in 2-D) */
+    const double* kinv;      /* n_levels x nk x nk row-major, nk = m + n_eq */
+    const double* level_rho; /* n_levels: the rho_o each table entry was built at */
+    const int32_t* level_ok; /* n_levels: 1 if that level passed the cond guard */
+    const double* q;         /* B x dim x m: -2 w_track P^T desired (solver_single.py:173) */
+    const double* bvals;     /* B x dim x n_eq boundary values */
+    const double* line_u;    /* m: lstsq(P, 1)      straight-line init xi = u p0 + v (p1 - p0) */
+    const double* line_v;    /* m: lstsq(P, tau)    (basis.py:207-217, used by tro_alg1_init) */
+} tro_alg1_consts;
+
+typedef struct tro_alg1_params {
+    double tol;               /* SingleParams.tol */
+    double rho_growth;        /* SingleParams.rho_growth */
+    double rho_cap;           /* SingleParams.rho_cap */
+    double stall_improvement; /* SingleParams.stall_improvement */
+    int32_t stall_window;     /* SingleParams.stall_window (<= 32) */
+    int32_t d_mode;           /* 0: d == 1 (cold start), 1: read state.d, 2: recompute from pos */
+    int32_t max_hist;         /* history capacity per member (0: no history output) */
+    int32_t flags;            /* TRO_FLAG_* */
+} tro_alg1_params;
+
+/* tro_alg1_params.flags */
+#define TRO_FLAG_NO_SCHEDULE 1 /* bare am_iteration: no convergence test, no penalty growth */
+
+typedef struct tro_alg1_state {
+    /* per element (B x n_o x n_p), storage type T */
+    void* alpha;
+    void* beta;    /* unused in 2-D */
+    void* lam;     /* W_lam planes of B x n_o x n_p: 3-D [lx ly lz lca lsa lcb lsb], 2-D [lx ly lca lsa] */
+    void* d;       /* optional: read when d_mode == 1, written (new d) when non-NULL */
+    void* copies;  /* optional export of the angle copies: 3-D [ca sa cb sb], 2-D [ca sa]; NULL = skip */
+    /* per member, fp64 */
+    double* xi;    /* B x dim x m */
+    double* pos;   /* B x dim x n_p  (positions of the current xi) */
+    double* sums;  /* B x 2 x dim x n_p : [sum_j lam_pos ; sum_j targets] for the next position step */
+    double* rho;
+    double* rho_o;
+    double* ring;     /* B x 2*stall_window: last max_abs values (oldest first, rolling) */
+    double* res_norm; /* B: residual norm of the latest iterate */
+    double* res_max;  /* B: residual max-abs of the latest iterate */
+    double* hist;     /* B x max_hist x 3 (norm, max_abs, rho_o) or NULL */
+    int32_t* level;       /* B: index into the K^-1 table of the current rho_o */
+    int32_t* iteration;   /* B: state.iteration */
+    int32_t* last_change; /* B: iteration of the last penalty growth (solve-local) */
+    int32_t* n_hist;      /* B: iterations recorded in this solve */
+    int32_t* status;      /* B: TRO_CONVERGED | TRO_FACTOR_FAILED */
+    int32_t* n_changes;   /* B: rho_o changes in this solve (new factorizations) */
+} tro_alg1_state;
+
+/* Sums for the first position step + positions of the current xi + residual of the
+ * current (copies-reset) state.  Call once before the first tro_alg1_iterate of a solve. */
+int tro_alg1_prime(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                   const tro_alg1_state* s, const tro_alg1_params* p, void* stream);
+
+/* Cold start (solver_single.init_state, solver_single.py:115-166): straight-line xi,
+ * angles from the line offsets, zero multipliers, d == 1; then everything tro_alg1_prime does. */
+int tro_alg1_init(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                  const tro_alg1_state* s, const tro_alg1_params* p, void* stream);
+
+/* One fused AM iteration for every non-frozen member (one kernel launch). */
+int tro_alg1_iterate(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                     const tro_alg1_state* s, const tro_alg1_params* p, void* stream);
+
+/* out (ncols x n) = rhs (ncols x n) * K^-T, i.e. out[c] = K^-1 rhs[c] for every column c.
+ * kinv: n x n row-major.  qpcore.solve_batch with the RHS block [-q ; b]. */
+int tro_kkt_apply_f64(const double* kinv, int32_t n, const double* rhs, int64_t ncols,
+                      double* out, void* stream);
+
+/* Stable ascending top-k: out_idx[0..k) = indices of the k smallest keys, ties broken
+ * by index (== np.argsort(keys, kind="stable")[:k]).  NaN sorts last.  keys: n fp64. */
+int tro_topk_stable_f64(const double* keys, int64_t n, int32_t k, int64_t* out_idx,
+                        void* workspace, int64_t workspace_bytes, void* stream);
+int64_t tro_topk_workspace_bytes(int64_t n, int32_t k);
+
+int32_t tro_version(void);
+const char* tro_error_string(int32_t code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRAJOPT_B200_H */

@@ -1,0 +1,282 @@
+"""Device engine for batched Alg. 1 (single-robot AM/AL, arXiv 2408.10731).
+
+Owns the device-resident SoA state of B independent members that share one
+basis and one obstacle set, the per-rho_o-level K^-1 table, and the launch
+sequence (one fused kernel launch per AM iteration, optionally replayed from a
+CUDA graph).  Host <-> device traffic happens only at solve boundaries.
+
+HBM layout (per member i, obstacle j, sample t; element e = (i*n_o + j)*n_p + t):
+    alpha[e], beta[e]                      storage dtype T (fp64 or fp32)
+    lam[w][e], w = lx ly lz lca lsa lcb lsb (3-D) | lx ly lca lsa (2-D)
+Per member (fp64): xi (dim, m), pos (dim, n_p), sums (2, dim, n_p), rho, rho_o,
+stall ring, status/level/iteration counters.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib, qpcore
+from .basis import BasisSet, boundary_matrix, line_basis_vectors
+
+
+def rho_chain(r0: float, growth: float, cap: float) -> list[float]:
+    """Distinct penalty values reached from r0 by repeated min(r * growth, cap) (solver_single.py:401-402)."""
+    vals = [float(r0)]
+    while True:
+        nxt = min(vals[-1] * growth, cap)
+        if nxt == vals[-1] or len(vals) > 10000:
+            return vals
+        vals.append(nxt)
+
+
+class LevelTable:
+    """K^-1 per rho_o level for the position-step saddle (solver_single.py:198-202)."""
+
+    def __init__(self, basis: BasisSet, n_o: int, w_smooth: float, w_track: float, starts, growth: float,
+                 cap: float, cond_limit: float = 1e12):
+        P, Pdd = basis.P, basis.Pddot
+        Q = 2.0 * (w_smooth * Pdd.T @ Pdd + w_track * P.T @ P)  # solver_single.py:172
+        PtP = P.T @ P
+        A = boundary_matrix(basis)
+        self.m = basis.n_var
+        self.n_eq = A.shape[0]
+        nk = self.m + self.n_eq
+        self.rhos: list[float] = []
+        self.factors: list[qpcore.KKTFactor | None] = []
+        self.offsets: dict[float, int] = {}
+        for r0 in sorted(set(float(r) for r in starts)):
+            self.offsets[r0] = len(self.rhos)
+            for r in rho_chain(r0, growth, cap):
+                D = Q + r * n_o * PtP if n_o else Q  # solver_single.py:199
+                try:
+                    f = qpcore._build(D, A, cond_limit)
+                except qpcore.FactorizationError as exc:
+                    if "rank-deficient" in str(exc):
+                        raise
+                    f = None
+                self.rhos.append(r)
+                self.factors.append(f)
+        self.kinv = np.zeros((len(self.rhos), nk, nk))
+        for k, f in enumerate(self.factors):
+            if f is not None:
+                self.kinv[k] = f.kinv
+        self.ok = np.array([f is not None for f in self.factors], dtype=np.int32)
+
+    def level_of(self, r0: float) -> int:
+        return self.offsets[float(r0)]
+
+    def error_for(self, level: int) -> qpcore.FactorizationError:
+        return qpcore.FactorizationError(
+            f"saddle matrix is near-singular at rho_o={self.rhos[level]!r} (cond guard 1e12)")
+
+
+class Alg1Engine:
+    """B members on one device.  All per-member inputs may be numpy or torch."""
+
+    def __init__(self, basis: BasisSet, tracks, shape_a, shape_b, bvals, q, *, params, rho0=None,
+                 w_smooth: float = 1.0, w_track: float = 1.0, dtype=torch.float64, device=None, groups: int = 0,
+                 max_hist: int = 0, export: bool = False, keep_d: bool = False, cond_limit: float = 1e12):
+        _lib.require_cuda()
+        self.lib = _lib.load()
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        dev = self.device
+        self.dtype = dtype
+        self.code = _lib.TRO_F64 if dtype == torch.float64 else _lib.TRO_F32
+        if dtype not in (torch.float64, torch.float32):
+            raise ValueError("storage dtype must be float64 or float32")
+        self.params = params
+        tracks = np.asarray(tracks, dtype=float)
+        n_o, n_p, dim = tracks.shape if tracks.size else (int(tracks.shape[0]), basis.n_p, int(bvals.shape[1]))
+        self.n_o, self.n_p, self.dim, self.m = int(n_o), int(n_p), int(dim), basis.n_var
+        self.B = int(bvals.shape[0])
+        if self.dim not in (2, 3):
+            raise ValueError("dim must be 2 or 3")
+        f64 = dict(dtype=torch.float64, device=dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        B, n_o, n_p, dim, m = self.B, self.n_o, self.n_p, self.dim, self.m
+
+        # ---- constants
+        rho0 = np.full(B, params.rho_start) if rho0 is None else np.broadcast_to(np.asarray(rho0, float), (B,))
+        self.table = LevelTable(basis, n_o, w_smooth, w_track, np.unique(rho0), params.rho_growth, params.rho_cap,
+                                cond_limit)
+        self.basis = basis
+        self.P = torch.as_tensor(np.ascontiguousarray(basis.P), **f64)
+        self.tracks = torch.as_tensor(np.ascontiguousarray(np.transpose(tracks, (2, 0, 1))) if n_o else
+                                      np.zeros((dim, 0, n_p)), **f64).contiguous()
+        self.shape_a = torch.as_tensor(np.asarray(shape_a, dtype=float).reshape(-1), **f64)
+        self.shape_b = torch.as_tensor(np.asarray(shape_b, dtype=float).reshape(-1), **f64)
+        if n_o == 0:
+            self.shape_a = torch.ones(1, **f64)
+            self.shape_b = torch.ones(1, **f64)
+        self.kinv = torch.as_tensor(self.table.kinv, **f64).contiguous()
+        self.level_rho = torch.as_tensor(np.asarray(self.table.rhos), **f64)
+        self.level_ok = torch.as_tensor(self.table.ok, **i32)
+        self.q = torch.as_tensor(q, **f64).reshape(B, dim, m).contiguous()
+        self.bvals = torch.as_tensor(bvals, **f64).reshape(B, dim, -1).contiguous()
+        self.n_eq = int(self.bvals.shape[2])
+        u, v = line_basis_vectors(basis)
+        self.line_u = torch.as_tensor(u, **f64)
+        self.line_v = torch.as_tensor(v, **f64)
+
+        # ---- state
+        T = dict(dtype=dtype, device=dev)
+        W = 7 if dim == 3 else 4
+        self.alpha = torch.empty((B, n_o, n_p), **T)
+        self.beta = torch.empty((B, n_o, n_p), **T) if dim == 3 else None
+        self.lam = torch.empty((W, B, n_o, n_p), **T)
+        self.d = torch.empty((B, n_o, n_p), **T) if (keep_d or export) else None
+        self.copies = torch.empty((4 if dim == 3 else 2, B, n_o, n_p), **T) if export else None
+        self.xi = torch.zeros((B, dim, m), **f64)
+        self.pos = torch.zeros((B, dim, n_p), **f64)
+        self.sums = torch.zeros((B, 2, dim, n_p), **f64)
+        self.rho = torch.as_tensor(rho0.copy(), **f64)
+        self.rho_o = torch.as_tensor(rho0.copy(), **f64)
+        self.ring = torch.zeros((B, 2 * params.stall_window), **f64)
+        self.res_norm = torch.zeros(B, **f64)
+        self.res_max = torch.zeros(B, **f64)
+        self.max_hist = int(max_hist)
+        self.hist = torch.zeros((B, max(self.max_hist, 1), 3), **f64) if self.max_hist else None
+        levels0 = np.array([self.table.level_of(r) for r in rho0], dtype=np.int32)
+        self.level0 = torch.as_tensor(levels0, **i32)
+        self.level = self.level0.clone()
+        self.iteration = torch.zeros(B, **i32)
+        self.last_change = torch.zeros(B, **i32)
+        self.n_hist = torch.zeros(B, **i32)
+        self.status = torch.zeros(B, **i32)
+        self.n_changes = torch.zeros(B, **i32)
+
+        self._dims = _lib.Alg1Dims(B, n_o, n_p, m, dim, self.n_eq, len(self.table.rhos), int(groups))
+        self._consts = _lib.Alg1Consts(
+            self.P.data_ptr(), self.tracks.data_ptr(), self.shape_a.data_ptr(), self.shape_b.data_ptr(),
+            self.kinv.data_ptr(), self.level_rho.data_ptr(), self.level_ok.data_ptr(), self.q.data_ptr(),
+            self.bvals.data_ptr(), self.line_u.data_ptr(), self.line_v.data_ptr())
+        p = _lib.ptr
+        self._state = _lib.Alg1State(
+            p(self.alpha), p(self.beta), p(self.lam), p(self.d), p(self.copies), p(self.xi), p(self.pos),
+            p(self.sums), p(self.rho), p(self.rho_o), p(self.ring), p(self.res_norm), p(self.res_max), p(self.hist),
+            p(self.level), p(self.iteration), p(self.last_change), p(self.n_hist), p(self.status),
+            p(self.n_changes))
+        self._graph = None
+        self._graph_n = 0
+
+    # ------------------------------------------------------------ launches
+    def _params(self, d_mode: int, flags: int = 0) -> _lib.Alg1Params:
+        pr = self.params
+        return _lib.Alg1Params(float(pr.tol), float(pr.rho_growth), float(pr.rho_cap), float(pr.stall_improvement),
+                               int(pr.stall_window), int(d_mode), self.max_hist, int(flags))
+
+    def _call(self, name: str, d_mode: int, flags: int = 0):
+        fn = getattr(self.lib, name)
+        prm = self._params(d_mode, flags)
+        with torch.cuda.device(self.device):
+            rc = fn(self.code, ctypes.byref(self._dims), ctypes.byref(self._consts), ctypes.byref(self._state),
+                    ctypes.byref(prm), ctypes.c_void_p(_lib.stream_handle()))
+        _lib.check(rc, name)
+
+    def cold_init(self):
+        """init_state (solver_single.py:115-166) for every member, on device; d == 1."""
+        self._call("tro_alg1_init", 0)
+        self.first_d_mode = 0
+
+    def prime(self, d_mode: int):
+        self._call("tro_alg1_prime", d_mode)
+        self.first_d_mode = d_mode
+
+    def iterate(self, d_mode: int = 2, flags: int = 0):
+        self._call("tro_alg1_iterate", d_mode, flags)
+
+    def reset_schedule(self):
+        """Solve-local bookkeeping of solve_single (history, last_change) restarts per call."""
+        self.last_change.zero_()
+        self.n_hist.zero_()
+        self.n_changes.zero_()
+        self.ring.zero_()
+        self.status.zero_()
+
+    def _capture(self, n: int):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            # warm-up launch outside capture is not needed: launches are plain kernels
+            pass
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        with torch.cuda.graph(g):
+            for _ in range(n):
+                self.iterate(2)
+        self._graph, self._graph_n = g, n
+
+    def run(self, n_iter: int, *, use_graph: bool = True, chunk: int = 25, check_every: int = 0) -> int:
+        """n_iter AM iterations (the first with the primed d_mode).  Returns iterations launched.
+
+        check_every > 0 stops early (host sync every `check_every` iterations) once every
+        member is frozen (converged or failed)."""
+        done = 0
+        if n_iter <= 0:
+            return 0
+        self.iterate(self.first_d_mode)
+        done = 1
+        since_check = 1
+        while done < n_iter:
+            if check_every and since_check >= check_every:
+                since_check = 0
+                if bool((self.status == 0).sum().item() == 0):
+                    break
+            n = min(chunk, n_iter - done)
+            if check_every:
+                n = min(n, check_every - since_check)
+            if use_graph and n == chunk:
+                if self._graph is None or self._graph_n != chunk:
+                    self._capture(chunk)
+                self._graph.replay()
+            else:
+                for _ in range(n):
+                    self.iterate(2)
+            done += n
+            since_check += n
+        return done
+
+    # ------------------------------------------------------------ host transfer
+    def load_state(self, *, xi, alpha, beta, lam_planes, d, rho, rho_o, iteration):
+        """Upload a warm state (numpy, member-major)."""
+        dev, T = self.device, self.dtype
+        self.xi.copy_(torch.as_tensor(np.asarray(xi, float).reshape(self.B, self.dim, self.m)))
+        if self.n_o:
+            self.alpha.copy_(torch.as_tensor(np.asarray(alpha)).to(T))
+            if self.dim == 3:
+                self.beta.copy_(torch.as_tensor(np.asarray(beta)).to(T))
+            self.lam.copy_(torch.as_tensor(np.asarray(lam_planes)).to(T))
+            if d is not None:
+                if self.d is None:
+                    self.d = torch.empty((self.B, self.n_o, self.n_p), dtype=T, device=dev)
+                    self._state.d = self.d.data_ptr()
+                self.d.copy_(torch.as_tensor(np.asarray(d)).to(T))
+        self.rho.copy_(torch.as_tensor(np.asarray(rho, float).reshape(self.B)))
+        self.rho_o.copy_(torch.as_tensor(np.asarray(rho_o, float).reshape(self.B)))
+        self.iteration.copy_(torch.as_tensor(np.asarray(iteration).reshape(self.B).astype(np.int32)))
+        lv = np.array([self._level_for(r) for r in np.asarray(rho_o, float).reshape(self.B)], dtype=np.int32)
+        self.level.copy_(torch.as_tensor(lv))
+
+    def load_schedule(self, max_hist_lists, last_change):
+        """Restore solve-local stall bookkeeping (history of max_abs, last_change) per member."""
+        w2 = 2 * self.params.stall_window
+        ring = np.zeros((self.B, w2))
+        n = np.zeros(self.B, dtype=np.int32)
+        for i, h in enumerate(max_hist_lists):
+            h = list(h)
+            n[i] = len(h)
+            for k in range(max(0, len(h) - w2), len(h)):
+                ring[i, k % w2] = h[k]
+        self.ring.copy_(torch.as_tensor(ring))
+        self.n_hist.copy_(torch.as_tensor(n))
+        self.last_change.copy_(torch.as_tensor(np.asarray(last_change).reshape(self.B).astype(np.int32)))
+
+    def _level_for(self, r: float) -> int:
+        for k, v in enumerate(self.table.rhos):
+            if v == float(r):
+                return k
+        raise ValueError(f"rho_o={r!r} is not in this engine's level table")

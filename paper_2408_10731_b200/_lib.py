@@ -1,0 +1,164 @@
+"""ctypes binding of libtrajopt_b200.so (the C-ABI in include/trajopt_b200.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2408_10731_b200/csrc``).  There is no CPU fallback: if the
+library is missing, or no CUDA device is present, every compute entry point
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int32, c_int64, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtrajopt_b200.so")
+
+TRO_F64 = 0
+TRO_F32 = 1
+TRO_CONVERGED = 1
+TRO_FACTOR_FAILED = 2
+TRO_FLAG_NO_SCHEDULE = 1
+TRO_EINVAL = -1
+
+# every symbol include/trajopt_b200.h declares (checked by tests/test_lib_exports.py)
+EXPORTS = (
+    "tro_alg1_prime",
+    "tro_alg1_init",
+    "tro_alg1_iterate",
+    "tro_kkt_apply_f64",
+    "tro_topk_stable_f64",
+    "tro_topk_workspace_bytes",
+    "tro_version",
+    "tro_error_string",
+)
+
+
+class Alg1Dims(ctypes.Structure):
+    _fields_ = [
+        ("n_members", c_int32),
+        ("n_obs", c_int32),
+        ("n_p", c_int32),
+        ("m", c_int32),
+        ("dim", c_int32),
+        ("n_eq", c_int32),
+        ("n_levels", c_int32),
+        ("groups", c_int32),
+    ]
+
+
+class Alg1Consts(ctypes.Structure):
+    _fields_ = [
+        ("P", c_void_p),
+        ("tracks", c_void_p),
+        ("shape_a", c_void_p),
+        ("shape_b", c_void_p),
+        ("kinv", c_void_p),
+        ("level_rho", c_void_p),
+        ("level_ok", c_void_p),
+        ("q", c_void_p),
+        ("bvals", c_void_p),
+        ("line_u", c_void_p),
+        ("line_v", c_void_p),
+    ]
+
+
+class Alg1Params(ctypes.Structure):
+    _fields_ = [
+        ("tol", c_double),
+        ("rho_growth", c_double),
+        ("rho_cap", c_double),
+        ("stall_improvement", c_double),
+        ("stall_window", c_int32),
+        ("d_mode", c_int32),
+        ("max_hist", c_int32),
+        ("flags", c_int32),
+    ]
+
+
+class Alg1State(ctypes.Structure):
+    _fields_ = [
+        ("alpha", c_void_p),
+        ("beta", c_void_p),
+        ("lam", c_void_p),
+        ("d", c_void_p),
+        ("copies", c_void_p),
+        ("xi", c_void_p),
+        ("pos", c_void_p),
+        ("sums", c_void_p),
+        ("rho", c_void_p),
+        ("rho_o", c_void_p),
+        ("ring", c_void_p),
+        ("res_norm", c_void_p),
+        ("res_max", c_void_p),
+        ("hist", c_void_p),
+        ("level", c_void_p),
+        ("iteration", c_void_p),
+        ("last_change", c_void_p),
+        ("n_hist", c_void_p),
+        ("status", c_void_p),
+        ("n_changes", c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the library (fails loudly: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"libtrajopt_b200.so not found at {LIB_PATH}; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    sig = [POINTER(Alg1Dims), POINTER(Alg1Consts), POINTER(Alg1State), POINTER(Alg1Params), c_void_p]
+    for name in ("tro_alg1_prime", "tro_alg1_init", "tro_alg1_iterate"):
+        f = getattr(lib, name)
+        f.argtypes = [c_int32] + sig
+        f.restype = c_int32
+    lib.tro_kkt_apply_f64.argtypes = [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p]
+    lib.tro_kkt_apply_f64.restype = c_int32
+    lib.tro_topk_stable_f64.argtypes = [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_int64, c_void_p]
+    lib.tro_topk_stable_f64.restype = c_int32
+    lib.tro_topk_workspace_bytes.argtypes = [c_int64, c_int32]
+    lib.tro_topk_workspace_bytes.restype = c_int64
+    lib.tro_version.argtypes = []
+    lib.tro_version.restype = c_int32
+    lib.tro_error_string.argtypes = [c_int32]
+    lib.tro_error_string.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().tro_error_string(int(rc)).decode()
+        raise RuntimeError(f"{what} failed: {msg} (code {rc})")
+
+
+def require_cuda():
+    """The compute path needs a CUDA device and the library; raise otherwise."""
+    import torch
+
+    load()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2408_10731_b200 needs a CUDA (sm_100a) device; no CPU fallback exists")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

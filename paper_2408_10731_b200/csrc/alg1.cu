@@ -1,0 +1,528 @@
+// Fused batched Alg. 1 AM/AL iteration (arXiv 2408.10731) for sm_100a.
+//
+// One CTA owns one member (an independent single-robot problem) for one AM
+// iteration.  The launch does, per member:
+//   prologue  : QP position step (solver_single.py:192-211) from the target /
+//               multiplier sums the previous launch left behind:
+//               q_lin = q + (sum_j lam) P - (rho_o sum_j T) P ;  xi = K^-1 [-q_lin ; b]
+//               with K^-1 the precomputed saddle inverse of this member's rho_o
+//               level, then positions P xi (kept in shared memory);
+//   body      : one coalesced, streaming pass over the member's n_o x n_p state
+//               elements: alpha copies -> alpha -> beta copies -> beta -> d ->
+//               residuals -> multipliers (solver_single.py:214-343), fully in
+//               registers; obstacle tracks are L2-resident constants;
+//   epilogue  : sum_j lam_pos and sum_j targets for the NEXT position step
+//               (fixed-order shared-memory reduction over obstacle groups),
+//               residual norm / max-abs (warp shuffles), history, and the
+//               stall / penalty-growth rule (solver_single.py:392-404, 419-427).
+// So an AM iteration is exactly one kernel launch and the state is read once
+// and written once (HBM-bound by design).
+//
+// Thread mapping: thread k of the CTA handles horizon sample t = k % n_p and
+// obstacles j = k / n_p, +G, +2G ...  For fixed j the n_p samples are
+// contiguous in memory, so consecutive threads touch consecutive addresses.
+#include "common.cuh"
+#include "../../include/trajopt_b200.h"
+
+namespace tro {
+
+constexpr int kMaxM = 16;
+constexpr int kMaxNk = 24;
+constexpr int kMaxRing = 64;
+constexpr int kMaxThreads = 512;
+
+struct Alg1Args {
+    tro_alg1_dims d;
+    tro_alg1_consts c;
+    tro_alg1_state s;
+    tro_alg1_params p;
+    int32_t G;
+};
+
+struct SmemLayout {
+    int P, pos_prev, pos_new, sums_in, red, shp, qlin, xi, warp;
+    int total;  // doubles
+};
+
+__host__ __device__ inline SmemLayout smem_layout(int n_p, int m, int dim, int n_o, int G) {
+    SmemLayout L;
+    int off = 0;
+    L.P = off;        off += n_p * m;
+    L.pos_prev = off; off += dim * n_p;
+    L.pos_new = off;  off += dim * n_p;
+    L.sums_in = off;  off += 2 * dim * n_p;
+    L.red = off;      off += G * 2 * dim * n_p;
+    L.shp = off;      off += 4 * (n_o > 0 ? n_o : 1);
+    L.qlin = off;     off += dim * kMaxM;
+    L.xi = off;       off += dim * kMaxM;
+    L.warp = off;     off += 2 * 32;
+    L.total = off;
+    return L;
+}
+
+template <int DIM, typename T>
+__global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode) {
+    // mode 0: AM iteration; 1: prime (sums + residual of the current state); 2: cold init + prime
+    const bool prime = mode != 0;
+    const bool init = mode == 2;
+    extern __shared__ double smem[];
+    const int i = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = (nthr + 31) >> 5;
+    const int n_o = A.d.n_obs, n_p = A.d.n_p, m = A.d.m, ne = A.d.n_eq;
+    const int nk = m + ne;
+    const int G = A.G;
+    const SmemLayout L = smem_layout(n_p, m, DIM, n_o, G);
+    double* sP = smem + L.P;
+    double* sPosPrev = smem + L.pos_prev;
+    double* sPosNew = smem + L.pos_new;
+    double* sSumIn = smem + L.sums_in;
+    double* sRed = smem + L.red;
+    double* sA = smem + L.shp;
+    double* sB = sA + n_o;
+    double* sIA2 = sB + n_o;
+    double* sIB2 = sIA2 + n_o;
+    double* sQlin = smem + L.qlin;
+    double* sXi = smem + L.xi;
+    double* sWarp = smem + L.warp;
+
+    // ---------------- frozen members (converged / failed) do nothing
+    const int status0 = A.s.status[i];
+    if (!prime && (status0 & (TRO_CONVERGED | TRO_FACTOR_FAILED))) return;
+    const int level = A.s.level[i];
+    if (!prime && !A.c.level_ok[level]) {
+        // qpcore.factorize raises when the new rho_o's saddle fails the cond guard
+        // (qpcore.py:108-110); the member stops here and the host raises.
+        if (tid == 0) A.s.status[i] = status0 | TRO_FACTOR_FAILED;
+        return;
+    }
+    const double rho = A.s.rho[i];
+    const double rho_o = A.s.rho_o[i];
+
+    // ---------------- stage constants + previous positions + incoming sums
+    for (int k = tid; k < n_p * m; k += nthr) sP[k] = ld_const(A.c.P + k);
+    const double* posg = A.s.pos + (int64_t)i * DIM * n_p;
+    for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
+    if (!prime) {
+        const double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
+        for (int k = tid; k < 2 * DIM * n_p; k += nthr) sSumIn[k] = sg[k];
+    }
+    for (int k = tid; k < n_o; k += nthr) {
+        double a = ld_const(A.c.shape_a + k), b = ld_const(A.c.shape_b + k);
+        sA[k] = a;
+        sB[k] = b;
+        sIA2[k] = 1.0 / (a * a);
+        sIB2[k] = 1.0 / (b * b);
+    }
+    __syncthreads();
+
+    if (prime) {
+        // positions of the current xi; d recompute (mode 2) uses these too
+        double* xg = A.s.xi + (int64_t)i * DIM * m;
+        if (init) {
+            // straight-line coefficients (solver_single.py:127, basis.py:207-217)
+            const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
+            for (int k = tid; k < DIM * m; k += nthr) {
+                const int ax = k / m, cc = k - ax * m;
+                const double p0 = bg[ax * ne + 0], p1 = bg[ax * ne + 3];
+                const double v = A.c.line_u[cc] * p0 + A.c.line_v[cc] * (p1 - p0);
+                sXi[k] = v;
+                xg[k] = v;
+            }
+        } else {
+            for (int k = tid; k < DIM * m; k += nthr) sXi[k] = xg[k];
+        }
+        __syncthreads();
+        for (int k = tid; k < DIM * n_p; k += nthr) {
+            const int ax = k / n_p, t = k - ax * n_p;
+            double acc = 0.0;
+            for (int cc = 0; cc < m; ++cc) acc += sP[t * m + cc] * sXi[ax * m + cc];
+            sPosNew[k] = acc;
+            sPosPrev[k] = acc;
+        }
+        __syncthreads();
+        for (int k = tid; k < DIM * n_p; k += nthr) A.s.pos[(int64_t)i * DIM * n_p + k] = sPosNew[k];
+    } else {
+        // ---------- QP position step (solver_single.py:204-211)
+        // q_lin[ax][c] = (q + sum_t Slam[ax][t] P[t][c]) - sum_t (rho_o ST[ax][t]) P[t][c]
+        const double* qg = A.c.q + (int64_t)i * DIM * m;
+        for (int o = warp; o < DIM * m; o += nwarps) {
+            const int ax = o / m, cc = o - ax * m;
+            double u = 0.0, v = 0.0;
+            for (int t = lane; t < n_p; t += 32) {
+                const double pt = sP[t * m + cc];
+                u += sSumIn[ax * n_p + t] * pt;
+                v += (rho_o * sSumIn[(DIM + ax) * n_p + t]) * pt;
+            }
+            u = warp_sum(u);
+            v = warp_sum(v);
+            if (lane == 0) sQlin[o] = (qg[o] + u) - v;
+        }
+        __syncthreads();
+        // xi = K^-1 [-q_lin ; b]  (first m rows of the saddle solution, qpcore.py:141-143)
+        const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
+        const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
+        for (int o = tid; o < DIM * m; o += nthr) {
+            const int ax = o / m, r = o - ax * m;
+            const double* Kr = Kl + r * nk;
+            double acc = 0.0;
+            for (int cc = 0; cc < m; ++cc) acc += ld_const(Kr + cc) * (-sQlin[ax * m + cc]);
+            for (int e = 0; e < ne; ++e) acc += ld_const(Kr + m + e) * bg[ax * ne + e];
+            sXi[o] = acc;
+            A.s.xi[(int64_t)i * DIM * m + o] = acc;
+        }
+        __syncthreads();
+        for (int k = tid; k < DIM * n_p; k += nthr) {
+            const int ax = k / n_p, t = k - ax * n_p;
+            double acc = 0.0;
+            for (int cc = 0; cc < m; ++cc) acc += sP[t * m + cc] * sXi[ax * m + cc];
+            sPosNew[k] = acc;
+            A.s.pos[(int64_t)i * DIM * n_p + k] = acc;  // previous positions already staged
+        }
+        __syncthreads();
+    }
+
+    // ---------------- fused element pass
+    const int t = tid % n_p;
+    const int g = tid / n_p;
+    const bool act = g < G;
+    double sumsq = 0.0, mx = 0.0;
+    double accL[DIM], accT[DIM];
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) accL[ax] = accT[ax] = 0.0;
+
+    if (act) {
+        const int64_t Nel = (int64_t)A.d.n_members * n_o * n_p;
+        T* alpha = reinterpret_cast<T*>(A.s.alpha);
+        T* beta = reinterpret_cast<T*>(A.s.beta);
+        T* lam = reinterpret_cast<T*>(A.s.lam);
+        T* dst = reinterpret_cast<T*>(A.s.d);
+        T* cop = reinterpret_cast<T*>(A.s.copies);
+        const double px = sPosNew[t], py = sPosNew[n_p + t];
+        const double pz = (DIM == 3) ? sPosNew[2 * n_p + t] : 0.0;
+        const double ox = sPosPrev[t], oy = sPosPrev[n_p + t];
+        const double oz = (DIM == 3) ? sPosPrev[2 * n_p + t] : 0.0;
+        const T trho = (T)rho, trho_o = (T)rho_o;
+        const int d_mode = A.p.d_mode;
+        const T one = (T)1.0, dcap = (T)1e6;
+
+        for (int j = g; j < n_o; j += G) {
+            const int64_t e = ((int64_t)i * n_o + j) * n_p + t;
+            const double trx = ld_const(A.c.tracks + (0 * (int64_t)n_o + j) * n_p + t);
+            const double trY = ld_const(A.c.tracks + (1 * (int64_t)n_o + j) * n_p + t);
+            const double trz = (DIM == 3) ? ld_const(A.c.tracks + (2 * (int64_t)n_o + j) * n_p + t) : 0.0;
+            const T a = (T)sA[j], b = (T)sB[j];
+            const T ia2 = (T)sIA2[j], ib2 = (T)sIB2[j];
+
+            // line-of-sight scale of the previous iterate (solver_single.py:274-291)
+            T dold;
+            if (d_mode == 0) {
+                dold = one;
+            } else if (d_mode == 1) {
+                dold = dst[e];
+            } else {
+                const T ex = (T)(ox - trx), ey = (T)(oy - trY);
+                T qd;
+                if (DIM == 3) {
+                    const T ez = (T)(oz - trz);
+                    qd = ex * ex * ia2 + ey * ey * ia2 + ez * ez * ib2;
+                } else {
+                    qd = ex * ex * ia2 + ey * ey * ib2;
+                }
+                dold = fmin_t(fmax_t(one, sqrt_t(qd)), dcap);
+            }
+            const T dx = (T)(px - trx), dy = (T)(py - trY);
+
+            if (DIM == 3) {
+                const T dz = (T)(pz - trz);
+                T al, be, lx, ly, lz, lca, lsa, lcb, lsb;
+                if (init) {
+                    // angles3d of the straight-line offsets (geometry.py:102-114)
+                    const double ex = px - trx, ey = py - trY, ez = pz - trz;
+                    double a0 = atan2(ey, ex);
+                    if (a0 == -M_PI) a0 = M_PI;  // angle2d remap (geometry.py:98-99)
+                    const double ad = sA[j], bd = sB[j];
+                    al = (T)a0;
+                    be = (T)atan2(hypot(ex / ad, ey / ad), ez / bd);
+                    lx = ly = lz = lca = lsa = lcb = lsb = (T)0;
+                } else {
+                    al = ld_stream(alpha + e);
+                    be = ld_stream(beta + e);
+                    lx = ld_stream(lam + 0 * Nel + e); ly = ld_stream(lam + 1 * Nel + e);
+                    lz = ld_stream(lam + 2 * Nel + e);
+                    lca = ld_stream(lam + 3 * Nel + e); lsa = ld_stream(lam + 4 * Nel + e);
+                    lcb = ld_stream(lam + 5 * Nel + e); lsb = ld_stream(lam + 6 * Nel + e);
+                }
+                T sa, ca, sb, cb;
+                sincos_t(al, &sa, &ca);  // copy reset (solver_single.py:375-380)
+                sincos_t(be, &sb, &cb);
+                T ca2, sa2, cb2, sb2, dn;
+                if (prime) {
+                    ca2 = ca; sa2 = sa; cb2 = cb; sb2 = sb; dn = dold;
+                } else {
+                    // alpha copies (solver_single.py:223-228)
+                    const T coef = a * dold * sb;
+                    const T den = trho + trho_o * (coef * coef);
+                    const T Lx = lx + trho_o * dx, Ly = ly + trho_o * dy, Lz = lz + trho_o * dz;
+                    ca2 = (trho * ca - lca + coef * Lx) / den;
+                    sa2 = (trho * sa - lsa + coef * Ly) / den;
+                    // beta copies with the new alpha copies (solver_single.py:253-266)
+                    const T ccb = b * dold;
+                    cb2 = (trho * cb - lcb + ccb * Lz) / (trho + trho_o * (ccb * ccb));
+                    const T csb = a * dold;
+                    const T num = trho * sb - lsb + csb * (ca2 * Lx + sa2 * Ly);
+                    const T den2 = trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2);
+                    sb2 = num / den2;
+                    // d from the new positions (solver_single.py:283-290)
+                    dn = fmin_t(fmax_t(one, sqrt_t(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2)), dcap);
+                }
+                T al2 = al, be2 = be, sA2 = sa, cA2 = ca, sB2 = sb, cB2 = cb;
+                if (!prime) {
+                    al2 = atan2_t(sa2, ca2);  // solver_single.py:242
+                    be2 = atan2_t(sb2, cb2);  // solver_single.py:271
+                    sincos_t(al2, &sA2, &cA2);
+                    sincos_t(be2, &sB2, &cB2);
+                }
+                // residual families (solver_single.py:303-312)
+                const T rx = dx - a * dn * ca2 * sb2;
+                const T ry = dy - a * dn * sa2 * sb2;
+                const T rz = dz - b * dn * cb2;
+                const T rcb = cb2 - cB2, rsb = sb2 - sB2, rca = ca2 - cA2, rsa = sa2 - sA2;
+                sumsq += (double)rx * rx + (double)ry * ry + (double)rz * rz + (double)rcb * rcb +
+                         (double)rsb * rsb + (double)rca * rca + (double)rsa * rsa;
+                T mloc = fmax_t(fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rz), fabs_t(rcb))),
+                                fmax_t(fmax_t(fabs_t(rsb), fabs_t(rca)), fabs_t(rsa)));
+                mx = fmax(mx, (double)mloc);
+                if (!prime || init) {
+                    if (!prime) {
+                        // multiplier ascent (solver_single.py:336-343)
+                        lx += trho_o * rx; ly += trho_o * ry; lz += trho_o * rz;
+                        lca += trho * rca; lsa += trho * rsa; lcb += trho * rcb; lsb += trho * rsb;
+                    }
+                    st_stream(alpha + e, al2);
+                    st_stream(beta + e, be2);
+                    st_stream(lam + 0 * Nel + e, lx);
+                    st_stream(lam + 1 * Nel + e, ly);
+                    st_stream(lam + 2 * Nel + e, lz);
+                    st_stream(lam + 3 * Nel + e, lca);
+                    st_stream(lam + 4 * Nel + e, lsa);
+                    st_stream(lam + 5 * Nel + e, lcb);
+                    st_stream(lam + 6 * Nel + e, lsb);
+                    if (dst) dst[e] = dn;
+                    if (cop) {
+                        cop[0 * Nel + e] = ca2; cop[1 * Nel + e] = sa2;
+                        cop[2 * Nel + e] = cb2; cop[3 * Nel + e] = sb2;
+                    }
+                }
+                // sums for the next position step: lam and targets with the reset copies
+                // cos/sin of the new angles (solver_single.py:177-189, 204-207)
+                accL[0] += (double)lx; accL[1] += (double)ly; accL[DIM - 1] += (double)lz;
+                accT[0] += trx + (double)(a * dn * cA2 * sB2);
+                accT[1] += trY + (double)(a * dn * sA2 * sB2);
+                accT[DIM - 1] += trz + (double)(b * dn * cB2);
+            } else {
+                T al, lx, ly, lca, lsa;
+                if (init) {
+                    // scaled planar angle of the line offsets (solver_single.py:138-143)
+                    double a0 = atan2((py - trY) / sB[j], (px - trx) / sA[j]);
+                    if (a0 == -M_PI) a0 = M_PI;
+                    al = (T)a0;
+                    lx = ly = lca = lsa = (T)0;
+                } else {
+                    al = ld_stream(alpha + e);
+                    lx = ld_stream(lam + 0 * Nel + e); ly = ld_stream(lam + 1 * Nel + e);
+                    lca = ld_stream(lam + 2 * Nel + e); lsa = ld_stream(lam + 3 * Nel + e);
+                }
+                T sa, ca;
+                sincos_t(al, &sa, &ca);
+                T ca2, sa2, dn;
+                if (prime) {
+                    ca2 = ca; sa2 = sa; dn = dold;
+                } else {
+                    // planar alpha copies (solver_single.py:229-237)
+                    const T cx = a * dold, cy = b * dold;
+                    ca2 = (trho * ca - lca + cx * (lx + trho_o * dx)) / (trho + trho_o * (cx * cx));
+                    sa2 = (trho * sa - lsa + cy * (ly + trho_o * dy)) / (trho + trho_o * (cy * cy));
+                    dn = fmin_t(fmax_t(one, sqrt_t(dx * dx * ia2 + dy * dy * ib2)), dcap);
+                }
+                T al2 = al, sA2 = sa, cA2 = ca;
+                if (!prime) {
+                    al2 = atan2_t(sa2, ca2);
+                    sincos_t(al2, &sA2, &cA2);
+                }
+                const T rx = dx - a * dn * ca2;
+                const T ry = dy - b * dn * sa2;
+                const T rca = ca2 - cA2, rsa = sa2 - sA2;
+                sumsq += (double)rx * rx + (double)ry * ry + (double)rca * rca + (double)rsa * rsa;
+                T mloc = fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rca), fabs_t(rsa)));
+                mx = fmax(mx, (double)mloc);
+                if (!prime || init) {
+                    if (!prime) {
+                        lx += trho_o * rx; ly += trho_o * ry;
+                        lca += trho * rca; lsa += trho * rsa;
+                    }
+                    st_stream(alpha + e, al2);
+                    st_stream(lam + 0 * Nel + e, lx);
+                    st_stream(lam + 1 * Nel + e, ly);
+                    st_stream(lam + 2 * Nel + e, lca);
+                    st_stream(lam + 3 * Nel + e, lsa);
+                    if (dst) dst[e] = dn;
+                    if (cop) { cop[0 * Nel + e] = ca2; cop[1 * Nel + e] = sa2; }
+                }
+                accL[0] += (double)lx; accL[1] += (double)ly;
+                accT[0] += trx + (double)(a * dn * cA2);
+                accT[1] += trY + (double)(b * dn * sA2);
+            }
+        }
+    }
+
+    // ---------------- epilogue: sums over obstacle groups (fixed order)
+    if (act) {
+#pragma unroll
+        for (int ax = 0; ax < DIM; ++ax) {
+            sRed[(g * 2 * DIM + ax) * n_p + t] = accL[ax];
+            sRed[(g * 2 * DIM + DIM + ax) * n_p + t] = accT[ax];
+        }
+    }
+    // residual reductions
+    sumsq = warp_sum(sumsq);
+    mx = warp_max(mx);
+    if (lane == 0) {
+        sWarp[warp] = sumsq;
+        sWarp[32 + warp] = mx;
+    }
+    __syncthreads();
+    double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
+    for (int k = tid; k < 2 * DIM * n_p; k += nthr) {
+        double acc = 0.0;
+        for (int gg = 0; gg < G; ++gg) acc += sRed[gg * 2 * DIM * n_p + k];
+        sg[k] = acc;
+    }
+    if (tid == 0) {
+        double ss = 0.0, mm = 0.0;
+        for (int w = 0; w < nwarps; ++w) {
+            ss += sWarp[w];
+            mm = fmax(mm, sWarp[32 + w]);
+        }
+        if (ss != ss) mm = ss;  // np.max propagates NaN
+        const double nrm = sqrt(ss);
+        A.s.res_norm[i] = nrm;
+        A.s.res_max[i] = mm;
+        if (!prime && (A.p.flags & TRO_FLAG_NO_SCHEDULE)) {
+            A.s.iteration[i] += 1;  // bare am_iteration (solver_single.py:388)
+        } else if (!prime) {
+            const int it = A.s.iteration[i] + 1;  // am_iteration: state.iteration += 1
+            A.s.iteration[i] = it;
+            const int nh = A.s.n_hist[i];
+            if (A.s.hist && nh < A.p.max_hist) {
+                double* h = A.s.hist + ((int64_t)i * A.p.max_hist + nh) * 3;
+                h[0] = nrm;
+                h[1] = mm;
+                h[2] = rho_o;
+            }
+            const int n = nh + 1;
+            A.s.n_hist[i] = n;
+            const int w = A.p.stall_window, w2 = 2 * w;
+            double* ring = A.s.ring + (int64_t)i * w2;
+            ring[(n - 1) % w2] = mm;
+            if (mm <= A.p.tol) {  // solver_single.py:424-426 (break before growth)
+                A.s.status[i] = status0 | TRO_CONVERGED;
+            } else {
+                const int lc = A.s.last_change[i];
+                if (n >= w2 && it - lc >= w) {  // solver_single.py:394
+                    double sr = 0.0, sp = 0.0;  // np.mean of <8 values: sequential sum / w
+                    for (int k = 0; k < w; ++k) sr += ring[(n - w + k) % w2];
+                    for (int k = 0; k < w; ++k) sp += ring[(n - w2 + k) % w2];
+                    const double recent = sr / (double)w, previous = sp / (double)w;
+                    if (!(previous <= fmax(A.p.tol, 0.0)) && (previous - recent) / previous < A.p.stall_improvement) {
+                        const double nr = fmin(rho * A.p.rho_growth, A.p.rho_cap);
+                        const double nro = fmin(rho_o * A.p.rho_growth, A.p.rho_cap);
+                        A.s.rho[i] = nr;
+                        A.s.rho_o[i] = nro;
+                        if (nro != rho_o) {
+                            A.s.level[i] = level + 1;
+                            A.s.n_changes[i] += 1;
+                        }
+                        A.s.last_change[i] = it;
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int DIM, typename T>
+static int launch(const Alg1Args& A, int mode, cudaStream_t st) {
+    const int n_p = A.d.n_p;
+    int threads = ((n_p * A.G + 31) / 32) * 32;
+    if (threads < 64) threads = 64;
+    const SmemLayout L = smem_layout(n_p, A.d.m, DIM, A.d.n_obs, A.G);
+    const size_t smem = (size_t)L.total * sizeof(double);
+    if (smem > 48 * 1024) {
+        // per-device attribute: cheap host call, set lazily per device
+        static bool attr_set[64] = {false};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+            cudaFuncSetAttribute(alg1_kernel<DIM, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            attr_set[dev] = true;
+        }
+    }
+    alg1_kernel<DIM, T><<<A.d.n_members, threads, smem, st>>>(A, mode);
+    return (int)cudaGetLastError();
+}
+
+static int auto_groups(const tro_alg1_dims* d) {
+    int G = d->groups;
+    if (G <= 0) {
+        G = 512 / d->n_p;
+        if (G < 1) G = 1;
+    }
+    if (d->n_obs > 0 && G > d->n_obs) G = d->n_obs;
+    if (G < 1) G = 1;
+    while (G > 1 && d->n_p * G > kMaxThreads) --G;
+    return G;
+}
+
+static int run(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c, const tro_alg1_state* s,
+               const tro_alg1_params* p, void* stream, int mode) {
+    if (!dims || !c || !s || !p) return TRO_EINVAL;
+    if (dims->dim != 2 && dims->dim != 3) return TRO_EINVAL;
+    if (dims->m < 1 || dims->m > kMaxM || dims->m + dims->n_eq > kMaxNk) return TRO_EINVAL;
+    if (dims->n_p < 2 || dims->n_p > kMaxThreads || dims->n_obs < 0) return TRO_EINVAL;
+    if (p->stall_window < 1 || 2 * p->stall_window > kMaxRing) return TRO_EINVAL;
+    if (dtype != TRO_F64 && dtype != TRO_F32) return TRO_EINVAL;
+    if (dims->n_members <= 0) return 0;
+    Alg1Args A;
+    A.d = *dims;
+    A.c = *c;
+    A.s = *s;
+    A.p = *p;
+    A.G = auto_groups(dims);
+    const SmemLayout L = smem_layout(dims->n_p, dims->m, dims->dim, dims->n_obs, A.G);
+    if ((size_t)L.total * sizeof(double) > 200 * 1024) return TRO_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dims->dim == 3) {
+        return dtype == TRO_F64 ? launch<3, double>(A, mode, st) : launch<3, float>(A, mode, st);
+    }
+    return dtype == TRO_F64 ? launch<2, double>(A, mode, st) : launch<2, float>(A, mode, st);
+}
+
+}  // namespace tro
+
+extern "C" int tro_alg1_prime(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                              const tro_alg1_state* s, const tro_alg1_params* p, void* stream) {
+    return tro::run(dtype, dims, c, s, p, stream, 1);
+}
+
+extern "C" int tro_alg1_iterate(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                                const tro_alg1_state* s, const tro_alg1_params* p, void* stream) {
+    return tro::run(dtype, dims, c, s, p, stream, 0);
+}
+
+extern "C" int tro_alg1_init(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                             const tro_alg1_state* s, const tro_alg1_params* p, void* stream) {
+    if (c && (!c->line_u || !c->line_v)) return TRO_EINVAL;
+    return tro::run(dtype, dims, c, s, p, stream, 2);
+}

@@ -1,0 +1,240 @@
+"""Generate golden fixtures from the LIVE reference package (run in the build container only).
+
+    PYTHONPATH=/root/reference/pkg/src OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden.py
+
+Imports the unmodified reference ``trajopt`` (arxiv/paper_2408_10731) from
+/root/reference/pkg/src and writes small npz fixtures next to this script.
+Nothing at test time reads /root/reference: the fixtures are committed.
+
+Fixtures (reduced to keep the repo small):
+  c1.npz        C1 (random-static 3-D, 10 obstacles, n_p 100): init state, a fixed
+                100-iteration run (tol 0) and the default converged solve.
+  flow3d_tf.npz C2 recipe (n_o 50) members 0/1: full-state snapshots at iteration
+                pairs (k, k+1) for teacher-forced one-step parity.
+  flow3d_hist.npz C2 recipe (n_o 50) members 0..7: 200-iteration residual / rho
+                histories, final xi, and the LU-vs-K^-1 twin-divergence iteration.
+  corridor2d.npz 2-D corridor (acceptance criterion 3 scenario): 200-iteration run
+                and a teacher-forced pair.
+  qp.npz        random saddle systems solved by qpcore.solve / solve_batch.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = os.environ.get("TRAJOPT_REF", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+
+from scipy.linalg import lu_solve  # noqa: E402
+
+from trajopt import qpcore, solver_single  # noqa: E402
+from trajopt.basis import build_basis  # noqa: E402
+from trajopt.bench.runner import single_problem_from_scenario  # noqa: E402
+from trajopt.bench.scenarios import Boundary, Horizon, RobotSpec, Scenario, ScenarioObstacle, gen_scenario  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(OUT, "..", "..")))
+from paper_2408_10731_b200.scenarios import flow3d_endpoints, flow3d_obstacles  # noqa: E402  (recipe only)
+
+
+def problem_arrays(prob):
+    b = prob.basis
+    tracks = np.stack([o.centers for o in prob.obstacles]) if prob.obstacles else np.zeros((0, b.n_p, prob.dim))
+    return dict(
+        P=b.P, Pd=b.Pdot, Pdd=b.Pddot, t=b.grid.timestamps,
+        tracks=tracks,
+        a=np.array([o.shape.a for o in prob.obstacles]),
+        b=np.array([o.shape.b for o in prob.obstacles]),
+        bvals=np.stack([bc.values() for bc in prob.boundary])[None],
+        desired=prob.desired[None],
+        w=np.array([prob.w_smooth, prob.w_track]),
+    )
+
+
+def state_arrays(st, prefix):
+    out = {f"{prefix}xi": st.xi.copy(), f"{prefix}d": st.d.copy(), f"{prefix}alpha": st.alpha.copy(),
+           f"{prefix}lam_pos": st.lam_pos.copy(), f"{prefix}lam_cos_a": st.lam_cos_a.copy(),
+           f"{prefix}lam_sin_a": st.lam_sin_a.copy(), f"{prefix}cos_a": st.cos_a.copy(),
+           f"{prefix}sin_a": st.sin_a.copy(),
+           f"{prefix}scal": np.array([st.rho, st.rho_o, st.iteration], dtype=float)}
+    if st.beta is not None:
+        out.update({f"{prefix}beta": st.beta.copy(), f"{prefix}lam_cos_b": st.lam_cos_b.copy(),
+                    f"{prefix}lam_sin_b": st.lam_sin_b.copy(), f"{prefix}cos_b": st.cos_b.copy(),
+                    f"{prefix}sin_b": st.sin_b.copy()})
+    return out
+
+
+def run_with_snapshots(prob, params, snap_at):
+    """solve_single's loop (solver_single.py:413-427), snapshotting the state after iteration k."""
+    import copy
+
+    state = solver_single.init_state(prob, params=params)
+    history, max_hist, last_change = [], [], 0
+    snaps = {}
+    if 0 in snap_at:
+        snaps[0] = (copy.deepcopy(state), list(max_hist), last_change)
+    for k in range(params.max_iter):
+        solver_single.am_iteration(state, prob)
+        norm, mx = solver_single._residual_extremes(state, prob)
+        history.append((norm, mx, state.rho_o))
+        max_hist.append(mx)
+        if mx <= params.tol:
+            break
+        last_change = solver_single._maybe_grow_penalties(state, params, max_hist, last_change)
+        if k + 1 in snap_at:
+            snaps[k + 1] = (copy.deepcopy(state), list(max_hist), last_change)
+    return np.array(history), state, snaps
+
+
+def flow3d_problem(n_o, member, basis):
+    specs = flow3d_obstacles(n_o, 0)
+    starts, goals = flow3d_endpoints([member])
+    sc = Scenario(kind="dynamic-flow", dim=3, horizon=Horizon(0.0, 10.0, 100),
+                  robot=RobotSpec(shape=[0.0, 0.0], v_max=3.0, a_max=3.0),
+                  obstacles=[ScenarioObstacle(a=o.a, b=o.b, center=[float(v) for v in o.center],
+                                              velocity=[float(v) for v in o.velocity]) for o in specs],
+                  boundary=Boundary(start=[float(v) for v in starts[0]], goal=[float(v) for v in goals[0]]),
+                  seed=0)
+    return single_problem_from_scenario(sc, basis)
+
+
+class KinvPatch:
+    """qpcore.solve_batch through an explicit fp64 K^-1 GEMM (SURVEY.md A.1 twin)."""
+
+    def __enter__(self):
+        self.orig = qpcore.solve_batch
+
+        def kinv_solve(factor, rhs):
+            K = lu_solve(factor._lu, np.eye(factor.size))
+            block = np.hstack([-rhs.qs, rhs.bs]).T
+            sol = K @ block
+            return sol[: factor.n_v].T, sol[factor.n_v:].T
+
+        qpcore.solve_batch = kinv_solve
+        solver_single.qpcore.solve_batch = kinv_solve
+        return self
+
+    def __exit__(self, *a):
+        qpcore.solve_batch = self.orig
+        solver_single.qpcore.solve_batch = self.orig
+
+
+def make_c1():
+    sc = gen_scenario("random-static", {"dim": 3, "n_o": 10, "n_p": 100}, seed=0)
+    basis = build_basis(sc.horizon.t0, sc.horizon.tf, sc.horizon.n_p, 10)
+    prob = single_problem_from_scenario(sc, basis)
+    out = problem_arrays(prob)
+    st0 = solver_single.init_state(prob)
+    out.update(state_arrays(st0, "init_"))
+    sol = solver_single.solve_single(prob, solver_single.SingleParams(max_iter=100, tol=0.0))
+    out["fixed_hist"] = np.array([[h["norm"], h["max_abs"], h["rho_o"]] for h in sol.residual_history])
+    out.update(state_arrays(sol.state, "fixed_"))
+    out["fixed_nfact"] = np.array([sol.n_factorizations])
+    sol = solver_single.solve_single(prob, solver_single.SingleParams())
+    out["conv_hist"] = np.array([[h["norm"], h["max_abs"], h["rho_o"]] for h in sol.residual_history])
+    out["conv_xi"] = sol.state.xi
+    out["conv_meta"] = np.array([sol.iterations, int(sol.converged), sol.n_factorizations, sol.residual_norm,
+                                 sol.residual_max, sol.smoothness_cost, sol.tracking_cost])
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), **out)
+    print("c1: converged in", sol.iterations, "iterations")
+
+
+def make_flow3d_tf():
+    basis = build_basis(0.0, 10.0, 100, 10)
+    params = solver_single.SingleParams(max_iter=200, tol=0.0)
+    out = {}
+    plan = {0: (0, 1, 60), 1: (10,)}
+    for member, ks in plan.items():
+        prob = flow3d_problem(50, member, basis)
+        if member == 0:
+            out.update(problem_arrays(prob))
+        out[f"m{member}_bvals"] = problem_arrays(prob)["bvals"]
+        out[f"m{member}_desired"] = problem_arrays(prob)["desired"]
+        snap_at = sorted(set(ks) | {k + 1 for k in ks})
+        _, _, snaps = run_with_snapshots(prob, params, set(snap_at))
+        for k in snap_at:
+            st, mh, lc = snaps[k]
+            out.update(state_arrays(st, f"m{member}_k{k}_"))
+            out[f"m{member}_k{k}_maxhist"] = np.array(mh)
+            out[f"m{member}_k{k}_last_change"] = np.array([lc])
+        out[f"m{member}_ks"] = np.array(ks)
+    np.savez_compressed(os.path.join(OUT, "flow3d_tf.npz"), **out)
+    print("flow3d_tf written")
+
+
+def make_flow3d_hist(members=range(8)):
+    basis = build_basis(0.0, 10.0, 100, 10)
+    params = solver_single.SingleParams(max_iter=200, tol=0.0)
+    hists, xis, twin = [], [], []
+    for mbr in members:
+        prob = flow3d_problem(50, mbr, basis)
+        if mbr == 0:
+            arrays = problem_arrays(prob)
+        sol = solver_single.solve_single(prob, params)
+        h = np.array([[x["norm"], x["max_abs"], x["rho_o"]] for x in sol.residual_history])
+        with KinvPatch():
+            sol2 = solver_single.solve_single(prob, params)
+        h2 = np.array([[x["norm"], x["max_abs"], x["rho_o"]] for x in sol2.residual_history])
+        rel = np.abs(h2[:, 0] - h[:, 0]) / np.abs(h[:, 0])
+        bad = np.nonzero(rel > 1e-9)[0]
+        twin.append(int(bad[0]) if bad.size else len(rel))
+        hists.append(h)
+        xis.append(sol.state.xi)
+    starts, goals = flow3d_endpoints(list(members))
+    np.savez_compressed(os.path.join(OUT, "flow3d_hist.npz"), hist=np.array(hists), xi=np.array(xis),
+                        twin=np.array(twin), starts=starts, goals=goals, members=np.array(list(members)),
+                        **{k: arrays[k] for k in ("P", "Pd", "Pdd", "t", "tracks", "a", "b", "w")})
+    print("flow3d_hist twin-divergence iterations:", twin)
+
+
+def make_corridor():
+    sc = gen_scenario("corridor", {"n_o": 10, "n_p": 100}, seed=0)
+    basis = build_basis(sc.horizon.t0, sc.horizon.tf, sc.horizon.n_p, 10)
+    prob = single_problem_from_scenario(sc, basis)
+    out = problem_arrays(prob)
+    params = solver_single.SingleParams(max_iter=200, tol=0.0)
+    hist, st, snaps = run_with_snapshots(prob, params, {5, 6, 80, 81})
+    out["hist"] = hist
+    out.update(state_arrays(st, "final_"))
+    for k in (5, 6, 80, 81):
+        s, mh, lc = snaps[k]
+        out.update(state_arrays(s, f"k{k}_"))
+        out[f"k{k}_maxhist"] = np.array(mh)
+        out[f"k{k}_last_change"] = np.array([lc])
+    with KinvPatch():
+        hist2, _, _ = run_with_snapshots(prob, params, set())
+    rel = np.abs(hist2[:, 0] - hist[:, 0]) / np.abs(hist[:, 0])
+    bad = np.nonzero(rel > 1e-9)[0]
+    out["twin"] = np.array([int(bad[0]) if bad.size else len(rel)])
+    np.savez_compressed(os.path.join(OUT, "corridor2d.npz"), **out)
+    print("corridor twin divergence:", out["twin"])
+
+
+def make_qp():
+    rng = np.random.default_rng(0)
+    out = {}
+    for c in range(6):
+        n_v = int(rng.integers(3, 21))
+        n_eq = int(rng.integers(1, min(n_v, 7)))
+        M = rng.normal(size=(n_v, n_v))
+        Q = M @ M.T + np.eye(n_v)
+        A = rng.normal(size=(n_eq, n_v))
+        qs = rng.normal(size=(40, n_v))
+        bs = rng.normal(size=(40, n_eq))
+        f = qpcore.factorize(Q, A)
+        xis, nus = qpcore.solve_batch(f, qpcore.BatchRHS(qs=qs, bs=bs))
+        out.update({f"c{c}_Q": Q, f"c{c}_A": A, f"c{c}_qs": qs, f"c{c}_bs": bs, f"c{c}_xis": xis,
+                    f"c{c}_nus": nus, f"c{c}_cond": np.array([f.cond_estimate])})
+    np.savez_compressed(os.path.join(OUT, "qp.npz"), **out)
+    print("qp written")
+
+
+if __name__ == "__main__":
+    make_qp()
+    make_c1()
+    make_corridor()
+    make_flow3d_tf()
+    make_flow3d_hist()

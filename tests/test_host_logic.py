@@ -1,0 +1,129 @@
+"""Host-side logic that needs no GPU: basis, level tables, scenario recipes, API guards."""
+
+import numpy as np
+import pytest
+
+from oracle import alg1 as O
+from paper_2408_10731_b200 import basis as B
+from paper_2408_10731_b200 import qpcore, scenarios
+from paper_2408_10731_b200._alg1 import LevelTable, rho_chain
+from paper_2408_10731_b200.solver_single import SingleBatch, SingleParams
+
+
+def test_basis_matches_golden(golden):
+    g = golden("c1.npz")
+    bs = B.build_basis(0.0, 10.0, 100, 10)
+    np.testing.assert_allclose(bs.P, g["P"], atol=1e-15)
+    np.testing.assert_allclose(bs.Pdot, g["Pd"], atol=1e-14)
+    np.testing.assert_allclose(bs.Pddot, g["Pdd"], atol=1e-13)
+
+
+def test_basis_guards():
+    with pytest.raises(ValueError):
+        B.build_basis(1.0, 1.0, 10, 3)
+    with pytest.raises(ValueError):
+        B.build_basis(0.0, 1.0, 1, 3)
+    with pytest.raises(ValueError):
+        B.build_basis(0.0, 1.0, 10, -1)
+
+
+def test_line_vectors_reproduce_lstsq():
+    bs = B.build_basis(0.0, 10.0, 100, 10)
+    u, v = B.line_basis_vectors(bs)
+    p0, p1 = np.array([0.0, -0.3, 0.2]), np.array([12.0, 0.7, -0.1])
+    ref = B.straight_line_coeffs(bs, p0, p1)
+    got = u[None, :] * p0[:, None] + v[None, :] * (p1 - p0)[:, None]
+    np.testing.assert_allclose(got, ref, atol=1e-13)
+
+
+def test_rho_chain_is_the_reference_schedule():
+    chain = rho_chain(1.0, 1.4, 1e3)
+    np.testing.assert_array_equal(chain, O.rho_levels(O.Params()))
+    assert len(chain) == 22
+
+
+def test_level_table_matches_oracle_kinv(golden):
+    g = golden("c1.npz")
+    bs = B.build_basis(0.0, 10.0, 100, 10)
+    tab = LevelTable(bs, 10, 1.0, 1.0, [1.0], 1.4, 1e3)
+    prob = O.Problem(P=g["P"], Pd=g["Pd"], Pdd=g["Pdd"], bvals=g["bvals"], desired=g["desired"],
+                     tracks=g["tracks"], a=g["a"], b=g["b"])
+    kkt = O.KKTCache(prob, mode="kinv")
+    for lv in (0, 5, 21):
+        ref = kkt.kinv(tab.rhos[lv])
+        np.testing.assert_allclose(tab.kinv[lv], ref, rtol=0, atol=1e-9 * np.abs(ref).max())
+    assert tab.ok.all()
+
+
+def test_level_table_cond_guard_marks_levels():
+    bs = B.build_basis(0.0, 10.0, 100, 10)
+    # a tiny cond limit makes every level fail the guard -> marked, not raised
+    tab = LevelTable(bs, 10, 1.0, 1.0, [1.0], 1.4, 1e3, cond_limit=10.0)
+    assert not tab.ok.any()
+    assert isinstance(tab.error_for(0), qpcore.FactorizationError)
+
+
+def test_factorize_guards_and_count():
+    before = qpcore.factorization_count()
+    Q = np.eye(3)
+    A = np.array([[1.0, 1.0, 1.0]])
+    f = qpcore.factorize(Q, A)
+    assert f.size == 4 and qpcore.factorization_count() == before + 1
+    np.testing.assert_allclose(f.kinv @ qpcore.saddle_matrix(Q, A), np.eye(4), atol=1e-12)
+    with pytest.raises(qpcore.FactorizationError):
+        qpcore.factorize(Q, np.array([[1.0, 1.0, 1.0], [2.0, 2.0, 2.0]]))
+    with pytest.raises(ValueError):
+        qpcore.factorize(np.array([[1.0, 2.0], [0.0, 1.0]]), np.array([[1.0, 0.0]]))
+    with pytest.raises(qpcore.FactorizationError):
+        qpcore.factorize(np.diag([1.0, 1e-14, 1.0]), np.array([[1.0, 0.0, 0.0]]))
+
+
+def test_batch_rhs_guards():
+    with pytest.raises(ValueError):
+        qpcore.BatchRHS(qs=np.zeros((2, 3)), bs=np.zeros((3, 1)))
+    with pytest.raises(ValueError):
+        qpcore.BatchRHS(qs=np.zeros((0, 3)), bs=np.zeros((0, 1)))
+
+
+def test_flow3d_recipe_matches_golden(golden):
+    g = golden("flow3d_hist.npz")
+    bs = B.build_basis(0.0, 10.0, 100, 10)
+    batch = scenarios.flow3d_batch(50, range(8), basis=bs)
+    tracks = np.stack([o.centers for o in batch.obstacles])
+    np.testing.assert_array_equal(tracks, g["tracks"])
+    np.testing.assert_array_equal([o.shape.a for o in batch.obstacles], g["a"])
+    np.testing.assert_array_equal(batch.bvals[:, :, 0], g["starts"])
+    np.testing.assert_array_equal(batch.bvals[:, :, 3], g["goals"])
+
+
+def test_c1_scenario_matches_golden(golden):
+    g = golden("c1.npz")
+    prob = scenarios.c1_problem()
+    np.testing.assert_array_equal(np.stack([o.centers for o in prob.obstacles]), g["tracks"])
+    np.testing.assert_array_equal(prob.desired, g["desired"][0])
+
+
+def test_batch_linear_terms_match_single_formula(golden):
+    g = golden("flow3d_tf.npz")
+    bs = B.build_basis(0.0, 10.0, 100, 10)
+    batch = scenarios.flow3d_batch(50, [0, 1], basis=bs)
+    q = batch.linear_terms()
+    for i in range(2):
+        ref = -2.0 * 1.0 * (g["P"].T @ g[f"m{i}_desired"][0]).T
+        np.testing.assert_allclose(q[i], ref, atol=1e-12)
+    p = batch.problem(1)
+    np.testing.assert_allclose(p.desired, g["m1_desired"][0], atol=1e-15)
+
+
+def test_single_params_defaults_match_reference():
+    p = SingleParams()
+    assert (p.max_iter, p.tol, p.rho_start, p.rho_growth, p.rho_cap, p.stall_window, p.stall_improvement) == (
+        300, 1e-3, 1.0, 1.4, 1e3, 5, 0.01)
+
+
+def test_from_problems_requires_shared_obstacles():
+    bs = B.build_basis(0.0, 10.0, 50, 8)
+    b1 = scenarios.flow3d_batch(5, [0], basis=bs).problem(0)
+    b2 = scenarios.flow3d_batch(6, [1], basis=bs).problem(0)
+    with pytest.raises(ValueError):
+        SingleBatch.from_problems([b1, b2])

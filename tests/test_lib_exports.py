@@ -1,0 +1,45 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol the header declares."""
+
+import ctypes
+import os
+import re
+
+from paper_2408_10731_b200 import _lib
+
+HEADER = os.path.join(os.path.dirname(__file__), "..", "include", "trajopt_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|const char\*)\s+(tro_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    names = declared_functions()
+    assert set(names) == set(_lib.EXPORTS), names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_struct_layouts_match_header():
+    # 8 int32 dims; 11 const pointers; 4 doubles + 4 int32; 20 pointers
+    assert ctypes.sizeof(_lib.Alg1Dims) == 32
+    assert ctypes.sizeof(_lib.Alg1Consts) == 11 * 8
+    assert ctypes.sizeof(_lib.Alg1Params) == 4 * 8 + 4 * 4
+    assert ctypes.sizeof(_lib.Alg1State) == 20 * 8
+
+
+def test_host_only_calls():
+    lib = _lib.load()
+    assert lib.tro_version() >= 1
+    assert lib.tro_error_string(0) == b"success"
+    assert b"invalid" in lib.tro_error_string(-1)
+    assert lib.tro_topk_workspace_bytes(1000, 10) == 8000
+    # argument validation happens before any CUDA call
+    assert lib.tro_topk_stable_f64(None, 10, 20, None, None, 0, None) == _lib.TRO_EINVAL
+    assert lib.tro_kkt_apply_f64(None, 4, None, 1, None, None) == _lib.TRO_EINVAL
+    assert lib.tro_alg1_iterate(0, None, None, None, None, None) == _lib.TRO_EINVAL
