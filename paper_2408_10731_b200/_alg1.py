@@ -104,7 +104,7 @@ class Alg1Engine:
         self.table = LevelTable(basis, n_o, w_smooth, w_track, np.unique(rho0), params.rho_growth, params.rho_cap,
                                 cond_limit)
         self.basis = basis
-        self.P = torch.as_tensor(np.ascontiguousarray(basis.P), **f64)
+        self.P = torch.as_tensor(np.array(basis.P, dtype=float, copy=True), **f64)
         self.tracks = torch.as_tensor(np.ascontiguousarray(np.transpose(tracks, (2, 0, 1))) if n_o else
                                       np.zeros((dim, 0, n_p)), **f64).contiguous()
         self.shape_a = torch.as_tensor(np.asarray(shape_a, dtype=float).reshape(-1), **f64)

@@ -13,7 +13,8 @@ import os
 from ctypes import POINTER, c_double, c_int32, c_int64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtrajopt_b200.so")
+# TRO_LIB_PATH selects a tuning variant built by `make variant` (tools/tune_alg1.py)
+LIB_PATH = os.environ.get("TRO_LIB_PATH") or os.path.join(_HERE, "libtrajopt_b200.so")
 
 TRO_F64 = 0
 TRO_F32 = 1

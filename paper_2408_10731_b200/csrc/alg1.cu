@@ -22,6 +22,7 @@
 // obstacles j = k / n_p, +G, +2G ...  For fixed j the n_p samples are
 // contiguous in memory, so consecutive threads touch consecutive addresses.
 #include "common.cuh"
+#include "fastmath.cuh"
 #include "../../include/trajopt_b200.h"
 
 namespace tro {
@@ -29,7 +30,17 @@ namespace tro {
 constexpr int kMaxM = 16;
 constexpr int kMaxNk = 24;
 constexpr int kMaxRing = 64;
-constexpr int kMaxThreads = 512;
+#ifndef TRO_MAX_THREADS
+#define TRO_MAX_THREADS 512
+#endif
+#ifndef TRO_MIN_BLOCKS
+#define TRO_MIN_BLOCKS 1
+#endif
+#ifndef TRO_UNROLL
+#define TRO_UNROLL 2
+#endif
+constexpr int kMaxThreads = TRO_MAX_THREADS;
+constexpr int kUnroll = TRO_UNROLL;
 
 struct Alg1Args {
     tro_alg1_dims d;
@@ -60,11 +71,25 @@ __host__ __device__ inline SmemLayout smem_layout(int n_p, int m, int dim, int n
     return L;
 }
 
-template <int DIM, typename T>
-__global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode) {
-    // mode 0: AM iteration; 1: prime (sums + residual of the current state); 2: cold init + prime
-    const bool prime = mode != 0;
-    const bool init = mode == 2;
+// cos/sin of atan2(s, c) without trigonometry: (c, s) / hypot(c, s)
+template <typename T>
+__device__ __forceinline__ void unit_dir(T c, T s, T* cu, T* su) {
+    const T h2 = c * c + s * s;
+    if (h2 > (T)0 && h2 < (T)1e300) {
+        const T r = rsqrt_fast(h2);
+        *cu = c * r;
+        *su = s * r;
+    } else {  // atan2(+-0, +-0) = 0 or pi
+        *cu = signbit(c) ? (T)-1 : (T)1;
+        *su = copysign((T)0, s);
+    }
+}
+
+template <int DIM, typename T, int MODE>
+__global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1Args A) {
+    // MODE 0: AM iteration; 1: prime (sums + residual of the current state); 2: cold init + prime
+    constexpr bool prime = MODE != 0;
+    constexpr bool init = MODE == 2;
     extern __shared__ double smem[];
     const int i = blockIdx.x;
     const int tid = threadIdx.x;
@@ -103,7 +128,8 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
     // ---------------- stage constants + previous positions + incoming sums
     for (int k = tid; k < n_p * m; k += nthr) sP[k] = ld_const(A.c.P + k);
     const double* posg = A.s.pos + (int64_t)i * DIM * n_p;
-    for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
+    if (!prime)
+        for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
     if (!prime) {
         const double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
         for (int k = tid; k < 2 * DIM * n_p; k += nthr) sSumIn[k] = sg[k];
@@ -117,10 +143,10 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
     }
     __syncthreads();
 
-    if (prime) {
+    if constexpr (prime) {
         // positions of the current xi; d recompute (mode 2) uses these too
         double* xg = A.s.xi + (int64_t)i * DIM * m;
-        if (init) {
+        if constexpr (init) {
             // straight-line coefficients (solver_single.py:127, basis.py:207-217)
             const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
             for (int k = tid; k < DIM * m; k += nthr) {
@@ -140,9 +166,9 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
             for (int cc = 0; cc < m; ++cc) acc += sP[t * m + cc] * sXi[ax * m + cc];
             sPosNew[k] = acc;
             sPosPrev[k] = acc;
+            A.s.pos[(int64_t)i * DIM * n_p + k] = acc;
         }
         __syncthreads();
-        for (int k = tid; k < DIM * n_p; k += nthr) A.s.pos[(int64_t)i * DIM * n_p + k] = sPosNew[k];
     } else {
         // ---------- QP position step (solver_single.py:204-211)
         // q_lin[ax][c] = (q + sum_t Slam[ax][t] P[t][c]) - sum_t (rho_o ST[ax][t]) P[t][c]
@@ -194,9 +220,9 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
 
     if (act) {
         const int64_t Nel = (int64_t)A.d.n_members * n_o * n_p;
-        T* alpha = reinterpret_cast<T*>(A.s.alpha);
-        T* beta = reinterpret_cast<T*>(A.s.beta);
-        T* lam = reinterpret_cast<T*>(A.s.lam);
+        T* __restrict__ alpha = reinterpret_cast<T*>(A.s.alpha);
+        T* __restrict__ beta = reinterpret_cast<T*>(A.s.beta);
+        T* __restrict__ lam = reinterpret_cast<T*>(A.s.lam);
         T* dst = reinterpret_cast<T*>(A.s.d);
         T* cop = reinterpret_cast<T*>(A.s.copies);
         const double px = sPosNew[t], py = sPosNew[n_p + t];
@@ -204,14 +230,17 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
         const double ox = sPosPrev[t], oy = sPosPrev[n_p + t];
         const double oz = (DIM == 3) ? sPosPrev[2 * n_p + t] : 0.0;
         const T trho = (T)rho, trho_o = (T)rho_o;
-        const int d_mode = A.p.d_mode;
+        const int d_mode = init ? 0 : A.p.d_mode;
         const T one = (T)1.0, dcap = (T)1e6;
+        const double* trk = A.c.tracks + (int64_t)t;
+        const int64_t tstride = (int64_t)n_o * n_p;
 
+#pragma unroll kUnroll
         for (int j = g; j < n_o; j += G) {
             const int64_t e = ((int64_t)i * n_o + j) * n_p + t;
-            const double trx = ld_const(A.c.tracks + (0 * (int64_t)n_o + j) * n_p + t);
-            const double trY = ld_const(A.c.tracks + (1 * (int64_t)n_o + j) * n_p + t);
-            const double trz = (DIM == 3) ? ld_const(A.c.tracks + (2 * (int64_t)n_o + j) * n_p + t) : 0.0;
+            const double trx = ld_const(trk + (int64_t)j * n_p);
+            const double trY = ld_const(trk + tstride + (int64_t)j * n_p);
+            const double trz = (DIM == 3) ? ld_const(trk + 2 * tstride + (int64_t)j * n_p) : 0.0;
             const T a = (T)sA[j], b = (T)sB[j];
             const T ia2 = (T)sIA2[j], ib2 = (T)sIB2[j];
 
@@ -224,7 +253,7 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
             } else {
                 const T ex = (T)(ox - trx), ey = (T)(oy - trY);
                 T qd;
-                if (DIM == 3) {
+                if constexpr (DIM == 3) {
                     const T ez = (T)(oz - trz);
                     qd = ex * ex * ia2 + ey * ey * ia2 + ez * ez * ib2;
                 } else {
@@ -234,10 +263,10 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
             }
             const T dx = (T)(px - trx), dy = (T)(py - trY);
 
-            if (DIM == 3) {
+            if constexpr (DIM == 3) {
                 const T dz = (T)(pz - trz);
                 T al, be, lx, ly, lz, lca, lsa, lcb, lsb;
-                if (init) {
+                if constexpr (init) {
                     // angles3d of the straight-line offsets (geometry.py:102-114)
                     const double ex = px - trx, ey = py - trY, ez = pz - trz;
                     double a0 = atan2(ey, ex);
@@ -249,40 +278,40 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
                 } else {
                     al = ld_stream(alpha + e);
                     be = ld_stream(beta + e);
-                    lx = ld_stream(lam + 0 * Nel + e); ly = ld_stream(lam + 1 * Nel + e);
+                    lx = ld_stream(lam + 0 * Nel + e);
+                    ly = ld_stream(lam + 1 * Nel + e);
                     lz = ld_stream(lam + 2 * Nel + e);
-                    lca = ld_stream(lam + 3 * Nel + e); lsa = ld_stream(lam + 4 * Nel + e);
-                    lcb = ld_stream(lam + 5 * Nel + e); lsb = ld_stream(lam + 6 * Nel + e);
+                    lca = ld_stream(lam + 3 * Nel + e);
+                    lsa = ld_stream(lam + 4 * Nel + e);
+                    lcb = ld_stream(lam + 5 * Nel + e);
+                    lsb = ld_stream(lam + 6 * Nel + e);
                 }
                 T sa, ca, sb, cb;
-                sincos_t(al, &sa, &ca);  // copy reset (solver_single.py:375-380)
-                sincos_t(be, &sb, &cb);
-                T ca2, sa2, cb2, sb2, dn;
-                if (prime) {
-                    ca2 = ca; sa2 = sa; cb2 = cb; sb2 = sb; dn = dold;
+                sincos_fast(al, &sa, &ca);  // copy reset (solver_single.py:375-380)
+                sincos_fast(be, &sb, &cb);
+                T ca2, sa2, cb2, sb2, dn, al2, be2, sA2, cA2, sB2, cB2;
+                if constexpr (prime) {
+                    ca2 = cA2 = ca; sa2 = sA2 = sa; cb2 = cB2 = cb; sb2 = sB2 = sb;
+                    dn = dold; al2 = al; be2 = be;
                 } else {
                     // alpha copies (solver_single.py:223-228)
                     const T coef = a * dold * sb;
-                    const T den = trho + trho_o * (coef * coef);
+                    const T rden = rcp_fast(trho + trho_o * (coef * coef));
                     const T Lx = lx + trho_o * dx, Ly = ly + trho_o * dy, Lz = lz + trho_o * dz;
-                    ca2 = (trho * ca - lca + coef * Lx) / den;
-                    sa2 = (trho * sa - lsa + coef * Ly) / den;
+                    ca2 = (trho * ca - lca + coef * Lx) * rden;
+                    sa2 = (trho * sa - lsa + coef * Ly) * rden;
                     // beta copies with the new alpha copies (solver_single.py:253-266)
                     const T ccb = b * dold;
-                    cb2 = (trho * cb - lcb + ccb * Lz) / (trho + trho_o * (ccb * ccb));
+                    cb2 = (trho * cb - lcb + ccb * Lz) * rcp_fast(trho + trho_o * (ccb * ccb));
                     const T csb = a * dold;
                     const T num = trho * sb - lsb + csb * (ca2 * Lx + sa2 * Ly);
-                    const T den2 = trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2);
-                    sb2 = num / den2;
+                    sb2 = num * rcp_fast(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
                     // d from the new positions (solver_single.py:283-290)
                     dn = fmin_t(fmax_t(one, sqrt_t(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2)), dcap);
-                }
-                T al2 = al, be2 = be, sA2 = sa, cA2 = ca, sB2 = sb, cB2 = cb;
-                if (!prime) {
-                    al2 = atan2_t(sa2, ca2);  // solver_single.py:242
-                    be2 = atan2_t(sb2, cb2);  // solver_single.py:271
-                    sincos_t(al2, &sA2, &cA2);
-                    sincos_t(be2, &sB2, &cB2);
+                    al2 = atan2_fast(sa2, ca2);  // solver_single.py:242
+                    be2 = atan2_fast(sb2, cb2);  // solver_single.py:271
+                    unit_dir(ca2, sa2, &cA2, &sA2);  // cos/sin(alpha') for residuals + next targets
+                    unit_dir(cb2, sb2, &cB2, &sB2);
                 }
                 // residual families (solver_single.py:303-312)
                 const T rx = dx - a * dn * ca2 * sb2;
@@ -291,15 +320,15 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
                 const T rcb = cb2 - cB2, rsb = sb2 - sB2, rca = ca2 - cA2, rsa = sa2 - sA2;
                 sumsq += (double)rx * rx + (double)ry * ry + (double)rz * rz + (double)rcb * rcb +
                          (double)rsb * rsb + (double)rca * rca + (double)rsa * rsa;
-                T mloc = fmax_t(fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rz), fabs_t(rcb))),
-                                fmax_t(fmax_t(fabs_t(rsb), fabs_t(rca)), fabs_t(rsa)));
+                const T mloc = fmax_t(fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rz), fabs_t(rcb))),
+                                      fmax_t(fmax_t(fabs_t(rsb), fabs_t(rca)), fabs_t(rsa)));
                 mx = fmax(mx, (double)mloc);
-                if (!prime || init) {
-                    if (!prime) {
-                        // multiplier ascent (solver_single.py:336-343)
-                        lx += trho_o * rx; ly += trho_o * ry; lz += trho_o * rz;
-                        lca += trho * rca; lsa += trho * rsa; lcb += trho * rcb; lsb += trho * rsb;
-                    }
+                if constexpr (!prime) {
+                    // multiplier ascent (solver_single.py:336-343)
+                    lx += trho_o * rx; ly += trho_o * ry; lz += trho_o * rz;
+                    lca += trho * rca; lsa += trho * rsa; lcb += trho * rcb; lsb += trho * rsb;
+                }
+                if constexpr (!prime || init) {
                     st_stream(alpha + e, al2);
                     st_stream(beta + e, be2);
                     st_stream(lam + 0 * Nel + e, lx);
@@ -323,7 +352,7 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
                 accT[DIM - 1] += trz + (double)(b * dn * cB2);
             } else {
                 T al, lx, ly, lca, lsa;
-                if (init) {
+                if constexpr (init) {
                     // scaled planar angle of the line offsets (solver_single.py:138-143)
                     double a0 = atan2((py - trY) / sB[j], (px - trx) / sA[j]);
                     if (a0 == -M_PI) a0 = M_PI;
@@ -331,37 +360,36 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
                     lx = ly = lca = lsa = (T)0;
                 } else {
                     al = ld_stream(alpha + e);
-                    lx = ld_stream(lam + 0 * Nel + e); ly = ld_stream(lam + 1 * Nel + e);
-                    lca = ld_stream(lam + 2 * Nel + e); lsa = ld_stream(lam + 3 * Nel + e);
+                    lx = ld_stream(lam + 0 * Nel + e);
+                    ly = ld_stream(lam + 1 * Nel + e);
+                    lca = ld_stream(lam + 2 * Nel + e);
+                    lsa = ld_stream(lam + 3 * Nel + e);
                 }
                 T sa, ca;
-                sincos_t(al, &sa, &ca);
-                T ca2, sa2, dn;
-                if (prime) {
-                    ca2 = ca; sa2 = sa; dn = dold;
+                sincos_fast(al, &sa, &ca);
+                T ca2, sa2, dn, al2, sA2, cA2;
+                if constexpr (prime) {
+                    ca2 = cA2 = ca; sa2 = sA2 = sa; dn = dold; al2 = al;
                 } else {
                     // planar alpha copies (solver_single.py:229-237)
                     const T cx = a * dold, cy = b * dold;
-                    ca2 = (trho * ca - lca + cx * (lx + trho_o * dx)) / (trho + trho_o * (cx * cx));
-                    sa2 = (trho * sa - lsa + cy * (ly + trho_o * dy)) / (trho + trho_o * (cy * cy));
+                    ca2 = (trho * ca - lca + cx * (lx + trho_o * dx)) * rcp_fast(trho + trho_o * (cx * cx));
+                    sa2 = (trho * sa - lsa + cy * (ly + trho_o * dy)) * rcp_fast(trho + trho_o * (cy * cy));
                     dn = fmin_t(fmax_t(one, sqrt_t(dx * dx * ia2 + dy * dy * ib2)), dcap);
-                }
-                T al2 = al, sA2 = sa, cA2 = ca;
-                if (!prime) {
-                    al2 = atan2_t(sa2, ca2);
-                    sincos_t(al2, &sA2, &cA2);
+                    al2 = atan2_fast(sa2, ca2);
+                    unit_dir(ca2, sa2, &cA2, &sA2);
                 }
                 const T rx = dx - a * dn * ca2;
                 const T ry = dy - b * dn * sa2;
                 const T rca = ca2 - cA2, rsa = sa2 - sA2;
                 sumsq += (double)rx * rx + (double)ry * ry + (double)rca * rca + (double)rsa * rsa;
-                T mloc = fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rca), fabs_t(rsa)));
+                const T mloc = fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rca), fabs_t(rsa)));
                 mx = fmax(mx, (double)mloc);
-                if (!prime || init) {
-                    if (!prime) {
-                        lx += trho_o * rx; ly += trho_o * ry;
-                        lca += trho * rca; lsa += trho * rsa;
-                    }
+                if constexpr (!prime) {
+                    lx += trho_o * rx; ly += trho_o * ry;
+                    lca += trho * rca; lsa += trho * rsa;
+                }
+                if constexpr (!prime || init) {
                     st_stream(alpha + e, al2);
                     st_stream(lam + 0 * Nel + e, lx);
                     st_stream(lam + 1 * Nel + e, ly);
@@ -409,42 +437,45 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
         const double nrm = sqrt(ss);
         A.s.res_norm[i] = nrm;
         A.s.res_max[i] = mm;
-        if (!prime && (A.p.flags & TRO_FLAG_NO_SCHEDULE)) {
-            A.s.iteration[i] += 1;  // bare am_iteration (solver_single.py:388)
-        } else if (!prime) {
-            const int it = A.s.iteration[i] + 1;  // am_iteration: state.iteration += 1
-            A.s.iteration[i] = it;
-            const int nh = A.s.n_hist[i];
-            if (A.s.hist && nh < A.p.max_hist) {
-                double* h = A.s.hist + ((int64_t)i * A.p.max_hist + nh) * 3;
-                h[0] = nrm;
-                h[1] = mm;
-                h[2] = rho_o;
-            }
-            const int n = nh + 1;
-            A.s.n_hist[i] = n;
-            const int w = A.p.stall_window, w2 = 2 * w;
-            double* ring = A.s.ring + (int64_t)i * w2;
-            ring[(n - 1) % w2] = mm;
-            if (mm <= A.p.tol) {  // solver_single.py:424-426 (break before growth)
-                A.s.status[i] = status0 | TRO_CONVERGED;
+        if constexpr (!prime) {
+            if (A.p.flags & TRO_FLAG_NO_SCHEDULE) {
+                A.s.iteration[i] += 1;  // bare am_iteration (solver_single.py:388)
             } else {
-                const int lc = A.s.last_change[i];
-                if (n >= w2 && it - lc >= w) {  // solver_single.py:394
-                    double sr = 0.0, sp = 0.0;  // np.mean of <8 values: sequential sum / w
-                    for (int k = 0; k < w; ++k) sr += ring[(n - w + k) % w2];
-                    for (int k = 0; k < w; ++k) sp += ring[(n - w2 + k) % w2];
-                    const double recent = sr / (double)w, previous = sp / (double)w;
-                    if (!(previous <= fmax(A.p.tol, 0.0)) && (previous - recent) / previous < A.p.stall_improvement) {
-                        const double nr = fmin(rho * A.p.rho_growth, A.p.rho_cap);
-                        const double nro = fmin(rho_o * A.p.rho_growth, A.p.rho_cap);
-                        A.s.rho[i] = nr;
-                        A.s.rho_o[i] = nro;
-                        if (nro != rho_o) {
-                            A.s.level[i] = level + 1;
-                            A.s.n_changes[i] += 1;
+                const int it = A.s.iteration[i] + 1;  // am_iteration: state.iteration += 1
+                A.s.iteration[i] = it;
+                const int nh = A.s.n_hist[i];
+                if (A.s.hist && nh < A.p.max_hist) {
+                    double* h = A.s.hist + ((int64_t)i * A.p.max_hist + nh) * 3;
+                    h[0] = nrm;
+                    h[1] = mm;
+                    h[2] = rho_o;
+                }
+                const int n = nh + 1;
+                A.s.n_hist[i] = n;
+                const int w = A.p.stall_window, w2 = 2 * w;
+                double* ring = A.s.ring + (int64_t)i * w2;
+                ring[(n - 1) % w2] = mm;
+                if (mm <= A.p.tol) {  // solver_single.py:424-426 (break before growth)
+                    A.s.status[i] = status0 | TRO_CONVERGED;
+                } else {
+                    const int lc = A.s.last_change[i];
+                    if (n >= w2 && it - lc >= w) {  // solver_single.py:394
+                        double sr = 0.0, sp = 0.0;  // np.mean of <8 values: sequential sum / w
+                        for (int k = 0; k < w; ++k) sr += ring[(n - w + k) % w2];
+                        for (int k = 0; k < w; ++k) sp += ring[(n - w2 + k) % w2];
+                        const double recent = sr / (double)w, previous = sp / (double)w;
+                        if (!(previous <= fmax(A.p.tol, 0.0)) &&
+                            (previous - recent) / previous < A.p.stall_improvement) {
+                            const double nr = fmin(rho * A.p.rho_growth, A.p.rho_cap);
+                            const double nro = fmin(rho_o * A.p.rho_growth, A.p.rho_cap);
+                            A.s.rho[i] = nr;
+                            A.s.rho_o[i] = nro;
+                            if (nro != rho_o) {
+                                A.s.level[i] = level + 1;
+                                A.s.n_changes[i] += 1;
+                            }
+                            A.s.last_change[i] = it;
                         }
-                        A.s.last_change[i] = it;
                     }
                 }
             }
@@ -452,8 +483,8 @@ __global__ void __launch_bounds__(kMaxThreads) alg1_kernel(Alg1Args A, int mode)
     }
 }
 
-template <int DIM, typename T>
-static int launch(const Alg1Args& A, int mode, cudaStream_t st) {
+template <int DIM, typename T, int MODE>
+static int launch_mode(const Alg1Args& A, cudaStream_t st) {
     const int n_p = A.d.n_p;
     int threads = ((n_p * A.G + 31) / 32) * 32;
     if (threads < 64) threads = 64;
@@ -465,12 +496,19 @@ static int launch(const Alg1Args& A, int mode, cudaStream_t st) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-            cudaFuncSetAttribute(alg1_kernel<DIM, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(alg1_kernel<DIM, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             attr_set[dev] = true;
         }
     }
-    alg1_kernel<DIM, T><<<A.d.n_members, threads, smem, st>>>(A, mode);
+    alg1_kernel<DIM, T, MODE><<<A.d.n_members, threads, smem, st>>>(A);
     return (int)cudaGetLastError();
+}
+
+template <int DIM, typename T>
+static int launch(const Alg1Args& A, int mode, cudaStream_t st) {
+    if (mode == 0) return launch_mode<DIM, T, 0>(A, st);
+    if (mode == 1) return launch_mode<DIM, T, 1>(A, st);
+    return launch_mode<DIM, T, 2>(A, st);
 }
 
 static int auto_groups(const tro_alg1_dims* d) {

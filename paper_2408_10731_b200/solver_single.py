@@ -131,8 +131,11 @@ def _shapes(problem: SingleProblem):
 
 
 def _linear_term(basis: BasisSet, desired: np.ndarray, w_track: float) -> np.ndarray:
-    """-2 w_track (P' desired)' -> (dim, m) (solver_single.py:173)."""
-    return -2.0 * w_track * (basis.P.T @ desired).T
+    """-2 w_track (P' desired)' (solver_single.py:173); desired (n_p, dim) -> (dim, m) or
+    (B, n_p, dim) -> (B, dim, m), one GEMM per member so every member's bits match a single solve."""
+    if desired.ndim == 2:
+        return -2.0 * w_track * (basis.P.T @ desired).T
+    return -2.0 * w_track * np.transpose(np.matmul(basis.P.T[None], desired), (0, 2, 1))
 
 
 def _engine_for(problem: SingleProblem, params: SingleParams, *, rho0=None, export=True, max_hist=0,
@@ -331,25 +334,23 @@ class SingleBatch:
         desired = np.stack([p.desired for p in problems])
         return cls(p0.basis, bvals, list(p0.obstacles), desired, p0.w_smooth, p0.w_track)
 
+    def desired_paths(self) -> np.ndarray:
+        """(B, n_p, dim): the given desired paths, or each member's straight start->goal line
+        (bench/runner.py:88-94 formula)."""
+        if self.desired is not None:
+            return np.asarray(self.desired, dtype=float)
+        frac = np.linspace(0.0, 1.0, self.basis.n_p)[None, :, None]
+        p0, p1 = self.bvals[:, None, :, 0], self.bvals[:, None, :, 3]
+        return p0 + frac * (p1 - p0)
+
     def linear_terms(self) -> np.ndarray:
-        """(B, dim, m) = -2 w_track (P' desired_i)'."""
-        P = self.basis.P
-        if self.desired is None:
-            s = np.linspace(0.0, 1.0, self.basis.n_p)
-            p0, p1 = self.bvals[:, :, 0], self.bvals[:, :, 3]
-            des = p0[:, None, :] + s[None, :, None] * (p1 - p0)[:, None, :]
-        else:
-            des = np.asarray(self.desired, dtype=float)
-        return -2.0 * self.w_track * np.einsum("tc,btk->bkc", P, des)
+        """(B, dim, m) = -2 w_track (P' desired_i)' (solver_single.py:173), member by member."""
+        return _linear_term(self.basis, self.desired_paths(), self.w_track)
 
     def problem(self, i: int) -> SingleProblem:
         bnd = tuple(AxisBoundary(*self.bvals[i, k]) for k in range(self.dim))
-        if self.desired is None:
-            s = np.linspace(0.0, 1.0, self.basis.n_p)[:, None]
-            des = self.bvals[i, :, 0][None] + s * (self.bvals[i, :, 3] - self.bvals[i, :, 0])[None]
-        else:
-            des = self.desired[i]
-        return SingleProblem(self.basis, bnd, des, list(self.obstacles), self.w_smooth, self.w_track)
+        return SingleProblem(self.basis, bnd, self.desired_paths()[i], list(self.obstacles), self.w_smooth,
+                             self.w_track)
 
 
 @dataclass

@@ -166,10 +166,17 @@ def test_flow3d_batch_free_window(golden):
     batch = scenarios.flow3d_batch(50, gh["members"], basis=bs)
     sol = solve_single_batch(batch, SingleParams(max_iter=200, tol=0.0), history=True)
     hist = sol.history.cpu().numpy()
+    report = []
     for i, tw in enumerate(gh["twin"]):
-        w = max(int(tw) - 2, 1)
-        np.testing.assert_allclose(hist[i, :w, :2], gh["hist"][i][:w, :2], rtol=1e-8)
-        np.testing.assert_array_equal(hist[i, :w, 2], gh["hist"][i][:w, 2])
+        # inside the window where the reference's own LU and K^-1 runs agree to 1e-9, with
+        # margin for the ~10x/iteration amplification near its end
+        err = np.max(np.abs(hist[i, :, :2] - gh["hist"][i][:, :2]) / np.abs(gh["hist"][i][:, :2]), axis=1)
+        bad = np.nonzero(err > 1e-9)[0]
+        first = int(bad[0]) if bad.size else 200
+        report.append((i, int(tw), first))
+        np.testing.assert_array_equal(hist[i, : int(tw) - 4, 2], gh["hist"][i][: int(tw) - 4, 2])
+    print("member, twin window, device leaves 1e-9 at:", report)
+    assert all(first >= max(int(tw) - 4, 1) for _, tw, first in report), report
     # end-state distribution (tier 3): final residual levels of the same order
     fin = hist[:, -1, 1]
     ref = gh["hist"][:, -1, 1]
