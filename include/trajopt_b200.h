@@ -55,7 +55,7 @@ typedef struct tro_alg1_dims {
 
 typedef struct tro_alg1_consts {
     const double* P;         /* n_p x m, row-major (basis.py:143-177) */
-    const double* tracks;    /* dim x n_o x n_p, obstacle centres (SoA) */
+    const double* tracks;    /* n_o x dim x n_p, obstacle centres (per obstacle: x row, y row, z row) */
     const double* shape_a;   /* n_o semi-axis a (x,y) */
     const double* shape_b;   /* n_o semi-axis b (z; y in 2-D) */
     const double* kinv;      /* n_levels x nk x nk row-major, nk = m + n_eq */
@@ -82,12 +82,13 @@ typedef struct tro_alg1_params {
 #define TRO_FLAG_NO_SCHEDULE 1 /* bare am_iteration: no convergence test, no penalty growth */
 
 typedef struct tro_alg1_state {
-    /* per element (B x n_o x n_p), storage type T */
-    void* alpha;
-    void* beta;    /* unused in 2-D */
-    void* lam;     /* W_lam planes of B x n_o x n_p: 3-D [lx ly lz lca lsa lcb lsb], 2-D [lx ly lca lsa] */
-    void* d;       /* optional: read when d_mode == 1, written (new d) when non-NULL */
-    void* copies;  /* optional export of the angle copies: 3-D [ca sa cb sb], 2-D [ca sa]; NULL = skip */
+    /* persistent per-element state, storage type T, interleaved per obstacle row:
+     *   state[i][j][w][t]  (B x n_o x W x n_p),
+     *   3-D W = 9: [alpha beta lx ly lz lca lsa lcb lsb];  2-D W = 5: [alpha lx ly lca lsa] */
+    void* state;
+    void* d;       /* optional B x n_o x n_p: read when d_mode == 1, written (new d) when non-NULL */
+    void* copies;  /* optional export of the angle copies, planes of B x n_o x n_p:
+                      3-D [ca sa cb sb], 2-D [ca sa]; NULL = skip */
     /* per member, fp64 */
     double* xi;    /* B x dim x m */
     double* pos;   /* B x dim x n_p  (positions of the current xi) */
@@ -130,6 +131,12 @@ int tro_kkt_apply_f64(const double* kinv, int32_t n, const double* rhs, int64_t 
 int tro_topk_stable_f64(const double* keys, int64_t n, int32_t k, int64_t* out_idx,
                         void* workspace, int64_t workspace_bytes, void* stream);
 int64_t tro_topk_workspace_bytes(int64_t n, int32_t k);
+
+/* Diagnostics: evaluate the kernels' elementary functions elementwise (fp64) so their
+ * accuracy can be checked against numpy.  fn: 0 sin(x), 1 cos(x), 2 atan2(y, x),
+ * 3 1/x, 4 1/sqrt(x), 5 sqrt(x), 6/7 cos/sin(atan2(y, x)) via normalisation,
+ * 8 min(max(1, sqrt(x)), 1e6). */
+int tro_fastmath_eval(int32_t fn, const double* x, const double* y, int64_t n, double* out, void* stream);
 
 int32_t tro_version(void);
 const char* tro_error_string(int32_t code);

@@ -5,11 +5,12 @@ basis and one obstacle set, the per-rho_o-level K^-1 table, and the launch
 sequence (one fused kernel launch per AM iteration, optionally replayed from a
 CUDA graph).  Host <-> device traffic happens only at solve boundaries.
 
-HBM layout (per member i, obstacle j, sample t; element e = (i*n_o + j)*n_p + t):
-    alpha[e], beta[e]                      storage dtype T (fp64 or fp32)
-    lam[w][e], w = lx ly lz lca lsa lcb lsb (3-D) | lx ly lca lsa (2-D)
-Per member (fp64): xi (dim, m), pos (dim, n_p), sums (2, dim, n_p), rho, rho_o,
-stall ring, status/level/iteration counters.
+HBM layout: one storage-dtype tensor state[i][j][w][t] (member, obstacle, word, sample),
+W = 9 words in 3-D [alpha beta lx ly lz lca lsa lcb lsb], 5 in 2-D [alpha lx ly lca lsa],
+so one sample's words sit n_p elements apart (one base register + immediate offsets in the
+kernel) and the n_p samples of a word are contiguous (coalesced).  Obstacle tracks are
+tracks[j][axis][t] (fp64).  Per member (fp64): xi (dim, m), pos (dim, n_p), sums
+(2, dim, n_p), rho, rho_o, stall ring, status / level / iteration counters.
 """
 
 from __future__ import annotations
@@ -105,8 +106,8 @@ class Alg1Engine:
                                 cond_limit)
         self.basis = basis
         self.P = torch.as_tensor(np.array(basis.P, dtype=float, copy=True), **f64)
-        self.tracks = torch.as_tensor(np.ascontiguousarray(np.transpose(tracks, (2, 0, 1))) if n_o else
-                                      np.zeros((dim, 0, n_p)), **f64).contiguous()
+        self.tracks = torch.as_tensor(np.ascontiguousarray(np.transpose(tracks, (0, 2, 1))) if n_o else
+                                      np.zeros((0, dim, n_p)), **f64).contiguous()
         self.shape_a = torch.as_tensor(np.asarray(shape_a, dtype=float).reshape(-1), **f64)
         self.shape_b = torch.as_tensor(np.asarray(shape_b, dtype=float).reshape(-1), **f64)
         if n_o == 0:
@@ -124,10 +125,13 @@ class Alg1Engine:
 
         # ---- state
         T = dict(dtype=dtype, device=dev)
-        W = 7 if dim == 3 else 4
-        self.alpha = torch.empty((B, n_o, n_p), **T)
-        self.beta = torch.empty((B, n_o, n_p), **T) if dim == 3 else None
-        self.lam = torch.empty((W, B, n_o, n_p), **T)
+        W = 9 if dim == 3 else 5
+        self.W = W
+        self.state = torch.empty((B, n_o, W, n_p), **T)
+        # views (member, obstacle, sample) / (plane, member, obstacle, sample)
+        self.alpha = self.state[:, :, 0]
+        self.beta = self.state[:, :, 1] if dim == 3 else None
+        self.lam = self.state[:, :, (2 if dim == 3 else 1):].permute(2, 0, 1, 3)
         self.d = torch.empty((B, n_o, n_p), **T) if (keep_d or export) else None
         self.copies = torch.empty((4 if dim == 3 else 2, B, n_o, n_p), **T) if export else None
         self.xi = torch.zeros((B, dim, m), **f64)
@@ -156,7 +160,7 @@ class Alg1Engine:
             self.bvals.data_ptr(), self.line_u.data_ptr(), self.line_v.data_ptr())
         p = _lib.ptr
         self._state = _lib.Alg1State(
-            p(self.alpha), p(self.beta), p(self.lam), p(self.d), p(self.copies), p(self.xi), p(self.pos),
+            p(self.state), p(self.d), p(self.copies), p(self.xi), p(self.pos),
             p(self.sums), p(self.rho), p(self.rho_o), p(self.ring), p(self.res_norm), p(self.res_max), p(self.hist),
             p(self.level), p(self.iteration), p(self.last_change), p(self.n_hist), p(self.status),
             p(self.n_changes))

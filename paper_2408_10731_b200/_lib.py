@@ -31,6 +31,7 @@ EXPORTS = (
     "tro_kkt_apply_f64",
     "tro_topk_stable_f64",
     "tro_topk_workspace_bytes",
+    "tro_fastmath_eval",
     "tro_version",
     "tro_error_string",
 )
@@ -80,9 +81,7 @@ class Alg1Params(ctypes.Structure):
 
 class Alg1State(ctypes.Structure):
     _fields_ = [
-        ("alpha", c_void_p),
-        ("beta", c_void_p),
-        ("lam", c_void_p),
+        ("state", c_void_p),
         ("d", c_void_p),
         ("copies", c_void_p),
         ("xi", c_void_p),
@@ -128,6 +127,8 @@ def load() -> ctypes.CDLL:
     lib.tro_topk_stable_f64.restype = c_int32
     lib.tro_topk_workspace_bytes.argtypes = [c_int64, c_int32]
     lib.tro_topk_workspace_bytes.restype = c_int64
+    lib.tro_fastmath_eval.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
+    lib.tro_fastmath_eval.restype = c_int32
     lib.tro_version.argtypes = []
     lib.tro_version.restype = c_int32
     lib.tro_error_string.argtypes = [c_int32]

@@ -72,30 +72,65 @@ __host__ __device__ inline SmemLayout smem_layout(int n_p, int m, int dim, int n
 }
 
 // cos/sin of atan2(s, c) without trigonometry: (c, s) / hypot(c, s)
-template <typename T>
-__device__ __forceinline__ void unit_dir(T c, T s, T* cu, T* su) {
-    const T h2 = c * c + s * s;
-    if (h2 > (T)0 && h2 < (T)1e300) {
-        const T r = rsqrt_fast(h2);
+__device__ __forceinline__ void unit_dir(double c, double s, double* cu, double* su) {
+    const double h2 = fma(c, c, s * s);
+    if (h2 > 0.0) {
+        const double r = rsqrt_fast(h2);
         *cu = c * r;
         *su = s * r;
     } else {  // atan2(+-0, +-0) = 0 or pi
-        *cu = signbit(c) ? (T)-1 : (T)1;
-        *su = copysign((T)0, s);
+        *cu = flip_sign(1.0, sign_bit(c));
+        *su = flip_sign(0.0, sign_bit(s));
+    }
+}
+__device__ __forceinline__ void unit_dir(float c, float s, float* cu, float* su) {
+    const float h2 = fmaf(c, c, s * s);
+    if (h2 > 0.0f) {
+        const float r = rsqrtf(h2);
+        *cu = c * r;
+        *su = s * r;
+    } else {
+        *cu = signbit(c) ? -1.0f : 1.0f;
+        *su = copysignf(0.0f, s);
     }
 }
 
-template <int DIM, typename T, int MODE>
+// d = min(max(1, sqrt(q)), 1e6) (solver_single.py:283-290) without fmin/fmax:
+// q <= 1 <=> sqrt(q) <= 1 and q >= 1e12 <=> sqrt(q) >= 1e6 (sqrt is monotone, exact at both)
+template <typename T>
+__device__ __forceinline__ T los_scale(T q) {
+    const T s = sqrt_fast(q > (T)1 ? q : (T)1);
+    return q > (T)1e12 ? (T)1e6 : s;
+}
+
+template <typename T>
+__device__ __forceinline__ T max_abs(T acc, T v) {
+    v = fabs(v);
+    return v > acc ? v : acc;
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_state(const T* p) { return ld_stream(p); }
+
+// Per-element state layout (interleaved per obstacle row):
+//   state[i][j][w][t], w = 0..W-1:  3-D [alpha beta lx ly lz lca lsa lcb lsb], 2-D [alpha lx ly lca lsa]
+//   tracks[j][ax][t]
+// For fixed (i, j) the W words of one sample are NP*sizeof(T) apart, so with a
+// compile-time NP every load/store of the element uses one base register plus an
+// immediate offset.
+template <int DIM, typename T, int MODE, int NP>
 __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1Args A) {
     // MODE 0: AM iteration; 1: prime (sums + residual of the current state); 2: cold init + prime
     constexpr bool prime = MODE != 0;
     constexpr bool init = MODE == 2;
+    constexpr int W = DIM == 3 ? 9 : 5;
     extern __shared__ double smem[];
     const int i = blockIdx.x;
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5, nwarps = (nthr + 31) >> 5;
-    const int n_o = A.d.n_obs, n_p = A.d.n_p, m = A.d.m, ne = A.d.n_eq;
+    const int n_o = A.d.n_obs, m = A.d.m, ne = A.d.n_eq;
+    const int n_p = NP ? NP : A.d.n_p;
     const int nk = m + ne;
     const int G = A.G;
     const SmemLayout L = smem_layout(n_p, m, DIM, n_o, G);
@@ -128,9 +163,8 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     // ---------------- stage constants + previous positions + incoming sums
     for (int k = tid; k < n_p * m; k += nthr) sP[k] = ld_const(A.c.P + k);
     const double* posg = A.s.pos + (int64_t)i * DIM * n_p;
-    if (!prime)
-        for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
     if (!prime) {
+        for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
         const double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
         for (int k = tid; k < 2 * DIM * n_p; k += nthr) sSumIn[k] = sg[k];
     }
@@ -144,7 +178,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     __syncthreads();
 
     if constexpr (prime) {
-        // positions of the current xi; d recompute (mode 2) uses these too
+        // positions of the current xi; d recompute (d_mode 2) uses these too
         double* xg = A.s.xi + (int64_t)i * DIM * m;
         if constexpr (init) {
             // straight-line coefficients (solver_single.py:127, basis.py:207-217)
@@ -219,10 +253,9 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     for (int ax = 0; ax < DIM; ++ax) accL[ax] = accT[ax] = 0.0;
 
     if (act) {
-        const int64_t Nel = (int64_t)A.d.n_members * n_o * n_p;
-        T* __restrict__ alpha = reinterpret_cast<T*>(A.s.alpha);
-        T* __restrict__ beta = reinterpret_cast<T*>(A.s.beta);
-        T* __restrict__ lam = reinterpret_cast<T*>(A.s.lam);
+        const int64_t Nel = (int64_t)A.d.n_members * n_o * n_p;  // planes of the optional d / copies
+        T* sbase = reinterpret_cast<T*>(A.s.state) + (int64_t)i * n_o * W * n_p + t;
+        const double* tbase = A.c.tracks + t;
         T* dst = reinterpret_cast<T*>(A.s.d);
         T* cop = reinterpret_cast<T*>(A.s.copies);
         const double px = sPosNew[t], py = sPosNew[n_p + t];
@@ -231,23 +264,22 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         const double oz = (DIM == 3) ? sPosPrev[2 * n_p + t] : 0.0;
         const T trho = (T)rho, trho_o = (T)rho_o;
         const int d_mode = init ? 0 : A.p.d_mode;
-        const T one = (T)1.0, dcap = (T)1e6;
-        const double* trk = A.c.tracks + (int64_t)t;
-        const int64_t tstride = (int64_t)n_o * n_p;
 
 #pragma unroll kUnroll
         for (int j = g; j < n_o; j += G) {
-            const int64_t e = ((int64_t)i * n_o + j) * n_p + t;
-            const double trx = ld_const(trk + (int64_t)j * n_p);
-            const double trY = ld_const(trk + tstride + (int64_t)j * n_p);
-            const double trz = (DIM == 3) ? ld_const(trk + 2 * tstride + (int64_t)j * n_p) : 0.0;
+            T* sp = sbase + j * (W * n_p);
+            const double* tp = tbase + j * (DIM * n_p);
+            const int64_t e = ((int64_t)i * n_o + j) * n_p + t;  // index into d / copies planes
+            const double trx = ld_const(tp);
+            const double trY = ld_const(tp + n_p);
+            const double trz = (DIM == 3) ? ld_const(tp + 2 * n_p) : 0.0;
             const T a = (T)sA[j], b = (T)sB[j];
             const T ia2 = (T)sIA2[j], ib2 = (T)sIB2[j];
 
             // line-of-sight scale of the previous iterate (solver_single.py:274-291)
             T dold;
             if (d_mode == 0) {
-                dold = one;
+                dold = (T)1;
             } else if (d_mode == 1) {
                 dold = dst[e];
             } else {
@@ -259,7 +291,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                 } else {
                     qd = ex * ex * ia2 + ey * ey * ib2;
                 }
-                dold = fmin_t(fmax_t(one, sqrt_t(qd)), dcap);
+                dold = los_scale(qd);
             }
             const T dx = (T)(px - trx), dy = (T)(py - trY);
 
@@ -276,15 +308,15 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                     be = (T)atan2(hypot(ex / ad, ey / ad), ez / bd);
                     lx = ly = lz = lca = lsa = lcb = lsb = (T)0;
                 } else {
-                    al = ld_stream(alpha + e);
-                    be = ld_stream(beta + e);
-                    lx = ld_stream(lam + 0 * Nel + e);
-                    ly = ld_stream(lam + 1 * Nel + e);
-                    lz = ld_stream(lam + 2 * Nel + e);
-                    lca = ld_stream(lam + 3 * Nel + e);
-                    lsa = ld_stream(lam + 4 * Nel + e);
-                    lcb = ld_stream(lam + 5 * Nel + e);
-                    lsb = ld_stream(lam + 6 * Nel + e);
+                    al = ld_state(sp + 0 * n_p);
+                    be = ld_state(sp + 1 * n_p);
+                    lx = ld_state(sp + 2 * n_p);
+                    ly = ld_state(sp + 3 * n_p);
+                    lz = ld_state(sp + 4 * n_p);
+                    lca = ld_state(sp + 5 * n_p);
+                    lsa = ld_state(sp + 6 * n_p);
+                    lcb = ld_state(sp + 7 * n_p);
+                    lsb = ld_state(sp + 8 * n_p);
                 }
                 T sa, ca, sb, cb;
                 sincos_fast(al, &sa, &ca);  // copy reset (solver_single.py:375-380)
@@ -307,37 +339,41 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                     const T num = trho * sb - lsb + csb * (ca2 * Lx + sa2 * Ly);
                     sb2 = num * rcp_fast(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
                     // d from the new positions (solver_single.py:283-290)
-                    dn = fmin_t(fmax_t(one, sqrt_t(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2)), dcap);
+                    dn = los_scale(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2);
                     al2 = atan2_fast(sa2, ca2);  // solver_single.py:242
                     be2 = atan2_fast(sb2, cb2);  // solver_single.py:271
                     unit_dir(ca2, sa2, &cA2, &sA2);  // cos/sin(alpha') for residuals + next targets
                     unit_dir(cb2, sb2, &cB2, &sB2);
                 }
                 // residual families (solver_single.py:303-312)
-                const T rx = dx - a * dn * ca2 * sb2;
-                const T ry = dy - a * dn * sa2 * sb2;
+                const T adn = a * dn;
+                const T rx = dx - adn * ca2 * sb2;
+                const T ry = dy - adn * sa2 * sb2;
                 const T rz = dz - b * dn * cb2;
                 const T rcb = cb2 - cB2, rsb = sb2 - sB2, rca = ca2 - cA2, rsa = sa2 - sA2;
-                sumsq += (double)rx * rx + (double)ry * ry + (double)rz * rz + (double)rcb * rcb +
-                         (double)rsb * rsb + (double)rca * rca + (double)rsa * rsa;
-                const T mloc = fmax_t(fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rz), fabs_t(rcb))),
-                                      fmax_t(fmax_t(fabs_t(rsb), fabs_t(rca)), fabs_t(rsa)));
-                mx = fmax(mx, (double)mloc);
+                T ss = rx * rx;
+                ss = fma(ry, ry, ss); ss = fma(rz, rz, ss); ss = fma(rcb, rcb, ss);
+                ss = fma(rsb, rsb, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
+                sumsq += (double)ss;
+                T ml = fabs(rx);
+                ml = max_abs(ml, ry); ml = max_abs(ml, rz); ml = max_abs(ml, rcb);
+                ml = max_abs(ml, rsb); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
+                mx = (double)ml > mx ? (double)ml : mx;
                 if constexpr (!prime) {
                     // multiplier ascent (solver_single.py:336-343)
                     lx += trho_o * rx; ly += trho_o * ry; lz += trho_o * rz;
                     lca += trho * rca; lsa += trho * rsa; lcb += trho * rcb; lsb += trho * rsb;
                 }
                 if constexpr (!prime || init) {
-                    st_stream(alpha + e, al2);
-                    st_stream(beta + e, be2);
-                    st_stream(lam + 0 * Nel + e, lx);
-                    st_stream(lam + 1 * Nel + e, ly);
-                    st_stream(lam + 2 * Nel + e, lz);
-                    st_stream(lam + 3 * Nel + e, lca);
-                    st_stream(lam + 4 * Nel + e, lsa);
-                    st_stream(lam + 5 * Nel + e, lcb);
-                    st_stream(lam + 6 * Nel + e, lsb);
+                    st_stream(sp + 0 * n_p, al2);
+                    st_stream(sp + 1 * n_p, be2);
+                    st_stream(sp + 2 * n_p, lx);
+                    st_stream(sp + 3 * n_p, ly);
+                    st_stream(sp + 4 * n_p, lz);
+                    st_stream(sp + 5 * n_p, lca);
+                    st_stream(sp + 6 * n_p, lsa);
+                    st_stream(sp + 7 * n_p, lcb);
+                    st_stream(sp + 8 * n_p, lsb);
                     if (dst) dst[e] = dn;
                     if (cop) {
                         cop[0 * Nel + e] = ca2; cop[1 * Nel + e] = sa2;
@@ -347,8 +383,8 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                 // sums for the next position step: lam and targets with the reset copies
                 // cos/sin of the new angles (solver_single.py:177-189, 204-207)
                 accL[0] += (double)lx; accL[1] += (double)ly; accL[DIM - 1] += (double)lz;
-                accT[0] += trx + (double)(a * dn * cA2 * sB2);
-                accT[1] += trY + (double)(a * dn * sA2 * sB2);
+                accT[0] += trx + (double)(adn * cA2 * sB2);
+                accT[1] += trY + (double)(adn * sA2 * sB2);
                 accT[DIM - 1] += trz + (double)(b * dn * cB2);
             } else {
                 T al, lx, ly, lca, lsa;
@@ -359,11 +395,11 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                     al = (T)a0;
                     lx = ly = lca = lsa = (T)0;
                 } else {
-                    al = ld_stream(alpha + e);
-                    lx = ld_stream(lam + 0 * Nel + e);
-                    ly = ld_stream(lam + 1 * Nel + e);
-                    lca = ld_stream(lam + 2 * Nel + e);
-                    lsa = ld_stream(lam + 3 * Nel + e);
+                    al = ld_state(sp + 0 * n_p);
+                    lx = ld_state(sp + 1 * n_p);
+                    ly = ld_state(sp + 2 * n_p);
+                    lca = ld_state(sp + 3 * n_p);
+                    lsa = ld_state(sp + 4 * n_p);
                 }
                 T sa, ca;
                 sincos_fast(al, &sa, &ca);
@@ -375,26 +411,29 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                     const T cx = a * dold, cy = b * dold;
                     ca2 = (trho * ca - lca + cx * (lx + trho_o * dx)) * rcp_fast(trho + trho_o * (cx * cx));
                     sa2 = (trho * sa - lsa + cy * (ly + trho_o * dy)) * rcp_fast(trho + trho_o * (cy * cy));
-                    dn = fmin_t(fmax_t(one, sqrt_t(dx * dx * ia2 + dy * dy * ib2)), dcap);
+                    dn = los_scale(dx * dx * ia2 + dy * dy * ib2);
                     al2 = atan2_fast(sa2, ca2);
                     unit_dir(ca2, sa2, &cA2, &sA2);
                 }
                 const T rx = dx - a * dn * ca2;
                 const T ry = dy - b * dn * sa2;
                 const T rca = ca2 - cA2, rsa = sa2 - sA2;
-                sumsq += (double)rx * rx + (double)ry * ry + (double)rca * rca + (double)rsa * rsa;
-                const T mloc = fmax_t(fmax_t(fabs_t(rx), fabs_t(ry)), fmax_t(fabs_t(rca), fabs_t(rsa)));
-                mx = fmax(mx, (double)mloc);
+                T ss = rx * rx;
+                ss = fma(ry, ry, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
+                sumsq += (double)ss;
+                T ml = fabs(rx);
+                ml = max_abs(ml, ry); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
+                mx = (double)ml > mx ? (double)ml : mx;
                 if constexpr (!prime) {
                     lx += trho_o * rx; ly += trho_o * ry;
                     lca += trho * rca; lsa += trho * rsa;
                 }
                 if constexpr (!prime || init) {
-                    st_stream(alpha + e, al2);
-                    st_stream(lam + 0 * Nel + e, lx);
-                    st_stream(lam + 1 * Nel + e, ly);
-                    st_stream(lam + 2 * Nel + e, lca);
-                    st_stream(lam + 3 * Nel + e, lsa);
+                    st_stream(sp + 0 * n_p, al2);
+                    st_stream(sp + 1 * n_p, lx);
+                    st_stream(sp + 2 * n_p, ly);
+                    st_stream(sp + 3 * n_p, lca);
+                    st_stream(sp + 4 * n_p, lsa);
                     if (dst) dst[e] = dn;
                     if (cop) { cop[0 * Nel + e] = ca2; cop[1 * Nel + e] = sa2; }
                 }
@@ -404,7 +443,6 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
             }
         }
     }
-
     // ---------------- epilogue: sums over obstacle groups (fixed order)
     if (act) {
 #pragma unroll
@@ -483,7 +521,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     }
 }
 
-template <int DIM, typename T, int MODE>
+template <int DIM, typename T, int MODE, int NP>
 static int launch_mode(const Alg1Args& A, cudaStream_t st) {
     const int n_p = A.d.n_p;
     int threads = ((n_p * A.G + 31) / 32) * 32;
@@ -496,19 +534,25 @@ static int launch_mode(const Alg1Args& A, cudaStream_t st) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-            cudaFuncSetAttribute(alg1_kernel<DIM, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(alg1_kernel<DIM, T, MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             attr_set[dev] = true;
         }
     }
-    alg1_kernel<DIM, T, MODE><<<A.d.n_members, threads, smem, st>>>(A);
+    alg1_kernel<DIM, T, MODE, NP><<<A.d.n_members, threads, smem, st>>>(A);
     return (int)cudaGetLastError();
 }
 
 template <int DIM, typename T>
 static int launch(const Alg1Args& A, int mode, cudaStream_t st) {
-    if (mode == 0) return launch_mode<DIM, T, 0>(A, st);
-    if (mode == 1) return launch_mode<DIM, T, 1>(A, st);
-    return launch_mode<DIM, T, 2>(A, st);
+    // the benchmark horizon (n_p = 100) gets compile-time strides; anything else runs the generic path
+    if (A.d.n_p == 100) {
+        if (mode == 0) return launch_mode<DIM, T, 0, 100>(A, st);
+        if (mode == 1) return launch_mode<DIM, T, 1, 100>(A, st);
+        return launch_mode<DIM, T, 2, 100>(A, st);
+    }
+    if (mode == 0) return launch_mode<DIM, T, 0, 0>(A, st);
+    if (mode == 1) return launch_mode<DIM, T, 1, 0>(A, st);
+    return launch_mode<DIM, T, 2, 0>(A, st);
 }
 
 static int auto_groups(const tro_alg1_dims* d) {
@@ -563,4 +607,37 @@ extern "C" int tro_alg1_init(int32_t dtype, const tro_alg1_dims* dims, const tro
                              const tro_alg1_state* s, const tro_alg1_params* p, void* stream) {
     if (c && (!c->line_u || !c->line_v)) return TRO_EINVAL;
     return tro::run(dtype, dims, c, s, p, stream, 2);
+}
+
+// ---------------------------------------------------------------- diagnostics
+namespace tro {
+__global__ void fastmath_eval_kernel(int fn, const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                                     double* __restrict__ out) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[k];
+        double s, c, r = 0.0;
+        switch (fn) {
+            case 0: sincos_fast(v, &s, &c); r = s; break;
+            case 1: sincos_fast(v, &s, &c); r = c; break;
+            case 2: r = atan2_fast(y[k], v); break;
+            case 3: r = rcp_fast(v); break;
+            case 4: r = rsqrt_fast(v); break;
+            case 5: r = sqrt_fast(v); break;
+            case 6: unit_dir(v, y[k], &c, &s); r = c; break;
+            case 7: unit_dir(v, y[k], &c, &s); r = s; break;
+            case 8: r = los_scale(v); break;
+            default: r = 0.0;
+        }
+        out[k] = r;
+    }
+}
+}  // namespace tro
+
+extern "C" int tro_fastmath_eval(int32_t fn, const double* x, const double* y, int64_t n, double* out, void* stream) {
+    if (!x || !out || n < 0 || fn < 0 || fn > 8 || ((fn == 2 || fn == 6 || fn == 7) && !y)) return TRO_EINVAL;
+    if (n == 0) return 0;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    tro::fastmath_eval_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(fn, x, y, n, out);
+    return (int)cudaGetLastError();
 }
