@@ -80,6 +80,7 @@ typedef struct tro_alg1_params {
 
 /* tro_alg1_params.flags */
 #define TRO_FLAG_NO_SCHEDULE 1 /* bare am_iteration: no convergence test, no penalty growth */
+#define TRO_FLAG_NO_TMA 2      /* force the one-CTA-per-member kernel (testing / tuning) */
 
 typedef struct tro_alg1_state {
     /* persistent per-element state, storage type T, interleaved per obstacle row:

@@ -80,7 +80,8 @@ class Alg1Engine:
 
     def __init__(self, basis: BasisSet, tracks, shape_a, shape_b, bvals, q, *, params, rho0=None,
                  w_smooth: float = 1.0, w_track: float = 1.0, dtype=torch.float64, device=None, groups: int = 0,
-                 max_hist: int = 0, export: bool = False, keep_d: bool = False, cond_limit: float = 1e12):
+                 max_hist: int = 0, export: bool = False, keep_d: bool = False, cond_limit: float = 1e12,
+                 use_tma: bool = True):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -166,6 +167,8 @@ class Alg1Engine:
             p(self.n_changes))
         self._graph = None
         self._graph_n = 0
+        # TMA-pipelined persistent kernel for the iteration unless disabled (flags bit 2)
+        self.base_flags = 0 if use_tma else _lib.TRO_FLAG_NO_TMA
 
     # ------------------------------------------------------------ launches
     def _params(self, d_mode: int, flags: int = 0) -> _lib.Alg1Params:
@@ -175,7 +178,7 @@ class Alg1Engine:
 
     def _call(self, name: str, d_mode: int, flags: int = 0):
         fn = getattr(self.lib, name)
-        prm = self._params(d_mode, flags)
+        prm = self._params(d_mode, flags | self.base_flags)
         with torch.cuda.device(self.device):
             rc = fn(self.code, ctypes.byref(self._dims), ctypes.byref(self._consts), ctypes.byref(self._state),
                     ctypes.byref(prm), ctypes.c_void_p(_lib.stream_handle()))

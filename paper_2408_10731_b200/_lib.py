@@ -21,6 +21,7 @@ TRO_F32 = 1
 TRO_CONVERGED = 1
 TRO_FACTOR_FAILED = 2
 TRO_FLAG_NO_SCHEDULE = 1
+TRO_FLAG_NO_TMA = 2
 TRO_EINVAL = -1
 
 # every symbol include/trajopt_b200.h declares (checked by tests/test_lib_exports.py)

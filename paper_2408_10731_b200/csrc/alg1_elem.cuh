@@ -1,0 +1,147 @@
+// Per-element AM/AL update of Alg. 1 (solver_single.py:214-343), shared by the
+// fused kernels.  Everything here is registers-only arithmetic on one
+// (member, obstacle, sample) element.
+#pragma once
+#include "common.cuh"
+#include "fastmath.cuh"
+
+namespace tro {
+
+// cos/sin of atan2(s, c) without trigonometry: (c, s) / hypot(c, s)
+__device__ __forceinline__ void unit_dir(double c, double s, double* cu, double* su) {
+    const double h2 = fma(c, c, s * s);
+    if (h2 > 0.0) {
+        const double r = rsqrt_fast(h2);
+        *cu = c * r;
+        *su = s * r;
+    } else {  // atan2(+-0, +-0) = 0 or pi
+        *cu = flip_sign(1.0, sign_bit(c));
+        *su = flip_sign(0.0, sign_bit(s));
+    }
+}
+__device__ __forceinline__ void unit_dir(float c, float s, float* cu, float* su) {
+    const float h2 = fmaf(c, c, s * s);
+    if (h2 > 0.0f) {
+        const float r = rsqrtf(h2);
+        *cu = c * r;
+        *su = s * r;
+    } else {
+        *cu = signbit(c) ? -1.0f : 1.0f;
+        *su = copysignf(0.0f, s);
+    }
+}
+
+// d = min(max(1, sqrt(q)), 1e6) (solver_single.py:283-290) without fmin/fmax:
+// q <= 1 <=> sqrt(q) <= 1 and q >= 1e12 <=> sqrt(q) >= 1e6 (sqrt is monotone, exact at both)
+template <typename T>
+__device__ __forceinline__ T los_scale(T q) {
+    const T s = sqrt_fast(q > (T)1 ? q : (T)1);
+    return q > (T)1e12 ? (T)1e6 : s;
+}
+
+template <typename T>
+__device__ __forceinline__ T max_abs(T acc, T v) {
+    v = fabs(v);
+    return v > acc ? v : acc;
+}
+
+template <int DIM>
+struct Words;
+template <>
+struct Words<3> {
+    static constexpr int W = 9;  // alpha beta lx ly lz lca lsa lcb lsb
+};
+template <>
+struct Words<2> {
+    static constexpr int W = 5;  // alpha lx ly lca lsa
+};
+
+// One AM iteration of one element.  v[W]: state words in / out.  d_old: the
+// line-of-sight scale of the previous iterate.  Outputs the new d, the angle
+// copies (for the optional export), and accumulates the residual norm/max and
+// the sums the next position step needs.
+template <int DIM, typename T>
+__device__ __forceinline__ void am_element(T* v, double trx, double trY, double trz, double px, double py, double pz,
+                                           T a, T b, T ia2, T ib2, T dold, T trho, T trho_o, double& sumsq,
+                                           double& mx, double* accL, double* accT, T& dn, T* copies) {
+    const T dx = (T)(px - trx), dy = (T)(py - trY);
+    if constexpr (DIM == 3) {
+        const T dz = (T)(pz - trz);
+        T sa, ca, sb, cb;
+        sincos_fast(v[0], &sa, &ca);  // copy reset (solver_single.py:375-380)
+        sincos_fast(v[1], &sb, &cb);
+        T lx = v[2], ly = v[3], lz = v[4], lca = v[5], lsa = v[6], lcb = v[7], lsb = v[8];
+        // alpha copies (solver_single.py:223-228)
+        const T coef = a * dold * sb;
+        const T rden = rcp_fast(trho + trho_o * (coef * coef));
+        const T Lx = lx + trho_o * dx, Ly = ly + trho_o * dy, Lz = lz + trho_o * dz;
+        const T ca2 = (trho * ca - lca + coef * Lx) * rden;
+        const T sa2 = (trho * sa - lsa + coef * Ly) * rden;
+        // beta copies with the new alpha copies (solver_single.py:253-266)
+        const T ccb = b * dold;
+        const T cb2 = (trho * cb - lcb + ccb * Lz) * rcp_fast(trho + trho_o * (ccb * ccb));
+        const T csb = a * dold;
+        const T num = trho * sb - lsb + csb * (ca2 * Lx + sa2 * Ly);
+        const T sb2 = num * rcp_fast(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
+        // d from the new positions (solver_single.py:283-290)
+        dn = los_scale(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2);
+        v[0] = atan2_fast(sa2, ca2);  // solver_single.py:242
+        v[1] = atan2_fast(sb2, cb2);  // solver_single.py:271
+        T cA2, sA2, cB2, sB2;
+        unit_dir(ca2, sa2, &cA2, &sA2);  // cos/sin(alpha') for residuals + next targets
+        unit_dir(cb2, sb2, &cB2, &sB2);
+        // residual families (solver_single.py:303-312)
+        const T adn = a * dn;
+        const T rx = dx - adn * ca2 * sb2;
+        const T ry = dy - adn * sa2 * sb2;
+        const T rz = dz - b * dn * cb2;
+        const T rcb = cb2 - cB2, rsb = sb2 - sB2, rca = ca2 - cA2, rsa = sa2 - sA2;
+        T ss = rx * rx;
+        ss = fma(ry, ry, ss); ss = fma(rz, rz, ss); ss = fma(rcb, rcb, ss);
+        ss = fma(rsb, rsb, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
+        sumsq += (double)ss;
+        T ml = fabs(rx);
+        ml = max_abs(ml, ry); ml = max_abs(ml, rz); ml = max_abs(ml, rcb);
+        ml = max_abs(ml, rsb); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
+        mx = (double)ml > mx ? (double)ml : mx;
+        // multiplier ascent (solver_single.py:336-343)
+        v[2] = lx + trho_o * rx; v[3] = ly + trho_o * ry; v[4] = lz + trho_o * rz;
+        v[5] = lca + trho * rca; v[6] = lsa + trho * rsa; v[7] = lcb + trho * rcb; v[8] = lsb + trho * rsb;
+        copies[0] = ca2; copies[1] = sa2; copies[2] = cb2; copies[3] = sb2;
+        // sums for the next position step with the reset copies cos/sin of the new angles
+        // (solver_single.py:177-189, 204-207)
+        accL[0] += (double)v[2]; accL[1] += (double)v[3]; accL[2] += (double)v[4];
+        accT[0] += trx + (double)(adn * cA2 * sB2);
+        accT[1] += trY + (double)(adn * sA2 * sB2);
+        accT[2] += trz + (double)(b * dn * cB2);
+    } else {
+        T sa, ca;
+        sincos_fast(v[0], &sa, &ca);
+        T lx = v[1], ly = v[2], lca = v[3], lsa = v[4];
+        // planar alpha copies (solver_single.py:229-237)
+        const T cx = a * dold, cy = b * dold;
+        const T ca2 = (trho * ca - lca + cx * (lx + trho_o * dx)) * rcp_fast(trho + trho_o * (cx * cx));
+        const T sa2 = (trho * sa - lsa + cy * (ly + trho_o * dy)) * rcp_fast(trho + trho_o * (cy * cy));
+        dn = los_scale(dx * dx * ia2 + dy * dy * ib2);
+        v[0] = atan2_fast(sa2, ca2);
+        T cA2, sA2;
+        unit_dir(ca2, sa2, &cA2, &sA2);
+        const T rx = dx - a * dn * ca2;
+        const T ry = dy - b * dn * sa2;
+        const T rca = ca2 - cA2, rsa = sa2 - sA2;
+        T ss = rx * rx;
+        ss = fma(ry, ry, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
+        sumsq += (double)ss;
+        T ml = fabs(rx);
+        ml = max_abs(ml, ry); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
+        mx = (double)ml > mx ? (double)ml : mx;
+        v[1] = lx + trho_o * rx; v[2] = ly + trho_o * ry;
+        v[3] = lca + trho * rca; v[4] = lsa + trho * rsa;
+        copies[0] = ca2; copies[1] = sa2;
+        accL[0] += (double)v[1]; accL[1] += (double)v[2];
+        accT[0] += trx + (double)(a * dn * cA2);
+        accT[1] += trY + (double)(b * dn * sA2);
+    }
+}
+
+}  // namespace tro
