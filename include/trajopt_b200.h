@@ -50,8 +50,15 @@ typedef struct tro_alg1_dims {
     int32_t dim;       /* 2 or 3 */
     int32_t n_eq;      /* boundary rows per axis (6: p,v,a at both ends) */
     int32_t n_levels;  /* entries of the K^-1 table */
-    int32_t groups;    /* obstacle groups per CTA; 0 = automatic */
+    int32_t groups;    /* obstacle groups per CTA (one-CTA-per-member kernel); 0 = automatic */
+    int32_t layout;    /* TRO_LAYOUT_ANGLE or TRO_LAYOUT_UNIT (words per element, see tro_alg1_state) */
+    int32_t reserved;
 } tro_alg1_dims;
+
+/* per-element state layouts */
+#define TRO_LAYOUT_ANGLE 0 /* 3-D [alpha beta lx ly lz lca lsa lcb lsb] (9 words), 2-D [alpha lx ly lca lsa] (5) */
+#define TRO_LAYOUT_UNIT 1  /* angles kept as unit vectors: 3-D [ca sa cb sb lx ly lz lca lsa lcb lsb] (11),
+                              2-D [ca sa lx ly lca lsa] (6) */
 
 typedef struct tro_alg1_consts {
     const double* P;         /* n_p x m, row-major (basis.py:143-177) */
@@ -84,8 +91,7 @@ typedef struct tro_alg1_params {
 
 typedef struct tro_alg1_state {
     /* persistent per-element state, storage type T, interleaved per obstacle row:
-     *   state[i][j][w][t]  (B x n_o x W x n_p),
-     *   3-D W = 9: [alpha beta lx ly lz lca lsa lcb lsb];  2-D W = 5: [alpha lx ly lca lsa] */
+     *   state[i][j][w][t]  (B x n_o x W x n_p), words per tro_alg1_dims.layout */
     void* state;
     void* d;       /* optional B x n_o x n_p: read when d_mode == 1, written (new d) when non-NULL */
     void* copies;  /* optional export of the angle copies, planes of B x n_o x n_p:

@@ -81,7 +81,7 @@ class Alg1Engine:
     def __init__(self, basis: BasisSet, tracks, shape_a, shape_b, bvals, q, *, params, rho0=None,
                  w_smooth: float = 1.0, w_track: float = 1.0, dtype=torch.float64, device=None, groups: int = 0,
                  max_hist: int = 0, export: bool = False, keep_d: bool = False, cond_limit: float = 1e12,
-                 use_tma: bool = True):
+                 use_tma: bool = True, layout: str = "angle"):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -126,13 +126,16 @@ class Alg1Engine:
 
         # ---- state
         T = dict(dtype=dtype, device=dev)
-        W = 9 if dim == 3 else 5
+        if layout not in ("angle", "unit"):
+            raise ValueError("layout must be 'angle' or 'unit'")
+        self.layout = layout
+        n_ang = 2 if dim == 3 else 1
+        self.NV = n_ang * (2 if layout == "unit" else 1)
+        W = self.NV + (7 if dim == 3 else 4)
         self.W = W
         self.state = torch.empty((B, n_o, W, n_p), **T)
-        # views (member, obstacle, sample) / (plane, member, obstacle, sample)
-        self.alpha = self.state[:, :, 0]
-        self.beta = self.state[:, :, 1] if dim == 3 else None
-        self.lam = self.state[:, :, (2 if dim == 3 else 1):].permute(2, 0, 1, 3)
+        # multiplier planes as a (plane, member, obstacle, sample) view
+        self.lam = self.state[:, :, self.NV:].permute(2, 0, 1, 3)
         self.d = torch.empty((B, n_o, n_p), **T) if (keep_d or export) else None
         self.copies = torch.empty((4 if dim == 3 else 2, B, n_o, n_p), **T) if export else None
         self.xi = torch.zeros((B, dim, m), **f64)
@@ -154,7 +157,8 @@ class Alg1Engine:
         self.status = torch.zeros(B, **i32)
         self.n_changes = torch.zeros(B, **i32)
 
-        self._dims = _lib.Alg1Dims(B, n_o, n_p, m, dim, self.n_eq, len(self.table.rhos), int(groups))
+        self._dims = _lib.Alg1Dims(B, n_o, n_p, m, dim, self.n_eq, len(self.table.rhos), int(groups),
+                                   _lib.TRO_LAYOUT_UNIT if layout == "unit" else _lib.TRO_LAYOUT_ANGLE, 0)
         self._consts = _lib.Alg1Consts(
             self.P.data_ptr(), self.tracks.data_ptr(), self.shape_a.data_ptr(), self.shape_b.data_ptr(),
             self.kinv.data_ptr(), self.level_rho.data_ptr(), self.level_ok.data_ptr(), self.q.data_ptr(),
@@ -169,6 +173,37 @@ class Alg1Engine:
         self._graph_n = 0
         # TMA-pipelined persistent kernel for the iteration unless disabled (flags bit 2)
         self.base_flags = 0 if use_tma else _lib.TRO_FLAG_NO_TMA
+
+    # ------------------------------------------------------------ angle views
+    @property
+    def alpha(self) -> torch.Tensor:
+        """(B, n_o, n_p) alpha (a view in the angle layout, atan2 of the stored unit vector otherwise)."""
+        if self.layout == "angle":
+            return self.state[:, :, 0]
+        return torch.atan2(self.state[:, :, 1], self.state[:, :, 0])
+
+    @property
+    def beta(self) -> torch.Tensor | None:
+        if self.dim != 3:
+            return None
+        if self.layout == "angle":
+            return self.state[:, :, 1]
+        return torch.atan2(self.state[:, :, 3], self.state[:, :, 2])
+
+    def _set_angles(self, alpha, beta):
+        T = self.dtype
+        a = torch.as_tensor(np.asarray(alpha), dtype=torch.float64, device=self.device)
+        if self.layout == "angle":
+            self.state[:, :, 0].copy_(a.to(T))
+            if self.dim == 3:
+                self.state[:, :, 1].copy_(torch.as_tensor(np.asarray(beta), device=self.device).to(T))
+            return
+        self.state[:, :, 0].copy_(torch.cos(a).to(T))
+        self.state[:, :, 1].copy_(torch.sin(a).to(T))
+        if self.dim == 3:
+            b = torch.as_tensor(np.asarray(beta), dtype=torch.float64, device=self.device)
+            self.state[:, :, 2].copy_(torch.cos(b).to(T))
+            self.state[:, :, 3].copy_(torch.sin(b).to(T))
 
     # ------------------------------------------------------------ launches
     def _params(self, d_mode: int, flags: int = 0) -> _lib.Alg1Params:
@@ -253,9 +288,7 @@ class Alg1Engine:
         dev, T = self.device, self.dtype
         self.xi.copy_(torch.as_tensor(np.asarray(xi, float).reshape(self.B, self.dim, self.m)))
         if self.n_o:
-            self.alpha.copy_(torch.as_tensor(np.asarray(alpha)).to(T))
-            if self.dim == 3:
-                self.beta.copy_(torch.as_tensor(np.asarray(beta)).to(T))
+            self._set_angles(alpha, beta)
             self.lam.copy_(torch.as_tensor(np.asarray(lam_planes)).to(T))
             if d is not None:
                 if self.d is None:

@@ -22,6 +22,8 @@ TRO_CONVERGED = 1
 TRO_FACTOR_FAILED = 2
 TRO_FLAG_NO_SCHEDULE = 1
 TRO_FLAG_NO_TMA = 2
+TRO_LAYOUT_ANGLE = 0
+TRO_LAYOUT_UNIT = 1
 TRO_EINVAL = -1
 
 # every symbol include/trajopt_b200.h declares (checked by tests/test_lib_exports.py)
@@ -48,6 +50,8 @@ class Alg1Dims(ctypes.Structure):
         ("n_eq", c_int32),
         ("n_levels", c_int32),
         ("groups", c_int32),
+        ("layout", c_int32),
+        ("reserved", c_int32),
     ]
 
 

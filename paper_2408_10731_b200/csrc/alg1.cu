@@ -126,21 +126,17 @@ __device__ __forceinline__ void alg1_schedule(const Alg1Args& A, int i, int stat
 
 namespace tro {
 
-template <typename T>
-__device__ __forceinline__ T ld_state(const T* p) { return ld_stream(p); }
-
-// Per-element state layout (interleaved per obstacle row):
-//   state[i][j][w][t], w = 0..W-1:  3-D [alpha beta lx ly lz lca lsa lcb lsb], 2-D [alpha lx ly lca lsa]
-//   tracks[j][ax][t]
-// For fixed (i, j) the W words of one sample are NP*sizeof(T) apart, so with a
-// compile-time NP every load/store of the element uses one base register plus an
-// immediate offset.
-template <int DIM, typename T, int MODE, int NP>
+// Per-element state layout (interleaved per obstacle row): state[i][j][w][t]
+// (member, obstacle, word, sample), words per Words<DIM, UNIT>; tracks[j][ax][t].
+// For fixed (i, j) the W words of one sample are n_p elements apart, so with a
+// compile-time NP every load/store of the element uses one base register plus
+// an immediate offset.
+template <int DIM, typename T, bool UNIT, int MODE, int NP>
 __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1Args A) {
     // MODE 0: AM iteration; 1: prime (sums + residual of the current state); 2: cold init + prime
     constexpr bool prime = MODE != 0;
     constexpr bool init = MODE == 2;
-    constexpr int W = DIM == 3 ? 9 : 5;
+    constexpr int W = Words<DIM, UNIT>::W;
     extern __shared__ double smem[];
     const int i = blockIdx.x;
     const int tid = threadIdx.x;
@@ -290,7 +286,6 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
             const double trx = ld_const(tp);
             const double trY = ld_const(tp + n_p);
             const double trz = (DIM == 3) ? ld_const(tp + 2 * n_p) : 0.0;
-            const T a = (T)sA[j], b = (T)sB[j];
             const T ia2 = (T)sIA2[j], ib2 = (T)sIB2[j];
 
             // line-of-sight scale of the previous iterate (solver_single.py:274-291)
@@ -310,156 +305,46 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                 }
                 dold = los_scale(qd);
             }
-            const T dx = (T)(px - trx), dy = (T)(py - trY);
-
-            if constexpr (DIM == 3) {
-                const T dz = (T)(pz - trz);
-                T al, be, lx, ly, lz, lca, lsa, lcb, lsb;
+            T v[W];
+            if constexpr (!init) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) v[w] = ld_stream(sp + w * n_p);
+            }
+            if constexpr (prime) {
+                prime_element<DIM, T, UNIT, init>(v, trx, trY, trz, px, py, pz, sA[j], sB[j], dold, sumsq, mx,
+                                                  accL, accT);
                 if constexpr (init) {
-                    // angles3d of the straight-line offsets (geometry.py:102-114)
-                    const double ex = px - trx, ey = py - trY, ez = pz - trz;
-                    double a0 = atan2(ey, ex);
-                    if (a0 == -M_PI) a0 = M_PI;  // angle2d remap (geometry.py:98-99)
-                    const double ad = sA[j], bd = sB[j];
-                    al = (T)a0;
-                    be = (T)atan2(hypot(ex / ad, ey / ad), ez / bd);
-                    lx = ly = lz = lca = lsa = lcb = lsb = (T)0;
-                } else {
-                    al = ld_state(sp + 0 * n_p);
-                    be = ld_state(sp + 1 * n_p);
-                    lx = ld_state(sp + 2 * n_p);
-                    ly = ld_state(sp + 3 * n_p);
-                    lz = ld_state(sp + 4 * n_p);
-                    lca = ld_state(sp + 5 * n_p);
-                    lsa = ld_state(sp + 6 * n_p);
-                    lcb = ld_state(sp + 7 * n_p);
-                    lsb = ld_state(sp + 8 * n_p);
-                }
-                T sa, ca, sb, cb;
-                sincos_fast(al, &sa, &ca);  // copy reset (solver_single.py:375-380)
-                sincos_fast(be, &sb, &cb);
-                T ca2, sa2, cb2, sb2, dn, al2, be2, sA2, cA2, sB2, cB2;
-                if constexpr (prime) {
-                    ca2 = cA2 = ca; sa2 = sA2 = sa; cb2 = cB2 = cb; sb2 = sB2 = sb;
-                    dn = dold; al2 = al; be2 = be;
-                } else {
-                    // alpha copies (solver_single.py:223-228)
-                    const T coef = a * dold * sb;
-                    const T rden = rcp_fast(trho + trho_o * (coef * coef));
-                    const T Lx = lx + trho_o * dx, Ly = ly + trho_o * dy, Lz = lz + trho_o * dz;
-                    ca2 = (trho * ca - lca + coef * Lx) * rden;
-                    sa2 = (trho * sa - lsa + coef * Ly) * rden;
-                    // beta copies with the new alpha copies (solver_single.py:253-266)
-                    const T ccb = b * dold;
-                    cb2 = (trho * cb - lcb + ccb * Lz) * rcp_fast(trho + trho_o * (ccb * ccb));
-                    const T csb = a * dold;
-                    const T num = trho * sb - lsb + csb * (ca2 * Lx + sa2 * Ly);
-                    sb2 = num * rcp_fast(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
-                    // d from the new positions (solver_single.py:283-290)
-                    dn = los_scale(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2);
-                    al2 = atan2_fast(sa2, ca2);  // solver_single.py:242
-                    be2 = atan2_fast(sb2, cb2);  // solver_single.py:271
-                    unit_dir(ca2, sa2, &cA2, &sA2);  // cos/sin(alpha') for residuals + next targets
-                    unit_dir(cb2, sb2, &cB2, &sB2);
-                }
-                // residual families (solver_single.py:303-312)
-                const T adn = a * dn;
-                const T rx = dx - adn * ca2 * sb2;
-                const T ry = dy - adn * sa2 * sb2;
-                const T rz = dz - b * dn * cb2;
-                const T rcb = cb2 - cB2, rsb = sb2 - sB2, rca = ca2 - cA2, rsa = sa2 - sA2;
-                T ss = rx * rx;
-                ss = fma(ry, ry, ss); ss = fma(rz, rz, ss); ss = fma(rcb, rcb, ss);
-                ss = fma(rsb, rsb, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
-                sumsq += (double)ss;
-                T ml = fabs(rx);
-                ml = max_abs(ml, ry); ml = max_abs(ml, rz); ml = max_abs(ml, rcb);
-                ml = max_abs(ml, rsb); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
-                mx = (double)ml > mx ? (double)ml : mx;
-                if constexpr (!prime) {
-                    // multiplier ascent (solver_single.py:336-343)
-                    lx += trho_o * rx; ly += trho_o * ry; lz += trho_o * rz;
-                    lca += trho * rca; lsa += trho * rsa; lcb += trho * rcb; lsb += trho * rsb;
-                }
-                if constexpr (!prime || init) {
-                    st_stream(sp + 0 * n_p, al2);
-                    st_stream(sp + 1 * n_p, be2);
-                    st_stream(sp + 2 * n_p, lx);
-                    st_stream(sp + 3 * n_p, ly);
-                    st_stream(sp + 4 * n_p, lz);
-                    st_stream(sp + 5 * n_p, lca);
-                    st_stream(sp + 6 * n_p, lsa);
-                    st_stream(sp + 7 * n_p, lcb);
-                    st_stream(sp + 8 * n_p, lsb);
-                    if (dst) dst[e] = dn;
+#pragma unroll
+                    for (int w = 0; w < W; ++w) st_stream(sp + w * n_p, v[w]);
+                    if (dst) dst[e] = dold;
                     if (cop) {
-                        cop[0 * Nel + e] = ca2; cop[1 * Nel + e] = sa2;
-                        cop[2 * Nel + e] = cb2; cop[3 * Nel + e] = sb2;
+                        T c4[4];
+                        if constexpr (UNIT) {
+#pragma unroll
+                            for (int c = 0; c < 2 * (DIM - 1); ++c) c4[c] = v[c];
+                        } else {
+                            sincos_fast(v[0], &c4[1], &c4[0]);
+                            if (DIM == 3) sincos_fast(v[1], &c4[3], &c4[2]);
+                        }
+#pragma unroll
+                        for (int c = 0; c < 2 * (DIM - 1); ++c) cop[c * Nel + e] = c4[c];
                     }
                 }
-                // sums for the next position step: lam and targets with the reset copies
-                // cos/sin of the new angles (solver_single.py:177-189, 204-207)
-                accL[0] += (double)lx; accL[1] += (double)ly; accL[DIM - 1] += (double)lz;
-                accT[0] += trx + (double)(adn * cA2 * sB2);
-                accT[1] += trY + (double)(adn * sA2 * sB2);
-                accT[DIM - 1] += trz + (double)(b * dn * cB2);
             } else {
-                T al, lx, ly, lca, lsa;
-                if constexpr (init) {
-                    // scaled planar angle of the line offsets (solver_single.py:138-143)
-                    double a0 = atan2((py - trY) / sB[j], (px - trx) / sA[j]);
-                    if (a0 == -M_PI) a0 = M_PI;
-                    al = (T)a0;
-                    lx = ly = lca = lsa = (T)0;
-                } else {
-                    al = ld_state(sp + 0 * n_p);
-                    lx = ld_state(sp + 1 * n_p);
-                    ly = ld_state(sp + 2 * n_p);
-                    lca = ld_state(sp + 3 * n_p);
-                    lsa = ld_state(sp + 4 * n_p);
+                T dn, cp4[4];
+                am_element<DIM, T, UNIT>(v, trx, trY, trz, px, py, pz, (T)sA[j], (T)sB[j], ia2, ib2, dold, trho,
+                                         trho_o, sumsq, mx, accL, accT, dn, cp4);
+#pragma unroll
+                for (int w = 0; w < W; ++w) st_stream(sp + w * n_p, v[w]);
+                if (dst) dst[e] = dn;
+                if (cop) {
+#pragma unroll
+                    for (int c = 0; c < 2 * (DIM - 1); ++c) cop[c * Nel + e] = cp4[c];
                 }
-                T sa, ca;
-                sincos_fast(al, &sa, &ca);
-                T ca2, sa2, dn, al2, sA2, cA2;
-                if constexpr (prime) {
-                    ca2 = cA2 = ca; sa2 = sA2 = sa; dn = dold; al2 = al;
-                } else {
-                    // planar alpha copies (solver_single.py:229-237)
-                    const T cx = a * dold, cy = b * dold;
-                    ca2 = (trho * ca - lca + cx * (lx + trho_o * dx)) * rcp_fast(trho + trho_o * (cx * cx));
-                    sa2 = (trho * sa - lsa + cy * (ly + trho_o * dy)) * rcp_fast(trho + trho_o * (cy * cy));
-                    dn = los_scale(dx * dx * ia2 + dy * dy * ib2);
-                    al2 = atan2_fast(sa2, ca2);
-                    unit_dir(ca2, sa2, &cA2, &sA2);
-                }
-                const T rx = dx - a * dn * ca2;
-                const T ry = dy - b * dn * sa2;
-                const T rca = ca2 - cA2, rsa = sa2 - sA2;
-                T ss = rx * rx;
-                ss = fma(ry, ry, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
-                sumsq += (double)ss;
-                T ml = fabs(rx);
-                ml = max_abs(ml, ry); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
-                mx = (double)ml > mx ? (double)ml : mx;
-                if constexpr (!prime) {
-                    lx += trho_o * rx; ly += trho_o * ry;
-                    lca += trho * rca; lsa += trho * rsa;
-                }
-                if constexpr (!prime || init) {
-                    st_stream(sp + 0 * n_p, al2);
-                    st_stream(sp + 1 * n_p, lx);
-                    st_stream(sp + 2 * n_p, ly);
-                    st_stream(sp + 3 * n_p, lca);
-                    st_stream(sp + 4 * n_p, lsa);
-                    if (dst) dst[e] = dn;
-                    if (cop) { cop[0 * Nel + e] = ca2; cop[1 * Nel + e] = sa2; }
-                }
-                accL[0] += (double)lx; accL[1] += (double)ly;
-                accT[0] += trx + (double)(a * dn * cA2);
-                accT[1] += trY + (double)(b * dn * sA2);
             }
         }
     }
+
     // ---------------- epilogue: sums over obstacle groups (fixed order)
     if (act) {
 #pragma unroll
@@ -496,7 +381,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     }
 }
 
-template <int DIM, typename T, int MODE, int NP>
+template <int DIM, typename T, bool UNIT, int MODE, int NP>
 static int launch_mode(const Alg1Args& A, cudaStream_t st) {
     const int n_p = A.d.n_p;
     int threads = ((n_p * A.G + 31) / 32) * 32;
@@ -509,11 +394,11 @@ static int launch_mode(const Alg1Args& A, cudaStream_t st) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-            cudaFuncSetAttribute(alg1_kernel<DIM, T, MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            cudaFuncSetAttribute(alg1_kernel<DIM, T, UNIT, MODE, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             attr_set[dev] = true;
         }
     }
-    alg1_kernel<DIM, T, MODE, NP><<<A.d.n_members, threads, smem, st>>>(A);
+    alg1_kernel<DIM, T, UNIT, MODE, NP><<<A.d.n_members, threads, smem, st>>>(A);
     return (int)cudaGetLastError();
 }
 
@@ -534,44 +419,49 @@ static int sm_count() {
 }
 
 // persistent TMA-pipelined AM iteration (n_p == 100); returns 1 if it launched
-template <int DIM, typename T>
+template <int DIM, typename T, bool UNIT>
 static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
     constexpr int G = TRO_TMA_G;
     constexpr int S = (sizeof(T) == 8 && DIM == 3) ? TRO_TMA_S : TRO_TMA_S + 1;
-    using C = TmaCfg<DIM, T, 100, G, S>;
+    using C = TmaCfg<DIM, T, UNIT, 100, G, S>;
     const TmaLayout L = tma_layout(C::kStageBytes, S, 100, A.d.m, DIM, A.d.n_obs, G, C::kConsumers);
     if (L.total > 227 * 1024) return 0;
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, 100, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, UNIT, 100, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024);
         attr_set[dev] = true;
     }
     Alg1Args B = A;
     B.G = G;
     const int grid = A.d.n_members < sm_count() ? A.d.n_members : sm_count();
-    alg1_tma_kernel<DIM, T, 100, G, S><<<grid, C::kThreads, L.total, st>>>(B);
+    alg1_tma_kernel<DIM, T, UNIT, 100, G, S><<<grid, C::kThreads, L.total, st>>>(B);
     *rc = (int)cudaGetLastError();
     return 1;
 }
 
-template <int DIM, typename T>
+template <int DIM, typename T, bool UNIT>
 static int launch(const Alg1Args& A, int mode, cudaStream_t st) {
     // the benchmark horizon (n_p = 100) gets compile-time strides; anything else runs the generic path
     if (A.d.n_p == 100) {
         if (mode == 0) {
             int rc = 0;
-            if (!(A.p.flags & TRO_FLAG_NO_TMA) && launch_tma<DIM, T>(A, st, &rc)) return rc;
-            return launch_mode<DIM, T, 0, 100>(A, st);
+            if (!(A.p.flags & TRO_FLAG_NO_TMA) && launch_tma<DIM, T, UNIT>(A, st, &rc)) return rc;
+            return launch_mode<DIM, T, UNIT, 0, 100>(A, st);
         }
-        if (mode == 1) return launch_mode<DIM, T, 1, 100>(A, st);
-        return launch_mode<DIM, T, 2, 100>(A, st);
+        if (mode == 1) return launch_mode<DIM, T, UNIT, 1, 100>(A, st);
+        return launch_mode<DIM, T, UNIT, 2, 100>(A, st);
     }
-    if (mode == 0) return launch_mode<DIM, T, 0, 0>(A, st);
-    if (mode == 1) return launch_mode<DIM, T, 1, 0>(A, st);
-    return launch_mode<DIM, T, 2, 0>(A, st);
+    if (mode == 0) return launch_mode<DIM, T, UNIT, 0, 0>(A, st);
+    if (mode == 1) return launch_mode<DIM, T, UNIT, 1, 0>(A, st);
+    return launch_mode<DIM, T, UNIT, 2, 0>(A, st);
+}
+
+template <int DIM, typename T>
+static int launch_layout(const Alg1Args& A, int mode, cudaStream_t st) {
+    return A.d.layout == TRO_LAYOUT_UNIT ? launch<DIM, T, true>(A, mode, st) : launch<DIM, T, false>(A, mode, st);
 }
 
 static int auto_groups(const tro_alg1_dims* d) {
@@ -594,6 +484,7 @@ static int run(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* 
     if (dims->n_p < 2 || dims->n_p > kMaxThreads || dims->n_obs < 0) return TRO_EINVAL;
     if (p->stall_window < 1 || 2 * p->stall_window > kMaxRing) return TRO_EINVAL;
     if (dtype != TRO_F64 && dtype != TRO_F32) return TRO_EINVAL;
+    if (dims->layout != TRO_LAYOUT_ANGLE && dims->layout != TRO_LAYOUT_UNIT) return TRO_EINVAL;
     if (dims->n_members <= 0) return 0;
     Alg1Args A;
     A.d = *dims;
@@ -605,9 +496,9 @@ static int run(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* 
     if ((size_t)L.total * sizeof(double) > 200 * 1024) return TRO_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (dims->dim == 3) {
-        return dtype == TRO_F64 ? launch<3, double>(A, mode, st) : launch<3, float>(A, mode, st);
+        return dtype == TRO_F64 ? launch_layout<3, double>(A, mode, st) : launch_layout<3, float>(A, mode, st);
     }
-    return dtype == TRO_F64 ? launch<2, double>(A, mode, st) : launch<2, float>(A, mode, st);
+    return dtype == TRO_F64 ? launch_layout<2, double>(A, mode, st) : launch_layout<2, float>(A, mode, st);
 }
 
 }  // namespace tro

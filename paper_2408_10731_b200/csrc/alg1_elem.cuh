@@ -45,32 +45,40 @@ __device__ __forceinline__ T max_abs(T acc, T v) {
     return v > acc ? v : acc;
 }
 
-template <int DIM>
-struct Words;
-template <>
-struct Words<3> {
-    static constexpr int W = 9;  // alpha beta lx ly lz lca lsa lcb lsb
-};
-template <>
-struct Words<2> {
-    static constexpr int W = 5;  // alpha lx ly lca lsa
+// Per-element words of the persistent state.
+//   angle layout (UNIT = false, the reference's variables):
+//     3-D [alpha beta lx ly lz lca lsa lcb lsb] (9), 2-D [alpha lx ly lca lsa] (5)
+//   unit layout (UNIT = true): each angle is kept as its unit vector (cos, sin), which removes
+//     the atan2 -> sincos round trip from every iteration at +2 (3-D) / +1 (2-D) words:
+//     3-D [ca sa cb sb lx ly lz lca lsa lcb lsb] (11), 2-D [ca sa lx ly lca lsa] (6)
+template <int DIM, bool UNIT>
+struct Words {
+    static constexpr int NA = DIM == 3 ? 2 : 1;          // angles
+    static constexpr int NL = DIM == 3 ? 7 : 4;          // multiplier planes
+    static constexpr int NV = UNIT ? 2 * NA : NA;        // words holding the angles
+    static constexpr int W = NV + NL;
 };
 
 // One AM iteration of one element.  v[W]: state words in / out.  d_old: the
 // line-of-sight scale of the previous iterate.  Outputs the new d, the angle
 // copies (for the optional export), and accumulates the residual norm/max and
 // the sums the next position step needs.
-template <int DIM, typename T>
+template <int DIM, typename T, bool UNIT>
 __device__ __forceinline__ void am_element(T* v, double trx, double trY, double trz, double px, double py, double pz,
                                            T a, T b, T ia2, T ib2, T dold, T trho, T trho_o, double& sumsq,
                                            double& mx, double* accL, double* accT, T& dn, T* copies) {
     const T dx = (T)(px - trx), dy = (T)(py - trY);
     if constexpr (DIM == 3) {
         const T dz = (T)(pz - trz);
+        constexpr int o = UNIT ? 4 : 2;  // first multiplier word
         T sa, ca, sb, cb;
-        sincos_fast(v[0], &sa, &ca);  // copy reset (solver_single.py:375-380)
-        sincos_fast(v[1], &sb, &cb);
-        T lx = v[2], ly = v[3], lz = v[4], lca = v[5], lsa = v[6], lcb = v[7], lsb = v[8];
+        if constexpr (UNIT) {
+            ca = v[0]; sa = v[1]; cb = v[2]; sb = v[3];
+        } else {
+            sincos_fast(v[0], &sa, &ca);  // copy reset (solver_single.py:375-380)
+            sincos_fast(v[1], &sb, &cb);
+        }
+        T lx = v[o], ly = v[o + 1], lz = v[o + 2], lca = v[o + 3], lsa = v[o + 4], lcb = v[o + 5], lsb = v[o + 6];
         // alpha copies (solver_single.py:223-228)
         const T coef = a * dold * sb;
         const T rden = rcp_fast(trho + trho_o * (coef * coef));
@@ -85,11 +93,15 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         const T sb2 = num * rcp_fast(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
         // d from the new positions (solver_single.py:283-290)
         dn = los_scale(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2);
-        v[0] = atan2_fast(sa2, ca2);  // solver_single.py:242
-        v[1] = atan2_fast(sb2, cb2);  // solver_single.py:271
         T cA2, sA2, cB2, sB2;
         unit_dir(ca2, sa2, &cA2, &sA2);  // cos/sin(alpha') for residuals + next targets
         unit_dir(cb2, sb2, &cB2, &sB2);
+        if constexpr (UNIT) {
+            v[0] = cA2; v[1] = sA2; v[2] = cB2; v[3] = sB2;
+        } else {
+            v[0] = atan2_fast(sa2, ca2);  // solver_single.py:242
+            v[1] = atan2_fast(sb2, cb2);  // solver_single.py:271
+        }
         // residual families (solver_single.py:303-312)
         const T adn = a * dn;
         const T rx = dx - adn * ca2 * sb2;
@@ -105,27 +117,37 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         ml = max_abs(ml, rsb); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
         mx = (double)ml > mx ? (double)ml : mx;
         // multiplier ascent (solver_single.py:336-343)
-        v[2] = lx + trho_o * rx; v[3] = ly + trho_o * ry; v[4] = lz + trho_o * rz;
-        v[5] = lca + trho * rca; v[6] = lsa + trho * rsa; v[7] = lcb + trho * rcb; v[8] = lsb + trho * rsb;
+        v[o] = lx + trho_o * rx; v[o + 1] = ly + trho_o * ry; v[o + 2] = lz + trho_o * rz;
+        v[o + 3] = lca + trho * rca; v[o + 4] = lsa + trho * rsa;
+        v[o + 5] = lcb + trho * rcb; v[o + 6] = lsb + trho * rsb;
         copies[0] = ca2; copies[1] = sa2; copies[2] = cb2; copies[3] = sb2;
         // sums for the next position step with the reset copies cos/sin of the new angles
         // (solver_single.py:177-189, 204-207)
-        accL[0] += (double)v[2]; accL[1] += (double)v[3]; accL[2] += (double)v[4];
+        accL[0] += (double)v[o]; accL[1] += (double)v[o + 1]; accL[2] += (double)v[o + 2];
         accT[0] += trx + (double)(adn * cA2 * sB2);
         accT[1] += trY + (double)(adn * sA2 * sB2);
         accT[2] += trz + (double)(b * dn * cB2);
     } else {
+        constexpr int o = UNIT ? 2 : 1;
         T sa, ca;
-        sincos_fast(v[0], &sa, &ca);
-        T lx = v[1], ly = v[2], lca = v[3], lsa = v[4];
+        if constexpr (UNIT) {
+            ca = v[0]; sa = v[1];
+        } else {
+            sincos_fast(v[0], &sa, &ca);
+        }
+        T lx = v[o], ly = v[o + 1], lca = v[o + 2], lsa = v[o + 3];
         // planar alpha copies (solver_single.py:229-237)
         const T cx = a * dold, cy = b * dold;
         const T ca2 = (trho * ca - lca + cx * (lx + trho_o * dx)) * rcp_fast(trho + trho_o * (cx * cx));
         const T sa2 = (trho * sa - lsa + cy * (ly + trho_o * dy)) * rcp_fast(trho + trho_o * (cy * cy));
         dn = los_scale(dx * dx * ia2 + dy * dy * ib2);
-        v[0] = atan2_fast(sa2, ca2);
         T cA2, sA2;
         unit_dir(ca2, sa2, &cA2, &sA2);
+        if constexpr (UNIT) {
+            v[0] = cA2; v[1] = sA2;
+        } else {
+            v[0] = atan2_fast(sa2, ca2);
+        }
         const T rx = dx - a * dn * ca2;
         const T ry = dy - b * dn * sa2;
         const T rca = ca2 - cA2, rsa = sa2 - sA2;
@@ -135,13 +157,72 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         T ml = fabs(rx);
         ml = max_abs(ml, ry); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
         mx = (double)ml > mx ? (double)ml : mx;
-        v[1] = lx + trho_o * rx; v[2] = ly + trho_o * ry;
-        v[3] = lca + trho * rca; v[4] = lsa + trho * rsa;
+        v[o] = lx + trho_o * rx; v[o + 1] = ly + trho_o * ry;
+        v[o + 2] = lca + trho * rca; v[o + 3] = lsa + trho * rsa;
         copies[0] = ca2; copies[1] = sa2;
-        accL[0] += (double)v[1]; accL[1] += (double)v[2];
+        accL[0] += (double)v[o]; accL[1] += (double)v[o + 1];
         accT[0] += trx + (double)(a * dn * cA2);
         accT[1] += trY + (double)(b * dn * sA2);
     }
+}
+
+// Cold-start angles / prime of a state (no update): fills v for INIT, then the
+// residual of the copies-reset state (copies == cos/sin of the angles, so only the
+// collision families are non-zero) and the sums the first position step needs.
+template <int DIM, typename T, bool UNIT, bool INIT>
+__device__ __forceinline__ void prime_element(T* v, double trx, double trY, double trz, double px, double py,
+                                              double pz, double ad, double bd, T dold, double& sumsq, double& mx,
+                                              double* accL, double* accT) {
+    constexpr int NL = Words<DIM, UNIT>::NL;
+    constexpr int o = Words<DIM, UNIT>::NV;
+    const double ex = px - trx, ey = py - trY, ez = pz - trz;
+    T ca, sa, cb = 0, sb = 0;
+    if constexpr (INIT) {
+        // angles of the straight-line offsets: angles3d (geometry.py:102-114) in 3-D, the
+        // ellipse-scaled angle2d in 2-D (solver_single.py:138-143); -pi folds onto pi
+        double a0 = DIM == 3 ? atan2(ey, ex) : atan2(ey / bd, ex / ad);
+        if (a0 == -M_PI) a0 = M_PI;
+        double b0 = DIM == 3 ? atan2(hypot(ex / ad, ey / ad), ez / bd) : 0.0;
+        double s0, c0, s1, c1;
+        sincos(a0, &s0, &c0);
+        sincos(b0, &s1, &c1);
+        if constexpr (UNIT) {
+            v[0] = (T)c0; v[1] = (T)s0;
+            if (DIM == 3) { v[2] = (T)c1; v[3] = (T)s1; }
+        } else {
+            v[0] = (T)a0;
+            if (DIM == 3) v[1] = (T)b0;
+        }
+#pragma unroll
+        for (int k = 0; k < NL; ++k) v[o + k] = (T)0;
+    }
+    if constexpr (UNIT) {
+        ca = v[0]; sa = v[1];
+        if (DIM == 3) { cb = v[2]; sb = v[3]; }
+    } else {
+        sincos_fast(v[0], &sa, &ca);
+        if (DIM == 3) sincos_fast(v[1], &sb, &cb);
+    }
+    const T a = (T)ad, b = (T)bd;
+    double rr, ml;
+    if constexpr (DIM == 3) {
+        const T rx = (T)ex - a * dold * ca * sb, ry = (T)ey - a * dold * sa * sb, rz = (T)ez - b * dold * cb;
+        rr = (double)rx * rx + (double)ry * ry + (double)rz * rz;
+        ml = fmax(fmax(fabs((double)rx), fabs((double)ry)), fabs((double)rz));
+        accT[0] += trx + (double)(a * dold * ca * sb);
+        accT[1] += trY + (double)(a * dold * sa * sb);
+        accT[2] += trz + (double)(b * dold * cb);
+    } else {
+        const T rx = (T)ex - a * dold * ca, ry = (T)ey - b * dold * sa;
+        rr = (double)rx * rx + (double)ry * ry;
+        ml = fmax(fabs((double)rx), fabs((double)ry));
+        accT[0] += trx + (double)(a * dold * ca);
+        accT[1] += trY + (double)(b * dold * sa);
+    }
+    sumsq += rr;
+    mx = ml > mx ? ml : mx;
+#pragma unroll
+    for (int ax = 0; ax < DIM; ++ax) accL[ax] += (double)v[o + ax];
 }
 
 }  // namespace tro

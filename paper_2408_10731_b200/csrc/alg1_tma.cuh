@@ -54,9 +54,9 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-template <int DIM, typename T, int NP, int G, int S>
+template <int DIM, typename T, bool UNIT, int NP, int G, int S>
 struct TmaCfg {
-    static constexpr int W = Words<DIM>::W;
+    static constexpr int W = Words<DIM, UNIT>::W;
     static constexpr int kRowBytes = W * NP * (int)sizeof(T);  // one obstacle row of state
     static constexpr int kTrkBytes = DIM * NP * 8;             // one obstacle row of tracks
     static constexpr int kStageBytes = G * (kRowBytes + kTrkBytes);
@@ -89,9 +89,9 @@ __host__ __device__ inline TmaLayout tma_layout(int stage_bytes, int S, int n_p,
     return L;
 }
 
-template <int DIM, typename T, int NP, int G, int S>
-__global__ void __launch_bounds__(TmaCfg<DIM, T, NP, G, S>::kThreads, 1) alg1_tma_kernel(Alg1Args A) {
-    using C = TmaCfg<DIM, T, NP, G, S>;
+template <int DIM, typename T, bool UNIT, int NP, int G, int S>
+__global__ void __launch_bounds__(TmaCfg<DIM, T, UNIT, NP, G, S>::kThreads, 1) alg1_tma_kernel(Alg1Args A) {
+    using C = TmaCfg<DIM, T, UNIT, NP, G, S>;
     constexpr int W = C::W;
     constexpr int NC = C::kConsumers;
     constexpr int NCW = NC / 32;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, NP, G, S>::kThreads, 1) alg1_tm
                     dold = los_scale(qd);
                 }
                 T dn, cp4[4];
-                am_element<DIM, T>(v, trx, trY, trz, px, py, pz, a, b, ia2, ib2, dold, trho, trho_o, sumsq, mx,
+                am_element<DIM, T, UNIT>(v, trx, trY, trz, px, py, pz, a, b, ia2, ib2, dold, trho, trho_o, sumsq, mx,
                                    accL, accT, dn, cp4);
                 T* gp = gbase + (int64_t)j * W * NP;
 #pragma unroll
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, NP, G, S>::kThreads, 1) alg1_tm
                 if (dst) dst[e] = dn;
                 if (cop) {
 #pragma unroll
-                    for (int c = 0; c < (DIM == 3 ? 4 : 2); ++c) cop[c * Nel + e] = cp4[c];
+                    for (int c = 0; c < 2 * (DIM - 1); ++c) cop[c * Nel + e] = cp4[c];
                 }
             }
             __syncwarp();

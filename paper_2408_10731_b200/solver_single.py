@@ -374,27 +374,31 @@ class BatchSolution:
 
 
 def make_batch_engine(batch: SingleBatch, params: SingleParams, *, dtype=torch.float64, device=None,
-                      history: bool = False, groups: int = 0, export: bool = False) -> Alg1Engine:
+                      history: bool = False, groups: int = 0, export: bool = False, layout: str = "angle",
+                      use_tma: bool = True) -> Alg1Engine:
     a = np.array([o.shape.a for o in batch.obstacles], dtype=float)
     b = np.array([o.shape.b for o in batch.obstacles], dtype=float)
     tracks = (np.stack([o.centers for o in batch.obstacles]) if batch.obstacles
               else np.zeros((0, batch.basis.n_p, batch.dim)))
     return Alg1Engine(batch.basis, tracks, a, b, batch.bvals, batch.linear_terms(), params=params,
                       w_smooth=batch.w_smooth, w_track=batch.w_track, dtype=dtype, device=device, groups=groups,
-                      max_hist=params.max_iter if history else 0, export=export)
+                      max_hist=params.max_iter if history else 0, export=export, layout=layout, use_tma=use_tma)
 
 
 def solve_single_batch(batch: SingleBatch | list, params: SingleParams | None = None, *, dtype=torch.float64,
                        device=None, history: bool = False, groups: int = 0, use_graph: bool = True,
-                       engine: Alg1Engine | None = None) -> BatchSolution:
+                       engine: Alg1Engine | None = None, layout: str = "angle") -> BatchSolution:
     """Solve B independent members (each = solve_single of its problem) in one device pass.
 
     dtype: storage of the per-element state (float64, or float32 with the QP step and all
-    per-member reductions kept in fp64)."""
+    per-member reductions kept in fp64).
+    layout: "angle" keeps the reference's angle variables (9 words / element in 3-D); "unit"
+    keeps each angle as its unit vector (11 words) and skips the atan2/sincos round trip."""
     params = params or SingleParams()
     if isinstance(batch, list):
         batch = SingleBatch.from_problems(batch)
-    eng = engine or make_batch_engine(batch, params, dtype=dtype, device=device, history=history, groups=groups)
+    eng = engine or make_batch_engine(batch, params, dtype=dtype, device=device, history=history, groups=groups,
+                                      layout=layout)
     eng.reset_schedule()
     eng.level.copy_(eng.level0)
     eng.cold_init()

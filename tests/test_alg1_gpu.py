@@ -42,12 +42,16 @@ def rel(a, b):
     return float(np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(np.max(np.abs(b)), 1e-300))
 
 
-def engine_from(g, bvals, desired, params, *, dtype=torch.float64, rho0=None, max_hist=0):
+def engine_from(g, bvals, desired, params, *, dtype=torch.float64, rho0=None, max_hist=0, layout="angle",
+                use_tma=True):
     basis = basis_from(g)
     q = -2.0 * float(g["w"][1]) * np.einsum("tc,btk->bkc", basis.P, desired)
     return Alg1Engine(basis, g["tracks"], g["a"], g["b"], bvals, q, params=params, rho0=rho0,
                       w_smooth=float(g["w"][0]), w_track=float(g["w"][1]), dtype=dtype, max_hist=max_hist,
-                      export=True, keep_d=True)
+                      export=True, keep_d=True, layout=layout, use_tma=use_tma)
+
+
+KERNELS = [("angle", True), ("angle", False), ("unit", True), ("unit", False)]
 
 
 def load_snapshot(eng, g, pre, dim):
@@ -109,14 +113,16 @@ def test_corridor2d_free_run(golden):
 CASES = [(0, 0), (0, 1), (0, 60), (1, 10)]
 
 
+@pytest.mark.parametrize("layout,tma", KERNELS)
 @pytest.mark.parametrize("member,k", CASES)
-def test_flow3d_teacher_forced_fp64(golden, member, k):
+def test_flow3d_teacher_forced_fp64(golden, member, k, layout, tma):
     g = golden("flow3d_tf.npz")
     gh = golden("flow3d_hist.npz")
     pre, nxt = f"m{member}_k{k}_", f"m{member}_k{k + 1}_"
     bvals, desired = g[f"m{member}_bvals"], g[f"m{member}_desired"]
     sc = g[pre + "scal"]
-    eng = engine_from(g, bvals, desired, SingleParams(max_iter=200, tol=0.0), rho0=[sc[1]], max_hist=4)
+    eng = engine_from(g, bvals, desired, SingleParams(max_iter=200, tol=0.0), rho0=[sc[1]], max_hist=4,
+                      layout=layout, use_tma=tma)
     load_snapshot(eng, g, pre, 3)
     eng.load_schedule([g[pre + "maxhist"]], [int(g[pre + "last_change"][0])])
     eng.prime(0 if k == 0 else 1)
@@ -137,15 +143,16 @@ def test_flow3d_teacher_forced_fp64(golden, member, k):
     assert eng.rho_o[0].item() == g[nxt + "scal"][1]  # identical penalty decision
 
 
+@pytest.mark.parametrize("layout,tma", KERNELS)
 @pytest.mark.parametrize("member,k", CASES)
-def test_flow3d_teacher_forced_fp32(golden, member, k):
+def test_flow3d_teacher_forced_fp32(golden, member, k, layout, tma):
     """fp32 per-element storage and arithmetic; QP step and reductions in fp64."""
     g = golden("flow3d_tf.npz")
     gh = golden("flow3d_hist.npz")
     pre, nxt = f"m{member}_k{k}_", f"m{member}_k{k + 1}_"
     sc = g[pre + "scal"]
     eng = engine_from(g, g[f"m{member}_bvals"], g[f"m{member}_desired"], SingleParams(max_iter=200, tol=0.0),
-                      dtype=torch.float32, rho0=[sc[1]])
+                      dtype=torch.float32, rho0=[sc[1]], layout=layout, use_tma=tma)
     load_snapshot(eng, g, pre, 3)
     eng.prime(0 if k == 0 else 1)
     eng.iterate(0 if k == 0 else 1)
@@ -189,6 +196,21 @@ def test_flow3d_batch_free_window(golden):
     assert 0.2 < np.median(fin) / np.median(ref) < 5.0
 
 
+@pytest.mark.parametrize("layout", ["angle", "unit"])
+def test_batch_layouts_agree_over_a_window(golden, layout):
+    """The unit-vector layout (11 words) reproduces the angle layout's C2 histories (the AM
+    map only sees cos/sin of the angles); chaos bounds the window like the twin test."""
+    gh = golden("flow3d_hist.npz")
+    bs = basis_from(gh)
+    batch = scenarios.flow3d_batch(50, gh["members"], basis=bs)
+    p = SingleParams(max_iter=200, tol=0.0)
+    h = solve_single_batch(batch, p, history=True, layout=layout).history.cpu().numpy()
+    for i in range(len(gh["members"])):
+        np.testing.assert_allclose(h[i, :8, :2], gh["hist"][i][:8, :2], rtol=1e-9)
+    fin, ref = h[:, -1, 1], gh["hist"][:, -1, 1]
+    assert 0.2 < np.median(fin) / np.median(ref) < 5.0
+
+
 def test_batch_members_equal_single_solves(golden):
     """A member's arithmetic does not depend on the batch it runs in (bitwise)."""
     bs = basis_from(golden("flow3d_hist.npz"))
@@ -201,21 +223,24 @@ def test_batch_members_equal_single_solves(golden):
         np.testing.assert_array_equal(one.state.xi, xi[i])
 
 
-def test_oracle_vs_device_n100_step(golden):
-    """C5 shape (n_o 100): device one step == oracle one step from an oracle mid-run state."""
-    bs = basis_from(golden("flow3d_hist.npz"))
+@pytest.mark.parametrize("n_p,layout", [(100, "angle"), (100, "unit"), (60, "angle"), (60, "unit")])
+def test_oracle_vs_device_step(golden, n_p, layout):
+    """C5 shape (n_o 100) and a generic horizon (n_p 60, the non-specialised kernel): device one
+    step == oracle one step from an oracle mid-run state."""
+    from paper_2408_10731_b200.basis import build_basis
+
+    bs = basis_from(golden("flow3d_hist.npz")) if n_p == 100 else build_basis(0.0, 10.0, n_p, 10)
     batch = scenarios.flow3d_batch(100, [5, 6], basis=bs)
     tracks = np.stack([o.centers for o in batch.obstacles])
     a = np.array([o.shape.a for o in batch.obstacles])
     b = np.array([o.shape.b for o in batch.obstacles])
-    s = np.linspace(0, 1, 100)
-    des = batch.bvals[:, :, 0][:, None, :] + s[None, :, None] * (batch.bvals[:, :, 3] - batch.bvals[:, :, 0])[:, None]
+    des = batch.desired_paths()
     prob = O.Problem(P=bs.P, Pd=bs.Pdot, Pdd=bs.Pddot, bvals=batch.bvals, desired=des, tracks=tracks, a=a, b=b)
     r = O.solve(prob, O.Params(max_iter=25, tol=0.0))
     st = r.state
     kkt = O.KKTCache(prob, mode="kinv")
     eng = Alg1Engine(bs, tracks, a, b, batch.bvals, batch.linear_terms(), params=SingleParams(max_iter=1, tol=0.0),
-                     rho0=st.rho_o, export=True, keep_d=True)
+                     rho0=st.rho_o, export=True, keep_d=True, layout=layout)
     eng.load_state(xi=st.xi, alpha=st.alpha, beta=st.beta,
                    lam_planes=np.stack([st.lam_pos[:, 0], st.lam_pos[:, 1], st.lam_pos[:, 2], st.lam_cos_a,
                                         st.lam_sin_a, st.lam_cos_b, st.lam_sin_b]),
@@ -226,6 +251,8 @@ def test_oracle_vs_device_n100_step(golden):
     torch.cuda.synchronize()
     assert rel(eng.xi.cpu().numpy(), st.xi) < 1e-10
     np.testing.assert_allclose(eng.alpha.cpu().numpy(), st.alpha, atol=1e-9)
+    np.testing.assert_allclose(eng.beta.cpu().numpy(), st.beta, atol=1e-9)
+    np.testing.assert_allclose(eng.d.cpu().numpy(), st.d, atol=1e-9)
     np.testing.assert_allclose(eng.lam[0].cpu().numpy(), st.lam_pos[:, 0], atol=1e-8 * np.abs(st.lam_pos).max())
 
 

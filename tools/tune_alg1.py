@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--tag", default=os.path.basename(os.environ.get("TRO_LIB_PATH", "default")))
     ap.add_argument("--no-tma", action="store_true")
+    ap.add_argument("--layout", default="angle")
     a = ap.parse_args()
     dtype = torch.float64 if a.dtype == "f64" else torch.float32
     s = 8 if a.dtype == "f64" else 4
@@ -33,7 +34,7 @@ def main():
     params = SingleParams(max_iter=a.iters, tol=0.0)
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6650.0
     for G in [int(x) for x in a.groups.split(",")]:
-        eng = make_batch_engine(batch, params, dtype=dtype, groups=G)
+        eng = make_batch_engine(batch, params, dtype=dtype, groups=G, layout=a.layout)
         if a.no_tma:
             eng.base_flags = 2
         eng.cold_init()
@@ -47,7 +48,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
         gbs = 2 * 9 * a.n_obs * 100 * s * a.members / (ms / 1e3) / 1e9
-        print(json.dumps({"tag": a.tag + ("" if not a.no_tma else "+notma"), "G": G, "ms_per_iter": round(ms, 4), "GBps": round(gbs, 1),
+        print(json.dumps({"tag": a.tag + ("" if not a.no_tma else "+notma") + "+" + a.layout, "G": G, "ms_per_iter": round(ms, 4), "GBps": round(gbs, 1),
                           "frac": round(gbs / peak, 3), "dtype": a.dtype, "members": a.members, "n_obs": a.n_obs}))
         del eng
         torch.cuda.empty_cache()
