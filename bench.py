@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--groups", type=int, default=0)
+    ap.add_argument("--layout", default="unit", choices=["unit", "angle"],
+                    help="per-element state layout (unit: 11 words, angle: the reference's 9 words)")
     ap.add_argument("--members", type=int, default=0, help="override the member count (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -190,7 +192,7 @@ def run_b200(args):
     else:
         batch = scenarios.flow3d_batch(n_o, range(lo, hi), basis=basis)
     params = SingleParams(max_iter=n_iter, tol=0.0)
-    eng = make_batch_engine(batch, params, dtype=dtype, groups=args.groups)
+    eng = make_batch_engine(batch, params, dtype=dtype, groups=args.groups, layout=args.layout)
     stream = torch.cuda.current_stream()
 
     def solve_device():
@@ -244,8 +246,10 @@ def run_b200(args):
     elapsed = float(t.item())
     value = members_total * n_iter * args.steps / elapsed
 
-    # roofline of the dominant kernel (tro_alg1_iterate): algorithmic bytes per launch / avg launch time
+    # roofline of the dominant kernel (tro_alg1_iterate): ALGORITHMIC bytes per launch (the reference's
+    # 9 persistent words per element) / avg launch time -- independent of the layout
     alg_bytes = 2 * WORDS_3D * n_o * 100 * s_bytes * B
+    moved_bytes = 2 * eng.W * n_o * 100 * s_bytes * B
     avg_launch_s = statistics.mean(run_ms) / 1e3 / n_iter
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / avg_launch_s / 1e9
@@ -301,11 +305,14 @@ def run_b200(args):
         "dtype": args.dtype,
         "data": "synthetic (seeded scenario recipe, SURVEY.md §8(d))",
         "config": {"workload": desc, "members": members_total, "n_obs": n_o, "n_p": 100, "am_iters": n_iter,
-                   "state_dtype": args.dtype, "qp_step": "f64", "parallelism": f"member-shard x{world}",
+                   "state_dtype": args.dtype, "state_layout": args.layout, "qp_step": "f64",
+                   "parallelism": f"member-shard x{world}",
                    "l2": "state >> L2 (no flush needed)" if alg_bytes > 126e6 else "state fits L2"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_s * 1e3,
+                     "layout": args.layout, "state_bytes_moved_per_launch": moved_bytes,
+                     "hbm_frac_of_moved_bytes": moved_bytes / avg_launch_s / 1e9 / peak,
                      "kernel": "tro_alg1_iterate (alg1_kernel<3,T>)"},
         "clocks": clk,
         "e2e": e2e,

@@ -403,7 +403,7 @@ static int launch_mode(const Alg1Args& A, cudaStream_t st) {
 }
 
 #ifndef TRO_TMA_G
-#define TRO_TMA_G 5
+#define TRO_TMA_G 4
 #endif
 #ifndef TRO_TMA_S
 #define TRO_TMA_S 3
