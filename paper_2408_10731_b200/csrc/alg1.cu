@@ -403,7 +403,7 @@ static int launch_mode(const Alg1Args& A, cudaStream_t st) {
 }
 
 #ifndef TRO_TMA_G
-#define TRO_TMA_G 4
+#define TRO_TMA_G 2
 #endif
 #ifndef TRO_TMA_S
 #define TRO_TMA_S 3
@@ -425,18 +425,19 @@ static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
     constexpr int S = (sizeof(T) == 8 && DIM == 3) ? TRO_TMA_S : TRO_TMA_S + 1;
     using C = TmaCfg<DIM, T, UNIT, 100, G, S>;
     const TmaLayout L = tma_layout(C::kStageBytes, S, 100, A.d.m, DIM, A.d.n_obs, G, C::kConsumers);
-    if (L.total > 227 * 1024) return 0;
+    if (L.total * kTmaMinBlocks > 227 * 1024) return 0;
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !attr_set[dev]) {
         cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, UNIT, 100, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
+                             227 * 1024 / kTmaMinBlocks);
         attr_set[dev] = true;
     }
     Alg1Args B = A;
     B.G = G;
-    const int grid = A.d.n_members < sm_count() ? A.d.n_members : sm_count();
+    const int slots = sm_count() * kTmaMinBlocks;
+    const int grid = A.d.n_members < slots ? A.d.n_members : slots;
     alg1_tma_kernel<DIM, T, UNIT, 100, G, S><<<grid, C::kThreads, L.total, st>>>(B);
     *rc = (int)cudaGetLastError();
     return 1;

@@ -89,8 +89,13 @@ __host__ __device__ inline TmaLayout tma_layout(int stage_bytes, int S, int n_p,
     return L;
 }
 
+#ifndef TRO_TMA_MINB
+#define TRO_TMA_MINB 2
+#endif
+constexpr int kTmaMinBlocks = TRO_TMA_MINB;  // resident CTAs per SM the kernel is compiled for
+
 template <int DIM, typename T, bool UNIT, int NP, int G, int S>
-__global__ void __launch_bounds__(TmaCfg<DIM, T, UNIT, NP, G, S>::kThreads, 1) alg1_tma_kernel(Alg1Args A) {
+__global__ void __launch_bounds__(TmaCfg<DIM, T, UNIT, NP, G, S>::kThreads, kTmaMinBlocks) alg1_tma_kernel(Alg1Args A) {
     using C = TmaCfg<DIM, T, UNIT, NP, G, S>;
     constexpr int W = C::W;
     constexpr int NC = C::kConsumers;
