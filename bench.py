@@ -250,11 +250,13 @@ def run_b200(args):
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / avg_launch_s / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"ncu_alg1_{args.config}_{args.dtype}.json")
+    # DRAM bytes per launch from the committed ncu --set full capture of the same kernel
+    # (same layout / dtype), scaled from per-element bytes to this launch's element count
+    tpath = os.path.join(ROOT, "profiles", f"ncu_alg1_{args.layout}_{args.dtype}.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             prof = json.load(fh)
-        traffic = prof.get("dram_bytes_per_member_launch", 0) * B or None
+        traffic = prof.get("dram_bytes_per_element_launch", 0) * B * n_o * 100 or None
 
     # e2e through the public API with host buffers
     e2e = None
