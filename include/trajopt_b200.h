@@ -128,6 +128,66 @@ int tro_alg1_init(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_const
 int tro_alg1_iterate(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
                      const tro_alg1_state* s, const tro_alg1_params* p, void* stream);
 
+/* ------------------------------------------------------------------ PRIEST / CEM (Alg. 3) */
+typedef struct tro_priest_dims {
+    int64_t n_samples; /* N */
+    int32_t n_p;       /* horizon samples */
+    int32_t m;         /* basis columns */
+    int32_t dim;       /* 2 or 3 */
+    int32_t n_obs;     /* obstacles */
+    int32_t n_eq;      /* boundary equality rows (all axes) */
+    int32_t n_inner;   /* inner projection iterations */
+} tro_priest_dims;
+
+typedef struct tro_priest_consts {
+    const double* P;       /* n_p x m */
+    const double* Pd;      /* n_p x m */
+    const double* Pdd;     /* n_p x m */
+    const double* tracks;  /* n_o x dim x n_p obstacle centres */
+    const double* shape_a; /* n_o */
+    const double* shape_b; /* n_o */
+    const double* kinv;    /* nk x nk row-major, nk = dim*m + n_eq: inverse of [[I + rho F'F, A'], [A, 0]] */
+    const double* FtF;     /* m x m: the (block-diagonal, per-axis) block of F'F */
+    const double* b_eq;    /* n_eq */
+    const double* s_min;   /* dim (box bounds, used when has_bounds) */
+    const double* s_max;   /* dim */
+    const double* mu;      /* dim*m sampling mean */
+    const double* draw_L;  /* dim*m x dim*m draw factor u sqrt(s) of svd(Sigma) */
+    const double* line;    /* barn-cost start/goal line: x0 y0 x1 y1 */
+    double v_max;          /* <= 0: no velocity rows */
+    double a_max;          /* <= 0: no acceleration rows */
+    double rho;
+    int32_t has_bounds;
+    int32_t reserved;
+} tro_priest_consts;
+
+typedef struct tro_priest_io {
+    const double* z;       /* N x dm standard normals: samples = mu + z L' (or NULL) */
+    const double* samples; /* N x dm samples when z == NULL */
+    double* samples_out;   /* optional N x dm */
+    double* xi;            /* N x dm projected coefficients */
+    double* scores;        /* N residual scores (solver_priest.py:290-301) */
+    double* history;       /* optional n_inner x N scores after every inner iteration */
+} tro_priest_io;
+
+/* project() (solver_priest.py:242-287): n_inner projection iterations per sample, then
+ * the residual scores of the result.  n_inner = 0 computes residual_scores only;
+ * n_inner = -1 only draws the samples (xi = samples). */
+int tro_priest_project_f64(const tro_priest_dims* dims, const tro_priest_consts* c, const tro_priest_io* io,
+                           void* stream);
+
+/* out[r] = w_barn * barn_cost(traj(xis[index[r]])) + w_score * scores[index[r]]
+ *          + w_penalty * cem_penalty(xis[index[r]])
+ * (solver_priest.py:475-498, :359-361, :396-419, :438-439).  index == NULL: r itself. */
+int tro_priest_cost_f64(const tro_priest_dims* dims, const tro_priest_consts* c, const double* xis,
+                        const int64_t* index, int64_t count, const double* scores, double w_barn,
+                        double w_score, double w_penalty, double* out, void* stream);
+
+/* Distribution refit from elites xis[rows[k]] with costs[k] (solver_priest.py:317-333); updates mu
+ * (dm) and cov (dm x dm) in place.  gamma == 0: plain CEM mean / population covariance (:442-444). */
+int tro_elite_update_f64(const double* xis, int32_t dm, const int64_t* rows, int32_t n_elite,
+                         const double* costs, double sigma, double gamma, double* mu, double* cov, void* stream);
+
 /* out (ncols x n) = rhs (ncols x n) * K^-T, i.e. out[c] = K^-1 rhs[c] for every column c.
  * kinv: n x n row-major.  qpcore.solve_batch with the RHS block [-q ; b]. */
 int tro_kkt_apply_f64(const double* kinv, int32_t n, const double* rhs, int64_t ncols,

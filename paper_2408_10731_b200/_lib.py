@@ -35,6 +35,9 @@ EXPORTS = (
     "tro_topk_stable_f64",
     "tro_topk_workspace_bytes",
     "tro_fastmath_eval",
+    "tro_priest_project_f64",
+    "tro_priest_cost_f64",
+    "tro_elite_update_f64",
     "tro_version",
     "tro_error_string",
 )
@@ -107,6 +110,33 @@ class Alg1State(ctypes.Structure):
     ]
 
 
+class PriestDims(ctypes.Structure):
+    _fields_ = [
+        ("n_samples", c_int64),
+        ("n_p", c_int32),
+        ("m", c_int32),
+        ("dim", c_int32),
+        ("n_obs", c_int32),
+        ("n_eq", c_int32),
+        ("n_inner", c_int32),
+    ]
+
+
+class PriestConsts(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("P", "Pd", "Pdd", "tracks", "shape_a", "shape_b", "kinv", "FtF", "b_eq",
+                                        "s_min", "s_max", "mu", "draw_L", "line")] + [
+        ("v_max", c_double),
+        ("a_max", c_double),
+        ("rho", c_double),
+        ("has_bounds", c_int32),
+        ("reserved", c_int32),
+    ]
+
+
+class PriestIO(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("z", "samples", "samples_out", "xi", "scores", "history")]
+
+
 _lib = None
 
 
@@ -132,6 +162,14 @@ def load() -> ctypes.CDLL:
     lib.tro_topk_stable_f64.restype = c_int32
     lib.tro_topk_workspace_bytes.argtypes = [c_int64, c_int32]
     lib.tro_topk_workspace_bytes.restype = c_int64
+    lib.tro_priest_project_f64.argtypes = [POINTER(PriestDims), POINTER(PriestConsts), POINTER(PriestIO), c_void_p]
+    lib.tro_priest_project_f64.restype = c_int32
+    lib.tro_priest_cost_f64.argtypes = [POINTER(PriestDims), POINTER(PriestConsts), c_void_p, c_void_p, c_int64,
+                                        c_void_p, c_double, c_double, c_double, c_void_p, c_void_p]
+    lib.tro_priest_cost_f64.restype = c_int32
+    lib.tro_elite_update_f64.argtypes = [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_double, c_double,
+                                         c_void_p, c_void_p, c_void_p]
+    lib.tro_elite_update_f64.restype = c_int32
     lib.tro_fastmath_eval.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     lib.tro_fastmath_eval.restype = c_int32
     lib.tro_version.argtypes = []

@@ -114,3 +114,13 @@ def flow3d_batch(n_o: int, members, n_p: int = 100, seed: int = 0, basis: BasisS
     bvals[:, :, 0] = starts
     bvals[:, :, 3] = goals
     return SingleBatch(basis=basis, bvals=bvals, obstacles=obstacles, desired=None)
+
+
+def priest_c4_centers(n_o: int = 100, seed: int = 1) -> np.ndarray:
+    """C4 obstacle centres: default_rng(1), per obstacle cx~U(1.5,10.5),
+    cy~U(-3,3), cz~U(-1.5,1.5); static spheres a = b = 0.4 (+5 cm planning margin)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((n_o, 3))
+    for k in range(n_o):
+        out[k] = (rng.uniform(1.5, 10.5), rng.uniform(-3.0, 3.0), rng.uniform(-1.5, 1.5))
+    return out

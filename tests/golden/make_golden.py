@@ -38,6 +38,7 @@ from trajopt.bench.scenarios import Boundary, Horizon, RobotSpec, Scenario, Scen
 OUT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.abspath(os.path.join(OUT, "..", "..")))
 from paper_2408_10731_b200.scenarios import flow3d_endpoints, flow3d_obstacles  # noqa: E402  (recipe only)
+from paper_2408_10731_b200.scenarios import priest_c4_centers  # noqa: E402  (recipe only)
 
 
 def problem_arrays(prob):
@@ -232,7 +233,89 @@ def make_qp():
     print("qp written")
 
 
+def priest_scenario(n_o, dim=3):
+    """C4 recipe scenario built with the reference's own classes."""
+    centers = priest_c4_centers(n_o)
+    obs = [ScenarioObstacle(a=0.4, b=0.4, center=[float(v) for v in c[:dim]], velocity=[0.0] * dim) for c in centers]
+    start, goal = [0.0] * dim, [12.0] + [0.0] * (dim - 1)
+    return Scenario(kind="random-static", dim=dim, horizon=Horizon(0.0, 10.0, 100),
+                    robot=RobotSpec(shape=[0.0, 0.0], v_max=3.0, a_max=3.0), obstacles=obs,
+                    boundary=Boundary(start=start, goal=goal), seed=1)
+
+
+def make_priest():
+    from trajopt import solver_priest
+    from trajopt.bench.runner import _barn_c1, default_sampling_distribution, priest_setup_from_scenario
+
+    out = {}
+    for tag, dim, n_o, N, n_ce, n_el, rounds in (("p3", 3, 20, 96, 48, 12, 3), ("p2", 2, 12, 64, 32, 8, 2)):
+        sc = priest_scenario(n_o, dim)
+        basis = build_basis(0.0, 10.0, 100, 10)
+        setup = priest_setup_from_scenario(sc, basis)
+        dist = default_sampling_distribution(sc, basis)
+        c1 = _barn_c1(sc)
+        params = solver_priest.PriestParams(n_outer=rounds, n_batch=N, n_constraint_elite=n_ce, n_elite=n_el,
+                                           n_inner=30, seed=0)
+        out[f"{tag}_P"], out[f"{tag}_Pd"], out[f"{tag}_Pdd"] = basis.P, basis.Pdot, basis.Pddot
+        out[f"{tag}_bvals"] = np.stack([bc.values() for bc in setup.boundary])
+        out[f"{tag}_tracks"] = setup.obs_pos
+        out[f"{tag}_a"], out[f"{tag}_b"] = setup.obs_a, setup.obs_b
+        out[f"{tag}_lims"] = np.array([setup.v_max, setup.a_max, setup.rho])
+        out[f"{tag}_smin"], out[f"{tag}_smax"] = setup.s_min, setup.s_max
+        out[f"{tag}_mu0"], out[f"{tag}_sigma0"] = dist.mu, dist.sigma_mat
+        out[f"{tag}_params"] = np.array([N, n_ce, n_el, 30, params.sigma, params.gamma, params.residual_weight])
+        # replicate priest_optimize's loop with the reference's pieces, capturing every intermediate
+        rng = np.random.default_rng(params.seed)
+        rng_z = np.random.default_rng(params.seed)
+        mu, sig = dist.mu.copy(), dist.sigma_mat.copy()
+        for r in range(rounds):
+            z = rng_z.standard_normal((N, mu.size))
+            samples = rng.multivariate_normal(mu, sig, size=N, method="svd")
+            u, sv, _ = np.linalg.svd(sig)
+            assert np.array_equal(samples, mu + z @ (u * np.sqrt(sv)).T), "multivariate_normal split not bit-exact"
+            projected = solver_priest.project(setup, samples, n_inner=params.n_inner)
+            residuals = np.array([p.residual for p in projected])
+            keep = np.argsort(residuals, kind="stable")[: params.n_constraint_elite]
+            for i in keep:
+                p = projected[i]
+                p.aug_cost = float(c1(p.trajectory)) + params.residual_weight * p.residual
+            scored = sorted((projected[i] for i in keep), key=lambda p: p.aug_cost)
+            elites = scored[: params.n_elite]
+            elite_idx = np.array([next(k for k in range(N) if projected[k] is e) for e in elites])
+            out[f"{tag}_r{r}_mu_in"], out[f"{tag}_r{r}_sigma_in"] = mu.copy(), sig.copy()
+            mu, sig = solver_priest.update_distribution(mu, sig, np.stack([p.projected for p in elites]),
+                                                        np.array([p.aug_cost for p in elites]), params.sigma,
+                                                        params.gamma)
+            out[f"{tag}_r{r}_z"] = z
+            out[f"{tag}_r{r}_xi"] = np.stack([p.projected for p in projected])
+            out[f"{tag}_r{r}_scores"] = residuals
+            out[f"{tag}_r{r}_keep"] = keep
+            out[f"{tag}_r{r}_aug"] = np.array([projected[i].aug_cost for i in keep])
+            out[f"{tag}_r{r}_elites"] = elite_idx
+            out[f"{tag}_r{r}_mu"], out[f"{tag}_r{r}_sigma"] = mu, sig
+        res = solver_priest.priest_optimize(setup, c1, dist, params)
+        assert np.array_equal(res.mu, mu) and np.array_equal(res.sigma_mat, sig), "replicate diverged"
+        out[f"{tag}_best_xi"] = res.best.projected
+        out[f"{tag}_best_hist"] = np.array([[h["best_aug_cost"], h["best_residual"], h["min_residual"]]
+                                            for h in res.history])
+        # CEM baseline on the same setup
+        cparams = solver_priest.CemParams(n_batch=N, n_elite=n_el, iterations=2, seed=3)
+        cres = solver_priest.cem_optimize(setup, c1, dist, cparams)
+        rng_z = np.random.default_rng(cparams.seed)
+        out[f"{tag}_cem_z"] = np.stack([rng_z.standard_normal((N, dist.mu.size)) for _ in range(2)])
+        out[f"{tag}_cem_mu"], out[f"{tag}_cem_sigma"] = cres.mu, cres.sigma_mat
+        out[f"{tag}_cem_best"] = np.array([cres.best_cost])
+        out[f"{tag}_cem_hist"] = np.array([[h["best_cost"], h["mean_cost"]] for h in cres.history])
+        out[f"{tag}_cem_penalty0"] = solver_priest._cem_penalty(setup, out[f"{tag}_r0_xi"])
+    np.savez_compressed(os.path.join(OUT, "priest.npz"), **out)
+    print("priest written")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[f"make_{name}"]()
+        sys.exit(0)
     make_qp()
     make_c1()
     make_corridor()
