@@ -39,7 +39,10 @@ CONFIGS = {
     "c5": (100, 131072, 200, "C5: 131072 traj x 100 dyn. ellipsoids x n_p 100, 200 AM its (3-D)"),
     "c2": (50, 1024, 200, "C2: 1024 traj x 50 dyn. ellipsoids x n_p 100, 200 AM its (3-D)"),
     "c1": (10, 1, 100, "C1: 1 quadrotor x 10 static ellipsoids x n_p 100, 100 AM its (3-D)"),
+    "c4": (100, 16384, 30, "C4: PRIEST CEM, 16384 samples, 8192 constraint elites, top-256, 100 static "
+                           "ellipsoids, n_p 100, 30 inner its, 10 rounds (3-D)"),
 }
+C4_ROUNDS, C4_NCE, C4_NEL = 10, 8192, 256
 WORDS_3D = 9  # persistent words per (member, obstacle, sample): alpha beta lx ly lz lca lsa lcb lsb
 
 
@@ -58,6 +61,174 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+def c4_problem():
+    """C4 scene: 100 static spheres a = b = 0.4 (+5 cm) from default_rng(1),
+    start (0,0,0) -> goal (12,0,0), v_max = a_max = 3, workspace box padded by 4, rho = 1."""
+    from paper_2408_10731_b200 import scenarios, solver_priest
+    from paper_2408_10731_b200.basis import AxisBoundary, build_basis, straight_line_coeffs
+
+    basis = build_basis(0.0, 10.0, 100, 10)
+    centers = scenarios.priest_c4_centers(100)
+    specs = [scenarios.ObstacleSpec(0.4, 0.4, c, np.zeros(3)) for c in centers]
+    obs = scenarios.tracks_on_grid(specs, basis.grid.timestamps)
+    start, goal = np.zeros(3), np.array([12.0, 0.0, 0.0])
+    pts = np.vstack([start, goal, centers])
+    setup = solver_priest.ProjectionSetup(basis, tuple(AxisBoundary(p0=start[k], p1=goal[k]) for k in range(3)), obs,
+                                          3.0, 3.0, pts.min(axis=0) - 4.0, pts.max(axis=0) + 4.0, 1.0)
+    mean = straight_line_coeffs(basis, start, goal).ravel()
+    dist = solver_priest.SamplingDistribution(mean, np.eye(mean.size) * 0.6**2)
+    return setup, dist, solver_priest.BarnCost(start, goal)
+
+
+def fp64_peak_tflops():
+    import ctypes
+
+    import torch
+
+    from paper_2408_10731_b200 import _lib
+
+    lib = _lib.load()
+    scratch = torch.zeros(256, dtype=torch.float64, device="cuda")
+    blocks = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count * 8
+    iters, best = 20000, 0.0
+    for k in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(lib.tro_fp64_fma_probe(iters, blocks, scratch.data_ptr(), ctypes.c_void_p(_lib.stream_handle())),
+                   "fp64 probe")
+        b.record()
+        torch.cuda.synchronize()
+        if k:
+            best = max(best, blocks * 256 * iters * 16 / (a.elapsed_time(b) / 1e3) / 1e12)
+    return best
+
+
+def run_c4(args):
+    import torch
+
+    from paper_2408_10731_b200 import solver_priest as SP
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    setup, dist, c1 = c4_problem()
+    n_o, N, n_inner, desc = CONFIGS["c4"]
+    params = SP.PriestParams(n_outer=C4_ROUNDS, n_batch=N, n_constraint_elite=C4_NCE, n_elite=C4_NEL,
+                             n_inner=n_inner, seed=0)
+    rng = np.random.default_rng(params.seed)
+    z_host = np.stack([rng.standard_normal((N, dist.mu.size)) for _ in range(C4_ROUNDS)])  # the sampler's stream
+    z_dev = torch.as_tensor(z_host, device="cuda")
+    z_pin = torch.as_tensor(z_host).pin_memory()
+    for _ in range(args.warmup):
+        SP.priest_optimize(setup, c1, dist, params, z_rounds=z_dev)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        res = SP.priest_optimize(setup, c1, dist, params, z_rounds=z_dev)
+    b.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_s = a.elapsed_time(b) / 1e3 / args.steps
+    # e2e: standard normals from pinned host memory each round, results back on the host
+    a.record()
+    for _ in range(args.steps):
+        res = SP.priest_optimize(setup, c1, dist, params, z_rounds=z_pin)
+    b.record()
+    torch.cuda.synchronize()
+    e2e_s = a.elapsed_time(b) / 1e3 / args.steps
+    # dominant kernel (projection) alone, CUDA events on its stream
+    d = setup.device()
+    d["L"].copy_(torch.as_tensor(SP._draw_factor(dist.sigma_mat)))
+    d["mu"].copy_(torch.as_tensor(dist.mu))
+    SP._run_project(setup, z=z_dev[0], n_inner=n_inner)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(3):
+        SP._run_project(setup, z=z_dev[0], n_inner=n_inner)
+    b.record()
+    torch.cuda.synchronize()
+    kern_s = a.elapsed_time(b) / 1e3 / 3
+    flops = 32.0 * N * n_o * 100 * n_inner  # SURVEY.md §8(d): 32 flop per sample-obstacle-timestep-inner-it
+    peak = fp64_peak_tflops()
+    value = N * n_inner * C4_ROUNDS / step_s
+    line = {
+        "metric": "sample-inner-iterations/sec (PRIEST projection, CEM rounds)",
+        "value": value, "unit": "sample-inner-it/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "ms_per_round": step_s * 1e3 / C4_ROUNDS, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded C4 scene, numpy standard normals of the reference sampler)",
+        "config": {"workload": desc, "samples": N, "n_obs": n_o, "n_p": 100, "n_inner": n_inner,
+                   "rounds": C4_ROUNDS, "constraint_elites": C4_NCE, "elites": C4_NEL, "l2": "on-chip (FP-bound)"},
+        "roofline": {"bound": "fp64", "achieved": flops / kern_s / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops / kern_s / 1e12 / peak, "traffic": None,
+                     "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)",
+                     "kernel": "tro_priest_project_f64 (priest_project_kernel<3>)",
+                     "avg_launch_ms": kern_s * 1e3, "algorithmic_flops_per_launch": flops},
+        "clocks": clk,
+        "e2e": {"value": N * n_inner * C4_ROUNDS / e2e_s, "unit": "sample-inner-it/s",
+                "h2d_bytes_per_step": int(z_host.nbytes), "d2h_bytes_per_step": int(8 * (33 * 33 + 33 + 3) * C4_ROUNDS)},
+        "gpu_launches": args.steps * C4_ROUNDS * 5,
+        "result": {"best_aug_cost": res.history[-1]["best_aug_cost"], "best_residual": res.best.residual},
+    }
+    if not args.no_cpu_baseline:
+        v, info = cpu_reference_c4()
+        line["cpu_baseline"] = {"value": v, "unit": "sample-inner-it/s", "cores": info["cores"], "kind": "port",
+                                "sample": info["sample"]}
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_project_chunk(args):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    lo, hi, n_inner = args
+    from oracle import priest as OP
+
+    setup, dist, _ = c4_problem_host()
+    rng = np.random.default_rng(0)
+    z = rng.standard_normal((16384, dist[0].size))[lo:hi]
+    samples = dist[0] + z @ OP.draw_transform(dist[0], dist[1]).T
+    t0 = time.perf_counter()
+    OP.project(setup, samples, n_inner)
+    return time.perf_counter() - t0
+
+
+def c4_problem_host():
+    """The C4 scene as oracle arrays (no GPU needed)."""
+    from oracle import priest as OP
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200.basis import build_basis, straight_line_coeffs
+
+    basis = build_basis(0.0, 10.0, 100, 10)
+    centers = scenarios.priest_c4_centers(100)
+    tracks = np.repeat(centers[:, None, :], 100, axis=1)
+    start, goal = np.zeros(3), np.array([12.0, 0.0, 0.0])
+    pts = np.vstack([start, goal, centers])
+    bvals = np.zeros((3, 6))
+    bvals[:, 0], bvals[:, 3] = start, goal
+    st = OP.make_setup(basis.P, basis.Pdot, basis.Pddot, bvals, tracks, np.full(100, 0.45), np.full(100, 0.45), 3.0,
+                       3.0, pts.min(axis=0) - 4.0, pts.max(axis=0) + 4.0, 1.0)
+    mean = straight_line_coeffs(basis, start, goal).ravel()
+    return st, (mean, np.eye(mean.size) * 0.36), None
+
+
+def cpu_reference_c4(procs=None, per_proc=8, n_inner=30):
+    """Reference CPU projection (oracle port of solver_priest.project, bit-exact with the reference
+    on the golden rounds) on a bounded sample: per_proc samples per core, all cores."""
+    import multiprocessing as mp
+
+    procs = procs or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    tasks = [(k * per_proc, (k + 1) * per_proc, n_inner) for k in range(procs)]
+    with ctx.Pool(procs) as pool:
+        pool.map(_oracle_project_chunk, [(0, 1, 1)] * procs)
+        t0 = time.perf_counter()
+        pool.map(_oracle_project_chunk, tasks, chunksize=1)
+        wall = time.perf_counter() - t0
+    n = procs * per_proc
+    return n * n_inner / wall, {"cores": procs, "sample": f"{n} C4 samples x {n_inner} inner its (one round's "
+                                                          f"projection slice), oracle port, wall {wall:.1f}s"}
 
 
 def measured_peaks():
@@ -361,6 +532,22 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if args.config == "c4":
+        vals = []
+        for k in range(args.warmup + args.steps):
+            v, info = cpu_reference_c4()
+            if k >= args.warmup:
+                vals.append(v)
+        value = statistics.mean(vals)
+        print(json.dumps({"impl": "reference", "metric": "sample-inner-iterations/sec (PRIEST projection, CEM rounds)",
+                          "value": value, "unit": "sample-inner-it/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic", "config": {"workload": CONFIGS["c4"][3]},
+                          "cpu_baseline": {"value": value, "unit": "sample-inner-it/s", "cores": info["cores"],
+                                           "kind": "port", "sample": info["sample"]},
+                          "e2e": {"value": value, "unit": "sample-inner-it/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
     n_o, members_total, n_iter, desc = CONFIGS[args.config]
     procs = os.cpu_count() or 1
     sample = procs if args.config != "c1" else 1
@@ -397,6 +584,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c4":
+        run_c4(args)
     else:
         run_b200(args)
 

@@ -205,6 +205,9 @@ int64_t tro_topk_workspace_bytes(int64_t n, int32_t k);
  * 8 min(max(1, sqrt(x)), 1e6). */
 int tro_fastmath_eval(int32_t fn, const double* x, const double* y, int64_t n, double* out, void* stream);
 
+/* FP64 FMA throughput probe: blocks x 256 threads x iters x 8 DFMA (2 flops each). */
+int tro_fp64_fma_probe(int64_t iters, int32_t blocks, double* scratch, void* stream);
+
 int32_t tro_version(void);
 const char* tro_error_string(int32_t code);
 

@@ -38,6 +38,7 @@ EXPORTS = (
     "tro_priest_project_f64",
     "tro_priest_cost_f64",
     "tro_elite_update_f64",
+    "tro_fp64_fma_probe",
     "tro_version",
     "tro_error_string",
 )
@@ -172,6 +173,8 @@ def load() -> ctypes.CDLL:
     lib.tro_elite_update_f64.restype = c_int32
     lib.tro_fastmath_eval.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     lib.tro_fastmath_eval.restype = c_int32
+    lib.tro_fp64_fma_probe.argtypes = [c_int64, c_int32, c_void_p, c_void_p]
+    lib.tro_fp64_fma_probe.restype = c_int32
     lib.tro_version.argtypes = []
     lib.tro_version.restype = c_int32
     lib.tro_error_string.argtypes = [c_int32]
