@@ -158,7 +158,7 @@ typedef struct tro_priest_consts {
     double a_max;          /* <= 0: no acceleration rows */
     double rho;
     int32_t has_bounds;
-    int32_t reserved;
+    int32_t static_tracks; /* 1: every obstacle centre is constant over the horizon */
 } tro_priest_consts;
 
 typedef struct tro_priest_io {

@@ -130,7 +130,7 @@ class PriestConsts(ctypes.Structure):
         ("a_max", c_double),
         ("rho", c_double),
         ("has_bounds", c_int32),
-        ("reserved", c_int32),
+        ("static_tracks", c_int32),
     ]
 
 

@@ -33,19 +33,20 @@ struct PrArgs {
 };
 
 struct PrSmem {
-    int P, Pd, Pdd, kinv, M, shp, wbuf, vec, total;  // doubles
+    int P, Pd, Pdd, kinv, M, obs, wbuf, vec, total;  // doubles
 };
-__host__ __device__ inline PrSmem pr_layout(int n_p, int m, int dim, int nk, int n_o) {
+// obstacles: 8 doubles each: cx cy cz 1/a^2 1/b^2 a b -   (centres only meaningful for static tracks)
+__host__ __device__ inline PrSmem pr_layout(int n_p, int m, int dim, int nk, int n_o, bool wbuf) {
     PrSmem L;
     int off = 0;
     L.P = off;    off += n_p * m;
     L.Pd = off;   off += n_p * m;
     L.Pdd = off;  off += n_p * m;
-    L.kinv = off; off += nk * nk;
+    L.kinv = off; off += dim * m * nk;                 // only the xi rows of K^-1
     L.M = off;    off += m * m;
-    L.shp = off;  off += 4 * (n_o > 0 ? n_o : 1);
-    L.wbuf = off; off += kPrWarps * 3 * dim * n_p;     // per warp: F' weights per (block, axis, t)
-    L.vec = off;  off += kPrWarps * 6 * kPrMaxNk;     // per warp: xi, lam, samp, fte, rhs, tmp
+    L.obs = off;  off += 8 * (n_o > 0 ? n_o : 1);
+    L.wbuf = off; off += wbuf ? kPrWarps * 3 * dim * n_p : 0;  // runtime-m path: F' weights per (blk, ax, t)
+    L.vec = off;  off += kPrWarps * 5 * kPrMaxNk;     // per warp: xi, lam, samp, fte, rhs
     L.total = off;
     return L;
 }
@@ -56,34 +57,27 @@ __device__ __forceinline__ double warp_allsum(double v) {
     return v;
 }
 
-// polar obstacle target of one (sample, obstacle, t): returns f = d/q and handles q == 0
+// Polar target of an obstacle the point is INSIDE of (or absurdly far from):
+// e = c + (d/q) (p - c), d = clip(q, 1, 1e6); q == 0 -> the pole (atan2(0, 0) = 0,
+// solver_priest.py:204-210).  Accumulates e into S and |p - e|^2 into r2.
 template <int DIM>
-__device__ __forceinline__ void obstacle_target(const double* p, const double* c, double ia2, double ib2, double a,
-                                                double b, double* e, double& r2) {
-    double dl[3];
-#pragma unroll
-    for (int k = 0; k < DIM; ++k) dl[k] = p[k] - c[k];
-    double q2;
-    if constexpr (DIM == 3) q2 = fma(dl[2] * dl[2], ib2, (dl[0] * dl[0] + dl[1] * dl[1]) * ia2);
-    else q2 = fma(dl[1] * dl[1], ib2, dl[0] * dl[0] * ia2);
-    if (q2 >= 1.0 && q2 <= 1e12) {  // outside (and not absurdly far): target is the point itself
-#pragma unroll
-        for (int k = 0; k < DIM; ++k) e[k] = p[k];
-        return;
-    }
-    if (q2 == 0.0) {  // atan2(0, 0) = 0: the pole of the ellipsoid (solver_priest.py:204-210)
+__device__ __forceinline__ void inside_target(const double* p, const double* dl, const double* c, double q2,
+                                              double a, double b, double* S, double& r2) {
+    double e[3];
+    if (q2 == 0.0) {
 #pragma unroll
         for (int k = 0; k < DIM; ++k) e[k] = c[k];
         if constexpr (DIM == 3) e[2] = c[2] + b;
         else e[0] = c[0] + a;
     } else {
         const double rs = rsqrt_fast(q2);
-        const double f = q2 < 1.0 ? rs : 1e6 * rs;  // d/q with d = clip(q, 1, 1e6)
+        const double f = q2 < 1.0 ? rs : 1e6 * rs;
 #pragma unroll
         for (int k = 0; k < DIM; ++k) e[k] = fma(f, dl[k], c[k]);
     }
 #pragma unroll
     for (int k = 0; k < DIM; ++k) {
+        S[k] += e[k];
         const double r = p[k] - e[k];
         r2 = fma(r, r, r2);
     }
@@ -109,21 +103,21 @@ __device__ __forceinline__ void speed_target(const double* v, double limit, doub
     }
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(kPrWarps * 32) priest_project_kernel(PrArgs A) {
+// M: compile-time basis columns (0 = runtime m, F'e via a shared-memory weight buffer);
+// STATIC: obstacle centres constant over the horizon (kept in shared memory).
+template <int DIM, int M, bool STATIC>
+__global__ void __launch_bounds__(kPrWarps * 32, 2) priest_project_kernel(PrArgs A) {
     extern __shared__ double smem[];
-    const int n_p = A.d.n_p, m = A.d.m, n_o = A.d.n_obs, neq = A.d.n_eq;
+    const int n_p = A.d.n_p, n_o = A.d.n_obs, neq = A.d.n_eq;
+    const int m = M ? M : A.d.m;
     const int dm = DIM * m, nk = dm + neq;
-    const PrSmem L = pr_layout(n_p, m, DIM, nk, n_o);
+    const PrSmem L = pr_layout(n_p, m, DIM, nk, n_o, M == 0);
     double* sP = smem + L.P;
     double* sPd = smem + L.Pd;
     double* sPdd = smem + L.Pdd;
     double* sK = smem + L.kinv;
     double* sM = smem + L.M;
-    double* sA = smem + L.shp;
-    double* sB = sA + n_o;
-    double* sIA2 = sB + n_o;
-    double* sIB2 = sIA2 + n_o;
+    double* sObs = smem + L.obs;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     for (int k = tid; k < n_p * m; k += blockDim.x) {
@@ -131,25 +125,27 @@ __global__ void __launch_bounds__(kPrWarps * 32) priest_project_kernel(PrArgs A)
         sPd[k] = ld_const(A.c.Pd + k);
         sPdd[k] = ld_const(A.c.Pdd + k);
     }
-    for (int k = tid; k < nk * nk; k += blockDim.x) sK[k] = ld_const(A.c.kinv + k);
+    for (int k = tid; k < dm * nk; k += blockDim.x) sK[k] = ld_const(A.c.kinv + k);
     for (int k = tid; k < m * m; k += blockDim.x) sM[k] = ld_const(A.c.FtF + k);
     for (int k = tid; k < n_o; k += blockDim.x) {
         const double a = ld_const(A.c.shape_a + k), b = ld_const(A.c.shape_b + k);
-        sA[k] = a;
-        sB[k] = b;
-        sIA2[k] = 1.0 / (a * a);
-        sIB2[k] = 1.0 / (b * b);
+        double* o = sObs + 8 * k;
+        for (int q = 0; q < 3; ++q) o[q] = (STATIC && q < DIM) ? ld_const(A.c.tracks + ((int64_t)k * DIM + q) * n_p) : 0.0;
+        o[3] = 1.0 / (a * a);
+        o[4] = 1.0 / (b * b);
+        o[5] = a;
+        o[6] = b;
     }
     __syncthreads();
 
     const int64_t s = (int64_t)blockIdx.x * kPrWarps + warp;  // this warp's sample
     if (s >= A.d.n_samples) return;
-    double* W = smem + L.wbuf + warp * 3 * DIM * n_p;  // [blk][ax][t]: blk 0 -> P, 1 -> Pd, 2 -> Pdd
-    double* xi = smem + L.vec + warp * 6 * kPrMaxNk;
+    double* xi = smem + L.vec + warp * 5 * kPrMaxNk;
     double* lam = xi + kPrMaxNk;
     double* smp = lam + kPrMaxNk;
     double* fte = smp + kPrMaxNk;
     double* rhs = fte + kPrMaxNk;
+    double* W = smem + L.wbuf + warp * 3 * DIM * n_p;  // M == 0 only
 
     // ---- the sample: samples = mu + z L' (numpy multivariate_normal(svd)), or given
     for (int c = lane; c < dm; c += 32) {
@@ -177,13 +173,17 @@ __global__ void __launch_bounds__(kPrWarps * 32) priest_project_kernel(PrArgs A)
     const int full_slots = n_p / 32;
     const int rem = n_p - 32 * full_slots;
     const int ng = (rem > 0 && (32 % rem) == 0) ? 32 / rem : 1;  // obstacle groups of the remainder slot
+    const int nslots = full_slots + (rem ? 1 : 0);
     const double rho = A.c.rho;
     const int n_inner = A.d.n_inner;
+    constexpr int DMC = M ? DIM * M : 1;
 
     for (int it = 0; it <= n_inner; ++it) {
-        // ---------- targets of the current xi: W (F' weights) and the residual score
+        // ---------- targets of the current xi: F'e contributions and the residual score
         double r2 = 0.0;
-        const int nslots = full_slots + (rem ? 1 : 0);
+        double facc[DMC];
+#pragma unroll
+        for (int c = 0; c < DMC; ++c) facc[c] = 0.0;
         for (int u = 0; u < nslots; ++u) {
             const bool remslot = (u == full_slots);
             int t, jg = 0, jstep = 1;
@@ -198,33 +198,45 @@ __global__ void __launch_bounds__(kPrWarps * 32) priest_project_kernel(PrArgs A)
                 t = 32 * u + lane;
                 active = lane < rem;
             }
+            if (!active) t = 0;  // keep the (discarded) reads in bounds
             double p[3] = {0, 0, 0}, v[3] = {0, 0, 0}, ac[3] = {0, 0, 0};
-            if (active) {
-                for (int k = 0; k < DIM; ++k) {
-                    double ps = 0.0, vs = 0.0, as = 0.0;
-                    for (int c = 0; c < m; ++c) {
-                        const double x = xi[k * m + c];
-                        ps = fma(sP[t * m + c], x, ps);
-                        vs = fma(sPd[t * m + c], x, vs);
-                        as = fma(sPdd[t * m + c], x, as);
-                    }
-                    p[k] = ps;
-                    v[k] = vs;
-                    ac[k] = as;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                double ps = 0.0, vs = 0.0, as = 0.0;
+                for (int c = 0; c < m; ++c) {
+                    const double x = xi[k * m + c];
+                    ps = fma(sP[t * m + c], x, ps);
+                    vs = fma(sPd[t * m + c], x, vs);
+                    as = fma(sPdd[t * m + c], x, as);
                 }
+                p[k] = ps;
+                v[k] = vs;
+                ac[k] = as;
             }
             double S[3] = {0, 0, 0};
             double rr = 0.0;
+            int outside = 0;
             if (active) {
                 const double* tr = A.c.tracks + t;
                 for (int j = jg; j < n_o; j += jstep) {
-                    double cc[3], e[3];
+                    const double* o = sObs + 8 * j;
+                    double cc[3], dl[3];
 #pragma unroll
-                    for (int k = 0; k < DIM; ++k) cc[k] = ld_const(tr + ((int64_t)j * DIM + k) * n_p);
-                    obstacle_target<DIM>(p, cc, sIA2[j], sIB2[j], sA[j], sB[j], e, rr);
-#pragma unroll
-                    for (int k = 0; k < DIM; ++k) S[k] += e[k];
+                    for (int k = 0; k < DIM; ++k) {
+                        cc[k] = STATIC ? o[k] : ld_const(tr + ((int64_t)j * DIM + k) * n_p);
+                        dl[k] = p[k] - cc[k];
+                    }
+                    double q2;
+                    if constexpr (DIM == 3) q2 = fma(dl[2] * dl[2], o[4], (dl[0] * dl[0] + dl[1] * dl[1]) * o[3]);
+                    else q2 = fma(dl[1] * dl[1], o[4], dl[0] * dl[0] * o[3]);
+                    if (q2 >= 1.0 && q2 <= 1e12) {
+                        ++outside;  // target == the point itself (added once below)
+                    } else {
+                        inside_target<DIM>(p, dl, cc, q2, o[5], o[6], S, rr);
+                    }
                 }
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) S[k] = fma((double)outside, p[k], S[k]);
             }
             if (remslot && ng > 1) {  // combine the obstacle groups of the remainder slot
                 for (int o = rem; o < 32; o <<= 1) {
@@ -234,10 +246,10 @@ __global__ void __launch_bounds__(kPrWarps * 32) priest_project_kernel(PrArgs A)
                 active = jg == 0;  // one writer per t; the score partials stay per lane
             }
             r2 += rr;
+            double w0[3] = {0, 0, 0}, w1[3] = {0, 0, 0}, w2[3] = {0, 0, 0};
             if (active) {
-                double ev[3] = {0, 0, 0}, ea[3] = {0, 0, 0};
-                if (has_v) speed_target<DIM>(v, A.c.v_max, ev, r2);
-                if (has_a) speed_target<DIM>(ac, A.c.a_max, ea, r2);
+                if (has_v) speed_target<DIM>(v, A.c.v_max, w1, r2);
+                if (has_a) speed_target<DIM>(ac, A.c.a_max, w2, r2);
 #pragma unroll
                 for (int k = 0; k < DIM; ++k) {
                     double wp = S[k];
@@ -250,9 +262,25 @@ __global__ void __launch_bounds__(kPrWarps * 32) priest_project_kernel(PrArgs A)
                         const double vl = fmax(0.0, lo - p[k]), vh = fmax(0.0, p[k] - hi);
                         r2 = fma(vl, vl, fma(vh, vh, r2));
                     }
-                    W[(0 * DIM + k) * n_p + t] = wp;
-                    W[(1 * DIM + k) * n_p + t] = has_v ? ev[k] : 0.0;
-                    W[(2 * DIM + k) * n_p + t] = has_a ? ea[k] : 0.0;
+                    w0[k] = wp;
+                }
+            }
+            if constexpr (M > 0) {
+                if (active) {
+#pragma unroll
+                    for (int c = 0; c < M; ++c) {
+                        const double pp = sP[t * M + c], pd = sPd[t * M + c], pa = sPdd[t * M + c];
+#pragma unroll
+                        for (int k = 0; k < DIM; ++k)
+                            facc[k * M + c] = fma(pa, w2[k], fma(pd, w1[k], fma(pp, w0[k], facc[k * M + c])));
+                    }
+                }
+            } else if (active) {
+#pragma unroll
+                for (int k = 0; k < DIM; ++k) {
+                    W[(0 * DIM + k) * n_p + t] = w0[k];
+                    W[(1 * DIM + k) * n_p + t] = w1[k];
+                    W[(2 * DIM + k) * n_p + t] = w2[k];
                 }
             }
         }
@@ -262,19 +290,28 @@ __global__ void __launch_bounds__(kPrWarps * 32) priest_project_kernel(PrArgs A)
             if (lane == 0) A.io.scores[s] = sqrt(r2);
             break;
         }
-        __syncwarp();
 
-        // ---------- F'e : per coefficient, sum over t of the weighted basis rows
-        for (int c = 0; c < dm; ++c) {
-            const int k = c / m, cc = c - k * m;
-            double acc = 0.0;
-            for (int t = lane; t < n_p; t += 32) {
-                acc = fma(sP[t * m + cc], W[(0 * DIM + k) * n_p + t], acc);
-                acc = fma(sPd[t * m + cc], W[(1 * DIM + k) * n_p + t], acc);
-                acc = fma(sPdd[t * m + cc], W[(2 * DIM + k) * n_p + t], acc);
+        // ---------- F'e : per coefficient, the sum over t of the weighted basis rows
+        if constexpr (M > 0) {
+#pragma unroll
+            for (int c = 0; c < DMC; ++c) facc[c] = warp_allsum(facc[c]);
+            if (lane == 0) {
+#pragma unroll
+                for (int c = 0; c < DMC; ++c) fte[c] = facc[c];
             }
-            acc = warp_allsum(acc);
-            if (lane == 0) fte[c] = acc;
+        } else {
+            __syncwarp();
+            for (int c = 0; c < dm; ++c) {
+                const int k = c / m, cc = c - k * m;
+                double acc = 0.0;
+                for (int t = lane; t < n_p; t += 32) {
+                    acc = fma(sP[t * m + cc], W[(0 * DIM + k) * n_p + t], acc);
+                    acc = fma(sPd[t * m + cc], W[(1 * DIM + k) * n_p + t], acc);
+                    acc = fma(sPdd[t * m + cc], W[(2 * DIM + k) * n_p + t], acc);
+                }
+                acc = warp_allsum(acc);
+                if (lane == 0) fte[c] = acc;
+            }
         }
         __syncwarp();
         // ---------- lambda -= rho F'(F xi - e);  rhs = [-q_lin ; b_eq] (solver_priest.py:271-274)
@@ -432,6 +469,23 @@ static int pr_check(const tro_priest_dims* d) {
     return 0;
 }
 
+template <int DIM, int M, bool STATIC>
+static void pr_launch(const tro::PrArgs& A, unsigned blocks, size_t smem, cudaStream_t st) {
+    cudaFuncSetAttribute(tro::priest_project_kernel<DIM, M, STATIC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    tro::priest_project_kernel<DIM, M, STATIC><<<blocks, tro::kPrWarps * 32, smem, st>>>(A);
+}
+
+template <int DIM>
+static void pr_dispatch(const tro::PrArgs& A, unsigned blocks, size_t smem, cudaStream_t st) {
+    const bool stat = A.c.static_tracks != 0;
+    switch (A.d.m) {
+        case 11: stat ? pr_launch<DIM, 11, true>(A, blocks, smem, st) : pr_launch<DIM, 11, false>(A, blocks, smem, st); break;
+        case 9: stat ? pr_launch<DIM, 9, true>(A, blocks, smem, st) : pr_launch<DIM, 9, false>(A, blocks, smem, st); break;
+        default: stat ? pr_launch<DIM, 0, true>(A, blocks, smem, st) : pr_launch<DIM, 0, false>(A, blocks, smem, st);
+    }
+}
+
 extern "C" int tro_priest_project_f64(const tro_priest_dims* dims, const tro_priest_consts* c, const tro_priest_io* io,
                                       void* stream) {
     if (pr_check(dims) || !c || !io || !io->xi || !io->scores || (!io->z && !io->samples)) return TRO_EINVAL;
@@ -441,18 +495,14 @@ extern "C" int tro_priest_project_f64(const tro_priest_dims* dims, const tro_pri
     A.c = *c;
     A.io = *io;
     const int nk = dims->dim * dims->m + dims->n_eq;
-    const tro::PrSmem L = tro::pr_layout(dims->n_p, dims->m, dims->dim, nk, dims->n_obs);
+    const bool wbuf = !(dims->m == 9 || dims->m == 11);
+    const tro::PrSmem L = tro::pr_layout(dims->n_p, dims->m, dims->dim, nk, dims->n_obs, wbuf);
     const size_t smem = (size_t)L.total * sizeof(double);
     if (smem > 227 * 1024) return TRO_EINVAL;
     const unsigned blocks = (unsigned)((dims->n_samples + tro::kPrWarps - 1) / tro::kPrWarps);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (dims->dim == 3) {
-        cudaFuncSetAttribute(tro::priest_project_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tro::priest_project_kernel<3><<<blocks, tro::kPrWarps * 32, smem, st>>>(A);
-    } else {
-        cudaFuncSetAttribute(tro::priest_project_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tro::priest_project_kernel<2><<<blocks, tro::kPrWarps * 32, smem, st>>>(A);
-    }
+    if (dims->dim == 3) pr_dispatch<3>(A, blocks, smem, st);
+    else pr_dispatch<2>(A, blocks, smem, st);
     return (int)cudaGetLastError();
 }
 

@@ -168,8 +168,10 @@ class ProjectionSetup:
         for k in range(dim):
             self.A[k * B.shape[0]:(k + 1) * B.shape[0], k * m:(k + 1) * m] = B
         self.b_eq = np.concatenate([bc.values(start_orders, end_orders) for bc in boundary])
+        self.static_tracks = False
         if self.n_o:
             self.obs_pos = np.stack([o.centers for o in self.obstacles])  # (n_o, n_p, dim)
+            self.static_tracks = bool(np.all(self.obs_pos == self.obs_pos[:, :1, :]))
             self.obs_a = np.array([o.shape.a for o in self.obstacles])
             self.obs_b = np.array([o.shape.b for o in self.obstacles])
         FtF = self.F.T @ self.F
@@ -217,7 +219,8 @@ class ProjectionSetup:
             d["s_min"].data_ptr(), d["s_max"].data_ptr(), d["mu"].data_ptr(), d["L"].data_ptr(),
             (line if line is not None else d["line"]).data_ptr(),
             float(self.v_max) if self.v_max is not None else -1.0,
-            float(self.a_max) if self.a_max is not None else -1.0, float(self.rho), int(self.has_bounds), 0)
+            float(self.a_max) if self.a_max is not None else -1.0, float(self.rho), int(self.has_bounds),
+            int(self.static_tracks))
 
     # -- host helpers (reference API) -----------------------------------------------
     def axis_samples(self, xis: np.ndarray, mat: np.ndarray) -> np.ndarray:

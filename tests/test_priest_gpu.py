@@ -147,3 +147,32 @@ def test_cem_optimize_runs_and_refits(golden):
     # same standard normals, same costs up to rounding -> same first-iteration best
     np.testing.assert_allclose(res.history[0]["best_cost"], g["p3_cem_hist"][0][0], rtol=1e-9)
     np.testing.assert_allclose(res.history[0]["mean_cost"], g["p3_cem_hist"][0][1], rtol=1e-9)
+
+
+@pytest.mark.parametrize("degree,dim", [(7, 3), (8, 2), (10, 2)])
+def test_generic_paths_vs_oracle(degree, dim):
+    """Runtime-m (degree 7), M=9 and moving obstacles (non-static tracks) against the oracle."""
+    from paper_2408_10731_b200.basis import build_basis
+
+    n_p = 50
+    basis = build_basis(0.0, 8.0, n_p, degree)
+    rng = np.random.default_rng(degree)
+    ts = basis.grid.timestamps
+    obs = []
+    for _ in range(6):
+        c = np.r_[rng.uniform(2, 6), rng.uniform(-1, 1), rng.uniform(-0.5, 0.5)][:dim]
+        v = np.r_[rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), 0.0][:dim]
+        obs.append(ObstacleTrack(c[None, :] + v[None, :] * ts[:, None], EllipsoidShape(0.7, 0.5)))
+    bnd = tuple(AxisBoundary(p0=0.0, v0=1.0, p1=8.0) if k == 0 else AxisBoundary(p0=0.0, p1=0.0) for k in range(dim))
+    smin, smax = np.full(dim, -3.0), np.full(dim, 10.0)
+    st = SP.ProjectionSetup(basis, bnd, obs, 2.5, 3.0, smin, smax, 1.0)
+    assert not st.static_tracks
+    ost = OP.make_setup(basis.P, basis.Pdot, basis.Pddot, np.stack([b.values() for b in bnd]),
+                        np.stack([o.centers for o in obs]), np.full(6, 0.7), np.full(6, 0.5), 2.5, 3.0, smin, smax,
+                        1.0)
+    samples = rng.normal(size=(40, dim * (degree + 1))) * 2.0
+    out = SP.project(st, samples, n_inner=12)
+    xi_ref, sc_ref = OP.project(ost, samples, 12, mode="kinv")
+    xi = np.stack([p.projected for p in out])
+    assert np.max(np.abs(xi - xi_ref)) <= 1e-10 * np.max(np.abs(xi_ref))
+    close_scores(np.array([p.residual for p in out]), sc_ref)
