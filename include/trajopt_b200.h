@@ -188,6 +188,68 @@ int tro_priest_cost_f64(const tro_priest_dims* dims, const tro_priest_consts* c,
 int tro_elite_update_f64(const double* xis, int32_t dm, const int64_t* rows, int32_t n_elite,
                          const double* costs, double sigma, double gamma, double* mu, double* cov, void* stream);
 
+/* ------------------------------------------------------------------ joint multi-agent (Alg. 5) */
+typedef struct tro_ma_dims {
+    int32_t n_problems; /* B independent joint problems sharing the pair structure */
+    int32_t n_agents;   /* N_a (2 * N_a <= 32) */
+    int32_t n_pairs;    /* N_a (N_a - 1) / 2 agent pairs, then N_a per static sphere */
+    int32_t n_static;   /* static spheres per problem */
+    int32_t n_p;
+    int32_t m;          /* basis columns (9 or 11) */
+    int32_t n_eq;       /* 6 N_a boundary rows per axis */
+    int32_t n_levels;   /* rho levels (one K^-1 each) */
+} tro_ma_dims;
+
+typedef struct tro_ma_consts {
+    const double* P;         /* n_p x m */
+    const double* kinv;      /* n_levels x nk x nk, nk = N_a m + n_eq: inverse of [[Q + rho A_fo'A_fo, A_eq'], [A_eq, 0]] */
+    const double* level_rho; /* n_levels */
+    const int32_t* pair_i;   /* n_pairs first agent */
+    const int32_t* pair_j;   /* n_pairs second agent, -1 for a static partner */
+    const int32_t* pair_s;   /* n_pairs static sphere index (static pairs) */
+    const double* pair_a;    /* n_pairs inflated semi-axes (solver_multiagent.py:108-130) */
+    const double* pair_b;
+    const int32_t* inc_ptr;  /* N_a + 1: CSR incidence lists */
+    const int32_t* inc_pair; /* p (agent is the first member, +) or -(p + 1) (second member, -) */
+    const double* b_eq;      /* B x 3 x n_eq boundary values per axis */
+    const double* statics;   /* B x n_static x 3 sphere centres (NULL if n_static == 0) */
+    const double* line_u;    /* m: straight-line init coefficients (see tro_alg1_consts) */
+    const double* line_v;
+} tro_ma_consts;
+
+typedef struct tro_ma_state {
+    double* state;    /* B x n_p x 3 x n_pairs: multipliers (pairs fastest) */
+    double* xi;       /* B x 3 x N_a m */
+    double* sums;     /* B x 2 x N_a x 3 x m: agent-contracted (recon + statics, lambda) for the next RHS */
+    double* ring;     /* B x 2 * stall_window residual norms */
+    double* res_norm; /* B */
+    double* res_max;  /* B */
+    double* hist;     /* B x max_hist x 3 (norm, max, rho) or NULL */
+    int32_t* level;
+    int32_t* iteration;
+    int32_t* last_change;
+    int32_t* n_hist;
+    int32_t* status;     /* TRO_CONVERGED */
+    double* export_d;    /* optional B x n_p x n_pairs: d of the latest iterate */
+    double* export_ab;   /* optional 2 planes of B x n_p x n_pairs: alpha, beta */
+} tro_ma_state;
+
+typedef struct tro_ma_params {
+    double tol_norm;          /* JointParams.tol_norm */
+    double stall_improvement; /* JointParams.stall_improvement */
+    int32_t stall_window;     /* JointParams.stall_window */
+    int32_t max_iter;         /* JointParams.max_iter (the level schedule needs it) */
+    int32_t max_hist;         /* history capacity (0: none) */
+    int32_t reserved;
+} tro_ma_params;
+
+/* mode 2: cold start (_init_state, solver_multiagent.py:228-249) + the first RHS sums;
+ * mode 1: prime the RHS sums of a given state (lambda in `state`, d / alpha / beta read from the
+ *         export planes) for a warm start;
+ * mode 0: one _iterate + residual + level schedule (solver_multiagent.py:252-335). */
+int tro_ma_run(int32_t mode, const tro_ma_dims* dims, const tro_ma_consts* c, const tro_ma_state* s,
+               const tro_ma_params* p, void* stream);
+
 /* out (ncols x n) = rhs (ncols x n) * K^-T, i.e. out[c] = K^-1 rhs[c] for every column c.
  * kinv: n x n row-major.  qpcore.solve_batch with the RHS block [-q ; b]. */
 int tro_kkt_apply_f64(const double* kinv, int32_t n, const double* rhs, int64_t ncols,

@@ -39,6 +39,7 @@ EXPORTS = (
     "tro_priest_cost_f64",
     "tro_elite_update_f64",
     "tro_fp64_fma_probe",
+    "tro_ma_run",
     "tro_version",
     "tro_error_string",
 )
@@ -138,6 +139,26 @@ class PriestIO(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in ("z", "samples", "samples_out", "xi", "scores", "history")]
 
 
+class MaDims(ctypes.Structure):
+    _fields_ = [(n, c_int32) for n in ("n_problems", "n_agents", "n_pairs", "n_static", "n_p", "m", "n_eq",
+                                       "n_levels")]
+
+
+class MaConsts(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("P", "kinv", "level_rho", "pair_i", "pair_j", "pair_s", "pair_a", "pair_b",
+                                        "inc_ptr", "inc_pair", "b_eq", "statics", "line_u", "line_v")]
+
+
+class MaState(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("state", "xi", "sums", "ring", "res_norm", "res_max", "hist", "level",
+                                        "iteration", "last_change", "n_hist", "status", "export_d", "export_ab")]
+
+
+class MaParams(ctypes.Structure):
+    _fields_ = [("tol_norm", c_double), ("stall_improvement", c_double), ("stall_window", c_int32),
+                ("max_iter", c_int32), ("max_hist", c_int32), ("reserved", c_int32)]
+
+
 _lib = None
 
 
@@ -173,6 +194,9 @@ def load() -> ctypes.CDLL:
     lib.tro_elite_update_f64.restype = c_int32
     lib.tro_fastmath_eval.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     lib.tro_fastmath_eval.restype = c_int32
+    lib.tro_ma_run.argtypes = [c_int32, POINTER(MaDims), POINTER(MaConsts), POINTER(MaState), POINTER(MaParams),
+                               c_void_p]
+    lib.tro_ma_run.restype = c_int32
     lib.tro_fp64_fma_probe.argtypes = [c_int64, c_int32, c_void_p, c_void_p]
     lib.tro_fp64_fma_probe.restype = c_int32
     lib.tro_version.argtypes = []

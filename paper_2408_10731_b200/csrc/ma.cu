@@ -1,0 +1,369 @@
+// Batched joint multi-agent AM iteration (arXiv 2408.10731, Alg. 5) for sm_100a.
+//
+// One CTA owns one joint problem (N_a agents, n_pairs = N_a(N_a-1)/2 agent pairs +
+// N_a per static sphere) for one iteration of solve_joint (solver_multiagent.py:252-335):
+//   prologue : the per-axis QP, xi = K_L^-1 [ rho A'B - A'C ; b_eq ], from the agent-
+//              contracted sums B (recon + statics) and C (lambda) the previous launch left
+//              behind (b_fo = recon - lambda/rho + statics, :266-268), then every agent's
+//              positions on the grid (shared memory);
+//   body     : warps walk the horizon, lanes the pairs (state[i][t][w][p], pairs fastest:
+//              coalesced).  Per (pair, t): alpha/beta of the new offsets in trig-free form
+//              (unit vectors), the multiplier-shifted d (:285-293), residual and multiplier
+//              ascent (:295-296).  Only the multipliers persist: alpha, beta come from the
+//              positions and d only feeds the next RHS, which is folded into the sums here.
+//   epilogue : each pair's recon and lambda are scattered to its two agents through an
+//              incidence list in a fixed order, contracted with P (per-lane accumulators),
+//              reduced across warps; residual norm / max; history; the staged level
+//              schedule (:313-335).
+// Deterministic: every reduction has a fixed order, so a problem's bits do not depend on
+// the batch or the GPU count.
+#include "common.cuh"
+#include "fastmath.cuh"
+#include "../../include/trajopt_b200.h"
+
+namespace tro {
+
+constexpr int kMaWarps = 8;
+constexpr int kMaMaxAgents = 32;
+constexpr int kMaMaxRing = 64;
+
+struct MaArgs {
+    tro_ma_dims d;
+    tro_ma_consts c;
+    tro_ma_state s;
+    tro_ma_params p;
+};
+
+struct MaSmem {
+    int P, pos, scratch, red, sumin, rhs, xi, warp, total;  // doubles
+};
+__host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs, int n_eq) {
+    MaSmem L;
+    int off = 0;
+    L.P = off;       off += n_p * m;
+    L.pos = off;     off += n_p * n_a * 3;               // positions [t][agent][axis]
+    L.scratch = off; off += kMaWarps * n_pairs * 6;      // per warp: (recon+static, lambda) per pair
+    // cross-warp reduction of the contracted sums reuses pos + scratch
+    const int red_need = kMaWarps * 2 * n_a * 3 * m;
+    const int have = off - L.pos;
+    L.red = L.pos;
+    if (red_need > have) off += red_need - have;
+    L.sumin = off;   off += 2 * n_a * 3 * m;
+    L.rhs = off;     off += 3 * (n_a * m + n_eq);
+    L.xi = off;      off += 3 * n_a * m;
+    L.warp = off;    off += 2 * kMaWarps;
+    L.total = off;
+    return L;
+}
+
+// cos/sin of atan2(y, x) as a unit vector, numpy's signed-zero conventions
+__device__ __forceinline__ void unit2(double x, double y, double* c, double* s) {
+    const double h2 = fma(x, x, y * y);
+    if (h2 > 0.0) {
+        const double r = rsqrt_fast(h2);
+        *c = x * r;
+        *s = y * r;
+    } else {
+        *c = flip_sign(1.0, sign_bit(x));
+        *s = flip_sign(0.0, sign_bit(y));
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode) {
+    // mode 0: iteration; 1: prime (sums of a given state: lambda in `state`, d / alpha / beta in
+    // the export planes); 2: cold init (straight lines, angles, d = 1, lambda = 0) + sums
+    const bool init = mode == 2;
+    const bool prime = mode == 1;
+    extern __shared__ double smem[];
+    const int i = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_p = A.d.n_p, n_a = A.d.n_agents, np_ = A.d.n_pairs, neq = A.d.n_eq;
+    const int m = M ? M : A.d.m;
+    const int nv = n_a * m, nk = nv + neq;
+    const MaSmem L = ma_layout(n_p, m, n_a, np_, neq);
+    double* sP = smem + L.P;
+    double* sPos = smem + L.pos;
+    double* sScr = smem + L.scratch + warp * np_ * 6;
+    double* sRed = smem + L.red;
+    double* sSumIn = smem + L.sumin;
+    double* sRhs = smem + L.rhs;
+    double* sXi = smem + L.xi;
+    double* sWarp = smem + L.warp;
+
+    const int status0 = A.s.status[i];
+    if (mode == 0 && (status0 & TRO_CONVERGED)) return;
+    const int level = A.s.level[i];
+    const double rho = A.c.level_rho[level];
+    for (int k = tid; k < n_p * m; k += blockDim.x) sP[k] = ld_const(A.c.P + k);
+    double* xg = A.s.xi + (int64_t)i * 3 * nv;
+    const double* bg = A.c.b_eq + (int64_t)i * 3 * neq;
+    if (init) {
+        // straight-line coefficients per agent and axis (solver_multiagent.py:230-235)
+        for (int k = tid; k < 3 * nv; k += blockDim.x) {
+            const int ax = k / nv, r = k - ax * nv, a = r / m, cc = r - a * m;
+            const double p0 = bg[ax * neq + 6 * a + 0], p1 = bg[ax * neq + 6 * a + 3];
+            const double v = A.c.line_u[cc] * p0 + A.c.line_v[cc] * (p1 - p0);
+            sXi[k] = v;
+            xg[k] = v;
+        }
+    } else if (prime) {
+        for (int k = tid; k < 3 * nv; k += blockDim.x) sXi[k] = xg[k];
+    } else {
+        const double* sg = A.s.sums + (int64_t)i * 2 * n_a * 3 * m;
+        for (int k = tid; k < 2 * n_a * 3 * m; k += blockDim.x) sSumIn[k] = sg[k];
+        __syncthreads();
+        // rhs_k = [ -q_k ; b_eq_k ],  -q = rho B - C  (contracted per agent: [a][k][c])
+        for (int k = tid; k < 3 * nk; k += blockDim.x) {
+            const int ax = k / nk, r = k - ax * nk;
+            double v;
+            if (r < nv) {
+                const int a = r / m, cc = r - a * m;
+                const int o = (a * 3 + ax) * m + cc;
+                v = rho * sSumIn[o] - sSumIn[n_a * 3 * m + o];
+            } else {
+                v = bg[ax * neq + (r - nv)];
+            }
+            sRhs[k] = v;
+        }
+        __syncthreads();
+        const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
+        for (int o = tid; o < 3 * nv; o += blockDim.x) {
+            const int ax = o / nv, r = o - ax * nv;
+            const double* Kr = Kl + (int64_t)r * nk;
+            const double* x = sRhs + ax * nk;
+            double acc = 0.0;
+            for (int q = 0; q < nk; ++q) acc = fma(ld_const(Kr + q), x[q], acc);
+            sXi[o] = acc;
+            xg[o] = acc;
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < n_p * n_a * 3; k += blockDim.x) {
+        const int t = k / (n_a * 3), r = k - t * n_a * 3, a = r / 3, ax = r - a * 3;
+        double acc = 0.0;
+        for (int cc = 0; cc < m; ++cc) acc = fma(sP[t * m + cc], sXi[ax * nv + a * m + cc], acc);
+        sPos[k] = acc;
+    }
+    __syncthreads();
+
+    // ---------------- element pass: warps over t, lanes over pairs
+    constexpr int MA = M ? M : 1;
+    double acc[3 * MA];  // per-lane contracted sums of one (agent, B|C) task  (M > 0)
+#pragma unroll
+    for (int c = 0; c < 3 * MA; ++c) acc[c] = 0.0;
+    const int tasks = 2 * n_a;
+    double sumsq = 0.0, mx = 0.0;
+    const int64_t rowW = 3 * (int64_t)np_;  // state[i][t][w][p], W = 3
+    double* st = A.s.state + (int64_t)i * n_p * rowW;
+    const double* statics = A.c.statics ? A.c.statics + (int64_t)i * A.d.n_static * 3 : nullptr;
+    const int64_t nplane = (int64_t)A.d.n_problems * n_p * np_;
+
+    for (int t = warp; t < n_p; t += kMaWarps) {
+        const double* pt = sPos + t * n_a * 3;
+        double* srow = st + t * rowW;
+        for (int p = lane; p < np_; p += 32) {
+            const int pi = A.c.pair_i[p], pj = A.c.pair_j[p];
+            const double pa = A.c.pair_a[p], pb = A.c.pair_b[p];
+            double cen[3];
+            if (pj >= 0) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) cen[k] = pt[pj * 3 + k];
+            } else {
+                const int sidx = A.c.pair_s[p];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) cen[k] = statics[sidx * 3 + k];
+            }
+            const double dx = pt[pi * 3 + 0] - cen[0], dy = pt[pi * 3 + 1] - cen[1], dz = pt[pi * 3 + 2] - cen[2];
+            // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) as unit vectors (:280-282)
+            double ca, sa, cb, sb;
+            const int64_t ex_i = ((int64_t)i * n_p + t) * np_ + p;
+            if (prime) {  // the given state's angles
+                sincos(A.s.export_ab[ex_i], &sa, &ca);
+                sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
+            } else {
+                unit2(dx, dy, &ca, &sa);
+                const double ipa = 1.0 / pa;
+                unit2(dz / pb, hypot(dx * ipa, dy * ipa), &cb, &sb);
+            }
+            double lx, ly, lz, d;
+            if (prime) {
+                lx = srow[p];
+                ly = srow[np_ + p];
+                lz = srow[2 * np_ + p];
+                d = A.s.export_d[ex_i];
+            } else if (init) {
+                lx = ly = lz = 0.0;
+                d = 1.0;
+            } else {
+                lx = ld_stream(srow + p);
+                ly = ld_stream(srow + np_ + p);
+                lz = ld_stream(srow + 2 * np_ + p);
+                // multiplier-shifted single-variable quadratic in d, clamped at [1, 1e6] (:285-293)
+                const double ir = 1.0 / rho;
+                const double num = pa * sb * (ca * (dx + lx * ir) + sa * (dy + ly * ir)) + pb * cb * (dz + lz * ir);
+                const double den = pa * pa * (sb * sb) + pb * pb * (cb * cb);
+                d = fmin(fmax(num / den, 1.0), 1e6);
+            }
+            const double rx = pa * d * sb * ca, ry = pa * d * sb * sa, rz = pb * d * cb;
+            if (prime) {
+            } else if (!init) {
+                const double ex = dx - rx, ey = dy - ry, ez = dz - rz;  // residual (:203-208)
+                sumsq = fma(ex, ex, fma(ey, ey, fma(ez, ez, sumsq)));
+                mx = fmax(mx, fmax(fabs(ex), fmax(fabs(ey), fabs(ez))));
+                lx = fma(rho, ex, lx);  // lambda += rho * res (:296)
+                ly = fma(rho, ey, ly);
+                lz = fma(rho, ez, lz);
+                st_stream(srow + p, lx);
+                st_stream(srow + np_ + p, ly);
+                st_stream(srow + 2 * np_ + p, lz);
+            } else {
+                srow[p] = 0.0;
+                srow[np_ + p] = 0.0;
+                srow[2 * np_ + p] = 0.0;
+            }
+            if (A.s.export_d && !prime) {
+                const int64_t e = ex_i;
+                A.s.export_d[e] = d;
+                A.s.export_ab[e] = atan2(sa, ca);           // the reference's stored angles
+                A.s.export_ab[nplane + e] = atan2(sb, cb);
+            }
+            // next RHS: recon (+ static centre) and lambda, scattered to the pair's agents below
+            double* sc = sScr + p * 6;
+            sc[0] = rx + (pj < 0 ? cen[0] : 0.0);
+            sc[1] = ry + (pj < 0 ? cen[1] : 0.0);
+            sc[2] = rz + (pj < 0 ? cen[2] : 0.0);
+            sc[3] = lx;
+            sc[4] = ly;
+            sc[5] = lz;
+        }
+        __syncwarp();
+        // per-agent signed incidence sums (fixed order), contracted with P[t][:]
+        for (int task = lane; task < tasks; task += 32) {
+            const int a = task % n_a, which = task / n_a;  // which 0: B (recon), 1: C (lambda)
+            double v[3] = {0.0, 0.0, 0.0};
+            for (int q = A.c.inc_ptr[a]; q < A.c.inc_ptr[a + 1]; ++q) {
+                const int pe = A.c.inc_pair[q];
+                const double sgn = pe >= 0 ? 1.0 : -1.0;
+                const double* sc = sScr + (pe >= 0 ? pe : -pe - 1) * 6 + 3 * which;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) v[k] = fma(sgn, sc[k], v[k]);
+            }
+            if constexpr (M > 0) {
+                if (task < 32) {  // M > 0 path keeps one task per lane (tasks <= 32)
+#pragma unroll
+                    for (int cc = 0; cc < M; ++cc) {
+                        const double pv = sP[t * M + cc];
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) acc[k * M + cc] = fma(pv, v[k], acc[k * M + cc]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+
+    // ---------------- reductions
+    sumsq = warp_sum(sumsq);
+    mx = warp_max(mx);
+    if (lane == 0) {
+        sWarp[warp] = sumsq;
+        sWarp[kMaWarps + warp] = mx;
+    }
+    __syncthreads();  // positions / scratch are dead from here: reuse them as the reduction buffer
+    const int per_task = 3 * m;
+    if constexpr (M > 0) {
+        if (lane < tasks) {
+            double* r = sRed + (warp * tasks + lane) * per_task;
+#pragma unroll
+            for (int c = 0; c < 3 * M; ++c) r[c] = acc[c];  // [k][c]
+        }
+    }
+    __syncthreads();
+    double* sg = A.s.sums + (int64_t)i * 2 * n_a * 3 * m;  // [which][a][k][c]
+    for (int o = tid; o < tasks * per_task; o += blockDim.x) {
+        const int task = o / per_task, r = o - task * per_task;
+        double v = 0.0;
+        for (int w = 0; w < kMaWarps; ++w) v += sRed[(w * tasks + task) * per_task + r];
+        const int a = task % n_a, which = task / n_a, k = r / m, cc = r - k * m;
+        sg[(int64_t)which * n_a * 3 * m + (a * 3 + k) * m + cc] = v;
+    }
+    if (tid == 0 && mode == 0) {
+        double ss = 0.0, mm = 0.0;
+        for (int w = 0; w < kMaWarps; ++w) {
+            ss += sWarp[w];
+            mm = fmax(mm, sWarp[kMaWarps + w]);
+        }
+        if (ss != ss) mm = ss;
+        const double nrm = sqrt(ss);
+        A.s.res_norm[i] = nrm;
+        A.s.res_max[i] = mm;
+        const int it = A.s.iteration[i] + 1;  // _iterate: state.iteration += 1
+        A.s.iteration[i] = it;
+        const int nh = A.s.n_hist[i];
+        if (A.s.hist && nh < A.p.max_hist) {
+            double* h = A.s.hist + ((int64_t)i * A.p.max_hist + nh) * 3;
+            h[0] = nrm;
+            h[1] = mm;
+            h[2] = rho;
+        }
+        const int n = nh + 1;
+        A.s.n_hist[i] = n;
+        const int w = A.p.stall_window, w2 = 2 * w;
+        double* ring = A.s.ring + (int64_t)i * w2;
+        ring[(n - 1) % w2] = nrm;
+        if (nrm <= A.p.tol_norm) {  // solver_multiagent.py:319-321
+            A.s.status[i] = status0 | TRO_CONVERGED;
+        } else {
+            const int nl = A.d.n_levels;
+            const int mi = A.p.max_iter > 1 ? A.p.max_iter : 1;
+            int scheduled = (int)((double)it * nl / (double)mi);  // :325
+            if (scheduled > nl - 1) scheduled = nl - 1;
+            bool stalled = false;
+            const int lc = A.s.last_change[i];
+            if (n >= w2 && it - lc >= w) {  // :327-331 (np.mean of <8 values: sequential sum / w)
+                double sr = 0.0, sp = 0.0;
+                for (int k = 0; k < w; ++k) sr += ring[(n - w + k) % w2];
+                for (int k = 0; k < w; ++k) sp += ring[(n - w2 + k) % w2];
+                const double recent = sr / (double)w, previous = sp / (double)w;
+                stalled = previous > 0.0 && (previous - recent) / previous < A.p.stall_improvement;
+            }
+            const int target = scheduled > (stalled ? level + 1 : level) ? scheduled : (stalled ? level + 1 : level);
+            if (target > level && level < nl - 1) {  // :332-335
+                A.s.level[i] = target < nl - 1 ? target : nl - 1;
+                A.s.last_change[i] = it;
+            }
+        }
+    }
+}
+
+}  // namespace tro
+
+extern "C" int tro_ma_run(int32_t mode, const tro_ma_dims* d, const tro_ma_consts* c, const tro_ma_state* s,
+                          const tro_ma_params* p, void* stream) {
+    if (!d || !c || !s || !p || mode < 0 || mode > 2) return TRO_EINVAL;
+    if (mode == 1 && (!s->export_d || !s->export_ab)) return TRO_EINVAL;
+    if (d->n_agents < 1 || d->n_agents > tro::kMaMaxAgents || d->n_p < 2 || d->m < 1 || d->n_pairs < 1 ||
+        d->n_levels < 1 || p->stall_window < 1 || 2 * p->stall_window > tro::kMaMaxRing)
+        return TRO_EINVAL;
+    if (d->m != 11 && d->m != 9) return TRO_EINVAL;  // per-lane register accumulators are compile-time sized
+    if (2 * d->n_agents > 32) return TRO_EINVAL;
+    if (d->n_problems <= 0) return 0;
+    tro::MaArgs A;
+    A.d = *d;
+    A.c = *c;
+    A.s = *s;
+    A.p = *p;
+    const tro::MaSmem L = tro::ma_layout(d->n_p, d->m, d->n_agents, d->n_pairs, d->n_eq);
+    const size_t smem = (size_t)L.total * sizeof(double);
+    if (smem > 227 * 1024) return TRO_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (d->m == 11) {
+        cudaFuncSetAttribute(tro::ma_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tro::ma_kernel<11><<<d->n_problems, tro::kMaWarps * 32, smem, st>>>(A, mode);
+    } else {
+        cudaFuncSetAttribute(tro::ma_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tro::ma_kernel<9><<<d->n_problems, tro::kMaWarps * 32, smem, st>>>(A, mode);
+    }
+    return (int)cudaGetLastError();
+}

@@ -124,3 +124,31 @@ def priest_c4_centers(n_o: int = 100, seed: int = 1) -> np.ndarray:
     for k in range(n_o):
         out[k] = (rng.uniform(1.5, 10.5), rng.uniform(-3.0, 3.0), rng.uniform(-1.5, 1.5))
     return out
+
+
+def square_antipodal(n_agents: int = 8, side: float = 6.0, radius: float = 0.4, seed: int = 0, z: float = 1.0,
+                     jitter: float = 0.05):
+    """(starts, goals) of the reference's "square-antipodal" roster (bench/scenarios.py:248-288 and
+    agent_boundaries :130-143): agents evenly spaced on the square's perimeter with jitter, goals
+    antipodal through the layout centre."""
+    rng = np.random.default_rng(seed)
+    perim = 4.0 * side
+    starts = []
+    for k in range(n_agents):
+        s = (k / n_agents) * perim
+        edge, off = int(s // side), s % side
+        if edge == 0:
+            p = (-side / 2 + off, -side / 2)
+        elif edge == 1:
+            p = (side / 2, -side / 2 + off)
+        elif edge == 2:
+            p = (side / 2 - off, side / 2)
+        else:
+            p = (-side / 2, side / 2 - off)
+        starts.append(np.array([p[0], p[1], z]) + np.array([rng.uniform(-jitter, jitter), rng.uniform(-jitter, jitter),
+                                                            0.0]))
+    centre = np.array([0.0, 0.0, z])
+    goal0 = 2.0 * centre - starts[0]
+    mid = 0.5 * (starts[0] + goal0)
+    goals = [goal0] + [2.0 * mid - s for s in starts[1:]]
+    return np.stack(starts), np.stack(goals)

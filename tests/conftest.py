@@ -1,9 +1,20 @@
 import os
 import sys
 
-import numpy as np
-import pytest
+# golden vectors were produced with one BLAS thread; multi-threaded GEMV/GEMM blocking changes
+# the last bits of large products (and chaotic runs amplify them)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
 
+import numpy as np  # noqa: E402
+import pytest  # noqa: E402
+
+try:
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)
+except ImportError:  # pragma: no cover
+    pass
 ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -243,6 +243,62 @@ def priest_scenario(n_o, dim=3):
                     boundary=Boundary(start=start, goal=goal), seed=1)
 
 
+def make_multiagent():
+    from trajopt import solver_multiagent as MA
+    from trajopt.basis import AxisBoundary
+    from trajopt.bench.runner import multiagent_problem_from_scenario
+    from trajopt.geometry import EllipsoidShape
+
+    basis = build_basis(0.0, 10.0, 100, 10)
+    out = {"P": basis.P, "Pd": basis.Pdot, "Pdd": basis.Pddot}
+    # (1) random roster, 6 agents + 1 static sphere: stable enough for a long free run
+    rng = np.random.default_rng(7)
+    bnds = []
+    for _ in range(6):
+        s0 = np.r_[rng.uniform(-4, 4), rng.uniform(-4, 4), rng.uniform(0.5, 1.5)]
+        g0 = np.r_[rng.uniform(-4, 4), rng.uniform(-4, 4), rng.uniform(0.5, 1.5)]
+        bnds.append(tuple(AxisBoundary(p0=float(s0[k]), p1=float(g0[k])) for k in range(3)))
+    statics = [MA.StaticSphere(center=np.array([0.3, -0.2, 1.0]), radius=0.6)]
+    prob = MA.MultiAgentProblem(basis=basis, boundaries=bnds, agent_shape=EllipsoidShape(0.3, 0.45),
+                                static_obstacles=statics)
+    params = MA.JointParams(max_iter=60, rho_final=1e3)
+    sol = MA.solve_joint(prob, params)
+    out["r6_bvals"] = np.array([[bc.values() for bc in b] for b in bnds])  # (n_a, 3, 6)
+    out["r6_static"] = np.array([[0.3, -0.2, 1.0, 0.6]])
+    out["r6_hist"] = np.array([[h["norm"], h["max_abs"], h["rho"]] for h in sol.residual_history])
+    out["r6_xi"] = sol.state.xi
+    out["r6_meta"] = np.array([sol.iterations, int(sol.converged), sol.residual_norm, sol.residual_max,
+                               sol.min_pair_distance])
+    struct = MA._JointStructure(prob, params)
+    st = MA._init_state(prob, struct)
+    # teacher-forced pairs at k = 0 -> 1 and 12 -> 13 (level schedule included)
+    for k in range(13):
+        if k in (0, 12):
+            out[f"r6_k{k}_xi"], out[f"r6_k{k}_d"] = st.xi.copy(), st.d.copy()
+            out[f"r6_k{k}_alpha"], out[f"r6_k{k}_beta"] = st.alpha.copy(), st.beta.copy()
+            out[f"r6_k{k}_lam"] = st.lam.copy()
+            out[f"r6_k{k}_meta"] = np.array([st.level, st.iteration])
+        MA._iterate(st, struct)
+        if k in (0, 12):
+            out[f"r6_k{k + 1}_xi"], out[f"r6_k{k + 1}_d"] = st.xi.copy(), st.d.copy()
+            out[f"r6_k{k + 1}_lam"] = st.lam.copy()
+            out[f"r6_k{k + 1}_alpha"], out[f"r6_k{k + 1}_beta"] = st.alpha.copy(), st.beta.copy()
+    # (2) C3 recipe problem (16 agents, square-antipodal, agent (0.3, 0.45), rho_final 1e3): short window
+    sc = gen_scenario("square-antipodal", {"n_agents": 16, "agent_radius": 0.3, "side": 8.0}, seed=0)
+    prob16 = multiagent_problem_from_scenario(sc, basis)
+    prob16.agent_shape = EllipsoidShape(0.3, 0.45)
+    p16 = MA.JointParams(max_iter=25, rho_final=1e3)
+    sol16 = MA.solve_joint(prob16, p16)
+    out["a16_bvals"] = np.array([[bc.values() for bc in b] for b in prob16.boundaries])
+    out["a16_hist"] = np.array([[h["norm"], h["max_abs"], h["rho"]] for h in sol16.residual_history])
+    out["a16_xi"] = sol16.state.xi
+    struct16 = MA._JointStructure(prob16, p16)
+    st16 = MA._init_state(prob16, struct16)
+    out["a16_init_alpha"], out["a16_init_beta"] = st16.alpha, st16.beta
+    np.savez_compressed(os.path.join(OUT, "multiagent.npz"), **out)
+    print("multiagent written; r6 iterations", sol.iterations, "converged", sol.converged)
+
+
 def make_priest():
     from trajopt import solver_priest
     from trajopt.bench.runner import _barn_c1, default_sampling_distribution, priest_setup_from_scenario
