@@ -43,6 +43,8 @@ CONFIGS = {
                            "ellipsoids, n_p 100, 30 inner its, 10 rounds (3-D)"),
 }
 C4_ROUNDS, C4_NCE, C4_NEL = 10, 8192, 256
+CONFIGS["c3"] = (16, 4096, 200, "C3: 4096 joint problems x 16 quadrotors (120 pairs, ellipsoid 0.3/0.45) x n_p 100, "
+                                "200 iterations (rho_final 1e3, tol 0: fixed work)")
 WORDS_3D = 9  # persistent words per (member, obstacle, sample): alpha beta lx ly lz lca lsa lcb lsb
 
 
@@ -178,6 +180,155 @@ def run_c4(args):
         line["cpu_baseline"] = {"value": v, "unit": "sample-inner-it/s", "cores": info["cores"], "kind": "port",
                                 "sample": info["sample"]}
     print(json.dumps(line), flush=True)
+
+
+def c3_problems(lo, hi):
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200 import solver_multiagent as MA
+    from paper_2408_10731_b200.basis import AxisBoundary, build_basis
+    from paper_2408_10731_b200.geometry import EllipsoidShape
+
+    b = build_basis(0.0, 10.0, 100, 10)
+    probs = []
+    for s in range(lo, hi):
+        starts, goals = scenarios.square_antipodal(16, 8.0, 0.3, seed=s)
+        bnds = [tuple(AxisBoundary(p0=float(starts[i, k]), p1=float(goals[i, k])) for k in range(3))
+                for i in range(16)]
+        probs.append(MA.MultiAgentProblem(basis=b, boundaries=bnds, agent_shape=EllipsoidShape(0.3, 0.45)))
+    return probs
+
+
+def run_c3(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_10731_b200 import solver_multiagent as MA
+    from paper_2408_10731_b200.distributed import gather_summaries, shard_range, shard_summary
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n_a, total, n_iter, desc = CONFIGS["c3"]
+    if args.members:
+        total = args.members
+    lo, hi = shard_range(total, rank, world)
+    probs = c3_problems(lo, hi)
+    params = MA.JointParams(max_iter=n_iter, rho_final=1e3, tol_norm=0.0)
+    struct = MA._Structure(probs[0], params)
+    b_eq = np.stack([MA._b_eq(p) for p in probs])
+    eng = MA.MaEngine(struct, b_eq, None, params)
+    stream = torch.cuda.current_stream()
+
+    def solve():
+        eng.reset()
+        eng.init()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.run(n_iter, use_graph=True, check_every=0)
+        e1.record(stream)
+        return e0, e1
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    runs = []
+    a.record(stream)
+    for _ in range(args.steps):
+        runs.append(solve())
+        if world > 1:
+            gather_summaries(shard_summary(eng.res_max, eng.res_norm, eng.res_norm <= 0.01, lo))
+    b.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    t = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    launch_s = statistics.mean(x.elapsed_time(y) for x, y in runs) / 1e3 / n_iter
+    n_pairs = struct.n_pairs
+    alg_bytes = 2 * 3 * n_pairs * 100 * 8 * (hi - lo)  # 3 persistent words (the multipliers) per pair-sample
+    peak, peak_src = measured_peaks()
+    # e2e: boundary values from pinned host memory each step, xi / residuals back
+    bv_pin = torch.as_tensor(b_eq).pin_memory()
+    xi_pin = torch.empty(eng.xi.shape, dtype=torch.float64).pin_memory()
+    r_pin = torch.empty((2, eng.B), dtype=torch.float64).pin_memory()
+    a.record(stream)
+    for _ in range(args.steps):
+        eng.b_eq.copy_(bv_pin, non_blocking=True)
+        solve()
+        xi_pin.copy_(eng.xi, non_blocking=True)
+        r_pin[0].copy_(eng.res_norm, non_blocking=True)
+        r_pin[1].copy_(eng.res_max, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    line = {
+        "metric": "problem-iterations/sec (joint 16-agent problems x iterations)",
+        "value": total * n_iter * args.steps / elapsed, "unit": "problem-it/s",
+        "agent_traj_it_per_s": 16 * total * n_iter * args.steps / elapsed,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (square-antipodal rosters, seeds 0..4095)",
+        "config": {"workload": desc, "problems": total, "agents": 16, "pairs": n_pairs, "n_p": 100,
+                   "iterations": n_iter, "parallelism": f"problem-shard x{world}", "l2": "state >> L2"},
+        "roofline": {"bound": "hbm", "achieved": alg_bytes / launch_s / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": alg_bytes / launch_s / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "tro_ma_run (ma_kernel<11>)", "avg_launch_ms": launch_s * 1e3,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "note": "3 words (multipliers) per pair-sample; SURVEY §8(d) counts 4 (d stored): d only "
+                             "feeds the next RHS and is folded into the agent sums"},
+        "clocks": clk,
+        "e2e": {"value": total * n_iter * args.steps / float(te.item()), "unit": "problem-it/s",
+                "h2d_bytes_per_step": int(b_eq.nbytes), "d2h_bytes_per_step": int(xi_pin.numel() * 8 + r_pin.numel() * 8)},
+        "gpu_launches": args.steps * (n_iter + 1),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, info = cpu_reference_c3()
+        line["cpu_baseline"] = {"value": v, "unit": "problem-it/s", "cores": info["cores"], "kind": "port",
+                                "sample": info["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _oracle_ma_solve(args):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    seed, n_iter = args
+    from oracle import multiagent as OM
+    from paper_2408_10731_b200 import solver_multiagent as MA
+
+    prob = c3_problems(seed, seed + 1)[0]
+    b = prob.basis
+    st = OM.make_structure(b.P, b.Pdot, b.Pddot, 16, 0.3, 0.45, rho_final=1e3)
+    t0 = time.perf_counter()
+    OM.solve(st, OM.Problem(b_eq=MA._b_eq(prob), statics=np.zeros((0, 3))), b.P, max_iter=n_iter, tol_norm=0.0)
+    return time.perf_counter() - t0
+
+
+def cpu_reference_c3(procs=None, n_iter=200):
+    """Oracle port of solve_joint (bit-exact with the reference), one problem per core."""
+    import multiprocessing as mp
+
+    procs = procs or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        pool.map(_oracle_ma_solve, [(0, 1)] * procs)
+        t0 = time.perf_counter()
+        pool.map(_oracle_ma_solve, [(s, n_iter) for s in range(procs)], chunksize=1)
+        wall = time.perf_counter() - t0
+    return procs * n_iter / wall, {"cores": procs, "sample": f"{procs} C3 problems x {n_iter} iterations, "
+                                                             f"oracle port (1 BLAS thread), wall {wall:.1f}s"}
 
 
 def _oracle_project_chunk(args):
@@ -532,6 +683,22 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if args.config == "c3":
+        vals = []
+        for k in range(args.warmup + args.steps):
+            v, info = cpu_reference_c3()
+            if k >= args.warmup:
+                vals.append(v)
+        value = statistics.mean(vals)
+        print(json.dumps({"impl": "reference", "metric": "problem-iterations/sec (joint 16-agent problems x iterations)",
+                          "value": value, "unit": "problem-it/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic", "config": {"workload": CONFIGS["c3"][3]},
+                          "cpu_baseline": {"value": value, "unit": "problem-it/s", "cores": info["cores"],
+                                           "kind": "port", "sample": info["sample"]},
+                          "e2e": {"value": value, "unit": "problem-it/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
     if args.config == "c4":
         vals = []
         for k in range(args.warmup + args.steps):
@@ -586,6 +753,8 @@ def main():
         run_reference(args)
     elif args.config == "c4":
         run_c4(args)
+    elif args.config == "c3":
+        run_c3(args)
     else:
         run_b200(args)
 
