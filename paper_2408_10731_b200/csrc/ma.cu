@@ -127,15 +127,28 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
             sRhs[k] = v;
         }
         __syncthreads();
+        // one warp per row of K^-1 (coalesced, read once for the three axes), shuffle-reduced
         const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
-        for (int o = tid; o < 3 * nv; o += blockDim.x) {
-            const int ax = o / nv, r = o - ax * nv;
+        for (int r = warp; r < nv; r += kMaWarps) {
             const double* Kr = Kl + (int64_t)r * nk;
-            const double* x = sRhs + ax * nk;
-            double acc = 0.0;
-            for (int q = 0; q < nk; ++q) acc = fma(ld_const(Kr + q), x[q], acc);
-            sXi[o] = acc;
-            xg[o] = acc;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+            for (int q = lane; q < nk; q += 32) {
+                const double kv = ld_const(Kr + q);
+                a0 = fma(kv, sRhs[q], a0);
+                a1 = fma(kv, sRhs[nk + q], a1);
+                a2 = fma(kv, sRhs[2 * nk + q], a2);
+            }
+            a0 = warp_sum(a0);
+            a1 = warp_sum(a1);
+            a2 = warp_sum(a2);
+            if (lane == 0) {
+                sXi[r] = a0;
+                sXi[nv + r] = a1;
+                sXi[2 * nv + r] = a2;
+                xg[r] = a0;
+                xg[nv + r] = a1;
+                xg[2 * nv + r] = a2;
+            }
         }
     }
     __syncthreads();
