@@ -250,6 +250,86 @@ typedef struct tro_ma_params {
 int tro_ma_run(int32_t mode, const tro_ma_dims* dims, const tro_ma_consts* c, const tro_ma_state* s,
                const tro_ma_params* p, void* stream);
 
+/* ------------------------------------------------------------------ 2-D batch optimizer (Alg. 2)
+ * Replaces solver_batch.batch_iteration + the residual / _maybe_grow_rho bookkeeping of
+ * solve_batch_opt (solver_batch.py:352-363, 396-406, 451-461) for the whole batch.  One CTA per
+ * member; alpha / d are never stored (they are functions of xi and the heading, :318-344): each
+ * launch folds them into F'g for the next launch's QP right-hand side. */
+typedef struct tro_b2_dims {
+    int64_t n_members; /* N_b */
+    int32_t n_obs;     /* n_o (0 allowed) */
+    int32_t n_c;       /* footprint circles (1..8) */
+    int32_t n_p;
+    int32_t m;         /* basis columns */
+    int32_t n_levels;  /* rho levels (one K_xi^-1 and one K_psi^-1 each) */
+    int32_t max_hist;  /* best_history capacity (0: none) */
+} tro_b2_dims;
+
+typedef struct tro_b2_consts {
+    const double* PT;            /* 3 x m x n_p: P', Pdot', Pddot' */
+    const double* Pr;            /* 3 x n_p x m: P, Pdot, Pddot */
+    const double* obs;           /* n_obs x 2 x n_p: track x row, y row */
+    const double* obs_ab;        /* n_obs x 2: semi-axes (a, b) */
+    const double* offsets;       /* n_c signed circle offsets (FootprintSpec.offsets) */
+    const double* q;             /* 4m linear cost (_Structure.q, solver_batch.py:170-177) */
+    const double* b;             /* 12 boundary values [x(6) | y(6)] */
+    const double* b_psi;         /* 2 heading boundary values */
+    const double* kinvT_xi;      /* n_levels x (4m + 12) x 4m: rows 0..4m-1 of K_xi^-1, transposed */
+    const double* kinvT_psi;     /* n_levels x (m + 2) x m: rows 0..m-1 of K_psi^-1, transposed */
+    const double* rho_chain;     /* n_levels: rho per level (min(rho * growth, cap) chain) */
+    const double* rho_psi_chain; /* n_levels: rho_psi per level */
+    const double* desired;       /* n_p x 2 (member costs, mode 3) */
+    double v_max, a_max, w_smooth, w_track;
+} tro_b2_consts;
+
+typedef struct tro_b2_state {
+    double* xi;        /* N_b x 4m: [xi_x | xi_c | xi_y | xi_s] */
+    double* xi_psi;    /* N_b x m */
+    double* lam;       /* N_b x 4m */
+    double* lam_psi;   /* N_b x m */
+    double* sums;      /* N_b x 4m: F'g of the current state (feeds the next xi step) */
+    double* res_max;   /* N_b: max |F xi - g| of the current state */
+    double* res_norm;  /* N_b: ||F xi - g|| */
+    double* ring;      /* 2 * stall_window: batch-min max-abs residuals (solver_batch.py:460) */
+    double* hist;      /* max_hist x 4: best member's (norm, max_abs, rho, index) per iteration */
+    int32_t* level;    /* current rho level (batch-global) */
+    int32_t* iteration;
+    int32_t* last_change;
+    int32_t* n_hist;
+    int32_t* n_changes;
+    uint32_t* counter; /* zero-initialised grid ticket (last-CTA-done reduction) */
+    /* mode 2 outputs (NULL to skip): BatchState arrays of the current iterate */
+    double* alpha_coll; /* N_b x n_c x n_obs x n_p */
+    double* d_coll;
+    double* alpha_v;    /* N_b x n_p each */
+    double* alpha_a;
+    double* d_v;
+    double* d_a;
+    double* psi;        /* N_b x n_p heading samples: read with TRO_B2_PSI_IN, written by modes 0, 2, 3, 5 */
+    double* rank;       /* mode 3: N_b x 6 (res_max, res_norm, min scaled distance, max speed, max accel, cost) */
+    double* psi_targets; /* mode 5: N_b x n_p unwrapped heading targets (BatchState._psi_targets) */
+} tro_b2_state;
+
+typedef struct tro_b2_params {
+    double tol;               /* BatchParams.tol */
+    double stall_improvement; /* BatchParams.stall_improvement */
+    int32_t stall_window;     /* BatchParams.stall_window */
+    int32_t flags;            /* TRO_FLAG_NO_SCHEDULE (bare batch_iteration) | TRO_B2_* */
+} tro_b2_params;
+
+#define TRO_B2_PSI_IN 16      /* the current heading is s.psi (state.psi), not P xi_psi */
+#define TRO_B2_GIVEN_AD 32    /* modes 1, 3: alpha / d are the state arrays, not implied by xi, psi */
+#define TRO_B2_GIVEN_ALPHA 64 /* mode 2: alpha from the state arrays, d computed from it (d_step) */
+
+/* mode 0: one batch_iteration + residual + best_history + batch-global rho rule;
+ * mode 1: prime F'g (sums) + residual of the state (init_state / warm start);
+ * mode 2: write the BatchState alpha / d (/ psi) arrays of the current iterate (alpha_step, d_step);
+ * mode 3: ranking quantities (solver_batch.py:366-393, 463-470) into state.rank (+ psi);
+ * mode 4: batch_xi_step alone (xi from the primed sums, :292-299);
+ * mode 5: heading_step alone (xi_psi, psi, psi_targets, :302-315). */
+int tro_b2_run(int32_t mode, const tro_b2_dims* dims, const tro_b2_consts* c, const tro_b2_state* s,
+               const tro_b2_params* p, void* stream);
+
 /* out (ncols x n) = rhs (ncols x n) * K^-T, i.e. out[c] = K^-1 rhs[c] for every column c.
  * kinv: n x n row-major.  qpcore.solve_batch with the RHS block [-q ; b]. */
 int tro_kkt_apply_f64(const double* kinv, int32_t n, const double* rhs, int64_t ncols,

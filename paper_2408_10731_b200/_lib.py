@@ -40,6 +40,7 @@ EXPORTS = (
     "tro_elite_update_f64",
     "tro_fp64_fma_probe",
     "tro_ma_run",
+    "tro_b2_run",
     "tro_version",
     "tro_error_string",
 )
@@ -159,6 +160,32 @@ class MaParams(ctypes.Structure):
                 ("max_iter", c_int32), ("max_hist", c_int32), ("reserved", c_int32)]
 
 
+class B2Dims(ctypes.Structure):
+    _fields_ = [("n_members", c_int64)] + [(n, c_int32) for n in ("n_obs", "n_c", "n_p", "m", "n_levels",
+                                                                  "max_hist")]
+
+
+class B2Consts(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("PT", "Pr", "obs", "obs_ab", "offsets", "q", "b", "b_psi", "kinvT_xi",
+                                        "kinvT_psi", "rho_chain", "rho_psi_chain", "desired")] + [
+        (n, c_double) for n in ("v_max", "a_max", "w_smooth", "w_track")]
+
+
+class B2State(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("xi", "xi_psi", "lam", "lam_psi", "sums", "res_max", "res_norm", "ring",
+                                        "hist", "level", "iteration", "last_change", "n_hist", "n_changes",
+                                        "counter", "alpha_coll", "d_coll", "alpha_v", "alpha_a", "d_v", "d_a",
+                                        "psi", "rank", "psi_targets")]
+
+
+class B2Params(ctypes.Structure):
+    _fields_ = [("tol", c_double), ("stall_improvement", c_double), ("stall_window", c_int32), ("flags", c_int32)]
+
+
+TRO_B2_PSI_IN = 16
+TRO_B2_GIVEN_AD = 32
+TRO_B2_GIVEN_ALPHA = 64
+
 _lib = None
 
 
@@ -197,6 +224,9 @@ def load() -> ctypes.CDLL:
     lib.tro_ma_run.argtypes = [c_int32, POINTER(MaDims), POINTER(MaConsts), POINTER(MaState), POINTER(MaParams),
                                c_void_p]
     lib.tro_ma_run.restype = c_int32
+    lib.tro_b2_run.argtypes = [c_int32, POINTER(B2Dims), POINTER(B2Consts), POINTER(B2State), POINTER(B2Params),
+                               c_void_p]
+    lib.tro_b2_run.restype = c_int32
     lib.tro_fp64_fma_probe.argtypes = [c_int64, c_int32, c_void_p, c_void_p]
     lib.tro_fp64_fma_probe.restype = c_int32
     lib.tro_version.argtypes = []

@@ -1,0 +1,591 @@
+// Batched 2-D footprint + heading AM iteration (arXiv 2408.10731, Alg. 2) for sm_100a.
+//
+// One CTA owns one batch member for one batch_iteration (solver_batch.py:352-363):
+//   prologue : xi = K_xi^-1 [-(q - lam - rho F'g) ; b] from the F'g sums the previous launch
+//              left behind (batch_xi_step, :292-299); F is never materialised;
+//   heading  : per sample, the copies' angle atan2(s, c), nearest-branch unwrapped against the
+//              previous heading (:308-310), contracted with P and pushed through K_psi^-1
+//              (:311-314);
+//   body     : per sample t (one thread), velocity / acceleration rows and every
+//              (circle, obstacle) element: footprint offset (:196-204), alpha_coll as a unit
+//              vector (atan2 is never needed: only its cos / sin enter, :318-326), the clipped
+//              scale d (:329-344), targets g (:207-227), residual F xi - g (:347-349);
+//   epilogue : per-sample partial sums contracted with P / Pdot / Pddot in a fixed order into
+//              F'g (next launch's RHS) and F'r (multiplier ascent, :359), the heading
+//              multiplier (:360-361), per-member max |r| and ||r||; the last CTA to finish reduces
+//              the batch (argmin of ||r||, min of max |r|, :454-460) and applies the
+//              batch-global stall rule (_maybe_grow_rho, :396-406).
+// alpha / d are never stored: they are pure functions of (xi, heading) and only feed F'g.
+#include "common.cuh"
+#include "fastmath.cuh"
+#include "../../include/trajopt_b200.h"
+
+namespace tro {
+
+constexpr int kB2Threads = 128;
+constexpr int kB2Warps = kB2Threads / 32;
+constexpr int kB2MaxRing = 64;
+constexpr int kB2MaxC = 8;
+
+struct B2Args {
+    tro_b2_dims d;
+    tro_b2_consts c;
+    tro_b2_state s;
+    tro_b2_params p;
+};
+
+// per-sample shared arrays
+enum {
+    kX, kY, kC, kS, kVX, kVY, kAX, kAY, kTgt,                // geometry of the new xi
+    kGVX, kGVY, kGAX, kGAY, kGX, kGY, kGCX, kGCY,           // F'g inputs
+    kRVX, kRVY, kRAX, kRAY, kRX, kRY, kRCX, kRCY, kDPsi,    // F'r / heading residual inputs
+    kNT
+};
+
+struct B2Smem {
+    int T, xi, rhs, po, pn, rp, out, red, total;
+};
+__host__ __device__ inline B2Smem b2_layout(int n_p, int m) {
+    B2Smem L;
+    const int nv = 4 * m, nk = nv + 12;
+    int off = 0;
+    L.T = off;   off += kNT * n_p;
+    L.xi = off;  off += nv;
+    L.rhs = off; off += nk;
+    L.po = off;  off += m;
+    L.pn = off;  off += m;
+    L.rp = off;  off += m + 2;
+    L.out = off; off += 2 * nv + m;
+    L.red = off; off += 2 * kB2Warps + 2;
+    L.total = off;
+    return L;
+}
+
+__device__ __forceinline__ double clip(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
+
+// last CTA: reduce the batch, record best_history, apply the stall rule (thread 0 writes)
+__device__ void b2_batch_epilogue(const B2Args& A, int level, double rho, double* red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t B = A.d.n_members;
+    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    int64_t bidx = -1;
+    double mmin = best;
+    bool nan_norm = false, nan_max = false;
+    int64_t nan_idx = B;
+    for (int64_t k = tid; k < B; k += kB2Threads) {
+        const double nv = __ldcg(A.s.res_norm + k), mv = __ldcg(A.s.res_max + k);
+        if (nv != nv) {
+            if (!nan_norm) nan_idx = k;
+            nan_norm = true;
+        } else if (bidx < 0 || nv < best) {
+            best = nv, bidx = k;
+        }
+        if (mv != mv) nan_max = true;
+        else mmin = fmin(mmin, mv);
+    }
+    // warp / block argmin with first-index tie-break (np.argmin); NaN wins (numpy propagates it)
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, (long long)bidx, o);
+        if (oi >= 0 && (bidx < 0 || ob < best || (ob == best && oi < bidx))) best = ob, bidx = oi;
+        const long long on = __shfl_xor_sync(0xffffffffu, (long long)nan_idx, o);
+        nan_idx = on < nan_idx ? on : nan_idx;
+        mmin = fmin(mmin, __shfl_xor_sync(0xffffffffu, mmin, o));
+    }
+    nan_max = __any_sync(0xffffffffu, nan_max);
+    __shared__ long long s_idx[kB2Warps], s_nan[kB2Warps];
+    __shared__ int s_nanmax[kB2Warps];
+    if (lane == 0) {
+        red[warp] = best;
+        red[kB2Warps + warp] = mmin;
+        s_idx[warp] = bidx;
+        s_nan[warp] = nan_idx;
+        s_nanmax[warp] = nan_max;
+    }
+    __syncthreads();
+    if (tid != 0) return;
+    for (int w = 1; w < kB2Warps; ++w) {
+        const double ob = red[w];
+        const long long oi = s_idx[w];
+        if (oi >= 0 && (bidx < 0 || ob < best || (ob == best && oi < bidx))) best = ob, bidx = oi;
+        nan_idx = s_nan[w] < nan_idx ? s_nan[w] : nan_idx;
+        mmin = fmin(mmin, red[kB2Warps + w]);
+        nan_max |= (bool)s_nanmax[w];
+    }
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    if (nan_idx < B) bidx = nan_idx, best = qnan;
+    if (nan_max) mmin = qnan;
+    const double best_max = __ldcg(A.s.res_max + bidx);
+
+    const int it = A.s.iteration[0] + 1;  // batch_iteration: state.iteration += 1 (:362)
+    A.s.iteration[0] = it;
+    const int nh = A.s.n_hist[0];
+    if (A.s.hist && nh < A.d.max_hist) {
+        double* h = A.s.hist + (int64_t)nh * 4;
+        h[0] = best;
+        h[1] = best_max;
+        h[2] = rho;
+        h[3] = (double)bidx;
+    }
+    const int n = nh + 1;
+    A.s.n_hist[0] = n;
+    const int w = A.p.stall_window, w2 = 2 * w;
+    A.s.ring[(n - 1) % w2] = mmin;
+    if (A.p.flags & TRO_FLAG_NO_SCHEDULE) return;
+    const int lc = A.s.last_change[0];
+    if (n >= w2 && it - lc >= w) {  // :398
+        double sr = 0.0, sp = 0.0;  // np.mean of < 8 values: sequential sum / w
+        for (int k = 0; k < w; ++k) sr += A.s.ring[(n - w + k) % w2];
+        for (int k = 0; k < w; ++k) sp += A.s.ring[(n - w2 + k) % w2];
+        const double recent = sr / (double)w, previous = sp / (double)w;
+        if (previous > fmax(A.p.tol, 0.0) && (previous - recent) / previous < A.p.stall_improvement) {
+            if (level + 1 < A.d.n_levels) {
+                A.s.level[0] = level + 1;
+                A.s.n_changes[0] += 1;
+            }
+            A.s.last_change[0] = it;  // rho = min(rho * growth, cap): the chain saturates at the cap
+        }
+    }
+}
+
+enum { kModeIter = 0, kModePrime = 1, kModeMaterialise = 2, kModeRank = 3, kModeXi = 4, kModeHeading = 5 };
+
+template <int NC, int MODE>
+__global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
+    constexpr bool iter = MODE == kModeIter;
+    constexpr bool qp_xi = MODE == kModeIter || MODE == kModeXi;
+    constexpr bool heading = MODE == kModeIter || MODE == kModeHeading;
+    constexpr bool body = MODE <= kModeRank;
+    extern __shared__ double smem[];
+    const int64_t i = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_p = A.d.n_p, m = A.d.m, nv = 4 * m, nk = nv + 12;
+    const int n_o = A.d.n_obs, n_c = NC ? NC : A.d.n_c;
+    const int flags = A.p.flags;
+    const bool psi_in = (flags & TRO_B2_PSI_IN) != 0;
+    const bool given_alpha = (MODE == kModePrime || MODE == kModeMaterialise || MODE == kModeRank) &&
+                             (flags & (TRO_B2_GIVEN_ALPHA | TRO_B2_GIVEN_AD)) != 0;
+    const bool given_d = (MODE == kModePrime || MODE == kModeRank) && (flags & TRO_B2_GIVEN_AD) != 0;
+    const B2Smem L = b2_layout(n_p, m);
+    double* sT = smem + L.T;
+    double* sXi = smem + L.xi;
+    double* sRhs = smem + L.rhs;
+    double* sPo = smem + L.po;
+    double* sPn = smem + L.pn;
+    double* sRp = smem + L.rp;
+    double* sOut = smem + L.out;
+    double* sRed = smem + L.red;
+
+    const int level = *A.s.level;
+    const double rho = A.c.rho_chain[level], rho_p = A.c.rho_psi_chain[level];
+    const double* PT = A.c.PT;
+    const double* PdT = PT + (int64_t)m * n_p;
+    const double* PddT = PdT + (int64_t)m * n_p;
+    const double* Pr = A.c.Pr;
+    const double* Pdr = Pr + (int64_t)n_p * m;
+    const double* Pddr = Pdr + (int64_t)n_p * m;
+    double* g_xi = A.s.xi + i * nv;
+    double* g_lam = A.s.lam + i * nv;
+    double* g_sum = A.s.sums + i * nv;
+    double* g_xp = A.s.xi_psi + i * m;
+    double* g_lp = A.s.lam_psi + i * m;
+    double* g_psi = A.s.psi ? A.s.psi + i * n_p : nullptr;
+
+    // ---------------- prologue: the xi-step QP (batch_xi_step, :292-299) or the current iterate
+    if (qp_xi) {
+        if (tid < nv) {
+            const double ql = (A.c.q[tid] - g_lam[tid]) - rho * g_sum[tid];  // q_lin (:297)
+            sRhs[tid] = -ql;                                                   // [-q ; b] (qpcore.py:141)
+        } else if (tid < nk) {
+            sRhs[tid] = A.c.b[tid - nv];
+        }
+        __syncthreads();
+        if (tid < nv) {
+            const double* K = A.c.kinvT_xi + (int64_t)level * nk * nv + tid;
+            double acc = 0.0;
+            for (int j = 0; j < nk; ++j) acc = fma(__ldg(K + (int64_t)j * nv), sRhs[j], acc);
+            sXi[tid] = acc;
+            if (MODE == kModeXi) g_xi[tid] = acc;
+        }
+        if (MODE == kModeXi) return;
+    } else {
+        if (tid < nv) sXi[tid] = g_xi[tid];
+    }
+    if (tid < m) (heading ? sPo : sPn)[tid] = g_xp[tid];
+    __syncthreads();
+
+    // ---------------- per-sample geometry of xi; heading targets (heading_step, :307-310)
+    for (int t = tid; t < n_p; t += kB2Threads) {
+        double x = 0, y = 0, c = 0, s = 0, vx = 0, vy = 0, ax = 0, ay = 0, po = 0;
+        for (int k = 0; k < m; ++k) {
+            const double p = __ldg(PT + k * n_p + t), pd = __ldg(PdT + k * n_p + t), pdd = __ldg(PddT + k * n_p + t);
+            x = fma(p, sXi[k], x);
+            c = fma(p, sXi[m + k], c);
+            y = fma(p, sXi[2 * m + k], y);
+            s = fma(p, sXi[3 * m + k], s);
+            vx = fma(pd, sXi[k], vx);
+            vy = fma(pd, sXi[2 * m + k], vy);
+            ax = fma(pdd, sXi[k], ax);
+            ay = fma(pdd, sXi[2 * m + k], ay);
+            if (heading) po = fma(p, sPo[k], po);
+        }
+        double* T = sT + t;
+        T[kX * n_p] = x;
+        T[kY * n_p] = y;
+        T[kC * n_p] = c;
+        T[kS * n_p] = s;
+        T[kVX * n_p] = vx;
+        T[kVY * n_p] = vy;
+        T[kAX * n_p] = ax;
+        T[kAY * n_p] = ay;
+        if (heading) {
+            if (psi_in) po = g_psi[t];  // state.psi (:310)
+            const double raw = atan2_fast(s, c);
+            const double two_pi = 6.283185307179586;
+            const double tgt = raw + two_pi * rint((po - raw) / two_pi);
+            T[kTgt * n_p] = tgt;
+            if (MODE == kModeHeading && A.s.psi_targets) A.s.psi_targets[i * n_p + t] = tgt;
+        }
+    }
+    __syncthreads();
+
+    // ---------------- heading QP (:311-314)
+    if (heading) {
+        if (tid < m) {
+            double acc = 0.0;
+            for (int t = 0; t < n_p; ++t) acc = fma(__ldg(Pr + t * m + tid), sT[kTgt * n_p + t], acc);
+            sRp[tid] = -(-g_lp[tid] - rho_p * acc);
+        } else if (tid < m + 2) {
+            sRp[tid] = A.c.b_psi[tid - m];
+        }
+        __syncthreads();
+        if (tid < m) {
+            const double* K = A.c.kinvT_psi + (int64_t)level * (m + 2) * m + tid;
+            double acc = 0.0;
+            for (int j = 0; j < m + 2; ++j) acc = fma(__ldg(K + j * m), sRp[j], acc);
+            sPn[tid] = acc;
+            if (MODE == kModeHeading) g_xp[tid] = acc;
+        }
+        __syncthreads();
+        if (MODE == kModeHeading) {
+            if (g_psi)
+                for (int t = tid; t < n_p; t += kB2Threads) {
+                    double psi = 0.0;
+                    for (int k = 0; k < m; ++k) psi = fma(__ldg(PT + k * n_p + t), sPn[k], psi);
+                    g_psi[t] = psi;
+                }
+            return;
+        }
+    }
+    if (!body) return;
+
+    // ---------------- body: per sample, rows of F xi - g
+    double rmax = 0.0, ss = 0.0;
+    double dmin = __longlong_as_double(0x7ff0000000000000LL), vmax2 = 0.0, amax2 = 0.0, cost_s = 0.0, cost_t = 0.0;
+    const double vmx = A.c.v_max, amx = A.c.a_max;
+    for (int t = tid; t < n_p; t += kB2Threads) {
+        double* T = sT + t;
+        const double x = T[kX * n_p], y = T[kY * n_p], c = T[kC * n_p], s = T[kS * n_p];
+        const double vx = T[kVX * n_p], vy = T[kVY * n_p], ax = T[kAX * n_p], ay = T[kAY * n_p];
+        double psi = 0.0, pacc = 0.0;
+        if (!iter && psi_in) {
+            psi = g_psi[t];
+        } else {
+            for (int k = 0; k < m; ++k) psi = fma(__ldg(PT + k * n_p + t), sPn[k], psi);
+        }
+        if (MODE == kModeRank)
+            for (int k = 0; k < m; ++k) pacc = fma(__ldg(PddT + k * n_p + t), sPn[k], pacc);
+        double sp, cp;
+        sincos_fast(psi, &sp, &cp);
+        const int64_t o1 = i * n_p + t;
+        // velocity / acceleration rows: alpha = atan2 (unit vector), d clipped to [0, 1] (:325-344)
+        double cav, sav, caa, saa;
+        if (given_alpha) {
+            sincos_fast(A.s.alpha_v[o1], &sav, &cav);
+            sincos_fast(A.s.alpha_a[o1], &saa, &caa);
+        } else {
+            unit2(vx, vy, &cav, &sav);
+            unit2(ax, ay, &caa, &saa);
+        }
+        double dv, da;
+        if (given_d) {
+            dv = A.s.d_v[o1];
+            da = A.s.d_a[o1];
+        } else {
+            dv = clip((vx * cav + vy * sav) / vmx, 0.0, 1.0);
+            da = clip((ax * caa + ay * saa) / amx, 0.0, 1.0);
+        }
+        const double gvx = vmx * dv * cav, gvy = vmx * dv * sav;
+        const double gax = amx * da * caa, gay = amx * da * saa;
+        const double rvx = vx - gvx, rvy = vy - gvy, rax = ax - gax, ray = ay - gay;
+        // heading copy rows [0, P] xi_c = cos(psi) (:225-226)
+        const double rhx = c - cp, rhy = s - sp;
+        rmax = fmax(rmax, fmax(fmax(fabs(rvx), fabs(rvy)), fmax(fabs(rax), fabs(ray))));
+        rmax = fmax(rmax, fmax(fabs(rhx), fabs(rhy)));
+        ss = fma(rvx, rvx, ss);
+        ss = fma(rvy, rvy, ss);
+        ss = fma(rax, rax, ss);
+        ss = fma(ray, ray, ss);
+        ss = fma(rhx, rhx, ss);
+        ss = fma(rhy, rhy, ss);
+        if (MODE == kModeMaterialise) {
+            if (!given_alpha) {
+                if (A.s.alpha_v) A.s.alpha_v[o1] = atan2_fast(vy, vx);
+                if (A.s.alpha_a) A.s.alpha_a[o1] = atan2_fast(ay, ax);
+            }
+            if (A.s.d_v) A.s.d_v[o1] = dv;
+            if (A.s.d_a) A.s.d_a[o1] = da;
+        }
+        if ((MODE == kModeMaterialise || MODE == kModeRank) && !psi_in && g_psi) g_psi[t] = psi;
+        // collision rows, per circle then obstacle
+        double Gx = 0, Gy = 0, Gcx = 0, Gcy = 0, Rx = 0, Ry = 0, Rcx = 0, Rcy = 0;
+        for (int ci = 0; ci < n_c; ++ci) {
+            const double r = __ldg(A.c.offsets + ci);
+            const double cx = fma(r, cp, x), cy = fma(r, sp, y);  // circle centre (:200-201)
+            const double fx = fma(r, c, x), fy = fma(r, s, y);    // F row [P, r P] xi (:155)
+            double gxs = 0, gys = 0, rxs = 0, rys = 0;
+            for (int o = 0; o < n_o; ++o) {
+                const double ox = __ldg(A.c.obs + (int64_t)o * 2 * n_p + t);
+                const double oy = __ldg(A.c.obs + (int64_t)o * 2 * n_p + n_p + t);
+                const double a = __ldg(A.c.obs_ab + 2 * o), b = __ldg(A.c.obs_ab + 2 * o + 1);
+                const double dx = cx - ox, dy = cy - oy;
+                const int64_t oe = ((i * n_c + ci) * n_o + o) * n_p + t;
+                double ca, sa;
+                if (given_alpha) sincos_fast(A.s.alpha_coll[oe], &sa, &ca);
+                else unit2(dx, dy, &ca, &sa);  // alpha_coll = atan2(dy, dx), unscaled (:324)
+                double d;
+                if (given_d) {
+                    d = A.s.d_coll[oe];
+                } else {
+                    const double num = a * dx * ca + b * dy * sa;
+                    const double den = a * a * (ca * ca) + b * b * (sa * sa);
+                    d = clip(num / den, 1.0, 1.0e6);  // :338-340
+                }
+                const double gx = ox + a * d * ca, gy = oy + b * d * sa;  // :221-222
+                const double rx = fx - gx, ry = fy - gy;
+                gxs += gx;
+                gys += gy;
+                rxs += rx;
+                rys += ry;
+                rmax = fmax(rmax, fmax(fabs(rx), fabs(ry)));
+                ss = fma(rx, rx, ss);
+                ss = fma(ry, ry, ss);
+                if (MODE == kModeMaterialise) {
+                    if (!given_alpha && A.s.alpha_coll) A.s.alpha_coll[oe] = atan2_fast(dy, dx);
+                    if (A.s.d_coll) A.s.d_coll[oe] = d;
+                }
+                if (MODE == kModeRank) dmin = fmin(dmin, hypot(dx / a, dy / b));  // :387-388
+            }
+            Gx += gxs;
+            Gy += gys;
+            Gcx = fma(r, gxs, Gcx);
+            Gcy = fma(r, gys, Gcy);
+            Rx += rxs;
+            Ry += rys;
+            Rcx = fma(r, rxs, Rcx);
+            Rcy = fma(r, rys, Rcy);
+        }
+        if (MODE == kModeRank) {
+            vmax2 = fmax(vmax2, hypot(vx, vy));
+            amax2 = fmax(amax2, hypot(ax, ay));
+            cost_s += ax * ax + ay * ay + pacc * pacc;
+            const double ex = x - __ldg(A.c.desired + 2 * t), ey = y - __ldg(A.c.desired + 2 * t + 1);
+            cost_t += ex * ex + ey * ey;
+        }
+        if (MODE <= kModePrime) {
+            T[kGVX * n_p] = gvx;
+            T[kGVY * n_p] = gvy;
+            T[kGAX * n_p] = gax;
+            T[kGAY * n_p] = gay;
+            T[kGX * n_p] = Gx;
+            T[kGY * n_p] = Gy;
+            T[kGCX * n_p] = Gcx + cp;
+            T[kGCY * n_p] = Gcy + sp;
+        }
+        if (iter) {
+            T[kRVX * n_p] = rvx;
+            T[kRVY * n_p] = rvy;
+            T[kRAX * n_p] = rax;
+            T[kRAY * n_p] = ray;
+            T[kRX * n_p] = Rx;
+            T[kRY * n_p] = Ry;
+            T[kRCX * n_p] = Rcx + rhx;
+            T[kRCY * n_p] = Rcy + rhy;
+            T[kDPsi * n_p] = psi - T[kTgt * n_p];
+            if (g_psi) g_psi[t] = psi;
+        }
+    }
+    if (MODE == kModeMaterialise) return;
+
+    // ---------------- per-member residual max / norm
+    rmax = warp_max(rmax);
+    ss = warp_sum(ss);
+    if (MODE == kModeRank) {
+        for (int o = 16; o > 0; o >>= 1) {
+            dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+            vmax2 = fmax(vmax2, __shfl_xor_sync(0xffffffffu, vmax2, o));
+            amax2 = fmax(amax2, __shfl_xor_sync(0xffffffffu, amax2, o));
+        }
+        cost_s = warp_sum(cost_s);
+        cost_t = warp_sum(cost_t);
+    }
+    __shared__ double s_rank[kB2Warps][5];
+    if (lane == 0) {
+        sRed[warp] = rmax;
+        sRed[kB2Warps + warp] = ss;
+        if (MODE == kModeRank) {
+            s_rank[warp][0] = dmin;
+            s_rank[warp][1] = vmax2;
+            s_rank[warp][2] = amax2;
+            s_rank[warp][3] = cost_s;
+            s_rank[warp][4] = cost_t;
+        }
+    }
+    __syncthreads();
+    if (MODE == kModeRank) {
+        if (tid == 0) {
+            double mm = sRed[0], s2 = sRed[kB2Warps], dm = s_rank[0][0], v2 = s_rank[0][1], a2 = s_rank[0][2];
+            double cs = s_rank[0][3], ct = s_rank[0][4];
+            for (int w = 1; w < kB2Warps; ++w) {
+                mm = fmax(mm, sRed[w]);
+                s2 += sRed[kB2Warps + w];
+                dm = fmin(dm, s_rank[w][0]);
+                v2 = fmax(v2, s_rank[w][1]);
+                a2 = fmax(a2, s_rank[w][2]);
+                cs += s_rank[w][3];
+                ct += s_rank[w][4];
+            }
+            double* rk = A.s.rank + i * 6;
+            rk[0] = mm;
+            rk[1] = sqrt(s2);
+            rk[2] = dm;
+            rk[3] = v2;
+            rk[4] = a2;
+            rk[5] = A.c.w_smooth * cs + A.c.w_track * ct;  // _member_costs (:366-374)
+        }
+        return;
+    }
+
+    // ---------------- contractions: F'g (iterate, prime), F'r and P'(psi - targets) (iterate)
+    const int n_out = iter ? 2 * nv + m : nv;
+    for (int u = tid; u < n_out; u += kB2Threads) {
+        double acc = 0.0;
+        if (u < 2 * nv) {
+            const bool res = u >= nv;
+            const int v = res ? u - nv : u;
+            const int blk = v / m, k = v - blk * m;
+            const int base = res ? kRVX : kGVX;  // (vx, vy, ax, ay, x, y, cx, cy) blocks align
+            if (blk == 0 || blk == 2) {          // xi_x / xi_y: Pdot' v + Pddot' a + P' sum
+                const int ax_ = blk == 0 ? 0 : 1;
+                const double* tv = sT + (base + 0 + ax_) * n_p;
+                const double* ta = sT + (base + 2 + ax_) * n_p;
+                const double* tg = sT + (base + 4 + ax_) * n_p;
+                for (int t = 0; t < n_p; ++t) {
+                    acc = fma(__ldg(Pdr + t * m + k), tv[t], acc);
+                    acc = fma(__ldg(Pddr + t * m + k), ta[t], acc);
+                    acc = fma(__ldg(Pr + t * m + k), tg[t], acc);
+                }
+            } else {  // xi_c / xi_s: P' (sum_c r_c sum_o . + heading row)
+                const double* tg = sT + (base + 6 + (blk == 1 ? 0 : 1)) * n_p;
+                for (int t = 0; t < n_p; ++t) acc = fma(__ldg(Pr + t * m + k), tg[t], acc);
+            }
+        } else {
+            const int k = u - 2 * nv;
+            for (int t = 0; t < n_p; ++t) acc = fma(__ldg(Pr + t * m + k), sT[kDPsi * n_p + t], acc);
+        }
+        sOut[u] = acc;
+    }
+    __syncthreads();
+    if (tid < nv) {
+        g_sum[tid] = sOut[tid];
+        if (iter) {
+            g_xi[tid] = sXi[tid];
+            g_lam[tid] = g_lam[tid] - rho * sOut[nv + tid];  // :359
+        }
+    }
+    if (iter && tid < m) {
+        g_xp[tid] = sPn[tid];
+        g_lp[tid] = g_lp[tid] - rho_p * sOut[2 * nv + tid];  // :360-361
+    }
+    if (tid == 0) {
+        double mm = sRed[0], s2 = sRed[kB2Warps];
+        for (int w = 1; w < kB2Warps; ++w) {
+            mm = fmax(mm, sRed[w]);
+            s2 += sRed[kB2Warps + w];
+        }
+        A.s.res_max[i] = mm;
+        A.s.res_norm[i] = sqrt(s2);
+    }
+    if (!iter) return;
+
+    // ---------------- last CTA: batch-global bookkeeping (:451-461)
+    __shared__ bool s_last;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(A.s.counter, 1u);
+        s_last = prev == (unsigned)(A.d.n_members - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    b2_batch_epilogue(A, level, rho, sRed);
+    if (tid == 0) *A.s.counter = 0u;
+}
+
+template <int NC, int MODE>
+static int b2_launch(const B2Args& A, size_t smem, cudaStream_t st) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && dev >= 0 && dev < 64 && !attr_set[dev]) {
+        cudaFuncSetAttribute(b2_kernel<NC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set[dev] = true;
+    }
+    b2_kernel<NC, MODE><<<(unsigned)A.d.n_members, kB2Threads, smem, st>>>(A);
+    return (int)cudaGetLastError();
+}
+
+template <int NC>
+static int b2_dispatch(const B2Args& A, int mode, size_t smem, cudaStream_t st) {
+    switch (mode) {
+        case kModeIter: return b2_launch<NC, kModeIter>(A, smem, st);
+        case kModePrime: return b2_launch<NC, kModePrime>(A, smem, st);
+        case kModeMaterialise: return b2_launch<NC, kModeMaterialise>(A, smem, st);
+        case kModeRank: return b2_launch<NC, kModeRank>(A, smem, st);
+        case kModeXi: return b2_launch<NC, kModeXi>(A, smem, st);
+        default: return b2_launch<NC, kModeHeading>(A, smem, st);
+    }
+}
+
+}  // namespace tro
+
+extern "C" int tro_b2_run(int32_t mode, const tro_b2_dims* d, const tro_b2_consts* c, const tro_b2_state* s,
+                          const tro_b2_params* p, void* stream) {
+    if (!d || !c || !s || !p || mode < 0 || mode > 5) return TRO_EINVAL;
+    if (d->n_c < 1 || d->n_c > tro::kB2MaxC || d->n_obs < 0 || d->n_p < 2 || d->m < 1 || d->n_levels < 1)
+        return TRO_EINVAL;
+    if (4 * d->m + 12 > tro::kB2Threads) return TRO_EINVAL;
+    if (mode == 0 && (p->stall_window < 1 || 2 * p->stall_window > tro::kB2MaxRing || !s->counter || !s->ring))
+        return TRO_EINVAL;
+    if (mode == 3 && !s->rank) return TRO_EINVAL;
+    if ((p->flags & TRO_B2_PSI_IN) && !s->psi) return TRO_EINVAL;
+    if ((mode == 1 || mode == 3) && (p->flags & TRO_B2_GIVEN_AD) &&
+        (!s->alpha_coll || !s->d_coll || !s->alpha_v || !s->alpha_a || !s->d_v || !s->d_a))
+        return TRO_EINVAL;
+    if (mode == 2 && (p->flags & TRO_B2_GIVEN_ALPHA) && (!s->alpha_coll || !s->alpha_v || !s->alpha_a))
+        return TRO_EINVAL;
+    if (d->n_members <= 0) return 0;
+    if (d->n_members > 0x7fffffffLL) return TRO_EINVAL;
+    tro::B2Args A;
+    A.d = *d;
+    A.c = *c;
+    A.s = *s;
+    A.p = *p;
+    const tro::B2Smem L = tro::b2_layout(d->n_p, d->m);
+    const size_t smem = (size_t)L.total * sizeof(double);
+    if (smem > 200 * 1024) return TRO_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (d->n_c == 1) return tro::b2_dispatch<1>(A, mode, smem, st);
+    return tro::b2_dispatch<0>(A, mode, smem, st);
+}

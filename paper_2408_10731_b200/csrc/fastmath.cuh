@@ -127,6 +127,19 @@ __device__ __forceinline__ double atan2_fast(double y, double x) {
     return flip_sign(th, sign_bit(y));
 }
 
+// cos/sin of atan2(y, x) as a unit vector, numpy's signed-zero conventions
+__device__ __forceinline__ void unit2(double x, double y, double* c, double* s) {
+    const double h2 = fma(x, x, y * y);
+    if (h2 > 0.0) {
+        const double r = rsqrt_fast(h2);
+        *c = x * r;
+        *s = y * r;
+    } else {
+        *c = flip_sign(1.0, sign_bit(x));
+        *s = flip_sign(0.0, sign_bit(y));
+    }
+}
+
 // ---------------------------------------------------------------- fp32
 __device__ __forceinline__ float rcp_fast(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ float rsqrt_fast(float x) { return rsqrtf(x); }

@@ -56,19 +56,6 @@ __host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs
     return L;
 }
 
-// cos/sin of atan2(y, x) as a unit vector, numpy's signed-zero conventions
-__device__ __forceinline__ void unit2(double x, double y, double* c, double* s) {
-    const double h2 = fma(x, x, y * y);
-    if (h2 > 0.0) {
-        const double r = rsqrt_fast(h2);
-        *c = x * r;
-        *s = y * r;
-    } else {
-        *c = flip_sign(1.0, sign_bit(x));
-        *s = flip_sign(0.0, sign_bit(y));
-    }
-}
-
 template <int M>
 __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode) {
     // mode 0: iteration; 1: prime (sums of a given state: lambda in `state`, d / alpha / beta in

@@ -152,3 +152,42 @@ def square_antipodal(n_agents: int = 8, side: float = 6.0, radius: float = 0.4, 
     mid = 0.5 * (starts[0] + goal0)
     goals = [goal0] + [2.0 * mid - s for s in starts[1:]]
     return np.stack(starts), np.stack(goals)
+
+
+def dynamic_flow(n_o: int = 10, seed: int = 0, length: float = 12.0, speed: float = 0.4, radius: float = 0.4):
+    """(obstacle specs, start, goal) of the reference's 2-D "dynamic-flow" scenario
+    (bench/scenarios.py:219-245): per obstacle x~U(0.3 L, 1.1 L), y~U(-2, 2),
+    v = (-speed U(0.5, 1), U(-0.05, 0.05))."""
+    rng = np.random.default_rng(seed)
+    specs = []
+    for _ in range(n_o):
+        x = rng.uniform(0.3 * length, 1.1 * length)
+        y = rng.uniform(-2.0, 2.0)
+        v = np.array([-speed * rng.uniform(0.5, 1.0), rng.uniform(-0.05, 0.05)])
+        specs.append(ObstacleSpec(radius, radius, np.array([x, y]), v))
+    return specs, np.zeros(2), np.array([length, 0.0])
+
+
+def batch2d_problem(n_o: int = 50, n_batch: int = 1024, n_p: int = 100, seed: int = 0, offsets=(0.0,),
+                    v_max: float = 3.0, a_max: float = 3.0, basis: BasisSet | None = None):
+    """Alg. 2 benchmark problem (SURVEY.md §8 a9 "C2-alt"): the dynamic-flow scenario through the
+    reference runner's batch_problem_from_scenario (bench/runner.py:113-129): heading boundary =
+    start->goal direction, straight-line desired path, 5 cm inflated tracks."""
+    from .solver_batch import BatchProblem, FootprintSpec
+
+    basis = basis or build_basis(0.0, 10.0, n_p, 10)
+    specs, start, goal = dynamic_flow(n_o, seed)
+    heading = float(np.arctan2(goal[1] - start[1], goal[0] - start[0]))
+    frac = np.linspace(0.0, 1.0, basis.n_p)[:, None]
+    desired = start[None, :] + frac * (goal - start)[None, :]
+    return BatchProblem(
+        basis=basis,
+        boundary=(AxisBoundary(p0=start[0], p1=goal[0]), AxisBoundary(p0=start[1], p1=goal[1])),
+        psi_boundary=(heading, heading),
+        desired=desired,
+        obstacles=tracks_on_grid(specs, basis.grid.timestamps),
+        footprint=FootprintSpec(offsets=tuple(offsets)),
+        v_max=v_max,
+        a_max=a_max,
+        n_batch=n_batch,
+    )

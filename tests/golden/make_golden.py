@@ -367,6 +367,93 @@ def make_priest():
     print("priest written")
 
 
+def _b2_snap(st, prefix, out):
+    for name in ("xi", "xi_psi", "psi", "alpha_coll", "alpha_v", "alpha_a", "d_coll", "d_v", "d_a", "lam",
+                 "lam_psi"):
+        out[prefix + name] = np.array(getattr(st, name), dtype=float)
+    out[prefix + "meta"] = np.array([st.rho, st.rho_psi, st.iteration])
+
+
+def _b2_run(problem, params, samples, snap_at, tag, out):
+    """solve_batch_opt's loop restated step by step (solver_batch.py:448-461) with snapshots; asserts it
+    reproduces solve_batch_opt bit for bit."""
+    from trajopt import solver_batch as SB
+
+    ranked = SB.solve_batch_opt(problem, params, samples=samples)
+    struct = SB._Structure(problem)
+    st = SB.init_state(problem, samples.copy(), params)
+    _b2_snap(st, f"{tag}_init_", out)
+    last_change, hist = 0, []
+    for k in range(params.max_iter):
+        if k in snap_at:
+            _b2_snap(st, f"{tag}_k{k}_", out)
+        SB.batch_iteration(st, problem, struct)
+        if k in snap_at:
+            _b2_snap(st, f"{tag}_k{k + 1}_", out)
+        res = SB._residual_matrix(st, problem, struct)
+        hist.append(float(np.max(np.abs(res), axis=1).min()))
+        last_change = SB._maybe_grow_rho(st, params, hist, last_change)
+    assert np.array_equal(st.xi, ranked.state.xi), "replicate diverged"
+    out[f"{tag}_samples"] = samples
+    out[f"{tag}_hist"] = np.array([[h["norm"], h["max_abs"], h["rho"]] for h in ranked.best_history])
+    out[f"{tag}_maxabs"] = np.array(hist)
+    _b2_snap(ranked.state, f"{tag}_final_", out)
+    out[f"{tag}_rank"] = np.stack([ranked.residual_max, ranked.residual_norm, ranked.costs, ranked.aug_costs,
+                                   ranked.feasible.astype(float)], axis=1)
+    out[f"{tag}_meta"] = np.array([-1 if ranked.best_index is None else ranked.best_index, ranked.iterations,
+                                   ranked.n_factorizations])
+    return ranked
+
+
+def make_batch2d():
+    """Alg. 2 (solver_batch): the reference tests' N_P 50 problem and the C2-alt recipe, reduced."""
+    from trajopt import solver_batch as SB
+    from trajopt.basis import AxisBoundary, straight_line_coeffs
+    from trajopt.bench.runner import batch_problem_from_scenario
+    from trajopt.geometry import EllipsoidShape, ObstacleTrack
+
+    out = {}
+    # (1) test_solver_batch.py:30-43 problem: two circles (0.3, -0.3), one static obstacle, N_P 50
+    n_p = 50
+    basis = build_basis(0.0, 10.0, n_p, 10)
+    obs = [ObstacleTrack(centers=np.tile([5.0, 0.2], (n_p, 1)), shape=EllipsoidShape(0.5, 0.5)),
+           ObstacleTrack(centers=np.column_stack([np.linspace(7.0, 3.0, n_p), np.linspace(-1.0, 1.0, n_p)]),
+                         shape=EllipsoidShape(0.6, 0.4))]
+    prob = SB.BatchProblem(basis=basis, boundary=(AxisBoundary(p0=0.0, p1=10.0), AxisBoundary(p0=0.0, p1=0.0)),
+                           psi_boundary=(0.0, 0.0), desired=np.column_stack([np.linspace(0.0, 10.0, n_p),
+                                                                             np.zeros(n_p)]),
+                           obstacles=obs, footprint=SB.FootprintSpec(offsets=(0.3, -0.3)), v_max=3.0, a_max=3.0,
+                           n_batch=8)
+    m = basis.n_var
+    mean = straight_line_coeffs(basis, [0.0, 0.0], [10.0, 0.0]).ravel()
+    samples = mean[None, :] + 0.5 * np.random.default_rng(1).normal(size=(8, 2 * m))
+    out["t50_P"], out["t50_Pd"], out["t50_Pdd"] = basis.P, basis.Pdot, basis.Pddot
+    out["t50_tracks"] = np.stack([o.centers for o in obs])
+    out["t50_ab"] = np.array([[o.shape.a, o.shape.b] for o in obs])
+    _b2_run(prob, SB.BatchParams(max_iter=40), samples, (0, 1, 7, 25), "t50", out)
+    # (2) C2-alt recipe (dynamic-flow, runner.batch_problem_from_scenario), n_o 10, 16 members, 60 iterations
+    basis = build_basis(0.0, 10.0, 100, 10)
+    sc = gen_scenario("dynamic-flow", {"n_o": 10, "n_p": 100}, seed=0)
+    prob = batch_problem_from_scenario(sc, basis, n_batch=16)
+    m = basis.n_var
+    line = np.linalg.lstsq(basis.P, np.column_stack([np.linspace(0, 12.0, 100), np.zeros(100)]), rcond=None)[0]
+    mean = np.concatenate([line[:, 0], line[:, 1]])
+    samples = SB.sample_initializations(mean, np.eye(2 * m) * 1.2**2, 16, 0)
+    out["f10_P"], out["f10_Pd"], out["f10_Pdd"] = basis.P, basis.Pdot, basis.Pddot
+    out["f10_tracks"] = np.stack([o.centers for o in prob.obstacles])
+    out["f10_ab"] = np.array([[o.shape.a, o.shape.b] for o in prob.obstacles])
+    out["f10_desired"] = prob.desired
+    out["f10_bvals"] = np.stack([bc.values() for bc in prob.boundary])
+    out["f10_psib"] = np.array(prob.psi_boundary)
+    ranked = _b2_run(prob, SB.BatchParams(max_iter=60), samples, (0, 10, 30), "f10", out)
+    # (3) default-sample path of solve_batch_opt (seed 3) on the same problem: the samples only
+    ranked_d = SB.solve_batch_opt(prob, SB.BatchParams(max_iter=1), seed=3)
+    out["f10_default_xi1"] = ranked_d.state.xi
+    np.savez_compressed(os.path.join(OUT, "batch2d.npz"), **out)
+    print("batch2d written; f10 best", ranked.best_index, "feasible", int(ranked.feasible.sum()),
+          "rho", ranked.state.rho)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:

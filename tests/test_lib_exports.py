@@ -43,3 +43,37 @@ def test_host_only_calls():
     assert lib.tro_topk_stable_f64(None, 10, 20, None, None, 0, None) == _lib.TRO_EINVAL
     assert lib.tro_kkt_apply_f64(None, 4, None, 1, None, None) == _lib.TRO_EINVAL
     assert lib.tro_alg1_iterate(0, None, None, None, None, None) == _lib.TRO_EINVAL
+
+
+def test_struct_sizes_match_c_compiler(tmp_path):
+    """sizeof / offsetof of every C-ABI struct from gcc equals the ctypes mirror."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        import pytest
+
+        pytest.skip("gcc not available")
+    pairs = {
+        "tro_alg1_dims": _lib.Alg1Dims, "tro_alg1_consts": _lib.Alg1Consts, "tro_alg1_params": _lib.Alg1Params,
+        "tro_alg1_state": _lib.Alg1State, "tro_priest_dims": _lib.PriestDims, "tro_priest_consts": _lib.PriestConsts,
+        "tro_priest_io": _lib.PriestIO, "tro_ma_dims": _lib.MaDims, "tro_ma_consts": _lib.MaConsts,
+        "tro_ma_state": _lib.MaState, "tro_ma_params": _lib.MaParams, "tro_b2_dims": _lib.B2Dims,
+        "tro_b2_consts": _lib.B2Consts, "tro_b2_state": _lib.B2State, "tro_b2_params": _lib.B2Params,
+    }
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{os.path.abspath(HEADER)}"', "int main(void) {"]
+    for cname, ct in pairs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in ct._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "sizes.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "sizes"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                       check=True).stdout.splitlines())
+    for cname, ct in pairs.items():
+        assert int(got[cname]) == ctypes.sizeof(ct), cname
+        for fname, _ in ct._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(ct, fname).offset, f"{cname}.{fname}"
