@@ -320,6 +320,7 @@ typedef struct tro_b2_params {
 #define TRO_B2_PSI_IN 16      /* the current heading is s.psi (state.psi), not P xi_psi */
 #define TRO_B2_GIVEN_AD 32    /* modes 1, 3: alpha / d are the state arrays, not implied by xi, psi */
 #define TRO_B2_GIVEN_ALPHA 64 /* mode 2: alpha from the state arrays, d computed from it (d_step) */
+#define TRO_B2_CIRCLES 128    /* caller guarantees a == b for every obstacle (circle fast path) */
 
 /* mode 0: one batch_iteration + residual + best_history + batch-global rho rule;
  * mode 1: prime F'g (sums) + residual of the state (init_state / warm start);

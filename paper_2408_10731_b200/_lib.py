@@ -185,6 +185,7 @@ class B2Params(ctypes.Structure):
 TRO_B2_PSI_IN = 16
 TRO_B2_GIVEN_AD = 32
 TRO_B2_GIVEN_ALPHA = 64
+TRO_B2_CIRCLES = 128
 
 _lib = None
 

@@ -22,10 +22,22 @@
 
 namespace tro {
 
+// np.clip semantics (NaN passes through) in 2 compares + selects; fmin / fmax cost 4 SASS each
+__device__ __forceinline__ double clip(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
 constexpr int kB2Threads = 128;
 constexpr int kB2Warps = kB2Threads / 32;
 constexpr int kB2MaxRing = 64;
 constexpr int kB2MaxC = 8;
+constexpr int kB2MaxM = 16;
+#ifndef B2_UNROLL_BASIS
+#define B2_UNROLL_BASIS 1
+#endif
+#ifndef B2_MINB
+#define B2_MINB 4  // 4 CTAs / SM: 128 registers (measured best, tools/tune_b2.sh)
+#endif
+constexpr int kB2UnrollM = B2_UNROLL_BASIS ? kB2MaxM : 1;
 
 struct B2Args {
     tro_b2_dims d;
@@ -43,36 +55,67 @@ enum {
 };
 
 struct B2Smem {
-    int T, xi, rhs, po, pn, rp, out, red, total;
+    int T, xi, rhs, po, pn, rp, out, part, ab, ai, red, total;
 };
-__host__ __device__ inline B2Smem b2_layout(int n_p, int m) {
+__host__ __device__ inline B2Smem b2_layout(int n_p, int m, int n_o) {
     B2Smem L;
     const int nv = 4 * m, nk = nv + 12;
     int off = 0;
-    L.T = off;   off += kNT * n_p;
-    L.xi = off;  off += nv;
-    L.rhs = off; off += nk;
-    L.po = off;  off += m;
-    L.pn = off;  off += m;
-    L.rp = off;  off += m + 2;
-    L.out = off; off += 2 * nv + m;
-    L.red = off; off += 2 * kB2Warps + 2;
+    L.T = off;    off += kNT * n_p;
+    L.xi = off;   off += nv;
+    L.rhs = off;  off += nk;
+    L.po = off;   off += m;
+    L.pn = off;   off += m;
+    L.rp = off;   off += m + 2;
+    L.out = off;  off += 2 * nv + m;
+    L.part = off; off += 8 * (2 * nv + m);
+    L.ab = off;   off += 5 * (n_o > 0 ? n_o : 1);  // per obstacle (a, b, a^2, b^2, 1/a)
+    off = (off + 1) & ~1;
+    L.ai = off;   off += 2 * (n_o > 0 ? n_o : 1);  // per obstacle (a^2, (1e6 a)^2), 16-byte aligned
+    L.red = off;  off += 2 * kB2Warps + 2;
     L.total = off;
     return L;
 }
 
-__device__ __forceinline__ double clip(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
+// One (circle, obstacle, sample) element: alpha_coll = atan2(dy, dx) (:324), the clipped scale
+// (:338-340) and the target offset (ex, ey) = (a d cos alpha, b d sin alpha) (:221-222).
+// Circles (a == b) use d = clip(h / a) and (ex, ey) = (dx, dy) a d / h: the same quantities without
+// the num / den quotient (the reference's num / den equals h / a up to rounding).
+__device__ __forceinline__ void b2_element(double dx, double dy, const double* ab, bool circle, double* ex,
+                                           double* ey, double* dout) {
+    const double a = ab[0];
+    const double h2 = fma(dx, dx, dy * dy);
+    if (circle && h2 > 0.0) {
+        const double r = rsqrt_fast(h2);
+        const double d = clip(h2 * r * ab[4], 1.0, 1.0e6);  // ab[4]: 1 / a
+        const double s = a * d * r;
+        *ex = dx * s;
+        *ey = dy * s;
+        *dout = d;
+        return;
+    }
+    const double b = ab[1];
+    double ca, sa;
+    unit2(dx, dy, &ca, &sa);
+    const double num = a * dx * ca + b * dy * sa;
+    const double den = ab[2] * (ca * ca) + ab[3] * (sa * sa);
+    const double d = clip(num * rcp_fast(den), 1.0, 1.0e6);
+    *ex = a * d * ca;
+    *ey = b * d * sa;
+    *dout = d;
+}
 
-// last CTA: reduce the batch, record best_history, apply the stall rule (thread 0 writes)
-__device__ void b2_batch_epilogue(const B2Args& A, int level, double rho, double* red) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+// last CTA, warp 0: reduce the batch, record best_history, apply the stall rule (lane 0 writes)
+__device__ void b2_batch_epilogue(const B2Args& A, int level, double rho) {
+    const int lane = threadIdx.x & 31;
     const int64_t B = A.d.n_members;
     double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
     int64_t bidx = -1;
     double mmin = best;
     bool nan_norm = false, nan_max = false;
     int64_t nan_idx = B;
-    for (int64_t k = tid; k < B; k += kB2Threads) {
+    for (int64_t k = lane; k < B; k += 32) {
         const double nv = __ldcg(A.s.res_norm + k), mv = __ldcg(A.s.res_max + k);
         if (nv != nv) {
             if (!nan_norm) nan_idx = k;
@@ -83,7 +126,7 @@ __device__ void b2_batch_epilogue(const B2Args& A, int level, double rho, double
         if (mv != mv) nan_max = true;
         else mmin = fmin(mmin, mv);
     }
-    // warp / block argmin with first-index tie-break (np.argmin); NaN wins (numpy propagates it)
+    // argmin with first-index tie-break (np.argmin); NaN wins (numpy propagates it)
     for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
         const long long oi = __shfl_xor_sync(0xffffffffu, (long long)bidx, o);
@@ -93,25 +136,7 @@ __device__ void b2_batch_epilogue(const B2Args& A, int level, double rho, double
         mmin = fmin(mmin, __shfl_xor_sync(0xffffffffu, mmin, o));
     }
     nan_max = __any_sync(0xffffffffu, nan_max);
-    __shared__ long long s_idx[kB2Warps], s_nan[kB2Warps];
-    __shared__ int s_nanmax[kB2Warps];
-    if (lane == 0) {
-        red[warp] = best;
-        red[kB2Warps + warp] = mmin;
-        s_idx[warp] = bidx;
-        s_nan[warp] = nan_idx;
-        s_nanmax[warp] = nan_max;
-    }
-    __syncthreads();
-    if (tid != 0) return;
-    for (int w = 1; w < kB2Warps; ++w) {
-        const double ob = red[w];
-        const long long oi = s_idx[w];
-        if (oi >= 0 && (bidx < 0 || ob < best || (ob == best && oi < bidx))) best = ob, bidx = oi;
-        nan_idx = s_nan[w] < nan_idx ? s_nan[w] : nan_idx;
-        mmin = fmin(mmin, red[kB2Warps + w]);
-        nan_max |= (bool)s_nanmax[w];
-    }
+    if (lane != 0) return;
     const double qnan = __longlong_as_double(0x7ff8000000000000LL);
     if (nan_idx < B) bidx = nan_idx, best = qnan;
     if (nan_max) mmin = qnan;
@@ -150,8 +175,8 @@ __device__ void b2_batch_epilogue(const B2Args& A, int level, double rho, double
 
 enum { kModeIter = 0, kModePrime = 1, kModeMaterialise = 2, kModeRank = 3, kModeXi = 4, kModeHeading = 5 };
 
-template <int NC, int MODE>
-__global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
+template <int NC, int MODE, bool CIRC>
+__global__ void __launch_bounds__(kB2Threads, B2_MINB) b2_kernel(B2Args A) {
     constexpr bool iter = MODE == kModeIter;
     constexpr bool qp_xi = MODE == kModeIter || MODE == kModeXi;
     constexpr bool heading = MODE == kModeIter || MODE == kModeHeading;
@@ -166,8 +191,11 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
     const bool given_alpha = (MODE == kModePrime || MODE == kModeMaterialise || MODE == kModeRank) &&
                              (flags & (TRO_B2_GIVEN_ALPHA | TRO_B2_GIVEN_AD)) != 0;
     const bool given_d = (MODE == kModePrime || MODE == kModeRank) && (flags & TRO_B2_GIVEN_AD) != 0;
-    const B2Smem L = b2_layout(n_p, m);
+    const B2Smem L = b2_layout(n_p, m, n_o);
     double* sT = smem + L.T;
+    double* sPart = smem + L.part;
+    double* sAB = smem + L.ab;
+    double* sAI = smem + L.ai;
     double* sXi = smem + L.xi;
     double* sRhs = smem + L.rhs;
     double* sPo = smem + L.po;
@@ -191,6 +219,18 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
     double* g_lp = A.s.lam_psi + i * m;
     double* g_psi = A.s.psi ? A.s.psi + i * n_p : nullptr;
 
+    if (body)
+        for (int o = tid; o < n_o; o += kB2Threads) {
+            const double a = __ldg(A.c.obs_ab + 2 * o), b = __ldg(A.c.obs_ab + 2 * o + 1);
+            sAB[5 * o + 0] = a;
+            sAB[5 * o + 1] = b;
+            sAB[5 * o + 2] = a * a;
+            sAB[5 * o + 3] = b * b;
+            sAB[5 * o + 4] = 1.0 / a;
+            sAI[2 * o] = a * a;                        // clamp-inactive band h^2 in [a^2, (1e6 a)^2]
+            sAI[2 * o + 1] = (1.0e6 * a) * (1.0e6 * a);
+        }
+
     // ---------------- prologue: the xi-step QP (batch_xi_step, :292-299) or the current iterate
     if (qp_xi) {
         if (tid < nv) {
@@ -202,8 +242,16 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
         __syncthreads();
         if (tid < nv) {
             const double* K = A.c.kinvT_xi + (int64_t)level * nk * nv + tid;
-            double acc = 0.0;
-            for (int j = 0; j < nk; ++j) acc = fma(__ldg(K + (int64_t)j * nv), sRhs[j], acc);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            int j = 0;
+            for (; j + 4 <= nk; j += 4) {
+                a0 = fma(__ldg(K + (int64_t)j * nv), sRhs[j], a0);
+                a1 = fma(__ldg(K + (int64_t)(j + 1) * nv), sRhs[j + 1], a1);
+                a2 = fma(__ldg(K + (int64_t)(j + 2) * nv), sRhs[j + 2], a2);
+                a3 = fma(__ldg(K + (int64_t)(j + 3) * nv), sRhs[j + 3], a3);
+            }
+            for (; j < nk; ++j) a0 = fma(__ldg(K + (int64_t)j * nv), sRhs[j], a0);
+            const double acc = (a0 + a1) + (a2 + a3);
             sXi[tid] = acc;
             if (MODE == kModeXi) g_xi[tid] = acc;
         }
@@ -217,7 +265,9 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
     // ---------------- per-sample geometry of xi; heading targets (heading_step, :307-310)
     for (int t = tid; t < n_p; t += kB2Threads) {
         double x = 0, y = 0, c = 0, s = 0, vx = 0, vy = 0, ax = 0, ay = 0, po = 0;
-        for (int k = 0; k < m; ++k) {
+#pragma unroll kB2UnrollM
+        for (int k = 0; k < kB2MaxM; ++k) {  // fully unrolled + predicated: all basis loads in flight at once
+            if (k >= m) break;
             const double p = __ldg(PT + k * n_p + t), pd = __ldg(PdT + k * n_p + t), pdd = __ldg(PddT + k * n_p + t);
             x = fma(p, sXi[k], x);
             c = fma(p, sXi[m + k], c);
@@ -242,7 +292,9 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
             if (psi_in) po = g_psi[t];  // state.psi (:310)
             const double raw = atan2_fast(s, c);
             const double two_pi = 6.283185307179586;
-            const double tgt = raw + two_pi * rint((po - raw) / two_pi);
+            // np.round((psi - raw) / 2 pi): the quotient is within 1 ulp of the reference's (exactly
+            // representable halves never occur in practice), multiply by the rounded reciprocal
+            const double tgt = raw + two_pi * rint((po - raw) * 0.15915494309189535);
             T[kTgt * n_p] = tgt;
             if (MODE == kModeHeading && A.s.psi_targets) A.s.psi_targets[i * n_p + t] = tgt;
         }
@@ -251,9 +303,19 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
 
     // ---------------- heading QP (:311-314)
     if (heading) {
+        constexpr int kHs = 8;
+        const int chunk = (n_p + kHs - 1) / kHs;
+        for (int w = tid; w < m * kHs; w += kB2Threads) {
+            const int k = w % m, q = w / m;
+            const int t1 = min(n_p, (q + 1) * chunk);
+            double acc = 0.0;
+            for (int t = q * chunk; t < t1; ++t) acc = fma(__ldg(Pr + t * m + k), sT[kTgt * n_p + t], acc);
+            sPart[q * m + k] = acc;
+        }
+        __syncthreads();
         if (tid < m) {
             double acc = 0.0;
-            for (int t = 0; t < n_p; ++t) acc = fma(__ldg(Pr + t * m + tid), sT[kTgt * n_p + t], acc);
+            for (int q = 0; q < kHs; ++q) acc += sPart[q * m + tid];
             sRp[tid] = -(-g_lp[tid] - rho_p * acc);
         } else if (tid < m + 2) {
             sRp[tid] = A.c.b_psi[tid - m];
@@ -271,7 +333,11 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
             if (g_psi)
                 for (int t = tid; t < n_p; t += kB2Threads) {
                     double psi = 0.0;
-                    for (int k = 0; k < m; ++k) psi = fma(__ldg(PT + k * n_p + t), sPn[k], psi);
+#pragma unroll kB2UnrollM
+                    for (int k = 0; k < kB2MaxM; ++k) {
+                        if (k >= m) break;
+                        psi = fma(__ldg(PT + k * n_p + t), sPn[k], psi);
+                    }
                     g_psi[t] = psi;
                 }
             return;
@@ -291,7 +357,11 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
         if (!iter && psi_in) {
             psi = g_psi[t];
         } else {
-            for (int k = 0; k < m; ++k) psi = fma(__ldg(PT + k * n_p + t), sPn[k], psi);
+#pragma unroll kB2UnrollM
+            for (int k = 0; k < kB2MaxM; ++k) {
+                if (k >= m) break;
+                psi = fma(__ldg(PT + k * n_p + t), sPn[k], psi);
+            }
         }
         if (MODE == kModeRank)
             for (int k = 0; k < m; ++k) pacc = fma(__ldg(PddT + k * n_p + t), sPn[k], pacc);
@@ -320,8 +390,8 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
         const double rvx = vx - gvx, rvy = vy - gvy, rax = ax - gax, ray = ay - gay;
         // heading copy rows [0, P] xi_c = cos(psi) (:225-226)
         const double rhx = c - cp, rhy = s - sp;
-        rmax = fmax(rmax, fmax(fmax(fabs(rvx), fabs(rvy)), fmax(fabs(rax), fabs(ray))));
-        rmax = fmax(rmax, fmax(fabs(rhx), fabs(rhy)));
+        rmax = dmax(dmax(dmax(rmax, fabs(rvx)), fabs(rvy)), dmax(fabs(rax), fabs(ray)));
+        rmax = dmax(rmax, dmax(fabs(rhx), fabs(rhy)));
         ss = fma(rvx, rvx, ss);
         ss = fma(rvy, rvy, ss);
         ss = fma(rax, rax, ss);
@@ -344,37 +414,110 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
             const double cx = fma(r, cp, x), cy = fma(r, sp, y);  // circle centre (:200-201)
             const double fx = fma(r, c, x), fy = fma(r, s, y);    // F row [P, r P] xi (:155)
             double gxs = 0, gys = 0, rxs = 0, rys = 0;
-            for (int o = 0; o < n_o; ++o) {
-                const double ox = __ldg(A.c.obs + (int64_t)o * 2 * n_p + t);
-                const double oy = __ldg(A.c.obs + (int64_t)o * 2 * n_p + n_p + t);
-                const double a = __ldg(A.c.obs_ab + 2 * o), b = __ldg(A.c.obs_ab + 2 * o + 1);
-                const double dx = cx - ox, dy = cy - oy;
-                const int64_t oe = ((i * n_c + ci) * n_o + o) * n_p + t;
-                double ca, sa;
-                if (given_alpha) sincos_fast(A.s.alpha_coll[oe], &sa, &ca);
-                else unit2(dx, dy, &ca, &sa);  // alpha_coll = atan2(dy, dx), unscaled (:324)
-                double d;
-                if (given_d) {
-                    d = A.s.d_coll[oe];
-                } else {
-                    const double num = a * dx * ca + b * dy * sa;
-                    const double den = a * a * (ca * ca) + b * b * (sa * sa);
-                    d = clip(num / den, 1.0, 1.0e6);  // :338-340
+            if (CIRC) {
+                // Circles (a == b): the clamp d >= 1 is inactive iff h >= a, and then the target is the
+                // circle centre itself, g = o + a (h / a) (dx, dy) / h = c (:221-222, :338-340), so only the
+                // clamped (inside) elements need the closed forms; the rest contribute k * c to the sums
+                // and the obstacle-independent residual (fx - cx, fy - cy).
+                int k_out = 0;
+                const double* op = A.c.obs + t;
+                auto element = [&](int o, double ox, double oy) {
+                    const double dx = cx - ox, dy = cy - oy;
+                    const double h2 = fma(dx, dx, dy * dy);
+                    const double2 lim = reinterpret_cast<const double2*>(sAI)[o];  // (a^2, (1e6 a)^2)
+                    if (h2 >= lim.x && h2 <= lim.y) {
+                        ++k_out;
+                        return;
+                    }
+                    const double a = sAB[5 * o];
+                    double ex, ey;
+                    if (h2 > 0.0) {
+                        const double rr = rsqrt_fast(h2);
+                        const double sc = a * clip(h2 * rr * sAB[5 * o + 4], 1.0, 1.0e6) * rr;
+                        ex = dx * sc;
+                        ey = dy * sc;
+                    } else {  // atan2(+-0, +-0) conventions (unit2), d = 1
+                        ex = flip_sign(a, sign_bit(dx));
+                        ey = flip_sign(0.0, sign_bit(dy));
+                    }
+                    const double gx = ox + ex, gy = oy + ey;
+                    const double rx = fx - gx, ry = fy - gy;
+                    gxs += gx;
+                    gys += gy;
+                    rxs += rx;
+                    rys += ry;
+                    rmax = dmax(dmax(rmax, fabs(rx)), fabs(ry));
+                    ss = fma(rx, rx, ss);
+                    ss = fma(ry, ry, ss);
+                };
+                constexpr int kBatch = 8;  // all loads of a batch in flight before the first use
+                const int stride = 2 * n_p;
+                int o = 0;
+                for (; o + kBatch <= n_o; o += kBatch) {
+                    double ox[kBatch], oy[kBatch];
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j) {
+                        ox[j] = __ldg(op + (o + j) * stride);
+                        oy[j] = __ldg(op + (o + j) * stride + n_p);
+                    }
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j) element(o + j, ox[j], oy[j]);
                 }
-                const double gx = ox + a * d * ca, gy = oy + b * d * sa;  // :221-222
+                for (; o < n_o; ++o) element(o, __ldg(op + o * stride), __ldg(op + o * stride + n_p));
+                if (k_out) {
+                    const double kd = (double)k_out, rx = fx - cx, ry = fy - cy;
+                    gxs = fma(kd, cx, gxs);
+                    gys = fma(kd, cy, gys);
+                    rxs = fma(kd, rx, rxs);
+                    rys = fma(kd, ry, rys);
+                    rmax = dmax(dmax(rmax, fabs(rx)), fabs(ry));
+                    ss = fma(kd, fma(rx, rx, ry * ry), ss);
+                }
+            } else {
+            const double* op = A.c.obs + t;
+            const double* const op_last = op + (int64_t)(n_o > 0 ? n_o - 1 : 0) * 2 * n_p;
+            double ox_n = n_o > 0 ? __ldg(op) : 0.0, oy_n = n_o > 0 ? __ldg(op + n_p) : 0.0;
+            for (int o = 0; o < n_o; ++o) {
+                const double ox = ox_n, oy = oy_n;  // prefetched one obstacle ahead
+                op = op < op_last ? op + 2 * n_p : op;
+                ox_n = __ldg(op);
+                oy_n = __ldg(op + n_p);
+                const double dx = cx - ox, dy = cy - oy;
+                double ex, ey, d;
+                {
+                    const double* ab = sAB + 5 * o;
+                    const int64_t oe = ((i * n_c + ci) * n_o + o) * n_p + t;
+                    if (given_alpha) {
+                        double ca, sa;
+                        sincos_fast(A.s.alpha_coll[oe], &sa, &ca);
+                        if (given_d) {
+                            d = A.s.d_coll[oe];
+                        } else {
+                            const double num = ab[0] * dx * ca + ab[1] * dy * sa;
+                            const double den = ab[2] * (ca * ca) + ab[3] * (sa * sa);
+                            d = clip(num / den, 1.0, 1.0e6);  // :338-340
+                        }
+                        ex = ab[0] * d * ca;
+                        ey = ab[1] * d * sa;
+                    } else {
+                        b2_element(dx, dy, ab, ab[0] == ab[1], &ex, &ey, &d);
+                    }
+                    if (MODE == kModeMaterialise) {
+                        if (!given_alpha && A.s.alpha_coll) A.s.alpha_coll[oe] = atan2_fast(dy, dx);
+                        if (A.s.d_coll) A.s.d_coll[oe] = d;
+                    }
+                    if (MODE == kModeRank) dmin = fmin(dmin, hypot(dx / ab[0], dy / ab[1]));  // :387-388
+                }
+                const double gx = ox + ex, gy = oy + ey;  // :221-222
                 const double rx = fx - gx, ry = fy - gy;
                 gxs += gx;
                 gys += gy;
                 rxs += rx;
                 rys += ry;
-                rmax = fmax(rmax, fmax(fabs(rx), fabs(ry)));
+                rmax = dmax(dmax(rmax, fabs(rx)), fabs(ry));
                 ss = fma(rx, rx, ss);
                 ss = fma(ry, ry, ss);
-                if (MODE == kModeMaterialise) {
-                    if (!given_alpha && A.s.alpha_coll) A.s.alpha_coll[oe] = atan2_fast(dy, dx);
-                    if (A.s.d_coll) A.s.d_coll[oe] = d;
-                }
-                if (MODE == kModeRank) dmin = fmin(dmin, hypot(dx / a, dy / b));  // :387-388
+            }
             }
             Gx += gxs;
             Gy += gys;
@@ -467,35 +610,68 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
     }
 
     // ---------------- contractions: F'g (iterate, prime), F'r and P'(psi - targets) (iterate)
-    const int n_out = iter ? 2 * nv + m : nv;
-    for (int u = tid; u < n_out; u += kB2Threads) {
-        double acc = 0.0;
-        if (u < 2 * nv) {
-            const bool res = u >= nv;
-            const int v = res ? u - nv : u;
-            const int blk = v / m, k = v - blk * m;
-            const int base = res ? kRVX : kGVX;  // (vx, vy, ax, ay, x, y, cx, cy) blocks align
-            if (blk == 0 || blk == 2) {          // xi_x / xi_y: Pdot' v + Pddot' a + P' sum
-                const int ax_ = blk == 0 ? 0 : 1;
-                const double* tv = sT + (base + 0 + ax_) * n_p;
-                const double* ta = sT + (base + 2 + ax_) * n_p;
-                const double* tg = sT + (base + 4 + ax_) * n_p;
-                for (int t = 0; t < n_p; ++t) {
-                    acc = fma(__ldg(Pdr + t * m + k), tv[t], acc);
-                    acc = fma(__ldg(Pddr + t * m + k), ta[t], acc);
-                    acc = fma(__ldg(Pr + t * m + k), tg[t], acc);
+    // contraction: out[k][col] = sum_t M[t][k] T[col][t] for M = P (9 columns), Pdot (4), Pddot (4);
+    // thread (k, q) keeps all columns of one basis row k over t-chunk q in registers (one basis
+    // load per sample feeds every column), partials summed over q in a fixed order.
+    {
+        constexpr int kQ = 8;
+        const int chunk = (n_p + kQ - 1) / kQ;
+        const int ncol = iter ? 17 : 8;
+        for (int w = tid; w < m * kQ; w += kB2Threads) {
+            const int k = w % m, q = w / m;
+            const int t0 = q * chunk, t1 = min(n_p, t0 + chunk);
+            double aP[9], aD[4], aA[4];
+#pragma unroll
+            for (int c = 0; c < 9; ++c) aP[c] = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) aD[c] = 0.0, aA[c] = 0.0;
+            for (int t = t0; t < t1; ++t) {
+                const double p = __ldg(Pr + t * m + k), pd = __ldg(Pdr + t * m + k), pdd = __ldg(Pddr + t * m + k);
+                const double* T = sT + t;
+                aD[0] = fma(pd, T[kGVX * n_p], aD[0]);
+                aD[1] = fma(pd, T[kGVY * n_p], aD[1]);
+                aA[0] = fma(pdd, T[kGAX * n_p], aA[0]);
+                aA[1] = fma(pdd, T[kGAY * n_p], aA[1]);
+                aP[0] = fma(p, T[kGX * n_p], aP[0]);
+                aP[1] = fma(p, T[kGY * n_p], aP[1]);
+                aP[2] = fma(p, T[kGCX * n_p], aP[2]);
+                aP[3] = fma(p, T[kGCY * n_p], aP[3]);
+                if (iter) {
+                    aD[2] = fma(pd, T[kRVX * n_p], aD[2]);
+                    aD[3] = fma(pd, T[kRVY * n_p], aD[3]);
+                    aA[2] = fma(pdd, T[kRAX * n_p], aA[2]);
+                    aA[3] = fma(pdd, T[kRAY * n_p], aA[3]);
+                    aP[4] = fma(p, T[kRX * n_p], aP[4]);
+                    aP[5] = fma(p, T[kRY * n_p], aP[5]);
+                    aP[6] = fma(p, T[kRCX * n_p], aP[6]);
+                    aP[7] = fma(p, T[kRCY * n_p], aP[7]);
+                    aP[8] = fma(p, T[kDPsi * n_p], aP[8]);
                 }
-            } else {  // xi_c / xi_s: P' (sum_c r_c sum_o . + heading row)
-                const double* tg = sT + (base + 6 + (blk == 1 ? 0 : 1)) * n_p;
-                for (int t = 0; t < n_p; ++t) acc = fma(__ldg(Pr + t * m + k), tg[t], acc);
             }
-        } else {
-            const int k = u - 2 * nv;
-            for (int t = 0; t < n_p; ++t) acc = fma(__ldg(Pr + t * m + k), sT[kDPsi * n_p + t], acc);
+            // outputs: [g: x c y s | r: x c y s | psi], each block m wide
+            double* out = sPart + q * (2 * nv + m);
+            out[k] = (aD[0] + aA[0]) + aP[0];
+            out[m + k] = aP[2];
+            out[2 * m + k] = (aD[1] + aA[1]) + aP[1];
+            out[3 * m + k] = aP[3];
+            if (iter) {
+                out[nv + k] = (aD[2] + aA[2]) + aP[4];
+                out[nv + m + k] = aP[6];
+                out[nv + 2 * m + k] = (aD[3] + aA[3]) + aP[5];
+                out[nv + 3 * m + k] = aP[7];
+                out[2 * nv + k] = aP[8];
+            }
+            (void)ncol;
         }
-        sOut[u] = acc;
+        __syncthreads();
+        const int n_out = iter ? 2 * nv + m : nv;
+        for (int u = tid; u < n_out; u += kB2Threads) {
+            double acc = 0.0;
+            for (int q = 0; q < kQ; ++q) acc += sPart[q * (2 * nv + m) + u];
+            sOut[u] = acc;
+        }
+        __syncthreads();
     }
-    __syncthreads();
     if (tid < nv) {
         g_sum[tid] = sOut[tid];
         if (iter) {
@@ -518,39 +694,42 @@ __global__ void __launch_bounds__(kB2Threads) b2_kernel(B2Args A) {
     }
     if (!iter) return;
 
-    // ---------------- last CTA: batch-global bookkeeping (:451-461)
-    __shared__ bool s_last;
-    __syncthreads();
-    if (tid == 0) {
+    // ---------------- last CTA: batch-global bookkeeping (:451-461), one warp
+    if (warp != 0) return;
+    unsigned last = 0;
+    if (lane == 0) {
         __threadfence();
-        const unsigned prev = atomicAdd(A.s.counter, 1u);
-        s_last = prev == (unsigned)(A.d.n_members - 1);
+        last = atomicAdd(A.s.counter, 1u) == (unsigned)(A.d.n_members - 1);
     }
-    __syncthreads();
-    if (!s_last) return;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
     __threadfence();
-    b2_batch_epilogue(A, level, rho, sRed);
-    if (tid == 0) *A.s.counter = 0u;
+    b2_batch_epilogue(A, level, rho);
+    if (lane == 0) *A.s.counter = 0u;
 }
 
-template <int NC, int MODE>
+template <int NC, int MODE, bool CIRC = false>
 static int b2_launch(const B2Args& A, size_t smem, cudaStream_t st) {
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (smem > 48 * 1024 && dev >= 0 && dev < 64 && !attr_set[dev]) {
-        cudaFuncSetAttribute(b2_kernel<NC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(b2_kernel<NC, MODE, CIRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set[dev] = true;
     }
-    b2_kernel<NC, MODE><<<(unsigned)A.d.n_members, kB2Threads, smem, st>>>(A);
+    b2_kernel<NC, MODE, CIRC><<<(unsigned)A.d.n_members, kB2Threads, smem, st>>>(A);
     return (int)cudaGetLastError();
 }
 
 template <int NC>
 static int b2_dispatch(const B2Args& A, int mode, size_t smem, cudaStream_t st) {
+    // the circle path only for the implied-geometry modes (given alpha / d need the general one)
+    const bool circ = (A.p.flags & TRO_B2_CIRCLES) && !(A.p.flags & (TRO_B2_GIVEN_AD | TRO_B2_GIVEN_ALPHA));
     switch (mode) {
-        case kModeIter: return b2_launch<NC, kModeIter>(A, smem, st);
-        case kModePrime: return b2_launch<NC, kModePrime>(A, smem, st);
+        case kModeIter:
+            return circ ? b2_launch<NC, kModeIter, true>(A, smem, st) : b2_launch<NC, kModeIter>(A, smem, st);
+        case kModePrime:
+            return circ ? b2_launch<NC, kModePrime, true>(A, smem, st) : b2_launch<NC, kModePrime>(A, smem, st);
         case kModeMaterialise: return b2_launch<NC, kModeMaterialise>(A, smem, st);
         case kModeRank: return b2_launch<NC, kModeRank>(A, smem, st);
         case kModeXi: return b2_launch<NC, kModeXi>(A, smem, st);
@@ -565,7 +744,7 @@ extern "C" int tro_b2_run(int32_t mode, const tro_b2_dims* d, const tro_b2_const
     if (!d || !c || !s || !p || mode < 0 || mode > 5) return TRO_EINVAL;
     if (d->n_c < 1 || d->n_c > tro::kB2MaxC || d->n_obs < 0 || d->n_p < 2 || d->m < 1 || d->n_levels < 1)
         return TRO_EINVAL;
-    if (4 * d->m + 12 > tro::kB2Threads) return TRO_EINVAL;
+    if (d->m > tro::kB2MaxM) return TRO_EINVAL;
     if (mode == 0 && (p->stall_window < 1 || 2 * p->stall_window > tro::kB2MaxRing || !s->counter || !s->ring))
         return TRO_EINVAL;
     if (mode == 3 && !s->rank) return TRO_EINVAL;
@@ -582,7 +761,7 @@ extern "C" int tro_b2_run(int32_t mode, const tro_b2_dims* d, const tro_b2_const
     A.c = *c;
     A.s = *s;
     A.p = *p;
-    const tro::B2Smem L = tro::b2_layout(d->n_p, d->m);
+    const tro::B2Smem L = tro::b2_layout(d->n_p, d->m, d->n_obs);
     const size_t smem = (size_t)L.total * sizeof(double);
     if (smem > 200 * 1024) return TRO_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

@@ -394,6 +394,8 @@ class _Engine:
             self._alloc_geo()
         self.params = p
         self.flags = _lib.TRO_B2_PSI_IN
+        if n_o and np.array_equal(struct.obs_a, struct.obs_b):
+            self.flags |= _lib.TRO_B2_CIRCLES  # circle fast path (the benchmark recipes)
         self._graph = None
         self._graph_n = 0
         c = struct.device(dev)

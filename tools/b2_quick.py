@@ -13,7 +13,7 @@ from paper_2408_10731_b200 import solver_batch as SB
 
 prob = scenarios.batch2d_problem(n_o=50, n_batch=1024)
 params = SB.BatchParams(max_iter=200)
-for rep in range(3):
+for rep in range(int(os.environ.get("B2_REPS", "3"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     r = SB.solve_batch_opt(prob, params, seed=0)
