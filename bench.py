@@ -45,6 +45,9 @@ CONFIGS = {
 C4_ROUNDS, C4_NCE, C4_NEL = 10, 8192, 256
 CONFIGS["c3"] = (16, 4096, 200, "C3: 4096 joint problems x 16 quadrotors (120 pairs, ellipsoid 0.3/0.45) x n_p 100, "
                                 "200 iterations (rho_final 1e3, tol 0: fixed work)")
+CONFIGS["c2alt"] = (50, 1024, 200, "C2-alt (Alg. 2): 1024 members x 50 dyn. circles (dynamic-flow, seed 0) x "
+                                   "n_p 100, 1 footprint circle + heading, 200 batch iterations (2-D)")
+B2_FLOPS_ELEM = 20  # per (circle, obstacle, sample): deltas, unit vector, num / den / d, targets, residual
 WORDS_3D = 9  # persistent words per (member, obstacle, sample): alpha beta lx ly lz lca lsa lcb lsb
 
 
@@ -196,6 +199,127 @@ def c3_problems(lo, hi):
                 for i in range(16)]
         probs.append(MA.MultiAgentProblem(basis=b, boundaries=bnds, agent_shape=EllipsoidShape(0.3, 0.45)))
     return probs
+
+
+def b2_flops_per_member_iter(m=11, n_p=100, n_c=1, n_o=50):
+    """Algorithmic fp64 flops of one batch_iteration of one member in the reference's formulation
+    (Alg. 2 roofline): xi QP, heading contraction + QP, geometry, elements, F' contractions."""
+    nv, nk = 4 * m, 4 * m + 12
+    return (2 * nv * nk + 2 * m * n_p + 2 * m * (m + 2) + 2 * m * n_p * 10
+            + B2_FLOPS_ELEM * n_c * n_o * n_p + 2 * m * n_p * 17)
+
+
+def run_c2alt(args):
+    import torch
+
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200 import solver_batch as SB
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    n_o, total, n_iter, desc = CONFIGS["c2alt"]
+    if args.members:
+        total = args.members
+    prob = scenarios.batch2d_problem(n_o=n_o, n_batch=total)
+    params = SB.BatchParams(max_iter=n_iter)
+    struct = SB._structure_for(prob)
+    samples = SB._default_samples(prob, struct.m, None, None, 0)
+    state0 = SB.init_state(prob, samples, params)
+    eng, lv, given = SB._engine_for(state0, prob, struct, params, max_hist=n_iter)
+    stream = torch.cuda.current_stream()
+
+    def solve():
+        eng.load(state0, 0)
+        eng.prime(given)
+        eng.run(n_iter)
+        eng.run_mode(3, eng.flags)
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        solve()
+    b.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_s = a.elapsed_time(b) / 1e3 / args.steps
+    # the iterate kernel alone (graph-replayed launches), CUDA events on its stream
+    eng.load(state0, 0)
+    eng.prime(given)
+    eng.run(25)
+    torch.cuda.synchronize()
+    a.record(stream)
+    eng.run(n_iter)
+    b.record(stream)
+    torch.cuda.synchronize()
+    launch_s = a.elapsed_time(b) / 1e3 / n_iter
+    # e2e: the public API (samples from the host, ranked solutions back)
+    SB.solve_batch_opt(prob, params, samples=samples)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(args.steps):
+        ranked = SB.solve_batch_opt(prob, params, samples=samples)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_s = a.elapsed_time(b) / 1e3 / args.steps
+    e_eng = SB._ENGINE_CACHE[next(reversed(SB._ENGINE_CACHE))]
+    flops = b2_flops_per_member_iter(n_o=n_o) * total
+    peak = fp64_peak_tflops()
+    line = {
+        "metric": "trajectory-iterations/sec (Alg. 2 batch x iterations)",
+        "value": total * n_iter / step_s, "unit": "traj-it/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference dynamic-flow generator, seed 0; default solve_batch_opt samples, seed 0)",
+        "config": {"workload": desc, "members": total, "n_obs": n_o, "n_c": 1, "n_p": 100, "iterations": n_iter,
+                   "parallelism": "replicas x1", "l2": "on-chip (latency-bound: state 1 MB, tracks 80 KB)"},
+        "roofline": {"bound": "fp64", "achieved": flops / launch_s / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops / launch_s / 1e12 / peak, "traffic": None,
+                     "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)",
+                     "kernel": "tro_b2_run mode 0 (b2_kernel<1, 0, circles>)", "avg_launch_ms": launch_s * 1e3,
+                     "algorithmic_flops_per_launch": flops,
+                     "note": "reference-formulation flops (bench.b2_flops_per_member_iter); the kernel is latency-"
+                             "bound at 1024 members (7 per SM) and skips the closed forms of clamp-inactive circles"},
+        "clocks": clk,
+        "e2e": {"value": total * n_iter / e2e_s, "unit": "traj-it/s", "h2d_bytes_per_step": int(e_eng.h2d_bytes),
+                "d2h_bytes_per_step": int(e_eng.d2h_bytes)},
+        "gpu_launches": args.steps * (n_iter + 2),
+        "result": {"best_index": ranked.best_index, "feasible": int(ranked.feasible.sum()),
+                   "min_residual_max": float(ranked.residual_max.min()), "rho": ranked.state.rho},
+    }
+    if not args.no_cpu_baseline:
+        v, info = cpu_reference_c2alt()
+        line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port",
+                                "sample": info["sample"]}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_reference_c2alt(n_iter=3):
+    """Oracle port of solve_batch_opt (bit-exact with the reference) on the full batch, all BLAS threads:
+    the reference is numpy-vectorised over the batch (solver_batch.py:352-363)."""
+    from oracle import batch2d as OB
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200 import solver_batch as SB
+
+    n_o, total, _, _ = CONFIGS["c2alt"]
+    prob = scenarios.batch2d_problem(n_o=n_o, n_batch=total)
+    b = prob.basis
+    st = OB.make_structure(b.P, b.Pdot, b.Pddot, np.stack([bc.values() for bc in prob.boundary]), prob.psi_boundary,
+                           prob.desired, np.stack([o.centers for o in prob.obstacles]),
+                           [o.shape.a for o in prob.obstacles], [o.shape.b for o in prob.obstacles], (0.0,), 3.0, 3.0)
+    samples = SB._default_samples(prob, b.n_var, None, None, 0)
+    OB.solve(st, samples[:8], 1, max_iter=1)
+    t0 = time.perf_counter()
+    OB.solve(st, samples, 1, max_iter=n_iter)
+    wall = time.perf_counter() - t0
+    cores = os.cpu_count() or 1
+    return total * n_iter / wall, {"cores": cores, "sample": f"{total} members x {n_iter} iterations (init + "
+                                                             f"ranking included), oracle port, numpy/BLAS "
+                                                             f"threads, wall {wall:.1f}s"}
 
 
 def run_c3(args):
@@ -393,16 +517,46 @@ def measured_peaks():
 
 # ---------------------------------------------------------------- clocks sampling
 class ClockSampler:
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML polled every 5 ms from a
+    thread (short regions still get samples); nvidia-smi -lms 200 when NVML is unavailable."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self._stop = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() else self.index
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            masks = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                     pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+
+            def poll():
+                while not self._stop.is_set():
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((sm, tuple(bool(r & mk) for mk in masks)))
+                    time.sleep(0.005)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -419,6 +573,13 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def stop(self):
+        if self.nvml is not None:
+            self._stop.set()
+            self.thread.join(timeout=1)
+            sm = [float(r[0]) for r in self.rows]
+            reasons = sorted({self.NAMES[k] for r in self.rows for k in range(4) if r[1][k]})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.max_mhz),
+                    "reasons": reasons, "samples": len(self.rows), "source": "nvml 5 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -428,10 +589,10 @@ class ClockSampler:
             self.proc.kill()
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[3 + k] and r[3 + k] != "Not Active"})
+        reasons = sorted({self.NAMES[k] for r in self.rows for k in range(4)
+                          if "Active" in r[3 + k] and r[3 + k] != "Not Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvidia-smi 200 ms"}
 
 
 # ---------------------------------------------------------------- CPU reference arm (oracle port)
@@ -699,6 +860,22 @@ def run_reference(args):
                           "e2e": {"value": value, "unit": "problem-it/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}), flush=True)
         return
+    if args.config == "c2alt":
+        vals = []
+        for k in range(args.warmup + args.steps):
+            v, info = cpu_reference_c2alt()
+            if k >= args.warmup:
+                vals.append(v)
+        value = statistics.mean(vals)
+        print(json.dumps({"impl": "reference", "metric": "trajectory-iterations/sec (Alg. 2 batch x iterations)",
+                          "value": value, "unit": "traj-it/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic", "config": {"workload": CONFIGS["c2alt"][3]},
+                          "cpu_baseline": {"value": value, "unit": "traj-it/s", "cores": info["cores"],
+                                           "kind": "port", "sample": info["sample"]},
+                          "e2e": {"value": value, "unit": "traj-it/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
     if args.config == "c4":
         vals = []
         for k in range(args.warmup + args.steps):
@@ -755,6 +932,8 @@ def main():
         run_c4(args)
     elif args.config == "c3":
         run_c3(args)
+    elif args.config == "c2alt":
+        run_c2alt(args)
     else:
         run_b200(args)
 

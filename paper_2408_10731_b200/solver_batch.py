@@ -132,8 +132,8 @@ class BatchState:
         self._geo = None
         self._implied = (self.xi.copy(), self.psi.copy(), struct)
 
-    def _implied_now(self, problem) -> bool:
-        return (self._geo is None and self._implied is not None and self._implied[2].problem is problem
+    def _implied_now(self, struct) -> bool:
+        return (self._geo is None and self._implied is not None and self._implied[2].key == struct.key
                 and np.array_equal(self._implied[0], self.xi) and np.array_equal(self._implied[1], self.psi))
 
     def _materialise(self) -> dict:
@@ -222,10 +222,43 @@ def sample_initializations(mean: np.ndarray, covariance: np.ndarray, n_batch: in
     return rng.multivariate_normal(mean, covariance, size=n_batch, method="svd")
 
 
+def _fingerprint(problem: BatchProblem) -> bytes:
+    """Content key of everything _Structure depends on (problems are mutable dataclasses)."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=20)
+    b = problem.basis
+    for a in (b.P, b.Pdot, b.Pddot, problem.desired):
+        h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    for o in problem.obstacles:
+        h.update(np.ascontiguousarray(o.centers, dtype=np.float64).tobytes())
+        h.update(np.array([o.shape.a, o.shape.b], dtype=np.float64).tobytes())
+    h.update(np.array([v for bc in problem.boundary for v in bc.values()] + list(problem.psi_boundary)
+                      + list(problem.footprint.offsets)
+                      + [problem.v_max, problem.a_max, problem.w_smooth, problem.w_track, problem.n_o],
+                      dtype=np.float64).tobytes())
+    return h.digest()
+
+
+_STRUCT_CACHE: dict = {}
+
+
+def _structure_for(problem: BatchProblem) -> "_Structure":
+    key = _fingerprint(problem)
+    st = _STRUCT_CACHE.get(key)
+    if st is None:
+        if len(_STRUCT_CACHE) > 16:
+            _STRUCT_CACHE.clear()
+            _ENGINE_CACHE.clear()
+        st = _STRUCT_CACHE[key] = _Structure(problem, key=key)
+    return st
+
+
 class _Structure:
     """Constant matrices of one BatchProblem (solver_batch.py:141-193) plus their device copies."""
 
-    def __init__(self, problem: BatchProblem):
+    def __init__(self, problem: BatchProblem, key: bytes | None = None):
+        self.key = key if key is not None else _fingerprint(problem)
         basis = problem.basis
         m, n_p = basis.n_var, basis.n_p
         self.problem = problem
@@ -398,6 +431,8 @@ class _Engine:
             self.flags |= _lib.TRO_B2_CIRCLES  # circle fast path (the benchmark recipes)
         self._graph = None
         self._graph_n = 0
+        self._pin = {}
+        self.h2d_bytes = self.d2h_bytes = 0
         c = struct.device(dev)
         lv = levels.device(dev)
         self._keep = (c, lv)
@@ -433,16 +468,38 @@ class _Engine:
             psi_targets=P(self.psi_targets) if self.psi_targets is not None else None, **g)
 
     # ---- host <-> device
+    def _pinned(self, name, like):
+        buf = self._pin.get(name)
+        if buf is None or buf.shape != like.shape or buf.dtype != like.dtype:
+            buf = torch.empty(like.shape, dtype=like.dtype, pin_memory=True)
+            self._pin[name] = buf
+        return buf
+
     def load(self, state: BatchState, level: int = 0):
-        t = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64))  # noqa: E731
-        self.xi.copy_(t(state.xi))
-        self.xi_psi.copy_(t(state.xi_psi))
-        self.psi.copy_(t(state.psi))
-        self.lam.copy_(t(state.lam))
-        self.lam_psi.copy_(t(state.lam_psi))
-        self.ints.copy_(torch.tensor([level, int(state.iteration), 0, 0, 0], dtype=torch.int32))
+        """Upload the state through pinned staging buffers (asynchronous H2D on the current stream)."""
+        for name in ("xi", "xi_psi", "psi", "lam", "lam_psi"):
+            dst = getattr(self, name)
+            pin = self._pinned(name, dst)
+            pin.numpy()[...] = getattr(state, name)
+            dst.copy_(pin, non_blocking=True)
+        ints = self._pinned("ints", self.ints)
+        ints.numpy()[...] = (level, int(state.iteration), 0, 0, 0)
+        self.ints.copy_(ints, non_blocking=True)
         self.counter.zero_()
         self.ring.zero_()
+        self.h2d_bytes = sum(getattr(self, n).numel() * 8 for n in ("xi", "xi_psi", "psi", "lam", "lam_psi")) + 20
+
+    def fetch(self, names) -> dict:
+        """Download device tensors through pinned buffers with one synchronisation."""
+        out = {}
+        for name in names:
+            src = getattr(self, name)
+            pin = self._pinned("out_" + name, src)
+            pin.copy_(src, non_blocking=True)
+            out[name] = pin
+        torch.cuda.current_stream(self.device).synchronize()
+        self.d2h_bytes = sum(v.numel() * v.element_size() for v in out.values())
+        return {k: v.numpy().copy() for k, v in out.items()}
 
     def load_geo(self, geo: dict):
         if not self.geo:
@@ -527,7 +584,7 @@ def init_state(problem: BatchProblem, samples: np.ndarray, params: BatchParams |
     consistent with the sampled geometry (implied, materialised on the device when read);
     multipliers start at zero."""
     params = params or BatchParams()
-    struct = _Structure(problem)
+    struct = _structure_for(problem)
     basis, m = problem.basis, struct.m
     samples = np.asarray(samples, dtype=float)
     n_b = samples.shape[0]
@@ -559,14 +616,32 @@ def _ensure_factors(state: BatchState, levels: _Levels, level: int) -> None:
     qpcore._bump(2)
 
 
+_ENGINE_CACHE: dict = {}
+
+
 def _engine_for(state: BatchState, problem: BatchProblem, struct: _Structure, params: BatchParams | None = None,
-                max_hist: int = 0):
-    """Engine loaded with the state; `given` = alpha / d must be read from explicit arrays."""
+                max_hist: int = 0, cached: bool = False):
+    """Engine loaded with the state; `given` = alpha / d must be read from explicit arrays.
+
+    cached=True reuses the device buffers and the captured CUDA graph of an earlier call with the
+    same problem content, batch size and parameters (one solver per stream)."""
     p = params or BatchParams()
     lv = _levels(struct, float(state.rho), float(state.rho_psi), p.rho_growth, p.rho_cap)
-    eng = _Engine(struct, state.xi.shape[0], lv, params=p, max_hist=max_hist)
+    n_b = state.xi.shape[0]
+    eng = None
+    if cached:
+        key = (struct.key, n_b, float(state.rho), float(state.rho_psi), float(p.rho_growth), float(p.rho_cap),
+               float(p.tol), float(p.stall_improvement), int(p.stall_window), int(max_hist),
+               torch.cuda.current_device())
+        eng = _ENGINE_CACHE.get(key)
+        if eng is None:
+            if len(_ENGINE_CACHE) > 8:
+                _ENGINE_CACHE.clear()
+            eng = _ENGINE_CACHE[key] = _Engine(struct, n_b, lv, params=p, max_hist=max_hist)
+    if eng is None:
+        eng = _Engine(struct, n_b, lv, params=p, max_hist=max_hist)
     eng.load(state, 0)
-    given = not state._implied_now(problem)
+    given = not state._implied_now(struct)
     if given:
         eng.load_geo(state._materialise())
     return eng, lv, given
@@ -586,7 +661,7 @@ def _download(eng: _Engine, state: BatchState, *, xi=True, xi_psi=True, psi=True
 
 def batch_xi_step(state: BatchState, problem: BatchProblem, struct: _Structure | None = None) -> None:
     """Shared-factor QP update of every member's stacked coefficients (:292-299)."""
-    struct = struct or _Structure(problem)
+    struct = struct or _structure_for(problem)
     eng, lv, given = _engine_for(state, problem, struct)
     _ensure_factors(state, lv, 0)
     eng.prime(given)  # F'g of the state's alpha / d / psi (:296)
@@ -596,7 +671,7 @@ def batch_xi_step(state: BatchState, problem: BatchProblem, struct: _Structure |
 
 def heading_step(state: BatchState, problem: BatchProblem, struct: _Structure | None = None) -> None:
     """Fit the heading block to unwrapped arctan2 targets from the copies (:302-315)."""
-    struct = struct or _Structure(problem)
+    struct = struct or _structure_for(problem)
     lv = _levels(struct, float(state.rho), float(state.rho_psi), BatchParams.rho_growth, BatchParams.rho_cap)
     eng = _Engine(struct, state.xi.shape[0], lv)
     eng.load(state, 0)
@@ -610,8 +685,8 @@ def heading_step(state: BatchState, problem: BatchProblem, struct: _Structure | 
 
 def alpha_step(state: BatchState, problem: BatchProblem, struct: _Structure | None = None) -> None:
     """alpha_coll / alpha_v / alpha_a of the current (xi, psi) (:318-326); d unchanged."""
-    struct = struct or _Structure(problem)
-    if state._implied_now(problem):
+    struct = struct or _structure_for(problem)
+    if state._implied_now(struct):
         return  # already functions of this (xi, psi)
     geo = dict(state._materialise())
     fresh = _device_geometry(struct, state.xi, state.psi)
@@ -622,8 +697,8 @@ def alpha_step(state: BatchState, problem: BatchProblem, struct: _Structure | No
 
 def d_step(state: BatchState, problem: BatchProblem, struct: _Structure | None = None) -> None:
     """Clamped scales of the current (xi, psi) and the state's alpha (:329-344)."""
-    struct = struct or _Structure(problem)
-    if state._implied_now(problem):
+    struct = struct or _structure_for(problem)
+    if state._implied_now(struct):
         return
     geo = state._materialise()
     fresh = _device_geometry(struct, state.xi, state.psi, alpha=geo)
@@ -633,7 +708,7 @@ def d_step(state: BatchState, problem: BatchProblem, struct: _Structure | None =
 
 def batch_iteration(state: BatchState, problem: BatchProblem, struct: _Structure | None = None) -> BatchState:
     """One fused device iteration (:352-363): xi step, heading step, alpha, d, multipliers."""
-    struct = struct or _Structure(problem)
+    struct = struct or _structure_for(problem)
     eng, lv, given = _engine_for(state, problem, struct)
     _ensure_factors(state, lv, 0)
     eng.prime(given)
@@ -646,7 +721,7 @@ def batch_iteration(state: BatchState, problem: BatchProblem, struct: _Structure
 
 def check_raw_feasibility(state, problem, struct, d_margin, kin_margin):
     """Direct evaluation of the original quadratic constraints per member (:377-393), on the device."""
-    struct = struct or _Structure(problem)
+    struct = struct or _structure_for(problem)
     rank = _rank(state, problem, struct)
     return _feasible_from_rank(rank, problem, d_margin, kin_margin)
 
@@ -701,7 +776,7 @@ def solve_batch_opt(
     covariance) (defaults: straight-line mean, diagonal covariance scaled to the start-goal
     distance).  Passing state warm-starts.  All iterations run on the device."""
     params = params or BatchParams()
-    struct = _Structure(problem)
+    struct = _structure_for(problem)
     m = struct.m
     if state is None:
         if samples is None:
@@ -709,18 +784,21 @@ def solve_batch_opt(
         state = init_state(problem, samples, params)
         state._implied = (state._implied[0], state._implied[1], struct)
 
-    eng, lv, given = _engine_for(state, problem, struct, params, max_hist=params.max_iter)
+    eng, lv, given = _engine_for(state, problem, struct, params, max_hist=params.max_iter, cached=True)
     n_iter = int(params.max_iter)
     if n_iter > 0:
         _ensure_factors(state, lv, 0)
         eng.prime(given)
         eng.run(n_iter, use_graph=use_graph)
     eng.run_mode(3, eng.flags | (_lib.TRO_B2_GIVEN_AD if (given and n_iter == 0) else 0))
-    ints = eng.ints_host()
-    hist = eng.hist[: ints["n_hist"]].cpu().numpy() if n_iter > 0 else np.zeros((0, 4))
-    rank = eng.rank.cpu().numpy()
+    got = eng.fetch(("ints", "hist", "rank") + (("xi", "xi_psi", "psi", "lam", "lam_psi") if n_iter > 0 else ()))
+    v = got["ints"]
+    ints = dict(level=int(v[0]), iteration=int(v[1]), last_change=int(v[2]), n_hist=int(v[3]), n_changes=int(v[4]))
+    hist = got["hist"][: ints["n_hist"]] if n_iter > 0 else np.zeros((0, 4))
+    rank = got["rank"]
     if n_iter > 0:
-        _download(eng, state)
+        for name in ("xi", "xi_psi", "psi", "lam", "lam_psi"):
+            setattr(state, name, got[name])
         state.iteration += n_iter
         level = ints["level"]
         # levels are visited in order: every one after the first is a new factor pair
