@@ -801,8 +801,10 @@ def solve_batch_opt(
             setattr(state, name, got[name])
         state.iteration += n_iter
         level = ints["level"]
-        # levels are visited in order: every one after the first is a new factor pair
-        for k in range(1, level + 1):
+        # a factor pair is built by the first batch_xi_step at each new rho (:282-289); a growth decided
+        # after the last iteration is never factorized.  Levels are visited in order.
+        used = _rho_level(lv, float(hist[-1, 2]), lv.rho_psi[lv.rho.index(float(hist[-1, 2]))])
+        for k in range(1, used + 1):
             _ensure_factors(state, lv, k)
         state.rho, state.rho_psi = lv.rho[level], lv.rho_psi[level]
         state._imply(struct)
