@@ -35,41 +35,54 @@ struct MaArgs {
 };
 
 struct MaSmem {
-    int P, pos, scratch, red, sumin, rhs, xi, warp, total;  // doubles
+    int P, pos, scratch, red, sumin, rhs, xi, warp, pair, ints, total;  // doubles
 };
-__host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs, int n_eq) {
+constexpr int kPairW = 9;  // per pair: a, b, 1/a, 1/b, a^2, b^2, static centre (3)
+__host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs, int n_eq, int n_inc) {
     MaSmem L;
     int off = 0;
     L.P = off;       off += n_p * m;
     L.pos = off;     off += n_p * n_a * 3;               // positions [t][agent][axis]
     L.scratch = off; off += kMaWarps * n_pairs * 6;      // per warp: (recon+static, lambda) per pair
+    // the prologue's buffers (sums in, RHS, xi) are dead before the element pass: they alias the scratch
+    const int pro = 2 * n_a * 3 * m + 3 * (n_a * m + n_eq) + 3 * n_a * m;
+    if (pro > kMaWarps * n_pairs * 6) off += pro - kMaWarps * n_pairs * 6;
+    L.sumin = L.scratch;
+    L.rhs = L.sumin + 2 * n_a * 3 * m;
+    L.xi = L.rhs + 3 * (n_a * m + n_eq);
     // cross-warp reduction of the contracted sums reuses pos + scratch
     const int red_need = kMaWarps * 2 * n_a * 3 * m;
     const int have = off - L.pos;
     L.red = L.pos;
     if (red_need > have) off += red_need - have;
-    L.sumin = off;   off += 2 * n_a * 3 * m;
-    L.rhs = off;     off += 3 * (n_a * m + n_eq);
-    L.xi = off;      off += 3 * n_a * m;
     L.warp = off;    off += 2 * kMaWarps;
+    L.pair = off;    off += kPairW * n_pairs;            // SoA [field][pair]
+    L.ints = off;    off += (2 * n_pairs + n_a + 1 + n_inc + 1) / 2 + 1;  // pair_i, pair_j, inc_ptr, inc_pair
     L.total = off;
     return L;
 }
 
-template <int M>
-__global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode) {
-    // mode 0: iteration; 1: prime (sums of a given state: lambda in `state`, d / alpha / beta in
+template <int M, int MODE>
+__global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
+    // MODE 0: iteration; 1: prime (sums of a given state: lambda in `state`, d / alpha / beta in
     // the export planes); 2: cold init (straight lines, angles, d = 1, lambda = 0) + sums
-    const bool init = mode == 2;
-    const bool prime = mode == 1;
+    constexpr int mode = MODE;
+    constexpr bool init = MODE == 2;
+    constexpr bool prime = MODE == 1;
     extern __shared__ double smem[];
     const int i = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_p = A.d.n_p, n_a = A.d.n_agents, np_ = A.d.n_pairs, neq = A.d.n_eq;
     const int m = M ? M : A.d.m;
     const int nv = n_a * m, nk = nv + neq;
-    const MaSmem L = ma_layout(n_p, m, n_a, np_, neq);
+    const int n_inc = A.c.inc_ptr[n_a];  // <= 2 n_pairs (the layout's bound)
+    const MaSmem L = ma_layout(n_p, m, n_a, np_, neq, 2 * np_);
     double* sP = smem + L.P;
+    double* sPair = smem + L.pair;
+    int* sPairI = reinterpret_cast<int*>(smem + L.ints);
+    int* sPairJ = sPairI + np_;
+    int* sIncPtr = sPairJ + np_;
+    int* sInc = sIncPtr + n_a + 1;
     double* sPos = smem + L.pos;
     double* sScr = smem + L.scratch + warp * np_ * 6;
     double* sRed = smem + L.red;
@@ -83,6 +96,26 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
     const int level = A.s.level[i];
     const double rho = A.c.level_rho[level];
     for (int k = tid; k < n_p * m; k += blockDim.x) sP[k] = ld_const(A.c.P + k);
+    {
+        // per-pair constants (no divisions in the element pass) and the incidence lists
+        const double* statics_i = A.c.statics ? A.c.statics + (int64_t)i * A.d.n_static * 3 : nullptr;
+        for (int p = tid; p < np_; p += blockDim.x) {
+            const double pa = A.c.pair_a[p], pb = A.c.pair_b[p];
+            const int pj = A.c.pair_j[p];
+            sPair[0 * np_ + p] = pa;
+            sPair[1 * np_ + p] = pb;
+            sPair[2 * np_ + p] = 1.0 / pa;
+            sPair[3 * np_ + p] = 1.0 / pb;
+            sPair[4 * np_ + p] = pa * pa;
+            sPair[5 * np_ + p] = pb * pb;
+            for (int k = 0; k < 3; ++k)
+                sPair[(6 + k) * np_ + p] = pj < 0 ? statics_i[A.c.pair_s[p] * 3 + k] : 0.0;
+            sPairI[p] = A.c.pair_i[p];
+            sPairJ[p] = pj;
+        }
+        for (int k = tid; k <= n_a; k += blockDim.x) sIncPtr[k] = A.c.inc_ptr[k];
+        for (int k = tid; k < n_inc; k += blockDim.x) sInc[k] = A.c.inc_pair[k];
+    }
     double* xg = A.s.xi + (int64_t)i * 3 * nv;
     const double* bg = A.c.b_eq + (int64_t)i * 3 * neq;
     if (init) {
@@ -159,20 +192,40 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
     const double* statics = A.c.statics ? A.c.statics + (int64_t)i * A.d.n_static * 3 : nullptr;
     const int64_t nplane = (int64_t)A.d.n_problems * n_p * np_;
 
+    const double ir = 1.0 / rho;
+    // lambda of this lane's next element, loaded one element ahead (two HBM loads in flight per lane)
+    double nlx = 0.0, nly = 0.0, nlz = 0.0;
+    if (MODE == 0 && warp < n_p && lane < np_) {
+        const double* r0 = st + warp * rowW;
+        nlx = ld_stream(r0 + lane);
+        nly = ld_stream(r0 + np_ + lane);
+        nlz = ld_stream(r0 + 2 * np_ + lane);
+    }
     for (int t = warp; t < n_p; t += kMaWarps) {
         const double* pt = sPos + t * n_a * 3;
         double* srow = st + t * rowW;
         for (int p = lane; p < np_; p += 32) {
-            const int pi = A.c.pair_i[p], pj = A.c.pair_j[p];
-            const double pa = A.c.pair_a[p], pb = A.c.pair_b[p];
+            double clx = 0.0, cly = 0.0, clz = 0.0;
+            if (MODE == 0) {
+                clx = nlx, cly = nly, clz = nlz;
+                int p2 = p + 32, t2 = t;
+                if (p2 >= np_) p2 = lane, t2 = t + kMaWarps;
+                if (t2 < n_p) {
+                    const double* r2 = st + t2 * rowW;
+                    nlx = ld_stream(r2 + p2);
+                    nly = ld_stream(r2 + np_ + p2);
+                    nlz = ld_stream(r2 + 2 * np_ + p2);
+                }
+            }
+            const int pi = sPairI[p], pj = sPairJ[p];
+            const double pa = sPair[p], pb = sPair[np_ + p];
             double cen[3];
             if (pj >= 0) {
 #pragma unroll
                 for (int k = 0; k < 3; ++k) cen[k] = pt[pj * 3 + k];
             } else {
-                const int sidx = A.c.pair_s[p];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) cen[k] = statics[sidx * 3 + k];
+                for (int k = 0; k < 3; ++k) cen[k] = sPair[(6 + k) * np_ + p];
             }
             const double dx = pt[pi * 3 + 0] - cen[0], dy = pt[pi * 3 + 1] - cen[1], dz = pt[pi * 3 + 2] - cen[2];
             // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) as unit vectors (:280-282)
@@ -182,9 +235,19 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
                 sincos(A.s.export_ab[ex_i], &sa, &ca);
                 sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
             } else {
-                unit2(dx, dy, &ca, &sa);
-                const double ipa = 1.0 / pa;
-                unit2(dz / pb, hypot(dx * ipa, dy * ipa), &cb, &sb);
+                const double h2 = fma(dx, dx, dy * dy);
+                double planar;
+                if (h2 > 0.0) {
+                    const double r = rsqrt_fast(h2);
+                    ca = dx * r;
+                    sa = dy * r;
+                    planar = h2 * r * sPair[2 * np_ + p];  // hypot(dx, dy) / pa
+                } else {
+                    ca = flip_sign(1.0, sign_bit(dx));
+                    sa = flip_sign(0.0, sign_bit(dy));
+                    planar = 0.0;
+                }
+                unit2(dz * sPair[3 * np_ + p], planar, &cb, &sb);
             }
             double lx, ly, lz, d;
             if (prime) {
@@ -196,21 +259,23 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
                 lx = ly = lz = 0.0;
                 d = 1.0;
             } else {
-                lx = ld_stream(srow + p);
-                ly = ld_stream(srow + np_ + p);
-                lz = ld_stream(srow + 2 * np_ + p);
+                lx = clx;
+                ly = cly;
+                lz = clz;
                 // multiplier-shifted single-variable quadratic in d, clamped at [1, 1e6] (:285-293)
-                const double ir = 1.0 / rho;
-                const double num = pa * sb * (ca * (dx + lx * ir) + sa * (dy + ly * ir)) + pb * cb * (dz + lz * ir);
-                const double den = pa * pa * (sb * sb) + pb * pb * (cb * cb);
-                d = fmin(fmax(num / den, 1.0), 1e6);
+                const double num = pa * sb * (ca * fma(lx, ir, dx) + sa * fma(ly, ir, dy)) + pb * cb * fma(lz, ir, dz);
+                const double den = sPair[4 * np_ + p] * (sb * sb) + sPair[5 * np_ + p] * (cb * cb);
+                const double q = num * rcp_fast(den);
+                d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
             }
             const double rx = pa * d * sb * ca, ry = pa * d * sb * sa, rz = pb * d * cb;
             if (prime) {
             } else if (!init) {
                 const double ex = dx - rx, ey = dy - ry, ez = dz - rz;  // residual (:203-208)
                 sumsq = fma(ex, ex, fma(ey, ey, fma(ez, ez, sumsq)));
-                mx = fmax(mx, fmax(fabs(ex), fmax(fabs(ey), fabs(ez))));
+                const double ae = fabs(ex) > fabs(ey) ? fabs(ex) : fabs(ey);
+                const double am = ae > fabs(ez) ? ae : fabs(ez);
+                mx = am > mx ? am : mx;
                 lx = fma(rho, ex, lx);  // lambda += rho * res (:296)
                 ly = fma(rho, ey, ly);
                 lz = fma(rho, ez, lz);
@@ -222,7 +287,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
                 srow[np_ + p] = 0.0;
                 srow[2 * np_ + p] = 0.0;
             }
-            if (A.s.export_d && !prime) {
+            if (!prime && A.s.export_d) {  // runtime: batch and single solves share one code path
                 const int64_t e = ex_i;
                 A.s.export_d[e] = d;
                 A.s.export_ab[e] = atan2(sa, ca);           // the reference's stored angles
@@ -242,8 +307,8 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
         for (int task = lane; task < tasks; task += 32) {
             const int a = task % n_a, which = task / n_a;  // which 0: B (recon), 1: C (lambda)
             double v[3] = {0.0, 0.0, 0.0};
-            for (int q = A.c.inc_ptr[a]; q < A.c.inc_ptr[a + 1]; ++q) {
-                const int pe = A.c.inc_pair[q];
+            for (int q = sIncPtr[a]; q < sIncPtr[a + 1]; ++q) {
+                const int pe = sInc[q];
                 const double sgn = pe >= 0 ? 1.0 : -1.0;
                 const double* sc = sScr + (pe >= 0 ? pe : -pe - 1) * 6 + 3 * which;
 #pragma unroll
@@ -337,6 +402,24 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A, int mode
     }
 }
 
+template <int M, int MODE>
+static int ma_launch(const MaArgs& A, size_t smem, cudaStream_t st) {
+    cudaFuncSetAttribute(ma_kernel<M, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ma_kernel<M, MODE><<<A.d.n_problems, kMaWarps * 32, smem, st>>>(A);
+    return (int)cudaGetLastError();
+}
+
+template <int M>
+static int ma_dispatch_m(const MaArgs& A, int mode, bool, size_t smem, cudaStream_t st) {
+    if (mode == 0) return ma_launch<M, 0>(A, smem, st);
+    if (mode == 1) return ma_launch<M, 1>(A, smem, st);
+    return ma_launch<M, 2>(A, smem, st);
+}
+
+static int ma_dispatch(const MaArgs& A, int mode, bool exp, size_t smem, cudaStream_t st) {
+    return A.d.m == 11 ? ma_dispatch_m<11>(A, mode, exp, smem, st) : ma_dispatch_m<9>(A, mode, exp, smem, st);
+}
+
 }  // namespace tro
 
 extern "C" int tro_ma_run(int32_t mode, const tro_ma_dims* d, const tro_ma_consts* c, const tro_ma_state* s,
@@ -354,16 +437,11 @@ extern "C" int tro_ma_run(int32_t mode, const tro_ma_dims* d, const tro_ma_const
     A.c = *c;
     A.s = *s;
     A.p = *p;
-    const tro::MaSmem L = tro::ma_layout(d->n_p, d->m, d->n_agents, d->n_pairs, d->n_eq);
+    // every pair appears in at most two agent incidence lists
+    const tro::MaSmem L = tro::ma_layout(d->n_p, d->m, d->n_agents, d->n_pairs, d->n_eq, 2 * d->n_pairs);
     const size_t smem = (size_t)L.total * sizeof(double);
     if (smem > 227 * 1024) return TRO_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (d->m == 11) {
-        cudaFuncSetAttribute(tro::ma_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tro::ma_kernel<11><<<d->n_problems, tro::kMaWarps * 32, smem, st>>>(A, mode);
-    } else {
-        cudaFuncSetAttribute(tro::ma_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tro::ma_kernel<9><<<d->n_problems, tro::kMaWarps * 32, smem, st>>>(A, mode);
-    }
-    return (int)cudaGetLastError();
+    const bool exp = s->export_d != nullptr && s->export_ab != nullptr;
+    return tro::ma_dispatch(A, mode, exp, smem, st);
 }
