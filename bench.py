@@ -211,12 +211,18 @@ def b2_flops_per_member_iter(m=11, n_p=100, n_c=1, n_o=50):
 
 def run_c2alt(args):
     import torch
+    import torch.distributed as dist
 
     from paper_2408_10731_b200 import scenarios
     from paper_2408_10731_b200 import solver_batch as SB
+    from paper_2408_10731_b200.distributed import shard_range, solve_batch_opt_sharded
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_o, total, n_iter, desc = CONFIGS["c2alt"]
     if args.members:
         total = args.members
@@ -224,19 +230,33 @@ def run_c2alt(args):
     params = SB.BatchParams(max_iter=n_iter)
     struct = SB._structure_for(prob)
     samples = SB._default_samples(prob, struct.m, None, None, 0)
-    state0 = SB.init_state(prob, samples, params)
-    eng, lv, given = SB._engine_for(state0, prob, struct, params, max_hist=n_iter)
+    lo, hi = shard_range(total, rank, world)
+    state0 = SB.init_state(prob, samples[lo:hi], params)
+    lv = SB._levels(struct, 1.0, 1.0, params.rho_growth, params.rho_cap)
+    eng = SB._Engine(struct, hi - lo, lv, params=params, max_hist=n_iter, member_offset=lo if world > 1 else None)
+    gathered = torch.zeros((world, 4), dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
+
+    def iterations(n):
+        if world == 1:
+            eng.run(n)  # CUDA graphs of 25 launches; the last CTA applies the batch-global rule
+            return
+        for _ in range(n):  # batch-global rule across ranks: 32 B all-gather per iteration
+            eng.iterate()
+            dist.all_gather_into_tensor(gathered, eng.shard)
+            eng.merge(gathered)
 
     def solve():
         eng.load(state0, 0)
-        eng.prime(given)
-        eng.run(n_iter)
+        eng.prime(False)
+        iterations(n_iter)
         eng.run_mode(3, eng.flags)
 
     for _ in range(args.warmup):
         solve()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -246,37 +266,57 @@ def run_c2alt(args):
     b.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    step_s = a.elapsed_time(b) / 1e3 / args.steps
-    # the iterate kernel alone (graph-replayed launches), CUDA events on its stream
+    t = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_s = float(t.item()) / args.steps
+    # the iterate kernel alone, CUDA events on its stream (single GPU: graph-replayed launches)
     eng.load(state0, 0)
-    eng.prime(given)
-    eng.run(25)
+    eng.prime(False)
+    iterations(25)
     torch.cuda.synchronize()
-    a.record(stream)
-    eng.run(n_iter)
-    b.record(stream)
-    torch.cuda.synchronize()
-    launch_s = a.elapsed_time(b) / 1e3 / n_iter
+    if world == 1:
+        a.record(stream)
+        eng.run(n_iter)
+        b.record(stream)
+        torch.cuda.synchronize()
+        launch_s = a.elapsed_time(b) / 1e3 / n_iter
+    else:
+        a.record(stream)
+        for _ in range(n_iter):
+            eng.iterate()
+        b.record(stream)
+        torch.cuda.synchronize()
+        launch_s = a.elapsed_time(b) / 1e3 / n_iter
     # e2e: the public API (samples from the host, ranked solutions back)
-    SB.solve_batch_opt(prob, params, samples=samples)
+    api = (lambda: SB.solve_batch_opt(prob, params, samples=samples)) if world == 1 else \
+        (lambda: solve_batch_opt_sharded(prob, params, samples=samples))
+    api()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     a.record(stream)
     for _ in range(args.steps):
-        ranked = SB.solve_batch_opt(prob, params, samples=samples)
+        ranked = api()
     b.record(stream)
     torch.cuda.synchronize()
-    e2e_s = a.elapsed_time(b) / 1e3 / args.steps
-    e_eng = SB._ENGINE_CACHE[next(reversed(SB._ENGINE_CACHE))]
-    flops = b2_flops_per_member_iter(n_o=n_o) * total
+    te = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item()) / args.steps
+    h2d = 8 * (hi - lo) * (4 * struct.m + struct.m + 100 + 4 * struct.m + struct.m) + 20
+    d2h = 8 * (hi - lo) * (4 * struct.m + struct.m + 100 + 4 * struct.m + struct.m + 6) + 8 * 4 * n_iter + 20
+    flops = b2_flops_per_member_iter(n_o=n_o) * (hi - lo)
     peak = fp64_peak_tflops()
     line = {
         "metric": "trajectory-iterations/sec (Alg. 2 batch x iterations)",
-        "value": total * n_iter / step_s, "unit": "traj-it/s", "n_gpus": 1, "steps": args.steps,
+        "value": total * n_iter / step_s, "unit": "traj-it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference dynamic-flow generator, seed 0; default solve_batch_opt samples, seed 0)",
         "config": {"workload": desc, "members": total, "n_obs": n_o, "n_c": 1, "n_p": 100, "iterations": n_iter,
-                   "parallelism": "replicas x1", "l2": "on-chip (latency-bound: state 1 MB, tracks 80 KB)"},
+                   "parallelism": f"member-shard x{world} (+ 32 B all-gather / iteration)" if world > 1 else
+                   "member-shard x1", "l2": "on-chip (latency-bound: state 1 MB, tracks 80 KB)"},
         "roofline": {"bound": "fp64", "achieved": flops / launch_s / 1e12, "peak": peak, "unit": "TFLOP/s",
                      "frac": flops / launch_s / 1e12 / peak, "traffic": None,
                      "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)",
@@ -285,17 +325,20 @@ def run_c2alt(args):
                      "note": "reference-formulation flops (bench.b2_flops_per_member_iter); the kernel is latency-"
                              "bound at 1024 members (7 per SM) and skips the closed forms of clamp-inactive circles"},
         "clocks": clk,
-        "e2e": {"value": total * n_iter / e2e_s, "unit": "traj-it/s", "h2d_bytes_per_step": int(e_eng.h2d_bytes),
-                "d2h_bytes_per_step": int(e_eng.d2h_bytes)},
-        "gpu_launches": args.steps * (n_iter + 2),
+        "e2e": {"value": total * n_iter / e2e_s, "unit": "traj-it/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": args.steps * (n_iter * (1 if world == 1 else 2) + 2),
         "result": {"best_index": ranked.best_index, "feasible": int(ranked.feasible.sum()),
                    "min_residual_max": float(ranked.residual_max.min()), "rho": ranked.state.rho},
     }
-    if not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_c2alt()
         line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port",
                                 "sample": info["sample"]}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def cpu_reference_c2alt(n_iter=3):

@@ -308,6 +308,9 @@ typedef struct tro_b2_state {
     double* psi;        /* N_b x n_p heading samples: read with TRO_B2_PSI_IN, written by modes 0, 2, 3, 5 */
     double* rank;       /* mode 3: N_b x 6 (res_max, res_norm, min scaled distance, max speed, max accel, cost) */
     double* psi_targets; /* mode 5: N_b x n_p unwrapped heading targets (BatchState._psi_targets) */
+    double* shard;       /* TRO_B2_SHARD, mode 0: this shard's summary (best norm, best global index, its
+                            max |r|, min max |r|) for the all-gather */
+    const double* shards_in; /* mode 6: n_shards x 4 all-gathered summaries, rank order */
 } tro_b2_state;
 
 typedef struct tro_b2_params {
@@ -315,19 +318,25 @@ typedef struct tro_b2_params {
     double stall_improvement; /* BatchParams.stall_improvement */
     int32_t stall_window;     /* BatchParams.stall_window */
     int32_t flags;            /* TRO_FLAG_NO_SCHEDULE (bare batch_iteration) | TRO_B2_* */
+    int64_t member_offset;    /* global index of this launch's member 0 (sharded batches) */
+    int32_t n_shards;         /* mode 6: number of shard summaries */
+    int32_t reserved;
 } tro_b2_params;
 
 #define TRO_B2_PSI_IN 16      /* the current heading is s.psi (state.psi), not P xi_psi */
 #define TRO_B2_GIVEN_AD 32    /* modes 1, 3: alpha / d are the state arrays, not implied by xi, psi */
 #define TRO_B2_GIVEN_ALPHA 64 /* mode 2: alpha from the state arrays, d computed from it (d_step) */
 #define TRO_B2_CIRCLES 128    /* caller guarantees a == b for every obstacle (circle fast path) */
+#define TRO_B2_SHARD 256      /* mode 0 writes this shard's summary instead of applying the schedule */
 
 /* mode 0: one batch_iteration + residual + best_history + batch-global rho rule;
  * mode 1: prime F'g (sums) + residual of the state (init_state / warm start);
  * mode 2: write the BatchState alpha / d (/ psi) arrays of the current iterate (alpha_step, d_step);
  * mode 3: ranking quantities (solver_batch.py:366-393, 463-470) into state.rank (+ psi);
  * mode 4: batch_xi_step alone (xi from the primed sums, :292-299);
- * mode 5: heading_step alone (xi_psi, psi, psi_targets, :302-315). */
+ * mode 5: heading_step alone (xi_psi, psi, psi_targets, :302-315);
+ * mode 6: merge all-gathered shard summaries and apply the batch-global rule (multi-GPU Alg. 2:
+ *         mode 0 with TRO_B2_SHARD on every rank, all-gather of the 4-double summaries, mode 6). */
 int tro_b2_run(int32_t mode, const tro_b2_dims* dims, const tro_b2_consts* c, const tro_b2_state* s,
                const tro_b2_params* p, void* stream);
 

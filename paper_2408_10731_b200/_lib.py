@@ -175,17 +175,19 @@ class B2State(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in ("xi", "xi_psi", "lam", "lam_psi", "sums", "res_max", "res_norm", "ring",
                                         "hist", "level", "iteration", "last_change", "n_hist", "n_changes",
                                         "counter", "alpha_coll", "d_coll", "alpha_v", "alpha_a", "d_v", "d_a",
-                                        "psi", "rank", "psi_targets")]
+                                        "psi", "rank", "psi_targets", "shard", "shards_in")]
 
 
 class B2Params(ctypes.Structure):
-    _fields_ = [("tol", c_double), ("stall_improvement", c_double), ("stall_window", c_int32), ("flags", c_int32)]
+    _fields_ = [("tol", c_double), ("stall_improvement", c_double), ("stall_window", c_int32), ("flags", c_int32),
+                ("member_offset", c_int64), ("n_shards", c_int32), ("reserved", c_int32)]
 
 
 TRO_B2_PSI_IN = 16
 TRO_B2_GIVEN_AD = 32
 TRO_B2_GIVEN_ALPHA = 64
 TRO_B2_CIRCLES = 128
+TRO_B2_SHARD = 256
 
 _lib = None
 

@@ -106,51 +106,82 @@ __device__ __forceinline__ void b2_element(double dx, double dy, const double* a
 }
 
 
-// last CTA, warp 0: reduce the batch, record best_history, apply the stall rule (lane 0 writes)
-__device__ void b2_batch_epilogue(const B2Args& A, int level, double rho) {
-    const int lane = threadIdx.x & 31;
-    const int64_t B = A.d.n_members;
-    double best = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-    int64_t bidx = -1;
-    double mmin = best;
-    bool nan_norm = false, nan_max = false;
-    int64_t nan_idx = B;
-    for (int64_t k = lane; k < B; k += 32) {
-        const double nv = __ldcg(A.s.res_norm + k), mv = __ldcg(A.s.res_max + k);
-        if (nv != nv) {
-            if (!nan_norm) nan_idx = k;
-            nan_norm = true;
-        } else if (bidx < 0 || nv < best) {
-            best = nv, bidx = k;
-        }
-        if (mv != mv) nan_max = true;
-        else mmin = fmin(mmin, mv);
-    }
-    // argmin with first-index tie-break (np.argmin); NaN wins (numpy propagates it)
-    for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const long long oi = __shfl_xor_sync(0xffffffffu, (long long)bidx, o);
-        if (oi >= 0 && (bidx < 0 || ob < best || (ob == best && oi < bidx))) best = ob, bidx = oi;
-        const long long on = __shfl_xor_sync(0xffffffffu, (long long)nan_idx, o);
-        nan_idx = on < nan_idx ? on : nan_idx;
-        mmin = fmin(mmin, __shfl_xor_sync(0xffffffffu, mmin, o));
-    }
-    nan_max = __any_sync(0xffffffffu, nan_max);
-    if (lane != 0) return;
-    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
-    if (nan_idx < B) bidx = nan_idx, best = qnan;
-    if (nan_max) mmin = qnan;
-    const double best_max = __ldcg(A.s.res_max + bidx);
+// Batch bookkeeping of one iteration (solver_batch.py:454-461): the best member (argmin of the
+// residual norm, first index on ties; numpy's argmin returns the first NaN if there is one), its
+// max |r|, and the batch minimum of max |r|.  A "summary" is (best norm, best global index, its max,
+// min max); shard summaries merge associatively, so a sharded batch (TRO_B2_SHARD + mode 6) makes
+// exactly the single-GPU decisions.
+struct B2Summary {
+    double best, best_max, mmin;
+    int64_t bidx;   // global member index, -1: none
+    bool nan_norm;  // best is the first NaN norm
+    bool nan_max;   // some max |r| is NaN
+};
 
+__device__ __forceinline__ bool b2_better(double nb, int64_t ni, bool nn, double ob, int64_t oi, bool on) {
+    if (ni < 0) return false;
+    if (oi < 0) return true;
+    if (nn != on) return nn;       // NaN beats numbers
+    if (nn) return ni < oi;        // first NaN
+    return nb < ob || (nb == ob && ni < oi);
+}
+
+__device__ B2Summary b2_warp_merge(B2Summary v) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, v.best, o);
+        const double om = __shfl_xor_sync(0xffffffffu, v.best_max, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, (long long)v.bidx, o);
+        const bool on = __shfl_xor_sync(0xffffffffu, (int)v.nan_norm, o) != 0;
+        if (b2_better(ob, oi, on, v.best, v.bidx, v.nan_norm)) v.best = ob, v.best_max = om, v.bidx = oi, v.nan_norm = on;
+        v.mmin = fmin(v.mmin, __shfl_xor_sync(0xffffffffu, v.mmin, o));
+    }
+    v.nan_max = __any_sync(0xffffffffu, v.nan_max);
+    return v;
+}
+
+// warp 0 of the last CTA: summary of this launch's members (global index = offset + k)
+__device__ B2Summary b2_member_summary(const B2Args& A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t B = A.d.n_members, off = A.p.member_offset;
+    B2Summary v{__longlong_as_double(0x7ff0000000000000LL), 0.0, __longlong_as_double(0x7ff0000000000000LL), -1,
+                false, false};
+    // this tail runs in one warp after every other CTA finished: keep 16 L2 loads in flight per lane
+    constexpr int kLd = 16;
+    for (int64_t base = 0; base < B; base += 32 * kLd) {
+        double nv[kLd], mv[kLd];
+#pragma unroll
+        for (int j = 0; j < kLd; ++j) {
+            const int64_t k = base + j * 32 + lane;
+            nv[j] = k < B ? __ldcg(A.s.res_norm + k) : 0.0;
+            mv[j] = k < B ? __ldcg(A.s.res_max + k) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kLd; ++j) {
+            const int64_t k = base + j * 32 + lane;
+            if (k >= B) break;
+            const bool nn = nv[j] != nv[j];
+            if (b2_better(nv[j], off + k, nn, v.best, v.bidx, v.nan_norm))
+                v.best = nv[j], v.best_max = mv[j], v.bidx = off + k, v.nan_norm = nn;
+            if (mv[j] != mv[j]) v.nan_max = true;
+            else v.mmin = fmin(v.mmin, mv[j]);
+        }
+    }
+    return b2_warp_merge(v);
+}
+
+// history row + stall rule (_maybe_grow_rho, :396-406); lane 0 only
+__device__ void b2_schedule(const B2Args& A, int level, double rho, const B2Summary& v) {
+    const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+    const double mmin = v.nan_max ? qnan : v.mmin;
     const int it = A.s.iteration[0] + 1;  // batch_iteration: state.iteration += 1 (:362)
     A.s.iteration[0] = it;
     const int nh = A.s.n_hist[0];
     if (A.s.hist && nh < A.d.max_hist) {
         double* h = A.s.hist + (int64_t)nh * 4;
-        h[0] = best;
-        h[1] = best_max;
+        h[0] = v.best;
+        h[1] = v.best_max;
         h[2] = rho;
-        h[3] = (double)bidx;
+        h[3] = (double)v.bidx;
     }
     const int n = nh + 1;
     A.s.n_hist[0] = n;
@@ -171,6 +202,41 @@ __device__ void b2_batch_epilogue(const B2Args& A, int level, double rho) {
             A.s.last_change[0] = it;  // rho = min(rho * growth, cap): the chain saturates at the cap
         }
     }
+}
+
+// last CTA, warp 0: single-GPU bookkeeping, or (TRO_B2_SHARD) this shard's summary for the all-gather
+__device__ void b2_batch_epilogue(const B2Args& A, int level, double rho) {
+    const B2Summary v = b2_member_summary(A);
+    if ((threadIdx.x & 31) != 0) return;
+    if (A.p.flags & TRO_B2_SHARD) {
+        double* o = A.s.shard;
+        o[0] = v.best;
+        o[1] = (double)v.bidx;
+        o[2] = v.best_max;
+        o[3] = v.nan_max ? __longlong_as_double(0x7ff8000000000000LL) : v.mmin;
+        return;
+    }
+    b2_schedule(A, level, rho, v);
+}
+
+// mode 6: merge the all-gathered shard summaries (n_shards x 4, rank order) and run the schedule
+__global__ void __launch_bounds__(32) b2_merge_kernel(B2Args A) {
+    const int lane = threadIdx.x;
+    B2Summary v{__longlong_as_double(0x7ff0000000000000LL), 0.0, __longlong_as_double(0x7ff0000000000000LL), -1,
+                false, false};
+    for (int r = lane; r < A.p.n_shards; r += 32) {
+        const double* s = A.s.shards_in + 4 * r;
+        const int64_t idx = (int64_t)s[1];
+        const bool nn = s[0] != s[0];
+        if (idx >= 0 && b2_better(s[0], idx, nn, v.best, v.bidx, v.nan_norm))
+            v.best = s[0], v.bidx = idx, v.best_max = s[2], v.nan_norm = nn;
+        if (s[3] != s[3]) v.nan_max = true;
+        else v.mmin = fmin(v.mmin, s[3]);
+    }
+    v = b2_warp_merge(v);
+    if (lane != 0) return;
+    const int level = *A.s.level;
+    b2_schedule(A, level, A.c.rho_chain[level], v);
 }
 
 enum { kModeIter = 0, kModePrime = 1, kModeMaterialise = 2, kModeRank = 3, kModeXi = 4, kModeHeading = 5 };
@@ -741,7 +807,20 @@ static int b2_dispatch(const B2Args& A, int mode, size_t smem, cudaStream_t st) 
 
 extern "C" int tro_b2_run(int32_t mode, const tro_b2_dims* d, const tro_b2_consts* c, const tro_b2_state* s,
                           const tro_b2_params* p, void* stream) {
-    if (!d || !c || !s || !p || mode < 0 || mode > 5) return TRO_EINVAL;
+    if (!d || !c || !s || !p || mode < 0 || mode > 6) return TRO_EINVAL;
+    if ((p->flags & TRO_B2_SHARD) && mode == 0 && !s->shard) return TRO_EINVAL;
+    if (mode == 6) {
+        if (!s->shards_in || p->n_shards < 1 || !s->ring || p->stall_window < 1 ||
+            2 * p->stall_window > tro::kB2MaxRing)
+            return TRO_EINVAL;
+        tro::B2Args A1;
+        A1.d = *d;
+        A1.c = *c;
+        A1.s = *s;
+        A1.p = *p;
+        tro::b2_merge_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(A1);
+        return (int)cudaGetLastError();
+    }
     if (d->n_c < 1 || d->n_c > tro::kB2MaxC || d->n_obs < 0 || d->n_p < 2 || d->m < 1 || d->n_levels < 1)
         return TRO_EINVAL;
     if (d->m > tro::kB2MaxM) return TRO_EINVAL;

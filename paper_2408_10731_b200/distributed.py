@@ -54,3 +54,125 @@ def gather_summaries(summary: torch.Tensor) -> dict:
     out = [torch.empty_like(summary) for _ in range(dist.get_world_size())]
     dist.all_gather(out, summary)
     return merge_summaries(out)
+
+
+# ------------------------------------------------------------------ Alg. 2 (batch-global rho)
+# solve_batch_opt's penalty rule is batch-global (solver_batch.py:454-461): each iteration needs the
+# best member (argmin of ||r||, first index; numpy returns the first NaN) and min_i max|r_i| over the
+# WHOLE batch.  Sharded, every rank's last CTA writes a 4-double summary (best norm, best global index,
+# its max|r|, min max|r|) (TRO_B2_SHARD), the summaries are all-gathered (NCCL, 32 B per rank per
+# iteration) and every rank merges them in rank order (tro_b2_run mode 6), so all ranks take the
+# single-GPU decisions bit for bit.  The numpy functions below state the same merge for the CPU tests.
+def b2_local_summary(res_norm, res_max, offset: int):
+    """numpy mirror of the kernel's shard summary: [best norm, best global index, its max, min max]."""
+    import numpy as np
+
+    res_norm, res_max = np.asarray(res_norm, float), np.asarray(res_max, float)
+    if res_norm.size == 0:
+        return np.array([np.inf, -1.0, 0.0, np.inf])
+    nan = np.isnan(res_norm)
+    k = int(np.argmax(nan)) if nan.any() else int(np.argmin(res_norm))
+    return np.array([res_norm[k], float(offset + k), res_max[k], np.min(res_max)])
+
+
+def b2_merge(rows):
+    """numpy mirror of mode 6: merge rank-ordered shard summaries -> (best, index, best_max, min_max)."""
+    import numpy as np
+
+    rows = np.asarray(rows, float)
+    ok = rows[:, 1] >= 0
+    cand = rows[ok]
+    nan = np.isnan(cand[:, 0])
+    if nan.any():
+        c = cand[nan]
+        j = int(np.argmin(c[:, 1]))
+    else:
+        c = cand
+        j = int(np.lexsort((c[:, 1], c[:, 0]))[0])
+    return float(c[j, 0]), int(c[j, 1]), float(c[j, 2]), float(np.min(rows[:, 3]))
+
+
+def b2_global_best(local_aug, local_feasible, offset: int, group=None):
+    """Global ranking (solver_batch.py:471): argmin of aug over feasible members of the whole batch, first
+    global index on ties; one all-gather of (best aug, index) per solve."""
+    import numpy as np
+
+    aug = np.where(np.asarray(local_feasible, bool), np.asarray(local_aug, float), np.inf)
+    if aug.size and np.isfinite(aug).any():
+        k = int(np.argmin(aug))
+        mine = torch.tensor([aug[k], float(offset + k)], dtype=torch.float64)
+    else:
+        mine = torch.tensor([np.inf, -1.0], dtype=torch.float64)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        parts = [torch.empty(2, dtype=torch.float64, device=dev) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(parts, mine.to(dev), group=group)
+        rows = np.stack([p.cpu().numpy() for p in parts])
+    else:
+        rows = mine.numpy()[None]
+    rows = rows[rows[:, 1] >= 0]
+    if rows.size == 0:
+        return None
+    return int(rows[np.lexsort((rows[:, 1], rows[:, 0]))[0], 1])
+
+
+def solve_batch_opt_sharded(problem, params=None, *, samples=None, mean=None, covariance=None, seed=0, group=None,
+                            use_graph=True):
+    """solve_batch_opt over all ranks of `group`: every rank draws the same samples (same seed), keeps its
+    contiguous member range, and the batch-global rho decisions are merged each iteration (see above).
+    Returns this rank's RankedSolutions (local members, best_index = GLOBAL index or None)."""
+    import numpy as np
+
+    from . import solver_batch as SB
+
+    params = params or SB.BatchParams()
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    struct = SB._structure_for(problem)
+    if samples is None:
+        samples = SB._default_samples(problem, struct.m, mean, covariance, seed)
+    samples = np.asarray(samples, float)
+    if samples.shape[0] < world:
+        raise ValueError("fewer members than ranks")
+    lo, hi = shard_range(samples.shape[0], rank, world)
+    state = SB.init_state(problem, samples[lo:hi], params)
+    lv = SB._levels(struct, float(state.rho), float(state.rho_psi), params.rho_growth, params.rho_cap)
+    eng = SB._Engine(struct, hi - lo, lv, params=params, max_hist=params.max_iter, member_offset=lo)
+    eng.load(state, 0)
+    gathered = torch.zeros((world, 4), dtype=torch.float64, device=eng.device)
+    n_iter = int(params.max_iter)
+    if n_iter > 0:
+        SB._ensure_factors(state, lv, 0)
+        eng.prime(False)
+    for _ in range(n_iter):
+        eng.iterate()
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, eng.shard, group=group)
+        else:
+            gathered.copy_(eng.shard[None])
+        eng.merge(gathered)
+    eng.run_mode(3, eng.flags)
+    got = eng.fetch(("ints", "hist", "rank", "xi", "xi_psi", "psi", "lam", "lam_psi"))
+    n_hist = int(got["ints"][3])
+    hist = got["hist"][:n_hist] if n_iter > 0 else np.zeros((0, 4))
+    if n_iter > 0:
+        for name in ("xi", "xi_psi", "psi", "lam", "lam_psi"):
+            setattr(state, name, got[name])
+        state.iteration += n_iter
+        used = SB._rho_level(lv, float(hist[-1, 2]), lv.rho_psi[lv.rho.index(float(hist[-1, 2]))])
+        for k in range(1, used + 1):
+            SB._ensure_factors(state, lv, k)
+        level = int(got["ints"][0])
+        state.rho, state.rho_psi = lv.rho[level], lv.rho_psi[level]
+        state._imply(struct)
+    rank_arr = got["rank"]
+    feasible = (rank_arr[:, 0] <= params.tol) & SB._feasible_from_rank(rank_arr, problem, params.d_margin,
+                                                                      params.kin_margin)
+    costs = rank_arr[:, 5].copy()
+    aug = costs + state.rho * rank_arr[:, 1]
+    best = b2_global_best(aug, feasible, lo, group)
+    return SB.RankedSolutions(
+        trajectories=SB._TrajectoryList(problem.basis, state.xi, state.psi, struct.m), costs=costs, aug_costs=aug,
+        residual_max=rank_arr[:, 0].copy(), residual_norm=rank_arr[:, 1].copy(), feasible=feasible, best_index=best,
+        best_history=[{"norm": float(h[0]), "max_abs": float(h[1]), "rho": float(h[2])} for h in hist],
+        iterations=state.iteration, n_factorizations=state.n_factorizations, state=state)

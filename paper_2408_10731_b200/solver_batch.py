@@ -395,7 +395,7 @@ class _Engine:
     """Device-resident state of one batch and the tro_b2_run launch sequence."""
 
     def __init__(self, struct: _Structure, n_b: int, levels: _Levels, *, params: BatchParams | None = None,
-                 max_hist: int = 0, geo: bool = False, device=None):
+                 max_hist: int = 0, geo: bool = False, device=None, member_offset: int | None = None):
         _lib.require_cuda()
         self.lib = _lib.load()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -422,6 +422,10 @@ class _Engine:
         self.hist = torch.zeros((max(self.max_hist, 1), 4), **f64)
         self.ints = torch.zeros(5, **i32)  # level, iteration, last_change, n_hist, n_changes
         self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        # sharded batch (multi-GPU Alg. 2): mode 0 writes this shard's summary; mode 6 merges them
+        self.member_offset = member_offset
+        self.shard = torch.zeros(4, **f64) if member_offset is not None else None
+        self.shards_in = None
         self.geo = {}
         if geo:
             self._alloc_geo()
@@ -465,7 +469,8 @@ class _Engine:
             res_max=P(self.res_max), res_norm=P(self.res_norm), ring=P(self.ring), hist=P(self.hist),
             level=base, iteration=base + 4, last_change=base + 8, n_hist=base + 12, n_changes=base + 16,
             counter=P(self.counter), psi=P(self.psi), rank=P(self.rank),
-            psi_targets=P(self.psi_targets) if self.psi_targets is not None else None, **g)
+            psi_targets=P(self.psi_targets) if self.psi_targets is not None else None,
+            shard=P(self.shard), shards_in=P(self.shards_in), **g)
 
     # ---- host <-> device
     def _pinned(self, name, like):
@@ -507,10 +512,13 @@ class _Engine:
         for k in _GEO:
             self.geo[k].copy_(torch.as_tensor(np.ascontiguousarray(geo[k], dtype=np.float64)))
 
-    def run_mode(self, mode: int, flags: int | None = None):
+    def run_mode(self, mode: int, flags: int | None = None, n_shards: int = 0):
+        fl = int(self.flags if flags is None else flags)
+        if self.member_offset is not None and mode == 0:
+            fl |= _lib.TRO_B2_SHARD
         prm = _lib.B2Params(tol=float(self.params.tol), stall_improvement=float(self.params.stall_improvement),
-                            stall_window=int(self.params.stall_window),
-                            flags=int(self.flags if flags is None else flags))
+                            stall_window=int(self.params.stall_window), flags=fl,
+                            member_offset=int(self.member_offset or 0), n_shards=int(n_shards))
         with torch.cuda.device(self.device):
             rc = self.lib.tro_b2_run(mode, ctypes.byref(self.dims), ctypes.byref(self.consts),
                                      ctypes.byref(self.state), ctypes.byref(prm), _lib.stream_handle())
@@ -521,6 +529,13 @@ class _Engine:
 
     def iterate(self, schedule: bool = True):
         self.run_mode(0, self.flags | (0 if schedule else _lib.TRO_FLAG_NO_SCHEDULE))
+
+    def merge(self, gathered: torch.Tensor):
+        """Mode 6: merge the all-gathered shard summaries (world x 4, rank order), apply the schedule."""
+        if self.shards_in is None or self.shards_in.data_ptr() != gathered.data_ptr():
+            self.shards_in = gathered
+            self._state_struct()
+        self.run_mode(6, n_shards=int(gathered.shape[0]))
 
     def _capture(self, n: int):
         g = torch.cuda.CUDAGraph()

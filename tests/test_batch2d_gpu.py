@@ -443,3 +443,49 @@ def test_c2alt_recipe_matches_oracle():
     assert rel(ranked.residual_max, out["rmax"]) <= TOL
     np.testing.assert_array_equal(ranked.feasible, out["feasible"])
     assert ranked.best_index == out["best"]
+
+
+# ------------------------------------------------------------------ multi-GPU semantics on one GPU
+def test_sharded_batch_is_bitwise_the_single_batch():
+    """Two member shards, each with its own engine, merged every iteration exactly as the ranks of a
+    multi-GPU run do (shard summary -> all-gather -> mode 6): bitwise the single-batch solve."""
+    import torch
+
+    prob = scenarios.batch2d_problem(n_o=50, n_batch=64)
+    samples = SB._default_samples(prob, prob.basis.n_var, None, None, 0)
+    params = SB.BatchParams(max_iter=60)
+    ref = SB.solve_batch_opt(prob, params, samples=samples)
+    struct = SB._structure_for(prob)
+    lv = SB._levels(struct, 1.0, 1.0, params.rho_growth, params.rho_cap)
+    engs = []
+    for lo, hi in ((0, 27), (27, 64)):
+        e = SB._Engine(struct, hi - lo, lv, params=params, max_hist=60, member_offset=lo)
+        e.load(SB.init_state(prob, samples[lo:hi], params), 0)
+        e.prime(False)
+        engs.append(e)
+    gathered = torch.zeros((2, 4), dtype=torch.float64, device="cuda")
+    for _ in range(60):
+        for e in engs:
+            e.iterate()
+        gathered.copy_(torch.stack([e.shard for e in engs]))
+        for e in engs:
+            e.merge(gathered)
+    np.testing.assert_array_equal(torch.cat([e.xi for e in engs]).cpu().numpy(), ref.state.xi)
+    np.testing.assert_array_equal(torch.cat([e.lam for e in engs]).cpu().numpy(), ref.state.lam)
+    h = np.array([[x["norm"], x["max_abs"], x["rho"]] for x in ref.best_history])
+    for e in engs:
+        np.testing.assert_array_equal(e.hist[:60, :3].cpu().numpy(), h)
+        assert e.ints_host()["level"] == engs[0].ints_host()["level"]
+
+
+def test_sharded_entry_point_single_rank():
+    from paper_2408_10731_b200.distributed import solve_batch_opt_sharded
+
+    prob = scenarios.batch2d_problem(n_o=50, n_batch=48)
+    params = SB.BatchParams(max_iter=40)
+    ref = SB.solve_batch_opt(prob, params, seed=5)
+    got = solve_batch_opt_sharded(prob, params, seed=5)
+    np.testing.assert_array_equal(got.state.xi, ref.state.xi)
+    np.testing.assert_array_equal(got.feasible, ref.feasible)
+    assert got.best_index == ref.best_index and got.n_factorizations == ref.n_factorizations
+    assert [h["rho"] for h in got.best_history] == [h["rho"] for h in ref.best_history]

@@ -66,3 +66,59 @@ def test_two_rank_gather_matches_single_rank():
     for _, merged in got:
         assert merged == single
     assert single["best_member"] == 3 and single["members"] == n and single["converged"] == int(conv.sum())
+
+
+# ------------------------------------------------------------------ Alg. 2: batch-global rho across ranks
+def _b2_truth(res_norm, res_max):
+    nan = np.isnan(res_norm)
+    k = int(np.argmax(nan)) if nan.any() else int(np.argmin(res_norm))
+    return res_norm[k], k, res_max[k], np.min(res_max)
+
+
+def _b2_worker(rank, world, port, res_norm, res_max, aug, feas, out_q):
+    from paper_2408_10731_b200.distributed import b2_global_best, b2_local_summary, b2_merge
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_range(len(res_norm), rank, world)
+    mine = torch.tensor(b2_local_summary(res_norm[lo:hi], res_max[lo:hi], lo))
+    parts = [torch.empty(4, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    merged = b2_merge(torch.stack(parts).numpy())
+    best = b2_global_best(aug[lo:hi], feas[lo:hi], lo)
+    out_q.put((rank, merged, best))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["ties", "nan"])
+def test_alg2_shard_summaries_merge_to_the_batch_decision(case):
+    """Two gloo ranks: the per-iteration shard summaries of a sharded Alg. 2 batch, all-gathered and merged
+    in rank order, give the single-batch argmin / min (solver_batch.py:454-460) and the final ranking."""
+    rng = np.random.default_rng(1)
+    n = 41
+    res_norm = np.round(rng.uniform(0, 1, n), 2)
+    res_norm[[7, 33]] = res_norm.min() - 0.25  # tie across the shard boundary: first index wins
+    res_max = rng.uniform(0, 1, n)
+    if case == "nan":
+        res_norm[[25, 30]] = np.nan  # numpy's argmin returns the first NaN
+        res_max[12] = np.nan
+    aug = np.round(rng.uniform(0, 3, n), 1)
+    feas = rng.uniform(0, 1, n) < 0.6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_b2_worker, args=(r, 2, port, res_norm, res_max, aug, feas, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    b, k, bm, mm = _b2_truth(res_norm, res_max)
+    full = np.where(feas, aug, np.inf)
+    for _, (mb, mk, mbm, mmm), best in got:
+        assert mk == k
+        assert (np.isnan(b) and np.isnan(mb)) or mb == b
+        assert mbm == bm or (np.isnan(bm) and np.isnan(mbm))
+        assert (np.isnan(mm) and np.isnan(mmm)) or mmm == mm
+        assert best == int(np.argmin(full))
