@@ -128,6 +128,13 @@ int tro_alg1_init(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_const
 int tro_alg1_iterate(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
                      const tro_alg1_state* s, const tro_alg1_params* p, void* stream);
 
+/* Up to n_iter fused AM iterations per member in ONE launch (one CTA loops its member; members are
+ * independent, so no grid synchronisation): bitwise the same as n_iter tro_alg1_iterate calls, each member
+ * stopping at convergence / factor failure.  For small batches (C1) it removes n launches and their
+ * pipeline fills; large batches keep the TMA-pipelined tro_alg1_iterate. */
+int tro_alg1_iterate_n(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                       const tro_alg1_state* s, const tro_alg1_params* p, int32_t n_iter, void* stream);
+
 /* ------------------------------------------------------------------ PRIEST / CEM (Alg. 3) */
 typedef struct tro_priest_dims {
     int64_t n_samples; /* N */

@@ -24,6 +24,9 @@ from . import _lib, qpcore
 from .basis import BasisSet, boundary_matrix, line_basis_vectors
 
 
+LOOP_MAX_MEMBERS = 64  # batches up to this size run all iterations in one launch (tro_alg1_iterate_n)
+
+
 def rho_chain(r0: float, growth: float, cap: float) -> list[float]:
     """Distinct penalty values reached from r0 by repeated min(r * growth, cap) (solver_single.py:401-402)."""
     vals = [float(r0)]
@@ -32,6 +35,22 @@ def rho_chain(r0: float, growth: float, cap: float) -> list[float]:
         if nxt == vals[-1] or len(vals) > 10000:
             return vals
         vals.append(nxt)
+
+
+_TABLE_CACHE: dict = {}
+
+
+def level_table(basis: BasisSet, n_o: int, w_smooth: float, w_track: float, starts, growth: float, cap: float,
+                cond_limit: float = 1e12) -> "LevelTable":
+    """LevelTable cached by content (22 saddle factorizations + inverses cost milliseconds on the host)."""
+    key = (basis.P.tobytes(), basis.Pddot.tobytes(), int(n_o), float(w_smooth), float(w_track),
+           tuple(sorted(set(float(r) for r in starts))), float(growth), float(cap), float(cond_limit))
+    t = _TABLE_CACHE.get(key)
+    if t is None:
+        if len(_TABLE_CACHE) > 64:
+            _TABLE_CACHE.clear()
+        t = _TABLE_CACHE[key] = LevelTable(basis, n_o, w_smooth, w_track, starts, growth, cap, cond_limit)
+    return t
 
 
 class LevelTable:
@@ -103,8 +122,8 @@ class Alg1Engine:
 
         # ---- constants
         rho0 = np.full(B, params.rho_start) if rho0 is None else np.broadcast_to(np.asarray(rho0, float), (B,))
-        self.table = LevelTable(basis, n_o, w_smooth, w_track, np.unique(rho0), params.rho_growth, params.rho_cap,
-                                cond_limit)
+        self.table = level_table(basis, n_o, w_smooth, w_track, np.unique(rho0), params.rho_growth, params.rho_cap,
+                                 cond_limit)
         self.basis = basis
         self.P = torch.as_tensor(np.array(basis.P, dtype=float, copy=True), **f64)
         self.tracks = torch.as_tensor(np.ascontiguousarray(np.transpose(tracks, (0, 2, 1))) if n_o else
@@ -141,6 +160,7 @@ class Alg1Engine:
         self.xi = torch.zeros((B, dim, m), **f64)
         self.pos = torch.zeros((B, dim, n_p), **f64)
         self.sums = torch.zeros((B, 2, dim, n_p), **f64)
+        self.rho0_dev = torch.as_tensor(rho0.copy(), **f64)
         self.rho = torch.as_tensor(rho0.copy(), **f64)
         self.rho_o = torch.as_tensor(rho0.copy(), **f64)
         self.ring = torch.zeros((B, 2 * params.stall_window), **f64)
@@ -231,6 +251,23 @@ class Alg1Engine:
     def iterate(self, d_mode: int = 2, flags: int = 0):
         self._call("tro_alg1_iterate", d_mode, flags)
 
+    def iterate_n(self, n: int, d_mode: int = 2):
+        """n AM iterations in ONE launch (each CTA loops its member until converged / n)."""
+        prm = self._params(d_mode, self.base_flags)
+        with torch.cuda.device(self.device):
+            rc = self.lib.tro_alg1_iterate_n(self.code, ctypes.byref(self._dims), ctypes.byref(self._consts),
+                                             ctypes.byref(self._state), ctypes.byref(prm), int(n),
+                                             ctypes.c_void_p(_lib.stream_handle()))
+        _lib.check(rc, "tro_alg1_iterate_n")
+
+    def reset_cold(self):
+        """Reuse this engine for a new cold-start solve of the same problem (penalties back to rho0)."""
+        self.rho.copy_(self.rho0_dev)
+        self.rho_o.copy_(self.rho0_dev)
+        self.level.copy_(self.level0)
+        self.iteration.zero_()
+        self.reset_schedule()
+
     def reset_schedule(self):
         """Solve-local bookkeeping of solve_single (history, last_change) restarts per call."""
         self.last_change.zero_()
@@ -252,7 +289,8 @@ class Alg1Engine:
                 self.iterate(2)
         self._graph, self._graph_n = g, n
 
-    def run(self, n_iter: int, *, use_graph: bool = True, chunk: int = 25, check_every: int = 0) -> int:
+    def run(self, n_iter: int, *, use_graph: bool = True, chunk: int = 25, check_every: int = 0,
+            loop: bool | None = None) -> int:
         """n_iter AM iterations (the first with the primed d_mode).  Returns iterations launched.
 
         check_every > 0 stops early (host sync every `check_every` iterations) once every
@@ -260,6 +298,13 @@ class Alg1Engine:
         done = 0
         if n_iter <= 0:
             return 0
+        if loop is None:
+            loop = self.B <= LOOP_MAX_MEMBERS
+        if loop:  # small batches: one launch for all iterations (members stop at convergence on device)
+            self.iterate(self.first_d_mode)
+            if n_iter > 1:
+                self.iterate_n(n_iter - 1)
+            return n_iter
         self.iterate(self.first_d_mode)
         done = 1
         since_check = 1

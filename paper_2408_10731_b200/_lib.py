@@ -31,6 +31,7 @@ EXPORTS = (
     "tro_alg1_prime",
     "tro_alg1_init",
     "tro_alg1_iterate",
+    "tro_alg1_iterate_n",
     "tro_kkt_apply_f64",
     "tro_topk_stable_f64",
     "tro_topk_workspace_bytes",
@@ -208,6 +209,8 @@ def load() -> ctypes.CDLL:
         f = getattr(lib, name)
         f.argtypes = [c_int32] + sig
         f.restype = c_int32
+    lib.tro_alg1_iterate_n.argtypes = [c_int32] + sig[:4] + [c_int32, c_void_p]
+    lib.tro_alg1_iterate_n.restype = c_int32
     lib.tro_kkt_apply_f64.argtypes = [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p]
     lib.tro_kkt_apply_f64.restype = c_int32
     lib.tro_topk_stable_f64.argtypes = [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_int64, c_void_p]

@@ -47,6 +47,7 @@ struct Alg1Args {
     tro_alg1_state s;
     tro_alg1_params p;
     int32_t G;
+    int32_t n_loop;  // MODE 3: AM iterations per launch
 };
 
 struct SmemLayout {
@@ -133,8 +134,10 @@ namespace tro {
 // an immediate offset.
 template <int DIM, typename T, bool UNIT, int MODE, int NP>
 __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1Args A) {
-    // MODE 0: AM iteration; 1: prime (sums + residual of the current state); 2: cold init + prime
-    constexpr bool prime = MODE != 0;
+    // MODE 0: AM iteration; 1: prime (sums + residual of the current state); 2: cold init + prime;
+    // 3: A.n_loop AM iterations in one launch (each CTA loops its own member: members are independent,
+    //    so no grid-wide synchronisation is needed; small batches skip n launches + pipeline fills)
+    constexpr bool prime = MODE == 1 || MODE == 2;
     constexpr bool init = MODE == 2;
     constexpr int W = Words<DIM, UNIT>::W;
     extern __shared__ double smem[];
@@ -160,6 +163,8 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     double* sXi = smem + L.xi;
     double* sWarp = smem + L.warp;
 
+    for (int rep_ = 0; rep_ < (MODE == 3 ? A.n_loop : 1); ++rep_) {
+    if (MODE == 3 && rep_ > 0) __syncthreads();  // the previous iteration's writes (tid 0: status, level, rho)
     // ---------------- frozen members (converged / failed) do nothing
     const int status0 = A.s.status[i];
     if (!prime && (status0 & (TRO_CONVERGED | TRO_FACTOR_FAILED))) return;
@@ -379,6 +384,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         A.s.res_max[i] = mm;
         if constexpr (!prime) alg1_schedule(A, i, status0, level, rho, rho_o, nrm, mm);
     }
+    }  // rep_
 }
 
 template <int DIM, typename T, bool UNIT, int MODE, int NP>
@@ -453,10 +459,12 @@ static int launch(const Alg1Args& A, int mode, cudaStream_t st) {
             return launch_mode<DIM, T, UNIT, 0, 100>(A, st);
         }
         if (mode == 1) return launch_mode<DIM, T, UNIT, 1, 100>(A, st);
+        if (mode == 3) return launch_mode<DIM, T, UNIT, 3, 100>(A, st);
         return launch_mode<DIM, T, UNIT, 2, 100>(A, st);
     }
     if (mode == 0) return launch_mode<DIM, T, UNIT, 0, 0>(A, st);
     if (mode == 1) return launch_mode<DIM, T, UNIT, 1, 0>(A, st);
+    if (mode == 3) return launch_mode<DIM, T, UNIT, 3, 0>(A, st);
     return launch_mode<DIM, T, UNIT, 2, 0>(A, st);
 }
 
@@ -478,7 +486,7 @@ static int auto_groups(const tro_alg1_dims* d) {
 }
 
 static int run(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c, const tro_alg1_state* s,
-               const tro_alg1_params* p, void* stream, int mode) {
+               const tro_alg1_params* p, void* stream, int mode, int n_loop = 1) {
     if (!dims || !c || !s || !p) return TRO_EINVAL;
     if (dims->dim != 2 && dims->dim != 3) return TRO_EINVAL;
     if (dims->m < 1 || dims->m > kMaxM || dims->m + dims->n_eq > kMaxNk) return TRO_EINVAL;
@@ -493,6 +501,7 @@ static int run(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* 
     A.s = *s;
     A.p = *p;
     A.G = auto_groups(dims);
+    A.n_loop = n_loop;
     const SmemLayout L = smem_layout(dims->n_p, dims->m, dims->dim, dims->n_obs, A.G);
     if ((size_t)L.total * sizeof(double) > 200 * 1024) return TRO_EINVAL;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -512,6 +521,13 @@ extern "C" int tro_alg1_prime(int32_t dtype, const tro_alg1_dims* dims, const tr
 extern "C" int tro_alg1_iterate(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
                                 const tro_alg1_state* s, const tro_alg1_params* p, void* stream) {
     return tro::run(dtype, dims, c, s, p, stream, 0);
+}
+
+extern "C" int tro_alg1_iterate_n(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
+                                  const tro_alg1_state* s, const tro_alg1_params* p, int32_t n_iter, void* stream) {
+    if (n_iter < 0) return TRO_EINVAL;
+    if (n_iter == 0) return 0;
+    return tro::run(dtype, dims, c, s, p, stream, 3, n_iter);
 }
 
 extern "C" int tro_alg1_init(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,

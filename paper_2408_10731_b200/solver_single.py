@@ -148,6 +148,29 @@ def _engine_for(problem: SingleProblem, params: SingleParams, *, rho0=None, expo
                       export=export, keep_d=True)
 
 
+_ENGINE_CACHE: dict = {}
+
+
+def _cached_engine(problem: SingleProblem, params: SingleParams, *, max_hist: int) -> Alg1Engine:
+    """Cold-start engines reused across solve_single calls on the same problem content and parameters:
+    the device buffers, constants and level table are built once (one solver per stream)."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=20)
+    b = problem.basis
+    for arr in (b.P, b.Pdot, b.Pddot, problem.desired, _tracks(problem), *_shapes(problem),
+                np.stack([bc.values() for bc in problem.boundary])):
+        h.update(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
+    key = (h.digest(), problem.w_smooth, problem.w_track, params.rho_start, params.rho_growth, params.rho_cap,
+           params.tol, params.stall_window, params.stall_improvement, int(max_hist), torch.cuda.current_device())
+    eng = _ENGINE_CACHE.get(key)
+    if eng is None:
+        if len(_ENGINE_CACHE) > 16:
+            _ENGINE_CACHE.clear()
+        eng = _ENGINE_CACHE[key] = _engine_for(problem, params, max_hist=max_hist)
+    return eng
+
+
 def _upload(eng: Alg1Engine, state: SingleState):
     dim = eng.dim
     if eng.n_o:
@@ -251,7 +274,8 @@ def solve_single(problem: SingleProblem, params: SingleParams | None = None,
     """AM loop until max_abs <= tol or max_iter (solver_single.py:407-450), fully on device."""
     params = params or SingleParams()
     if state is None:
-        eng = _engine_for(problem, params, max_hist=max(params.max_iter, 1))
+        eng = _cached_engine(problem, params, max_hist=max(params.max_iter, 1))
+        eng.reset_cold()
         eng.cold_init()
         state = SingleState(xi=None, d=None, alpha=None, beta=None, cos_a=None, sin_a=None, cos_b=None,
                             sin_b=None, lam_pos=None, lam_cos_a=None, lam_sin_a=None, lam_cos_b=None,
