@@ -112,10 +112,16 @@ def fp64_peak_tflops():
 
 def run_c4(args):
     import torch
+    import torch.distributed as tdist
 
     from paper_2408_10731_b200 import solver_priest as SP
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     setup, dist, c1 = c4_problem()
     n_o, N, n_inner, desc = CONFIGS["c4"]
     params = SP.PriestParams(n_outer=C4_ROUNDS, n_batch=N, n_constraint_elite=C4_NCE, n_elite=C4_NEL,
@@ -124,49 +130,59 @@ def run_c4(args):
     z_host = np.stack([rng.standard_normal((N, dist.mu.size)) for _ in range(C4_ROUNDS)])  # the sampler's stream
     z_dev = torch.as_tensor(z_host, device="cuda")
     z_pin = torch.as_tensor(z_host).pin_memory()
+    # one GPU: the single-device rounds; N GPUs: sample shards + one candidate all-gather per round
+    opt = SP.priest_optimize if world == 1 else SP.priest_optimize_sharded
+
+    def timed(fn):
+        if world > 1:
+            tdist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / 1e3 / args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item()), out
+
     for _ in range(args.warmup):
-        SP.priest_optimize(setup, c1, dist, params, z_rounds=z_dev)
+        opt(setup, c1, dist, params, z_rounds=z_dev)
     torch.cuda.synchronize()
-    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks = ClockSampler(local)
     clocks.start()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(args.steps):
-        res = SP.priest_optimize(setup, c1, dist, params, z_rounds=z_dev)
-    b.record()
-    torch.cuda.synchronize()
+    step_s, res = timed(lambda: opt(setup, c1, dist, params, z_rounds=z_dev))
     clk = clocks.stop()
-    step_s = a.elapsed_time(b) / 1e3 / args.steps
     # e2e: standard normals from pinned host memory each round, results back on the host
-    a.record()
-    for _ in range(args.steps):
-        res = SP.priest_optimize(setup, c1, dist, params, z_rounds=z_pin)
-    b.record()
-    torch.cuda.synchronize()
-    e2e_s = a.elapsed_time(b) / 1e3 / args.steps
+    e2e_s, res = timed(lambda: opt(setup, c1, dist, params, z_rounds=z_pin))
     # dominant kernel (projection) alone, CUDA events on its stream
     d = setup.device()
     d["L"].copy_(torch.as_tensor(SP._draw_factor(dist.sigma_mat)))
     d["mu"].copy_(torch.as_tensor(dist.mu))
-    SP._run_project(setup, z=z_dev[0], n_inner=n_inner)
+    z_shard = z_dev[0][rank * (N // world):(rank + 1) * (N // world)].contiguous()
+    SP._run_project(setup, z=z_shard, n_inner=n_inner)
     torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(3):
-        SP._run_project(setup, z=z_dev[0], n_inner=n_inner)
+        SP._run_project(setup, z=z_shard, n_inner=n_inner)
     b.record()
     torch.cuda.synchronize()
     kern_s = a.elapsed_time(b) / 1e3 / 3
-    flops = 32.0 * N * n_o * 100 * n_inner  # 32 flop per sample-obstacle-timestep-inner-it
+    n_loc = N // world
+    flops = 32.0 * n_loc * n_o * 100 * n_inner  # 32 flop per sample-obstacle-timestep-inner-it
     peak = fp64_peak_tflops()
     value = N * n_inner * C4_ROUNDS / step_s
     line = {
         "metric": "sample-inner-iterations/sec (PRIEST projection, CEM rounds)",
-        "value": value, "unit": "sample-inner-it/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "value": value, "unit": "sample-inner-it/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_s * 1e3, "ms_per_round": step_s * 1e3 / C4_ROUNDS, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded C4 scene, numpy standard normals of the reference sampler)",
         "config": {"workload": desc, "samples": N, "n_obs": n_o, "n_p": 100, "n_inner": n_inner,
-                   "rounds": C4_ROUNDS, "constraint_elites": C4_NCE, "elites": C4_NEL, "l2": "on-chip (FP-bound)"},
+                   "rounds": C4_ROUNDS, "constraint_elites": C4_NCE, "elites": C4_NEL, "l2": "on-chip (FP-bound)",
+                   "parallelism": f"sample-shard x{world} (+ candidate all-gather / round)"},
         "roofline": {"bound": "fp64", "achieved": flops / kern_s / 1e12, "peak": peak, "unit": "TFLOP/s",
                      "frac": flops / kern_s / 1e12 / peak, "traffic": None,
                      "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)",
@@ -178,11 +194,14 @@ def run_c4(args):
         "gpu_launches": args.steps * C4_ROUNDS * 5,
         "result": {"best_aug_cost": res.history[-1]["best_aug_cost"], "best_residual": res.best.residual},
     }
-    if not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_c4()
         line["cpu_baseline"] = {"value": v, "unit": "sample-inner-it/s", "cores": info["cores"], "kind": "port",
                                 "sample": info["sample"]}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
 
 
 def c3_problems(lo, hi):

@@ -493,3 +493,97 @@ def barn_cost(pos: np.ndarray, vel: np.ndarray, acc: np.ndarray, line_start, lin
         along = rel @ (axis / length)
         dist2 = (rel**2).sum(axis=1) - along**2
     return smooth + c_kappa + float(np.sum(np.maximum(dist2, 0.0)))
+
+
+# ---------------------------------------------------------------- multi-GPU (sample sharding)
+class ShardedRound:
+    """One priest_optimize round split into a per-rank LOCAL phase and a replicated GLOBAL phase.
+
+    local(z_shard, lo): project this rank's samples [lo, hi), keep its stable top-min(N_ce, n) by score and
+    pack (score, global index, xi, sample) rows.  The rank-ordered all-gather of those rows lists equal
+    scores in ascending global index (ranks own contiguous ranges and each block is in stable order), so a
+    stable top-k over the gathered scores IS the global np.argsort(scores, kind="stable")[:N_ce]
+    (solver_priest.py:358).  global_(rows) then runs the costs, the elite top-k and the refit on the
+    gathered rows; every rank computes it identically, so mu / Sigma stay replicated with no broadcast and
+    the result is bitwise the single-GPU round."""
+
+    def __init__(self, setup: ProjectionSetup, c1, params: PriestParams):
+        self.setup, self.c1, self.params = setup, c1, params
+        d = setup.device()
+        self.dev = d["device"]
+        self.dm = setup.dim * setup.m
+        self.line = c1.line(self.dev) if isinstance(c1, BarnCost) else None
+
+    def local(self, z_shard: torch.Tensor, lo: int) -> torch.Tensor:
+        p = self.params
+        xi, scores, _, smp = _run_project(self.setup, z=z_shard, n_inner=p.n_inner, keep_samples=True)
+        k = min(p.n_constraint_elite, int(scores.numel()))
+        cand = _topk(scores, k)
+        return torch.cat([scores[cand, None], (cand + lo).double()[:, None], xi[cand], smp[cand]], dim=1)
+
+    def global_(self, rows: torch.Tensor, mu: torch.Tensor, sig: torch.Tensor) -> dict:
+        p, dm = self.params, self.dm
+        g_scores = rows[:, 0].contiguous()
+        g_xi = rows[:, 2:2 + dm].contiguous()
+        keep = _topk(g_scores, min(p.n_constraint_elite, int(g_scores.numel())))
+        if self.line is not None:
+            aug = _run_cost(self.setup, g_xi, keep, g_scores, 1.0, p.residual_weight, 0.0, self.line)
+        else:
+            xk, sk = g_xi[keep].cpu().numpy(), g_scores[keep].cpu().numpy()
+            aug = torch.as_tensor(np.array([float(self.c1(self.setup.trajectory_of(xk[i]))) + p.residual_weight
+                                            * sk[i] for i in range(xk.shape[0])]), device=self.dev)
+        erank = _topk(aug, p.n_elite)
+        sel = keep[erank].contiguous()
+        ecost = aug[erank].contiguous()
+        _refit(g_xi, sel, ecost, p.sigma, p.gamma, mu, sig)
+        b = int(sel[0].item())
+        entry = torch.stack([ecost[0], g_scores[b], g_scores.min()]).cpu().numpy()
+        return {"entry": entry, "best_row": rows[b]}
+
+
+def priest_optimize_sharded(setup: ProjectionSetup, c1, distribution: SamplingDistribution,
+                            params: PriestParams | None = None, *, z_rounds=None, group=None) -> PriestResult:
+    """priest_optimize over the ranks of a torch.distributed group: samples shard into contiguous ranges
+    (n_batch % world == 0), one all-gather of the candidate rows per round (see ShardedRound)."""
+    import torch.distributed as dist
+
+    from .distributed import shard_range
+
+    params = params or PriestParams()
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    if params.n_batch % world:
+        raise ValueError("n_batch must be a multiple of the world size")
+    lo, hi = shard_range(params.n_batch, rank, world)
+    d = setup.device()
+    dev = d["device"]
+    rng = np.random.default_rng(params.seed)
+    mu = torch.as_tensor(distribution.mu.copy(), device=dev)
+    sig = torch.as_tensor(distribution.sigma_mat.copy(), device=dev)
+    sig_h = distribution.sigma_mat.copy()
+    rnd = ShardedRound(setup, c1, params)
+    history, best = [], None
+    for r in range(params.n_outer):
+        d["L"].copy_(torch.as_tensor(_draw_factor(sig_h)))
+        d["mu"].copy_(mu)
+        if z_rounds is not None:
+            z = torch.as_tensor(z_rounds[r][lo:hi], device=dev).contiguous()
+        else:  # every rank draws the whole round (the shared stream) and keeps its rows
+            z = torch.as_tensor(_draw_z(rng, params.n_batch, mu.numel())[lo:hi], device=dev).contiguous()
+        mine = rnd.local(z, lo)
+        if world > 1:
+            rows = torch.empty((world * mine.shape[0], mine.shape[1]), dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(rows, mine, group=group)
+        else:
+            rows = mine
+        out = rnd.global_(rows, mu, sig)
+        sig_h = sig.cpu().numpy()
+        e = out["entry"]
+        history.append({"best_aug_cost": float(e[0]), "best_residual": float(e[1]), "min_residual": float(e[2])})
+        if r == params.n_outer - 1:
+            row = out["best_row"].cpu().numpy()
+            dm = rnd.dm
+            bx = row[2:2 + dm]
+            best = ProjectedSample(original=row[2 + dm:2 + 2 * dm], projected=bx, residual=float(e[1]),
+                                   trajectory=setup.trajectory_of(bx), aug_cost=float(e[0]))
+    return PriestResult(best=best, mu=mu.cpu().numpy(), sigma_mat=sig_h, history=history, params=params)

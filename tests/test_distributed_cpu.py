@@ -122,3 +122,39 @@ def test_alg2_shard_summaries_merge_to_the_batch_decision(case):
         assert mbm == bm or (np.isnan(bm) and np.isnan(mbm))
         assert (np.isnan(mm) and np.isnan(mmm)) or mmm == mm
         assert best == int(np.argmin(full))
+
+
+# ------------------------------------------------------------------ PRIEST: candidate all-gather == global stable top-k
+def _topk_worker(rank, world, port, scores, k, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_range(len(scores), rank, world)
+    local = scores[lo:hi]
+    cand = np.argsort(local, kind="stable")[:min(k, hi - lo)]
+    mine = torch.tensor(np.stack([local[cand], cand + lo], axis=1))
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    rows = torch.cat(parts).numpy()
+    keep = np.argsort(rows[:, 0], kind="stable")[:k]
+    out_q.put((rank, rows[keep, 1].astype(np.int64)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("k", [5, 30])
+def test_priest_candidate_gather_is_the_global_stable_topk(k):
+    """ShardedRound's merge on two gloo ranks: local stable top-k, rank-ordered all-gather, stable top-k
+    of the gathered scores == np.argsort(all scores, kind='stable')[:k] (ties across the boundary)."""
+    rng = np.random.default_rng(2)
+    scores = np.round(rng.uniform(0, 1, 40), 1)  # many ties, across the shard boundary
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_topk_worker, args=(r, 2, port, scores, k, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for _, idx in got:
+        np.testing.assert_array_equal(idx, np.argsort(scores, kind="stable")[:k])

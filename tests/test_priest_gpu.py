@@ -176,3 +176,39 @@ def test_generic_paths_vs_oracle(degree, dim):
     xi = np.stack([p.projected for p in out])
     assert np.max(np.abs(xi - xi_ref)) <= 1e-10 * np.max(np.abs(xi_ref))
     close_scores(np.array([p.residual for p in out]), sc_ref)
+
+
+@pytest.mark.parametrize("n_ce", [48, 20])
+def test_sharded_rounds_are_bitwise_the_single_gpu_rounds(golden, n_ce):
+    """Multi-GPU PRIEST semantics on one GPU: 3 sample shards run their local phase (projection + local
+    stable top-k), their candidate rows are concatenated in rank order exactly as the all-gather
+    delivers them, and the replicated global phase (keep set, costs, elites, refit) reproduces the
+    single-GPU priest_optimize bit for bit.  n_ce 20 < shard size exercises the local pre-selection."""
+    g = golden("priest.npz")
+    st = setup_from(g, "p3")
+    dist = SP.SamplingDistribution(g["p3_mu0"], g["p3_sigma0"])
+    params = SP.PriestParams(n_outer=3, n_batch=96, n_constraint_elite=n_ce, n_elite=12, n_inner=30, seed=0)
+    c1 = SP.BarnCost(np.zeros(3), np.array([12.0, 0.0, 0.0]))
+    ref = SP.priest_optimize(st, c1, dist, params)
+    rng = np.random.default_rng(params.seed)
+    z_rounds = [rng.standard_normal((params.n_batch, dist.mu.size)) for _ in range(params.n_outer)]
+    d = st.device()
+    mu = torch.as_tensor(dist.mu.copy(), device="cuda")
+    sig = torch.as_tensor(dist.sigma_mat.copy(), device="cuda")
+    rnd = SP.ShardedRound(st, c1, params)
+    hist = []
+    for r in range(params.n_outer):
+        d["L"].copy_(torch.as_tensor(SP._draw_factor(sig.cpu().numpy())))
+        d["mu"].copy_(mu)
+        parts = [rnd.local(torch.as_tensor(z_rounds[r][lo:lo + 32], device="cuda").contiguous(), lo)
+                 for lo in (0, 32, 64)]
+        out = rnd.global_(torch.cat(parts), mu, sig)
+        hist.append(out["entry"])
+    np.testing.assert_array_equal(mu.cpu().numpy(), ref.mu)
+    np.testing.assert_array_equal(sig.cpu().numpy(), ref.sigma_mat)
+    np.testing.assert_array_equal(np.array(hist), np.array([[h["best_aug_cost"], h["best_residual"],
+                                                             h["min_residual"]] for h in ref.history]))
+    one = SP.priest_optimize_sharded(st, c1, dist, params)  # the entry point, world size 1
+    np.testing.assert_array_equal(one.mu, ref.mu)
+    np.testing.assert_array_equal(one.best.projected, ref.best.projected)
+    np.testing.assert_array_equal(one.best.original, ref.best.original)
