@@ -60,8 +60,9 @@ def parse():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--groups", type=int, default=0)
-    ap.add_argument("--layout", default="unit", choices=["unit", "angle"],
-                    help="per-element state layout (unit: 11 words, angle: the reference's 9 words)")
+    ap.add_argument("--layout", default="unit", choices=["unit", "angle", "half"],
+                    help="per-element state layout (unit: 11 words; angle: the reference's 9 words; half: 9 words, "
+                         "angles as folded half-angle tangents)")
     ap.add_argument("--members", type=int, default=0, help="override the member count (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

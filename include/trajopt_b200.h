@@ -59,6 +59,8 @@ typedef struct tro_alg1_dims {
 #define TRO_LAYOUT_ANGLE 0 /* 3-D [alpha beta lx ly lz lca lsa lcb lsb] (9 words), 2-D [alpha lx ly lca lsa] (5) */
 #define TRO_LAYOUT_UNIT 1  /* angles kept as unit vectors: 3-D [ca sa cb sb lx ly lz lca lsa lcb lsb] (11),
                               2-D [ca sa lx ly lca lsa] (6) */
+#define TRO_LAYOUT_HALF 2  /* the reference's word count (9 / 5), each angle as a folded half-angle tangent
+                              w: |w| <= 1: tan(a/2); else 3 sgn(w) + tan((a - pi sgn(w)) / 2) */
 
 typedef struct tro_alg1_consts {
     const double* P;         /* n_p x m, row-major (basis.py:143-177) */

@@ -16,6 +16,7 @@ tracks[j][axis][t] (fp64).  Per member (fp64): xi (dim, m), pos (dim, n_p), sums
 from __future__ import annotations
 
 import ctypes
+import math
 
 import numpy as np
 import torch
@@ -145,8 +146,8 @@ class Alg1Engine:
 
         # ---- state
         T = dict(dtype=dtype, device=dev)
-        if layout not in ("angle", "unit"):
-            raise ValueError("layout must be 'angle' or 'unit'")
+        if layout not in ("angle", "unit", "half"):
+            raise ValueError("layout must be 'angle', 'unit' or 'half'")
         self.layout = layout
         n_ang = 2 if dim == 3 else 1
         self.NV = n_ang * (2 if layout == "unit" else 1)
@@ -178,7 +179,8 @@ class Alg1Engine:
         self.n_changes = torch.zeros(B, **i32)
 
         self._dims = _lib.Alg1Dims(B, n_o, n_p, m, dim, self.n_eq, len(self.table.rhos), int(groups),
-                                   _lib.TRO_LAYOUT_UNIT if layout == "unit" else _lib.TRO_LAYOUT_ANGLE, 0)
+                                   {"unit": _lib.TRO_LAYOUT_UNIT, "half": _lib.TRO_LAYOUT_HALF}.get(
+                                       layout, _lib.TRO_LAYOUT_ANGLE), 0)
         self._consts = _lib.Alg1Consts(
             self.P.data_ptr(), self.tracks.data_ptr(), self.shape_a.data_ptr(), self.shape_b.data_ptr(),
             self.kinv.data_ptr(), self.level_rho.data_ptr(), self.level_ok.data_ptr(), self.q.data_ptr(),
@@ -195,11 +197,31 @@ class Alg1Engine:
         self.base_flags = 0 if use_tma else _lib.TRO_FLAG_NO_TMA
 
     # ------------------------------------------------------------ angle views
+    @staticmethod
+    def _half_angle(w: torch.Tensor) -> torch.Tensor:
+        """Angle of a folded half-angle tangent (half_decode in alg1_elem.cuh), in (-pi, pi]."""
+        w = w.double()
+        inner = w.abs() <= 1
+        sg = torch.where(torch.signbit(w), -1.0, 1.0).to(w)
+        t = torch.where(inner, w, w - 3.0 * sg)
+        ang = 2.0 * torch.atan(t)
+        return torch.where(inner, ang, ang + math.pi * sg)
+
+    @staticmethod
+    def _half_of(a: torch.Tensor) -> torch.Tensor:
+        c, s = torch.cos(a), torch.sin(a)
+        pos = c >= 0
+        sg = torch.where(torch.signbit(s), -1.0, 1.0).to(a)
+        t = s / torch.where(pos, 1.0 + c, 1.0 - c)
+        return torch.where(pos, t, 3.0 * sg - t)
+
     @property
     def alpha(self) -> torch.Tensor:
-        """(B, n_o, n_p) alpha (a view in the angle layout, atan2 of the stored unit vector otherwise)."""
+        """(B, n_o, n_p) alpha (a view in the angle layout, decoded from the stored words otherwise)."""
         if self.layout == "angle":
             return self.state[:, :, 0]
+        if self.layout == "half":
+            return self._half_angle(self.state[:, :, 0])
         return torch.atan2(self.state[:, :, 1], self.state[:, :, 0])
 
     @property
@@ -208,6 +230,8 @@ class Alg1Engine:
             return None
         if self.layout == "angle":
             return self.state[:, :, 1]
+        if self.layout == "half":
+            return self._half_angle(self.state[:, :, 1])
         return torch.atan2(self.state[:, :, 3], self.state[:, :, 2])
 
     def _set_angles(self, alpha, beta):
@@ -217,6 +241,12 @@ class Alg1Engine:
             self.state[:, :, 0].copy_(a.to(T))
             if self.dim == 3:
                 self.state[:, :, 1].copy_(torch.as_tensor(np.asarray(beta), device=self.device).to(T))
+            return
+        if self.layout == "half":
+            self.state[:, :, 0].copy_(self._half_of(a).to(T))
+            if self.dim == 3:
+                b = torch.as_tensor(np.asarray(beta), dtype=torch.float64, device=self.device)
+                self.state[:, :, 1].copy_(self._half_of(b).to(T))
             return
         self.state[:, :, 0].copy_(torch.cos(a).to(T))
         self.state[:, :, 1].copy_(torch.sin(a).to(T))

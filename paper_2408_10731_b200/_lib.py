@@ -24,6 +24,7 @@ TRO_FLAG_NO_SCHEDULE = 1
 TRO_FLAG_NO_TMA = 2
 TRO_LAYOUT_ANGLE = 0
 TRO_LAYOUT_UNIT = 1
+TRO_LAYOUT_HALF = 2
 TRO_EINVAL = -1
 
 # every symbol include/trajopt_b200.h declares (checked by tests/test_lib_exports.py)

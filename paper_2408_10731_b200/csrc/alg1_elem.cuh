@@ -46,34 +46,63 @@ __device__ __forceinline__ T max_abs(T acc, T v) {
 }
 
 // Per-element words of the persistent state.
-//   angle layout (UNIT = false, the reference's variables):
+//   angle layout (LAY 0, the reference's variables):
 //     3-D [alpha beta lx ly lz lca lsa lcb lsb] (9), 2-D [alpha lx ly lca lsa] (5)
-//   unit layout (UNIT = true): each angle is kept as its unit vector (cos, sin), which removes
+//   unit layout (LAY 1): each angle is kept as its unit vector (cos, sin), which removes
 //     the atan2 -> sincos round trip from every iteration at +2 (3-D) / +1 (2-D) words:
 //     3-D [ca sa cb sb lx ly lz lca lsa lcb lsb] (11), 2-D [ca sa lx ly lca lsa] (6)
-template <int DIM, bool UNIT>
+//   half layout (LAY 2): the reference's word count (9 / 5) with each angle stored as a folded
+//     half-angle tangent (half_encode): cos / sin come back through one reciprocal and a few FMAs
+//     (half_decode), so neither atan2 nor sin / cos runs per element and per iteration.
+constexpr int kLayAngle = 0, kLayUnit = 1, kLayHalf = 2;
+template <int DIM, int LAY>
 struct Words {
     static constexpr int NA = DIM == 3 ? 2 : 1;          // angles
     static constexpr int NL = DIM == 3 ? 7 : 4;          // multiplier planes
-    static constexpr int NV = UNIT ? 2 * NA : NA;        // words holding the angles
+    static constexpr int NV = LAY == kLayUnit ? 2 * NA : NA;  // words holding the angles
     static constexpr int W = NV + NL;
 };
+
+// Folded half-angle tangent of a unit vector (c, s) = (cos a, sin a):
+//   c >= 0: w = tan(a / 2) = s / (1 + c) in [-1, 1];
+//   c <  0: w = 3 sgn(s) + tan(b / 2) with b = a - pi sgn(s) (cos b = -c > 0): |w| in (2, 3].
+// Both branches divide by a number >= 1, so the encoding never loses precision (tan(a / 2) alone
+// blows up at a = pi).  Decoding is the rational parametrisation (1 - t^2, 2 t) / (1 + t^2).
+template <typename T>
+__device__ __forceinline__ T half_encode(T c, T s) {
+    const bool pos = c >= (T)0;
+    const T t = s * rcp_fast(pos ? (T)1 + c : (T)1 - c);
+    return pos ? t : copysign((T)3, s) - t;
+}
+template <typename T>
+__device__ __forceinline__ void half_decode(T w, T* c, T* s) {
+    const bool inner = fabs(w) <= (T)1;
+    const T t = inner ? w : w - copysign((T)3, w);
+    const T t2 = t * t;
+    const T q = rcp_fast((T)1 + t2);
+    const T cc = ((T)1 - t2) * q, ss = (T)2 * t * q;
+    *c = inner ? cc : -cc;
+    *s = inner ? ss : -ss;
+}
 
 // One AM iteration of one element.  v[W]: state words in / out.  d_old: the
 // line-of-sight scale of the previous iterate.  Outputs the new d, the angle
 // copies (for the optional export), and accumulates the residual norm/max and
 // the sums the next position step needs.
-template <int DIM, typename T, bool UNIT>
+template <int DIM, typename T, int LAY>
 __device__ __forceinline__ void am_element(T* v, double trx, double trY, double trz, double px, double py, double pz,
                                            T a, T b, T ia2, T ib2, T dold, T trho, T trho_o, double& sumsq,
                                            double& mx, double* accL, double* accT, T& dn, T* copies) {
     const T dx = (T)(px - trx), dy = (T)(py - trY);
     if constexpr (DIM == 3) {
         const T dz = (T)(pz - trz);
-        constexpr int o = UNIT ? 4 : 2;  // first multiplier word
+        constexpr int o = LAY == kLayUnit ? 4 : 2;  // first multiplier word
         T sa, ca, sb, cb;
-        if constexpr (UNIT) {
+        if constexpr (LAY == kLayUnit) {
             ca = v[0]; sa = v[1]; cb = v[2]; sb = v[3];
+        } else if constexpr (LAY == kLayHalf) {
+            half_decode(v[0], &ca, &sa);
+            half_decode(v[1], &cb, &sb);
         } else {
             sincos_fast(v[0], &sa, &ca);  // copy reset (solver_single.py:375-380)
             sincos_fast(v[1], &sb, &cb);
@@ -96,8 +125,11 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         T cA2, sA2, cB2, sB2;
         unit_dir(ca2, sa2, &cA2, &sA2);  // cos/sin(alpha') for residuals + next targets
         unit_dir(cb2, sb2, &cB2, &sB2);
-        if constexpr (UNIT) {
+        if constexpr (LAY == kLayUnit) {
             v[0] = cA2; v[1] = sA2; v[2] = cB2; v[3] = sB2;
+        } else if constexpr (LAY == kLayHalf) {
+            v[0] = half_encode(cA2, sA2);
+            v[1] = half_encode(cB2, sB2);
         } else {
             v[0] = atan2_fast(sa2, ca2);  // solver_single.py:242
             v[1] = atan2_fast(sb2, cb2);  // solver_single.py:271
@@ -128,10 +160,12 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         accT[1] += trY + (double)(adn * sA2 * sB2);
         accT[2] += trz + (double)(b * dn * cB2);
     } else {
-        constexpr int o = UNIT ? 2 : 1;
+        constexpr int o = LAY == kLayUnit ? 2 : 1;
         T sa, ca;
-        if constexpr (UNIT) {
+        if constexpr (LAY == kLayUnit) {
             ca = v[0]; sa = v[1];
+        } else if constexpr (LAY == kLayHalf) {
+            half_decode(v[0], &ca, &sa);
         } else {
             sincos_fast(v[0], &sa, &ca);
         }
@@ -143,8 +177,10 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         dn = los_scale(dx * dx * ia2 + dy * dy * ib2);
         T cA2, sA2;
         unit_dir(ca2, sa2, &cA2, &sA2);
-        if constexpr (UNIT) {
+        if constexpr (LAY == kLayUnit) {
             v[0] = cA2; v[1] = sA2;
+        } else if constexpr (LAY == kLayHalf) {
+            v[0] = half_encode(cA2, sA2);
         } else {
             v[0] = atan2_fast(sa2, ca2);
         }
@@ -169,12 +205,12 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
 // Cold-start angles / prime of a state (no update): fills v for INIT, then the
 // residual of the copies-reset state (copies == cos/sin of the angles, so only the
 // collision families are non-zero) and the sums the first position step needs.
-template <int DIM, typename T, bool UNIT, bool INIT>
+template <int DIM, typename T, int LAY, bool INIT>
 __device__ __forceinline__ void prime_element(T* v, double trx, double trY, double trz, double px, double py,
                                               double pz, double ad, double bd, T dold, double& sumsq, double& mx,
                                               double* accL, double* accT) {
-    constexpr int NL = Words<DIM, UNIT>::NL;
-    constexpr int o = Words<DIM, UNIT>::NV;
+    constexpr int NL = Words<DIM, LAY>::NL;
+    constexpr int o = Words<DIM, LAY>::NV;
     const double ex = px - trx, ey = py - trY, ez = pz - trz;
     T ca, sa, cb = 0, sb = 0;
     if constexpr (INIT) {
@@ -186,9 +222,12 @@ __device__ __forceinline__ void prime_element(T* v, double trx, double trY, doub
         double s0, c0, s1, c1;
         sincos(a0, &s0, &c0);
         sincos(b0, &s1, &c1);
-        if constexpr (UNIT) {
+        if constexpr (LAY == kLayUnit) {
             v[0] = (T)c0; v[1] = (T)s0;
             if (DIM == 3) { v[2] = (T)c1; v[3] = (T)s1; }
+        } else if constexpr (LAY == kLayHalf) {
+            v[0] = half_encode((T)c0, (T)s0);
+            if (DIM == 3) v[1] = half_encode((T)c1, (T)s1);
         } else {
             v[0] = (T)a0;
             if (DIM == 3) v[1] = (T)b0;
@@ -196,9 +235,12 @@ __device__ __forceinline__ void prime_element(T* v, double trx, double trY, doub
 #pragma unroll
         for (int k = 0; k < NL; ++k) v[o + k] = (T)0;
     }
-    if constexpr (UNIT) {
+    if constexpr (LAY == kLayUnit) {
         ca = v[0]; sa = v[1];
         if (DIM == 3) { cb = v[2]; sb = v[3]; }
+    } else if constexpr (LAY == kLayHalf) {
+        half_decode(v[0], &ca, &sa);
+        if (DIM == 3) half_decode(v[1], &cb, &sb);
     } else {
         sincos_fast(v[0], &sa, &ca);
         if (DIM == 3) sincos_fast(v[1], &sb, &cb);

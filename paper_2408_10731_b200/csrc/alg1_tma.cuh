@@ -22,9 +22,9 @@
 
 namespace tro {
 
-template <int DIM, typename T, bool UNIT, int NP, int G, int S>
+template <int DIM, typename T, int LAY, int NP, int G, int S>
 struct TmaCfg {
-    static constexpr int W = Words<DIM, UNIT>::W;
+    static constexpr int W = Words<DIM, LAY>::W;
     static constexpr int kRowBytes = W * NP * (int)sizeof(T);  // one obstacle row of state
     static constexpr int kTrkBytes = DIM * NP * 8;             // one obstacle row of tracks
     static constexpr int kStageBytes = G * (kRowBytes + kTrkBytes);
@@ -62,9 +62,9 @@ __host__ __device__ inline TmaLayout tma_layout(int stage_bytes, int S, int n_p,
 #endif
 constexpr int kTmaMinBlocks = TRO_TMA_MINB;  // resident CTAs per SM the kernel is compiled for
 
-template <int DIM, typename T, bool UNIT, int NP, int G, int S>
-__global__ void __launch_bounds__(TmaCfg<DIM, T, UNIT, NP, G, S>::kThreads, kTmaMinBlocks) alg1_tma_kernel(Alg1Args A) {
-    using C = TmaCfg<DIM, T, UNIT, NP, G, S>;
+template <int DIM, typename T, int LAY, int NP, int G, int S>
+__global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaMinBlocks) alg1_tma_kernel(Alg1Args A) {
+    using C = TmaCfg<DIM, T, LAY, NP, G, S>;
     constexpr int W = C::W;
     constexpr int NC = C::kConsumers;
     constexpr int NCW = NC / 32;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, UNIT, NP, G, S>::kThreads, kTma
                     dold = los_scale(qd);
                 }
                 T dn, cp4[4];
-                am_element<DIM, T, UNIT>(v, trx, trY, trz, px, py, pz, a, b, ia2, ib2, dold, trho, trho_o, sumsq, mx,
+                am_element<DIM, T, LAY>(v, trx, trY, trz, px, py, pz, a, b, ia2, ib2, dold, trho, trho_o, sumsq, mx,
                                    accL, accT, dn, cp4);
                 T* gp = gbase + (int64_t)j * W * NP;
 #pragma unroll

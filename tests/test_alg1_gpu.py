@@ -51,7 +51,7 @@ def engine_from(g, bvals, desired, params, *, dtype=torch.float64, rho0=None, ma
                       export=True, keep_d=True, layout=layout, use_tma=use_tma)
 
 
-KERNELS = [("angle", True), ("angle", False), ("unit", True), ("unit", False)]
+KERNELS = [("angle", True), ("angle", False), ("unit", True), ("unit", False), ("half", True), ("half", False)]
 
 
 def load_snapshot(eng, g, pre, dim):
@@ -196,7 +196,7 @@ def test_flow3d_batch_free_window(golden):
     assert 0.2 < np.median(fin) / np.median(ref) < 5.0
 
 
-@pytest.mark.parametrize("layout", ["angle", "unit"])
+@pytest.mark.parametrize("layout", ["angle", "unit", "half"])
 def test_batch_layouts_agree_over_a_window(golden, layout):
     """The unit-vector layout (11 words) reproduces the angle layout's C2 histories (the AM
     map only sees cos/sin of the angles); chaos bounds the window like the twin test."""
@@ -223,7 +223,7 @@ def test_batch_members_equal_single_solves(golden):
         np.testing.assert_array_equal(one.state.xi, xi[i])
 
 
-@pytest.mark.parametrize("n_p,layout", [(100, "angle"), (100, "unit"), (60, "angle"), (60, "unit")])
+@pytest.mark.parametrize("n_p,layout", [(100, "angle"), (100, "unit"), (100, "half"), (60, "angle"), (60, "unit"), (60, "half")])
 def test_oracle_vs_device_step(golden, n_p, layout):
     """C5 shape (n_o 100) and a generic horizon (n_p 60, the non-specialised kernel): device one
     step == oracle one step from an oracle mid-run state."""
