@@ -185,7 +185,7 @@ def run_c4(args):
                    "rounds": C4_ROUNDS, "constraint_elites": C4_NCE, "elites": C4_NEL, "l2": "on-chip (FP-bound)",
                    "parallelism": f"sample-shard x{world} (+ candidate all-gather / round)"},
         "roofline": {"bound": "fp64", "achieved": flops / kern_s / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": flops / kern_s / 1e12 / peak, "traffic": None,
+                     "frac": flops / kern_s / 1e12 / peak, "traffic": traffic_for("c4") if world == 1 else None,
                      "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)",
                      "kernel": "tro_priest_project_f64 (priest_project_kernel<3>)",
                      "avg_launch_ms": kern_s * 1e3, "algorithmic_flops_per_launch": flops},
@@ -338,7 +338,7 @@ def run_c2alt(args):
                    "parallelism": f"member-shard x{world} (+ 32 B all-gather / iteration)" if world > 1 else
                    "member-shard x1", "l2": "on-chip (latency-bound: state 1 MB, tracks 80 KB)"},
         "roofline": {"bound": "fp64", "achieved": flops / launch_s / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": flops / launch_s / 1e12 / peak, "traffic": None,
+                     "frac": flops / launch_s / 1e12 / peak, "traffic": traffic_for("c2alt") if world == 1 else None,
                      "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)",
                      "kernel": "tro_b2_run mode 0 (b2_kernel<1, 0, circles>)", "avg_launch_ms": launch_s * 1e3,
                      "algorithmic_flops_per_launch": flops,
@@ -469,7 +469,8 @@ def run_c3(args):
         "config": {"workload": desc, "problems": total, "agents": 16, "pairs": n_pairs, "n_p": 100,
                    "iterations": n_iter, "parallelism": f"problem-shard x{world}", "l2": "state >> L2"},
         "roofline": {"bound": "hbm", "achieved": alg_bytes / launch_s / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": alg_bytes / launch_s / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": alg_bytes / launch_s / 1e9 / peak, "traffic": traffic_for("c3") if world == 1 else None,
+                     "peak_source": peak_src,
                      "kernel": "tro_ma_run (ma_kernel<11>)", "avg_launch_ms": launch_s * 1e3,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "note": "3 words (multipliers) per pair-sample; SURVEY §8(d) counts 4 (d stored): d only "
@@ -567,6 +568,17 @@ def cpu_reference_c4(procs=None, per_proc=8, n_inner=30):
     n = procs * per_proc
     return n * n_inner / wall, {"cores": procs, "sample": f"{n} C4 samples x {n_inner} inner its (one round's "
                                                           f"projection slice), oracle port, wall {wall:.1f}s"}
+
+
+def traffic_for(cfg: str):
+    """dram__bytes_read + dram__bytes_write of one launch of the config's dominant kernel, from the committed
+    ncu capture (profiles/ncu_traffic_r1.json, tools/ncu_traffic.sh); None when absent."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic_r1.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        d = json.load(fh)
+    return d.get(cfg, {}).get("dram_bytes_per_launch")
 
 
 def measured_peaks():
