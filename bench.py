@@ -570,6 +570,12 @@ def cpu_reference_c4(procs=None, per_proc=8, n_inner=30):
                                                           f"projection slice), oracle port, wall {wall:.1f}s"}
 
 
+def _alg1_loop_max() -> int:
+    from paper_2408_10731_b200 import _alg1
+
+    return _alg1.LOOP_MAX_MEMBERS
+
+
 def traffic_for(cfg: str):
     """dram__bytes_read + dram__bytes_write of one launch of the config's dominant kernel, from the committed
     ncu capture (profiles/ncu_traffic_r1.json, tools/ncu_traffic.sh); None when absent."""
@@ -822,9 +828,10 @@ def run_b200(args):
         bv_host = torch.as_tensor(batch.bvals, dtype=torch.float64).pin_memory()
         q_host = torch.as_tensor(batch.linear_terms(), dtype=torch.float64).pin_memory()
         xi_host = torch.empty(eng.xi.shape, dtype=torch.float64).pin_memory()
-        res_host = torch.empty((3, B), dtype=torch.float64).pin_memory()
+        res_host = torch.empty((2, B), dtype=torch.float64).pin_memory()
+        st_host = torch.empty(B, dtype=torch.int32).pin_memory()  # same dtype: a plain async D2H copy
         h2d = (bv_host.numel() + q_host.numel()) * 8
-        d2h = (xi_host.numel() + res_host.numel()) * 8
+        d2h = (xi_host.numel() + res_host.numel()) * 8 + st_host.numel() * 4
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -838,7 +845,7 @@ def run_b200(args):
             xi_host.copy_(eng.xi, non_blocking=True)
             res_host[0].copy_(eng.res_max, non_blocking=True)
             res_host[1].copy_(eng.res_norm, non_blocking=True)
-            res_host[2].copy_(eng.status, non_blocking=True)
+            st_host.copy_(eng.status, non_blocking=True)
         b.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
@@ -846,6 +853,24 @@ def run_b200(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": members_total * n_iter * args.steps / float(te.item()), "unit": "traj-it/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        if args.config == "c1" and world == 1:
+            # C1 is the reference's single-problem case: the call a user makes is solve_single (numpy in,
+            # SingleSolution out: trajectory, histories, state), timed on the stream around the call
+            from paper_2408_10731_b200 import scenarios as _sc
+            from paper_2408_10731_b200 import solver_single as _ss
+
+            prob = _sc.c1_problem()
+            prm = _ss.SingleParams(max_iter=n_iter, tol=0.0)
+            _ss.solve_single(prob, prm)
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(args.steps):
+                sol = _ss.solve_single(prob, prm)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e = {"value": n_iter * args.steps / (a.elapsed_time(b) / 1e3), "unit": "traj-it/s",
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(sol.state.xi.nbytes + 8 * 3 * n_iter),
+                   "api": "solver_single.solve_single"}
 
     line = {
         "metric": "trajectory-iterations/sec (batch x AM iters)",
@@ -872,7 +897,8 @@ def run_b200(args):
                      "kernel": "tro_alg1_iterate (alg1_kernel<3,T>)"},
         "clocks": clk,
         "e2e": e2e,
-        "gpu_launches": args.steps * (1 + n_iter),
+        # init + per-iteration launches; batches up to LOOP_MAX_MEMBERS run iterations 2..n in one launch
+        "gpu_launches": args.steps * ((1 + n_iter) if B > _alg1_loop_max() else 3),
     }
     if args.config == "c1" and rank == 0:
         # second headline of the metric: ms per converged solve (C1, SingleParams() defaults,
