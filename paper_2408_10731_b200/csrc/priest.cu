@@ -44,6 +44,7 @@ __host__ __device__ inline PrSmem pr_layout(int n_p, int m, int dim, int nk, int
     L.Pdd = off;  off += n_p * m;
     L.kinv = off; off += dim * m * nk;                 // only the xi rows of K^-1
     L.M = off;    off += m * m;
+    off = (off + 1) & ~1;  // 16-byte aligned obstacle records (double2 loads)
     L.obs = off;  off += 8 * (n_o > 0 ? n_o : 1);
     L.wbuf = off; off += wbuf ? kPrWarps * 3 * dim * n_p : 0;  // runtime-m path: F' weights per (blk, ax, t)
     L.vec = off;  off += kPrWarps * 5 * kPrMaxNk;     // per warp: xi, lam, samp, fte, rhs
@@ -218,20 +219,56 @@ __global__ void __launch_bounds__(kPrWarps * 32, 2) priest_project_kernel(PrArgs
             int outside = 0;
             if (active) {
                 const double* tr = A.c.tracks + t;
-                for (int j = jg; j < n_o; j += jstep) {
+                // the scaled distances of kB obstacles first (independent: ILP across obstacles), then the
+                // rare inside targets; ncu showed the one-obstacle-at-a-time chain stalled on fixed latency
+                constexpr int kB = 4;
+                auto q2_of = [&](int j, double* dl, double* cc) -> double {
                     const double* o = sObs + 8 * j;
-                    double cc[3], dl[3];
-#pragma unroll
-                    for (int k = 0; k < DIM; ++k) {
-                        cc[k] = STATIC ? o[k] : ld_const(tr + ((int64_t)j * DIM + k) * n_p);
-                        dl[k] = p[k] - cc[k];
-                    }
-                    double q2;
-                    if constexpr (DIM == 3) q2 = fma(dl[2] * dl[2], o[4], (dl[0] * dl[0] + dl[1] * dl[1]) * o[3]);
-                    else q2 = fma(dl[1] * dl[1], o[4], dl[0] * dl[0] * o[3]);
-                    if (q2 >= 1.0 && q2 <= 1e12) {
-                        ++outside;  // target == the point itself (added once below)
+                    double ia2;
+                    if constexpr (STATIC) {
+                        const double2 c01 = reinterpret_cast<const double2*>(o)[0];
+                        const double2 c2i = reinterpret_cast<const double2*>(o)[1];
+                        cc[0] = c01.x;
+                        cc[1] = c01.y;
+                        cc[2] = c2i.x;
+                        ia2 = c2i.y;
                     } else {
+#pragma unroll
+                        for (int k = 0; k < DIM; ++k) cc[k] = ld_const(tr + ((int64_t)j * DIM + k) * n_p);
+                        ia2 = o[3];
+                    }
+#pragma unroll
+                    for (int k = 0; k < DIM; ++k) dl[k] = p[k] - cc[k];
+                    if constexpr (DIM == 3) return fma(dl[2] * dl[2], o[4], (dl[0] * dl[0] + dl[1] * dl[1]) * ia2);
+                    else return fma(dl[1] * dl[1], o[4], dl[0] * dl[0] * ia2);
+                };
+                int j = jg;
+                for (; j + (kB - 1) * jstep < n_o; j += kB * jstep) {
+                    double q2[kB];
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        double dl[3], cc[3];
+                        q2[u] = q2_of(j + u * jstep, dl, cc);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kB; ++u) {
+                        if (q2[u] >= 1.0 && q2[u] <= 1e12) {
+                            ++outside;  // target == the point itself (added once below)
+                        } else {  // rare: recompute the offsets (keeping kB of them live costs registers)
+                            double dl[3], cc[3];
+                            const double qq = q2_of(j + u * jstep, dl, cc);
+                            const double* o = sObs + 8 * (j + u * jstep);
+                            inside_target<DIM>(p, dl, cc, qq, o[5], o[6], S, rr);
+                        }
+                    }
+                }
+                for (; j < n_o; j += jstep) {
+                    double dl[3], cc[3];
+                    const double q2 = q2_of(j, dl, cc);
+                    if (q2 >= 1.0 && q2 <= 1e12) {
+                        ++outside;
+                    } else {
+                        const double* o = sObs + 8 * j;
                         inside_target<DIM>(p, dl, cc, q2, o[5], o[6], S, rr);
                     }
                 }
