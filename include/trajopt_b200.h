@@ -168,6 +168,8 @@ typedef struct tro_priest_consts {
     double rho;
     int32_t has_bounds;
     int32_t static_tracks; /* 1: every obstacle centre is constant over the horizon */
+    int32_t spheres;       /* 1: every obstacle has a == b (one scaled-distance multiplier) */
+    int32_t reserved;
 } tro_priest_consts;
 
 typedef struct tro_priest_io {

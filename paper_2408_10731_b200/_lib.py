@@ -135,6 +135,8 @@ class PriestConsts(ctypes.Structure):
         ("rho", c_double),
         ("has_bounds", c_int32),
         ("static_tracks", c_int32),
+        ("spheres", c_int32),
+        ("reserved", c_int32),
     ]
 
 

@@ -106,7 +106,7 @@ __device__ __forceinline__ void speed_target(const double* v, double limit, doub
 
 // M: compile-time basis columns (0 = runtime m, F'e via a shared-memory weight buffer);
 // STATIC: obstacle centres constant over the horizon (kept in shared memory).
-template <int DIM, int M, bool STATIC>
+template <int DIM, int M, bool STATIC, bool SPH>
 __global__ void __launch_bounds__(kPrWarps * 32, 2) priest_project_kernel(PrArgs A) {
     extern __shared__ double smem[];
     const int n_p = A.d.n_p, n_o = A.d.n_obs, neq = A.d.n_eq;
@@ -239,6 +239,10 @@ __global__ void __launch_bounds__(kPrWarps * 32, 2) priest_project_kernel(PrArgs
                     }
 #pragma unroll
                     for (int k = 0; k < DIM; ++k) dl[k] = p[k] - cc[k];
+                    if constexpr (SPH) {  // a == b: one multiplier, no 1/b^2 load
+                        if constexpr (DIM == 3) return fma(dl[2], dl[2], fma(dl[1], dl[1], dl[0] * dl[0])) * ia2;
+                        else return fma(dl[1], dl[1], dl[0] * dl[0]) * ia2;
+                    }
                     if constexpr (DIM == 3) return fma(dl[2] * dl[2], o[4], (dl[0] * dl[0] + dl[1] * dl[1]) * ia2);
                     else return fma(dl[1] * dl[1], o[4], dl[0] * dl[0] * ia2);
                 };
@@ -250,15 +254,24 @@ __global__ void __launch_bounds__(kPrWarps * 32, 2) priest_project_kernel(PrArgs
                         double dl[3], cc[3];
                         q2[u] = q2_of(j + u * jstep, dl, cc);
                     }
+                    // outside (target == the point itself, added once below): branch-free count; the rare
+                    // inside elements are handled behind one branch per batch
+                    unsigned inside = 0;
 #pragma unroll
                     for (int u = 0; u < kB; ++u) {
-                        if (q2[u] >= 1.0 && q2[u] <= 1e12) {
-                            ++outside;  // target == the point itself (added once below)
-                        } else {  // rare: recompute the offsets (keeping kB of them live costs registers)
-                            double dl[3], cc[3];
-                            const double qq = q2_of(j + u * jstep, dl, cc);
-                            const double* o = sObs + 8 * (j + u * jstep);
-                            inside_target<DIM>(p, dl, cc, qq, o[5], o[6], S, rr);
+                        const bool out = q2[u] >= 1.0 && q2[u] <= 1e12;
+                        outside += out ? 1 : 0;
+                        inside |= out ? 0u : (1u << u);
+                    }
+                    if (inside) {  // per-lane (lanes of the remainder slot walk different obstacle groups)
+#pragma unroll
+                        for (int u = 0; u < kB; ++u) {
+                            if (inside & (1u << u)) {  // recompute the offsets (keeping kB live costs registers)
+                                double dl[3], cc[3];
+                                const double qq = q2_of(j + u * jstep, dl, cc);
+                                const double* o = sObs + 8 * (j + u * jstep);
+                                inside_target<DIM>(p, dl, cc, qq, o[5], o[6], S, rr);
+                            }
                         }
                     }
                 }
@@ -508,9 +521,15 @@ static int pr_check(const tro_priest_dims* d) {
 
 template <int DIM, int M, bool STATIC>
 static void pr_launch(const tro::PrArgs& A, unsigned blocks, size_t smem, cudaStream_t st) {
-    cudaFuncSetAttribute(tro::priest_project_kernel<DIM, M, STATIC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (A.c.spheres) {
+        cudaFuncSetAttribute(tro::priest_project_kernel<DIM, M, STATIC, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tro::priest_project_kernel<DIM, M, STATIC, true><<<blocks, tro::kPrWarps * 32, smem, st>>>(A);
+        return;
+    }
+    cudaFuncSetAttribute(tro::priest_project_kernel<DIM, M, STATIC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    tro::priest_project_kernel<DIM, M, STATIC><<<blocks, tro::kPrWarps * 32, smem, st>>>(A);
+    tro::priest_project_kernel<DIM, M, STATIC, false><<<blocks, tro::kPrWarps * 32, smem, st>>>(A);
 }
 
 template <int DIM>

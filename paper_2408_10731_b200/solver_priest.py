@@ -220,7 +220,7 @@ class ProjectionSetup:
             (line if line is not None else d["line"]).data_ptr(),
             float(self.v_max) if self.v_max is not None else -1.0,
             float(self.a_max) if self.a_max is not None else -1.0, float(self.rho), int(self.has_bounds),
-            int(self.static_tracks))
+            int(self.static_tracks), int(self.n_o > 0 and bool(np.array_equal(self.obs_a, self.obs_b))), 0)
 
     # -- host helpers (reference API) -----------------------------------------------
     def axis_samples(self, xis: np.ndarray, mat: np.ndarray) -> np.ndarray:
