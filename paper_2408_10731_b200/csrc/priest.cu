@@ -259,7 +259,10 @@ __global__ void __launch_bounds__(kPrWarps * 32, 2) priest_project_kernel(PrArgs
                     unsigned inside = 0;
 #pragma unroll
                     for (int u = 0; u < kB; ++u) {
-                        const bool out = q2[u] >= 1.0 && q2[u] <= 1e12;
+                        // 1 <= q2 <= 1e12 as one unsigned range test on the bit pattern (q2 >= 0, so
+                        // the patterns are monotone; NaN falls outside): integer pipe, not fp64
+                        const unsigned long long qb = (unsigned long long)__double_as_longlong(q2[u]);
+                        const bool out = qb - 0x3FF0000000000000ull <= 0x426D1A94A2000000ull - 0x3FF0000000000000ull;
                         outside += out ? 1 : 0;
                         inside |= out ? 0u : (1u << u);
                     }
