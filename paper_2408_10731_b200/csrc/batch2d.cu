@@ -35,7 +35,7 @@ constexpr int kB2MaxM = 16;
 #define B2_UNROLL_BASIS 1
 #endif
 #ifndef B2_MINB
-#define B2_MINB 4  // 4 CTAs / SM: 128 registers (measured best, tools/tune_b2.sh)
+#define B2_MINB 7  // 7 CTAs / SM (72 registers, some spills): C2-alt's 1024 members in one wave; 6 % faster than 4 CTAs / 128 registers at 1024 and 8192 members (tools/tune_b2.sh)
 #endif
 constexpr int kB2UnrollM = B2_UNROLL_BASIS ? kB2MaxM : 1;
 

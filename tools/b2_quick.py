@@ -11,7 +11,8 @@ import torch
 from paper_2408_10731_b200 import scenarios
 from paper_2408_10731_b200 import solver_batch as SB
 
-prob = scenarios.batch2d_problem(n_o=50, n_batch=1024)
+NB = int(os.environ.get("B2_NB", "1024"))
+prob = scenarios.batch2d_problem(n_o=50, n_batch=NB)
 params = SB.BatchParams(max_iter=200)
 for rep in range(int(os.environ.get("B2_REPS", "3"))):
     torch.cuda.synchronize()
@@ -19,7 +20,7 @@ for rep in range(int(os.environ.get("B2_REPS", "3"))):
     r = SB.solve_batch_opt(prob, params, seed=0)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(f"rep {rep}: {dt * 1e3:.1f} ms/solve  {1024 * 200 / dt:.3e} traj-it/s  best={r.best_index} "
+    print(f"rep {rep}: {dt * 1e3:.1f} ms/solve  {NB * 200 / dt:.3e} traj-it/s  best={r.best_index} "
           f"feasible={int(r.feasible.sum())} rho={r.state.rho:.3f}")
 # device-only timing of the iteration loop
 struct = SB._Structure(prob)
@@ -34,4 +35,4 @@ eng.run(200)
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
-print(f"device loop: {ms:.3f} ms / 200 it = {ms / 200 * 1e3:.1f} us/it, {1024 * 200 / ms * 1e3:.3e} traj-it/s")
+print(f"device loop: {ms:.3f} ms / 200 it = {ms / 200 * 1e3:.1f} us/it, {NB * 200 / ms * 1e3:.3e} traj-it/s")
