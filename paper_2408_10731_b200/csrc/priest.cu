@@ -23,6 +23,9 @@
 namespace tro {
 
 constexpr int kPrWarps = 8;
+#ifndef PR_MINB
+#define PR_MINB 2  // 2 CTAs / SM at the 128-register cap (3 spills heavily)
+#endif
 constexpr int kPrMaxDm = 48;  // dim * m
 constexpr int kPrMaxNk = 72;  // dim * m + n_eq
 
@@ -107,7 +110,7 @@ __device__ __forceinline__ void speed_target(const double* v, double limit, doub
 // M: compile-time basis columns (0 = runtime m, F'e via a shared-memory weight buffer);
 // STATIC: obstacle centres constant over the horizon (kept in shared memory).
 template <int DIM, int M, bool STATIC, bool SPH>
-__global__ void __launch_bounds__(kPrWarps * 32, 2) priest_project_kernel(PrArgs A) {
+__global__ void __launch_bounds__(kPrWarps * 32, PR_MINB) priest_project_kernel(PrArgs A) {
     extern __shared__ double smem[];
     const int n_p = A.d.n_p, n_o = A.d.n_obs, neq = A.d.n_eq;
     const int m = M ? M : A.d.m;
