@@ -489,3 +489,29 @@ def test_sharded_entry_point_single_rank():
     np.testing.assert_array_equal(got.feasible, ref.feasible)
     assert got.best_index == ref.best_index and got.n_factorizations == ref.n_factorizations
     assert [h["rho"] for h in got.best_history] == [h["rho"] for h in ref.best_history]
+
+
+def test_three_circle_footprint_with_ellipses_matches_oracle():
+    """Generic path (n_c = 3 > the compiled specialisations, ellipses a != b, n_p 60): 25 iterations of the
+    full solve against the oracle (bit-exact with the reference) within 1e-9."""
+    n_p = 60
+    basis = build_basis(0.0, 8.0, n_p, 10)
+    rng = np.random.default_rng(11)
+    obs = []
+    for _ in range(6):
+        c0 = np.array([rng.uniform(2, 7), rng.uniform(-1.5, 1.5)])
+        v = np.array([rng.uniform(-0.3, 0.0), rng.uniform(-0.1, 0.1)])
+        cen = c0[None, :] + v[None, :] * basis.grid.timestamps[:, None]
+        obs.append(ObstacleTrack(centers=cen, shape=EllipsoidShape(rng.uniform(0.3, 0.6), rng.uniform(0.3, 0.6))))
+    prob = SB.BatchProblem(basis=basis, boundary=(AxisBoundary(p0=0.0, p1=9.0), AxisBoundary(p0=0.5, p1=-0.5)),
+                           psi_boundary=(0.1, -0.1),
+                           desired=np.column_stack([np.linspace(0.0, 9.0, n_p), np.linspace(0.5, -0.5, n_p)]),
+                           obstacles=obs, footprint=SB.FootprintSpec(offsets=(0.4, 0.0, -0.4)), v_max=2.5, a_max=2.0,
+                           n_batch=12)
+    samples = SB._default_samples(prob, basis.n_var, None, None, 4)
+    ranked = SB.solve_batch_opt(prob, SB.BatchParams(max_iter=25), samples=samples)
+    out = OB.solve(_oracle_struct(prob), samples, 3, max_iter=25)
+    for name in ("xi", "xi_psi", "lam", "lam_psi"):
+        assert rel(getattr(ranked.state, name), getattr(out["state"], name)) <= TOL, name
+    np.testing.assert_array_equal(np.array([h["rho"] for h in ranked.best_history]), out["best_hist"][:, 2])
+    np.testing.assert_array_equal(ranked.feasible, out["feasible"])
