@@ -65,10 +65,12 @@ __host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs
 template <int M, int MODE>
 __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
     // MODE 0: iteration; 1: prime (sums of a given state: lambda in `state`, d / alpha / beta in
-    // the export planes); 2: cold init (straight lines, angles, d = 1, lambda = 0) + sums
-    constexpr int mode = MODE;
+    // the export planes); 2: cold init (straight lines, angles, d = 1, lambda = 0) + sums;
+    // 4: iteration whose QP step already ran (ma_qp_kernel wrote xi): the element pass alone
+    constexpr int mode = MODE == 4 ? 0 : MODE;
     constexpr bool init = MODE == 2;
     constexpr bool prime = MODE == 1;
+    constexpr bool pre_qp = MODE == 4;
     extern __shared__ double smem[];
     const int i = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
             sXi[k] = v;
             xg[k] = v;
         }
-    } else if (prime) {
+    } else if (prime || pre_qp) {
         for (int k = tid; k < 3 * nv; k += blockDim.x) sXi[k] = xg[k];
     } else {
         const double* sg = A.s.sums + (int64_t)i * 2 * n_a * 3 * m;
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
     const double ir = 1.0 / rho;
     // lambda of this lane's next element, loaded one element ahead (two HBM loads in flight per lane)
     double nlx = 0.0, nly = 0.0, nlz = 0.0;
-    if (MODE == 0 && warp < n_p && lane < np_) {
+    if (mode == 0 && warp < n_p && lane < np_) {
         const double* r0 = st + warp * rowW;
         nlx = ld_stream(r0 + lane);
         nly = ld_stream(r0 + np_ + lane);
@@ -206,7 +208,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
         double* srow = st + t * rowW;
         for (int p = lane; p < np_; p += 32) {
             double clx = 0.0, cly = 0.0, clz = 0.0;
-            if (MODE == 0) {
+            if (mode == 0) {
                 clx = nlx, cly = nly, clz = nlz;
                 int p2 = p + 32, t2 = t;
                 if (p2 >= np_) p2 = lane, t2 = t + kMaWarps;
@@ -402,6 +404,112 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
     }
 }
 
+// ---------------------------------------------------------------- batched QP step on the fp64 tensor cores
+// xi_i = K_L^-1 [ rho B_i - C_i ; b_eq_i ] for every axis of every non-converged problem, as one GEMM per
+// CTA: D[nv x 3P] = K_L^-1[0:nv, 0:nk] x R[nk x 3P] with DMMA (mma.sync m8n8k4 f64), P = 16 problems.
+// The fused kernel's per-problem GEMV reads the nv x nk inverse once per problem (~36 k instructions per
+// problem); here a CTA reads it once for 16 problems and the tensor cores do the FMAs.  Problems of a tile
+// at different rho levels are handled level by level (the schedule keeps them together almost always).
+constexpr int kQpP = 16;               // problems per CTA
+constexpr int kQpCols = 3 * kQpP;      // 48 RHS columns
+constexpr int kQpLd = kQpCols + 4;     // padded smem row (bank spread of the B fragments)
+constexpr int kQpMt = 3;               // m-tiles per warp (8 warps x 3 x 8 rows >= nv = 176)
+
+__device__ __forceinline__ void dmma884(double* d, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) ma_qp_kernel(MaArgs A) {
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n_a = A.d.n_agents, neq = A.d.n_eq;
+    constexpr int m = M;
+    const int nv = n_a * m, nk = nv + neq, nk4 = (nk + 3) & ~3;
+    const int i0 = blockIdx.x * kQpP;
+    const int npb = min(kQpP, A.d.n_problems - i0);
+    double* sR = smem;                          // [nk4][kQpLd]
+    int* sLev = reinterpret_cast<int*>(smem + nk4 * kQpLd);  // [kQpP] level, -1: skip
+    if (tid < kQpP) {
+        int lv = -1;
+        if (tid < npb && !(A.s.status[i0 + tid] & TRO_CONVERGED)) lv = A.s.level[i0 + tid];
+        sLev[tid] = lv;
+    }
+    __syncthreads();
+    // RHS columns (problem p, axis ax) = [ rho B - C ; b_eq ]  (agent sums [which][a][k][c])
+    for (int e = tid; e < nk4 * kQpCols; e += blockDim.x) {
+        const int r = e / kQpCols, col = e - r * kQpCols;
+        const int p = col / 3, ax = col - 3 * p;
+        double v = 0.0;
+        const int lv = sLev[p];
+        if (lv >= 0 && r < nk) {
+            const int i = i0 + p;
+            if (r < nv) {
+                const int a = r / m, cc = r - a * m;
+                const double* sg = A.s.sums + (int64_t)i * 2 * n_a * 3 * m;
+                const int o = (a * 3 + ax) * m + cc;
+                v = A.c.level_rho[lv] * sg[o] - sg[n_a * 3 * m + o];
+            } else {
+                v = A.c.b_eq[(int64_t)i * 3 * neq + ax * neq + (r - nv)];
+            }
+        }
+        sR[r * kQpLd + col] = v;
+    }
+    __syncthreads();
+    const int arow = lane >> 2, acol = lane & 3;  // A fragment: A[row][k]; B fragment: B[k = lane & 3][col = lane >> 2]
+    for (int pass = 0; pass < kQpP; ++pass) {
+        // the level of this pass: the first not-yet-done problem's (uniform across the CTA)
+        int lv = -1;
+        for (int p = 0; p < kQpP; ++p) {
+            if (sLev[p] >= 0) {
+                lv = sLev[p];
+                break;
+            }
+        }
+        if (lv < 0) break;
+        const double* K = A.c.kinv + (int64_t)lv * nk * nk;
+        double acc[kQpMt][kQpCols / 8][2];
+#pragma unroll
+        for (int t = 0; t < kQpMt; ++t)
+#pragma unroll
+            for (int n = 0; n < kQpCols / 8; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
+        for (int k0 = 0; k0 < nk4; k0 += 4) {
+            const int kk = k0 + acol;
+            double af[kQpMt];
+#pragma unroll
+            for (int t = 0; t < kQpMt; ++t) {
+                const int row = (warp + 8 * t) * 8 + arow;
+                af[t] = (row < nv && kk < nk) ? ld_const(K + (int64_t)row * nk + kk) : 0.0;
+            }
+#pragma unroll
+            for (int n = 0; n < kQpCols / 8; ++n) {
+                const double bf = sR[(k0 + acol) * kQpLd + n * 8 + arow];
+#pragma unroll
+                for (int t = 0; t < kQpMt; ++t) dmma884(acc[t][n], af[t], bf);
+            }
+        }
+        // D fragment: rows (mtile * 8 + lane >> 2), columns n * 8 + 2 (lane & 3) + {0, 1}
+#pragma unroll
+        for (int t = 0; t < kQpMt; ++t) {
+            const int row = (warp + 8 * t) * 8 + arow;
+            if (row >= nv) continue;
+#pragma unroll
+            for (int n = 0; n < kQpCols / 8; ++n)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = n * 8 + 2 * acol + h;
+                    const int p = col / 3, ax = col - 3 * p;
+                    if (sLev[p] == lv) A.s.xi[(int64_t)(i0 + p) * 3 * nv + ax * nv + row] = acc[t][n][h];
+                }
+        }
+        __syncthreads();
+        if (tid < kQpP && sLev[tid] == lv) sLev[tid] = -1;  // done
+        __syncthreads();
+    }
+}
+
 template <int M, int MODE>
 static int ma_launch(const MaArgs& A, size_t smem, cudaStream_t st) {
     cudaFuncSetAttribute(ma_kernel<M, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -413,6 +521,15 @@ template <int M>
 static int ma_dispatch_m(const MaArgs& A, int mode, bool, size_t smem, cudaStream_t st) {
     if (mode == 0) return ma_launch<M, 0>(A, smem, st);
     if (mode == 1) return ma_launch<M, 1>(A, smem, st);
+    if (mode == 4) return ma_launch<M, 4>(A, smem, st);
+    if (mode == 3) {
+        const int nk = A.d.n_agents * M + A.d.n_eq, nk4 = (nk + 3) & ~3;
+        const size_t qsm = (size_t)nk4 * kQpLd * sizeof(double) + kQpP * sizeof(int);
+        if (qsm > 227 * 1024 || A.d.n_agents * M > 8 * kQpMt * 8) return TRO_EINVAL;
+        cudaFuncSetAttribute(ma_qp_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
+        ma_qp_kernel<M><<<(A.d.n_problems + kQpP - 1) / kQpP, 256, qsm, st>>>(A);
+        return (int)cudaGetLastError();
+    }
     return ma_launch<M, 2>(A, smem, st);
 }
 
@@ -424,7 +541,7 @@ static int ma_dispatch(const MaArgs& A, int mode, bool exp, size_t smem, cudaStr
 
 extern "C" int tro_ma_run(int32_t mode, const tro_ma_dims* d, const tro_ma_consts* c, const tro_ma_state* s,
                           const tro_ma_params* p, void* stream) {
-    if (!d || !c || !s || !p || mode < 0 || mode > 2) return TRO_EINVAL;
+    if (!d || !c || !s || !p || mode < 0 || mode > 4) return TRO_EINVAL;
     if (mode == 1 && (!s->export_d || !s->export_ab)) return TRO_EINVAL;
     if (d->n_agents < 1 || d->n_agents > tro::kMaMaxAgents || d->n_p < 2 || d->m < 1 || d->n_pairs < 1 ||
         d->n_levels < 1 || p->stall_window < 1 || 2 * p->stall_window > tro::kMaMaxRing)

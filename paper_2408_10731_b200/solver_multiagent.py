@@ -173,7 +173,8 @@ class MaEngine:
     """B problems sharing one _Structure, resident on one device."""
 
     def __init__(self, struct: _Structure, b_eq: np.ndarray, statics: np.ndarray | None, params: JointParams, *,
-                 device=None, max_hist: int = 0, export: bool = False):
+                 device=None, max_hist: int = 0, export: bool = False, split_qp: bool = True):
+        self.split_qp = split_qp  # tro_ma_run modes 3 + 4 (DMMA QP) instead of the fused mode 0
         _lib.require_cuda()
         self.lib = _lib.load()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -263,7 +264,11 @@ class MaEngine:
         self._call(2)
 
     def iterate(self):
-        self._call(0)
+        if self.split_qp:  # QP step batched on the fp64 tensor cores, then the element pass
+            self._call(3)
+            self._call(4)
+        else:  # one fused launch (per-problem QP in the kernel prologue)
+            self._call(0)
 
     def run(self, n_iter: int, *, use_graph: bool = True, chunk: int = 25, check_every: int = 50) -> int:
         done = 0
