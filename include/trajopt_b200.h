@@ -259,7 +259,7 @@ typedef struct tro_ma_params {
  *         export planes) for a warm start;
  * mode 0: one _iterate + residual + level schedule (solver_multiagent.py:252-335);
  * mode 3: the QP step of _iterate alone for every non-converged problem (:266-269), batched on the fp64
- *         tensor cores (mma.sync m8n8k4 f64, 16 problems per CTA, one K^-1 read per CTA);
+ *         tensor cores (mma.sync m8n8k4 f64, 8 problems per CTA, one K^-1 read per CTA);
  * mode 4: the rest of _iterate (angles, d, residual, multipliers, sums, schedule) given mode 3's xi.
  * Modes 3 + 4 == mode 0 (up to the GEMM's summation order). */
 int tro_ma_run(int32_t mode, const tro_ma_dims* dims, const tro_ma_consts* c, const tro_ma_state* s,

@@ -406,11 +406,11 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
 
 // ---------------------------------------------------------------- batched QP step on the fp64 tensor cores
 // xi_i = K_L^-1 [ rho B_i - C_i ; b_eq_i ] for every axis of every non-converged problem, as one GEMM per
-// CTA: D[nv x 3P] = K_L^-1[0:nv, 0:nk] x R[nk x 3P] with DMMA (mma.sync m8n8k4 f64), P = 16 problems.
+// CTA: D[nv x 3P] = K_L^-1[0:nv, 0:nk] x R[nk x 3P] with DMMA (mma.sync m8n8k4 f64), P = 8 problems.
 // The fused kernel's per-problem GEMV reads the nv x nk inverse once per problem (~36 k instructions per
-// problem); here a CTA reads it once for 16 problems and the tensor cores do the FMAs.  Problems of a tile
+// problem); here a CTA reads it once for 8 problems and the tensor cores do the FMAs.  Problems of a tile
 // at different rho levels are handled level by level (the schedule keeps them together almost always).
-constexpr int kQpP = 16;               // problems per CTA
+constexpr int kQpP = 8;                // problems per CTA (16: 117 us, 8: 87 us, 4: 116 us at C3)
 constexpr int kQpCols = 3 * kQpP;      // 48 RHS columns
 constexpr int kQpLd = kQpCols + 4;     // padded smem row (bank spread of the B fragments)
 constexpr int kQpMt = 3;               // m-tiles per warp (8 warps x 3 x 8 rows >= nv = 176)
@@ -475,19 +475,34 @@ __global__ void __launch_bounds__(256) ma_qp_kernel(MaArgs A) {
         for (int t = 0; t < kQpMt; ++t)
 #pragma unroll
             for (int n = 0; n < kQpCols / 8; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
-        for (int k0 = 0; k0 < nk4; k0 += 4) {
+        // A fragments (K^-1 from L2) loaded kPre k-steps ahead: a k-step's 18 DMMA do not cover an L2 load
+        constexpr int kPre = 4;
+        auto load_a = [&](int k0, double* af) {
             const int kk = k0 + acol;
-            double af[kQpMt];
 #pragma unroll
             for (int t = 0; t < kQpMt; ++t) {
                 const int row = (warp + 8 * t) * 8 + arow;
                 af[t] = (row < nv && kk < nk) ? ld_const(K + (int64_t)row * nk + kk) : 0.0;
             }
+        };
+        double ring[kPre][kQpMt];
 #pragma unroll
-            for (int n = 0; n < kQpCols / 8; ++n) {
-                const double bf = sR[(k0 + acol) * kQpLd + n * 8 + arow];
+        for (int u = 0; u < kPre; ++u) load_a(4 * u, ring[u]);
+        for (int k0 = 0; k0 < nk4; k0 += 4 * kPre) {
 #pragma unroll
-                for (int t = 0; t < kQpMt; ++t) dmma884(acc[t][n], af[t], bf);
+            for (int u = 0; u < kPre; ++u) {
+                const int kc = k0 + 4 * u;
+                if (kc >= nk4) break;
+                double af[kQpMt];
+#pragma unroll
+                for (int t = 0; t < kQpMt; ++t) af[t] = ring[u][t];
+                load_a(kc + 4 * kPre, ring[u]);  // rows beyond nk read as zero
+#pragma unroll
+                for (int n = 0; n < kQpCols / 8; ++n) {
+                    const double bf = sR[(kc + acol) * kQpLd + n * 8 + arow];
+#pragma unroll
+                    for (int t = 0; t < kQpMt; ++t) dmma884(acc[t][n], af[t], bf);
+                }
             }
         }
         // D fragment: rows (mtile * 8 + lane >> 2), columns n * 8 + 2 (lane & 3) + {0, 1}
