@@ -471,14 +471,14 @@ def run_c3(args):
         "roofline": {"bound": "hbm", "achieved": alg_bytes / launch_s / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": alg_bytes / launch_s / 1e9 / peak, "traffic": traffic_for("c3") if world == 1 else None,
                      "peak_source": peak_src,
-                     "kernel": "tro_ma_run (ma_kernel<11>)", "avg_launch_ms": launch_s * 1e3,
+                     "kernel": "tro_ma_run modes 3 + 4 (ma_qp_kernel<11>: DMMA QP; ma_kernel<11, 4>: element pass), per iteration", "avg_launch_ms": launch_s * 1e3,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "note": "3 words (multipliers) per pair-sample; SURVEY §8(d) counts 4 (d stored): d only "
                              "feeds the next RHS and is folded into the agent sums"},
         "clocks": clk,
         "e2e": {"value": total * n_iter * args.steps / float(te.item()), "unit": "problem-it/s",
                 "h2d_bytes_per_step": int(b_eq.nbytes), "d2h_bytes_per_step": int(xi_pin.numel() * 8 + r_pin.numel() * 8)},
-        "gpu_launches": args.steps * (n_iter + 1),
+        "gpu_launches": args.steps * (n_iter * (2 if eng.split_qp else 1) + 1),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_c3()
