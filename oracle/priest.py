@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 from scipy.linalg import lu_factor, lu_solve
 
-from .alg1 import D_CAP, boundary_matrix
+from .alg1 import D_CAP
 
 _SPEED_EPS = 1e-6  # solver_priest.py:32
 

@@ -28,7 +28,7 @@ import torch
 from . import _lib, qpcore
 from ._alg1 import rho_chain
 from .basis import AxisBoundary, BasisSet, Trajectory, boundary_matrix
-from .geometry import D_CAP, ObstacleTrack
+from .geometry import D_CAP, ObstacleTrack  # noqa: F401  (re-exported like the reference module)
 
 __all__ = [
     "FootprintSpec", "BatchProblem", "BatchParams", "BatchState", "RankedSolutions", "sample_initializations",

@@ -23,8 +23,8 @@ import numpy as np
 import torch
 
 from . import _lib, qpcore
-from .basis import AxisBoundary, BasisSet, Trajectory, boundary_matrix, line_basis_vectors
-from .geometry import D_CAP, EllipsoidShape
+from .basis import AxisBoundary, BasisSet, Trajectory, boundary_matrix, line_basis_vectors  # noqa: F401
+from .geometry import D_CAP, EllipsoidShape  # noqa: F401
 
 __all__ = [
     "StaticSphere",

@@ -26,8 +26,8 @@ import numpy as np
 import torch
 
 from . import _lib, qpcore
-from .basis import AxisBoundary, BasisSet, Trajectory, boundary_matrix
-from .geometry import ObstacleTrack
+from .basis import AxisBoundary, BasisSet, Trajectory, boundary_matrix  # noqa: F401
+from .geometry import ObstacleTrack  # noqa: F401
 
 _SPEED_EPS = 1e-6
 

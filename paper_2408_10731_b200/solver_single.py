@@ -23,7 +23,7 @@ import torch
 from . import _lib, qpcore
 from ._alg1 import Alg1Engine
 from .basis import AxisBoundary, BasisSet, Trajectory
-from .geometry import ObstacleTrack
+from .geometry import ObstacleTrack  # noqa: F401
 
 __all__ = [
     "SingleProblem",

@@ -5,7 +5,6 @@ import time
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 
-import numpy as np
 import torch
 
 from paper_2408_10731_b200 import scenarios

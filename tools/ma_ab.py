@@ -1,4 +1,4 @@
-import os, sys, json
+import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
 import bench
