@@ -355,6 +355,41 @@ typedef struct tro_b2_params {
 int tro_b2_run(int32_t mode, const tro_b2_dims* dims, const tro_b2_consts* c, const tro_b2_state* s,
                const tro_b2_params* p, void* stream);
 
+/* ------------------------------------------------------------------ batched post-solve validation (§8(f) 3)
+ * Replaces bench/metrics.py eval_metrics / check_collision_free / clearance_lower_bound (metrics.py:26-95)
+ * for a batch of trajectories against the RAW scenario geometry (constant-velocity obstacles, scenarios.py:
+ * 118-127).  One warp per member. */
+typedef struct tro_val_dims {
+    int64_t n_members;
+    int32_t n_obs;
+    int32_t n_p;
+    int32_t m;                  /* basis columns (coefficient input) */
+    int32_t dim;                /* 2 or 3 */
+    int32_t per_member_desired; /* 1: desired is n_members x n_p x dim, 0: n_p x dim shared */
+    int32_t reserved;
+} tro_val_dims;
+
+typedef struct tro_val_consts {
+    const double* P;          /* n_p x m (coefficient input) */
+    const double* Pdd;        /* n_p x m */
+    const double* t;          /* n_p sample times */
+    const double* centers;    /* n_obs x dim obstacle centres at t[0] */
+    const double* velocities; /* n_obs x dim */
+    const double* shape_a;    /* n_obs raw semi-axes (no planning inflation) */
+    const double* shape_b;
+    const double* desired;    /* NULL: tracking = 0 */
+    double margin;            /* check_collision_free margin on the scaled-distance axis */
+} tro_val_consts;
+
+typedef struct tro_val_io {
+    const double* xi;  /* n_members x dim x m coefficients, or NULL to use pos / acc samples */
+    const double* pos; /* n_members x n_p x dim */
+    const double* acc; /* n_members x n_p x dim */
+    double* out;       /* n_members x 5: smoothness, tracking, arc length, worst incursion, clearance bound */
+} tro_val_io;
+
+int tro_validate_f64(const tro_val_dims* dims, const tro_val_consts* c, const tro_val_io* io, void* stream);
+
 /* out (ncols x n) = rhs (ncols x n) * K^-T, i.e. out[c] = K^-1 rhs[c] for every column c.
  * kinv: n x n row-major.  qpcore.solve_batch with the RHS block [-q ; b]. */
 int tro_kkt_apply_f64(const double* kinv, int32_t n, const double* rhs, int64_t ncols,

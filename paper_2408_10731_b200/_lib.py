@@ -43,6 +43,7 @@ EXPORTS = (
     "tro_fp64_fma_probe",
     "tro_ma_run",
     "tro_b2_run",
+    "tro_validate_f64",
     "tro_version",
     "tro_error_string",
 )
@@ -187,6 +188,20 @@ class B2Params(ctypes.Structure):
                 ("member_offset", c_int64), ("n_shards", c_int32), ("reserved", c_int32)]
 
 
+class ValDims(ctypes.Structure):
+    _fields_ = [("n_members", c_int64)] + [(n, c_int32) for n in ("n_obs", "n_p", "m", "dim", "per_member_desired",
+                                                                  "reserved")]
+
+
+class ValConsts(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("P", "Pdd", "t", "centers", "velocities", "shape_a", "shape_b",
+                                        "desired")] + [("margin", c_double)]
+
+
+class ValIO(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("xi", "pos", "acc", "out")]
+
+
 TRO_B2_PSI_IN = 16
 TRO_B2_GIVEN_AD = 32
 TRO_B2_GIVEN_ALPHA = 64
@@ -236,6 +251,8 @@ def load() -> ctypes.CDLL:
     lib.tro_b2_run.argtypes = [c_int32, POINTER(B2Dims), POINTER(B2Consts), POINTER(B2State), POINTER(B2Params),
                                c_void_p]
     lib.tro_b2_run.restype = c_int32
+    lib.tro_validate_f64.argtypes = [POINTER(ValDims), POINTER(ValConsts), POINTER(ValIO), c_void_p]
+    lib.tro_validate_f64.restype = c_int32
     lib.tro_fp64_fma_probe.argtypes = [c_int64, c_int32, c_void_p, c_void_p]
     lib.tro_fp64_fma_probe.restype = c_int32
     lib.tro_version.argtypes = []

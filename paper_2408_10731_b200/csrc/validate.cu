@@ -1,0 +1,167 @@
+// Batched post-solve validation for sm_100a.
+//
+// The reference evaluates each trajectory in Python against the RAW scenario geometry
+// (bench/metrics.py:26-95): smoothness sum(acc^2), tracking sum((pos - desired)^2), arc length
+// sum |pos[t+1] - pos[t]|, the worst incursion max(1 + margin - dist) and the clearance lower bound
+// min((dist - 1) min(a, b)) with dist the ellipsoidal distance sqrt(dx^2/a^2 + dy^2/a^2 [+ dz^2/b^2])
+// to every obstacle's constant-velocity track (scenarios.py:118-127).  Here one warp owns one member:
+// lanes own samples, positions / accelerations come from the coefficients (P xi, Pddot xi) or from
+// given samples, obstacle centres are predicted on the fly (c + v (t - t0)), and every reduction runs
+// in a fixed order so a member's numbers do not depend on the batch.
+#include "common.cuh"
+#include "fastmath.cuh"
+#include "../../include/trajopt_b200.h"
+
+namespace tro {
+
+constexpr int kValWarps = 4;  // members per CTA
+
+struct ValArgs {
+    tro_val_dims d;
+    tro_val_consts c;
+    tro_val_io io;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(kValWarps * 32) validate_kernel(ValArgs A) {
+    extern __shared__ double smem[];
+    const int n_p = A.d.n_p, m = A.d.m, n_o = A.d.n_obs;
+    const bool coeffs = A.io.xi != nullptr;
+    double* sP = smem;                         // n_p x m   (coefficient mode)
+    double* sPdd = sP + n_p * m;               // n_p x m
+    double* sObs = sPdd + n_p * m;             // n_o x 8: c(3) v(3) inv a^2... see below
+    double* sPos = sObs + 8 * (n_o > 0 ? n_o : 1) + kValWarps * 0;  // kValWarps x n_p x DIM
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (coeffs)
+        for (int k = tid; k < n_p * m; k += blockDim.x) {
+            sP[k] = __ldg(A.c.P + k);
+            sPdd[k] = __ldg(A.c.Pdd + k);
+        }
+    // obstacle record: centre (3), velocity (3), 1/a^2, 1/b^2 ; a / b (for min(a, b)) read from global
+    for (int j = tid; j < n_o; j += blockDim.x) {
+        double* o = sObs + 8 * j;
+        for (int k = 0; k < 3; ++k) {
+            o[k] = k < DIM ? __ldg(A.c.centers + j * DIM + k) : 0.0;
+            o[3 + k] = k < DIM ? __ldg(A.c.velocities + j * DIM + k) : 0.0;
+        }
+        const double a = __ldg(A.c.shape_a + j), b = __ldg(A.c.shape_b + j);
+        o[6] = a * a;
+        o[7] = b * b;
+    }
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * kValWarps + warp;
+    if (i >= A.d.n_members) return;
+    double* pw = sPos + (int64_t)warp * n_p * DIM;
+    const double* xi = coeffs ? A.io.xi + i * DIM * m : nullptr;
+    const double t0 = __ldg(A.c.t);
+    double smooth = 0.0, track = 0.0, worst = -__longlong_as_double(0x7ff0000000000000LL);
+    double clear = __longlong_as_double(0x7ff0000000000000LL);
+    for (int t = lane; t < n_p; t += 32) {
+        double p[3] = {0, 0, 0}, ac[3] = {0, 0, 0};
+        if (coeffs) {
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                double ps = 0.0, as = 0.0;
+                for (int c = 0; c < m; ++c) {
+                    const double x = __ldg(xi + k * m + c);
+                    ps = fma(sP[t * m + c], x, ps);
+                    as = fma(sPdd[t * m + c], x, as);
+                }
+                p[k] = ps;
+                ac[k] = as;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                p[k] = __ldg(A.io.pos + (i * n_p + t) * DIM + k);
+                ac[k] = __ldg(A.io.acc + (i * n_p + t) * DIM + k);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            pw[t * DIM + k] = p[k];
+            smooth = fma(ac[k], ac[k], smooth);
+        }
+        if (A.c.desired) {
+            const double* dd = A.c.desired + (A.d.per_member_desired ? (i * n_p + t) * DIM : (int64_t)t * DIM);
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                const double e = p[k] - __ldg(dd + k);
+                track = fma(e, e, track);
+            }
+        }
+        const double tau = __ldg(A.c.t + t) - t0;  // predict_obstacles: c + v (t_now + t - t0), t_now = 0
+        for (int j = 0; j < n_o; ++j) {
+            const double* o = sObs + 8 * j;
+            double q = 0.0;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                const double d = p[k] - (o[k] + o[3 + k] * tau);
+                // metrics.py:63-65: the last axis uses b (z in 3-D, y in 2-D), the others a
+                q += d * d / (k == DIM - 1 ? o[7] : o[6]);
+            }
+            const double dist = sqrt(q);
+            const double w = 1.0 + A.c.margin - dist;
+            worst = w > worst ? w : worst;
+            const double a = __ldg(A.c.shape_a + j), b = __ldg(A.c.shape_b + j);
+            const double cl = (dist - 1.0) * (a < b ? a : b);
+            clear = cl < clear ? cl : clear;
+        }
+    }
+    __syncwarp();
+    // arc length over the warp's stored positions (metrics.py:39-40), fixed order: lanes own segments
+    double arc = 0.0;
+    for (int t = lane; t + 1 < n_p; t += 32) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const double e = pw[(t + 1) * DIM + k] - pw[t * DIM + k];
+            s = fma(e, e, s);
+        }
+        arc += sqrt(s);
+    }
+    smooth = warp_sum(smooth);
+    track = warp_sum(track);
+    arc = warp_sum(arc);
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ow = __shfl_xor_sync(0xffffffffu, worst, o), oc = __shfl_xor_sync(0xffffffffu, clear, o);
+        worst = ow > worst ? ow : worst;
+        clear = oc < clear ? oc : clear;
+    }
+    if (lane == 0) {
+        double* out = A.io.out + i * 5;
+        out[0] = smooth;
+        out[1] = track;
+        out[2] = arc;
+        out[3] = worst;   // -inf without obstacles (check_collision_free)
+        out[4] = clear;   // +inf without obstacles (clearance_lower_bound)
+    }
+}
+
+}  // namespace tro
+
+extern "C" int tro_validate_f64(const tro_val_dims* d, const tro_val_consts* c, const tro_val_io* io, void* stream) {
+    if (!d || !c || !io || !io->out || (d->dim != 2 && d->dim != 3) || d->n_p < 2 || d->n_obs < 0 || !c->t)
+        return TRO_EINVAL;
+    if (io->xi ? (d->m < 1 || !c->P || !c->Pdd) : (!io->pos || !io->acc)) return TRO_EINVAL;
+    if (d->n_obs > 0 && (!c->centers || !c->velocities || !c->shape_a || !c->shape_b)) return TRO_EINVAL;
+    if (d->n_members <= 0) return 0;
+    tro::ValArgs A;
+    A.d = *d;
+    A.c = *c;
+    A.io = *io;
+    const int m = io->xi ? d->m : 0;
+    const size_t smem = sizeof(double) * ((size_t)2 * d->n_p * m + 8 * (d->n_obs > 0 ? d->n_obs : 1) +
+                                          (size_t)tro::kValWarps * d->n_p * d->dim);
+    if (smem > 200 * 1024) return TRO_EINVAL;
+    const unsigned blocks = (unsigned)((d->n_members + tro::kValWarps - 1) / tro::kValWarps);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (d->dim == 3) {
+        cudaFuncSetAttribute(tro::validate_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tro::validate_kernel<3><<<blocks, tro::kValWarps * 32, smem, st>>>(A);
+    } else {
+        cudaFuncSetAttribute(tro::validate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        tro::validate_kernel<2><<<blocks, tro::kValWarps * 32, smem, st>>>(A);
+    }
+    return (int)cudaGetLastError();
+}

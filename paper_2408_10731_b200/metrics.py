@@ -1,0 +1,139 @@
+"""Run metrics and direct constraint checking against raw scenario geometry, on the GPU.
+
+Drop-in for the reference ``trajopt.bench.metrics`` (arXiv 2408.10731, bench/metrics.py:1-95) plus the
+batched form SURVEY.md §8(f) row 3 asks for: ``validate_batch`` evaluates smoothness, tracking, arc
+length, the worst incursion and the clearance lower bound of B trajectories against every obstacle's
+constant-velocity track in one launch of ``tro_validate_f64`` (csrc/validate.cu).  The per-trajectory
+functions keep the reference signatures and run the same kernel on a batch of one.
+
+``scenario`` is any object with ``dim`` and ``obstacles`` (each with ``a``, ``b``, ``center``,
+``velocity``), e.g. the reference's ``bench.scenarios.Scenario``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+__all__ = ["RunMetrics", "eval_metrics", "check_collision_free", "clearance_lower_bound", "validate_batch"]
+
+
+@dataclass
+class RunMetrics:
+    """metrics.py:14-23."""
+
+    smoothness: float
+    tracking: float
+    arc_length: float
+    success: bool
+    iters: int
+    residual_final: float
+    min_clearance: float
+    wall_time_ms: float
+
+
+def _obstacle_arrays(scenario):
+    obs = list(scenario.obstacles)
+    dim = int(scenario.dim)
+    if not obs:
+        z = np.zeros((0, dim))
+        return z, z, np.zeros(0), np.zeros(0)
+    c = np.array([np.asarray(o.center, float) for o in obs])
+    v = np.array([np.asarray(o.velocity, float) for o in obs])
+    return c, v, np.array([float(o.a) for o in obs]), np.array([float(o.b) for o in obs])
+
+
+def validate_batch(scenario, t, *, xi=None, basis=None, pos=None, acc=None, desired=None, margin: float = 0.0,
+                   device=None) -> dict:
+    """Metrics of B trajectories on the sample times ``t`` (n_p) against the raw scenario geometry.
+
+    Either coefficients ``xi`` (B, dim, m) with the ``basis`` they refer to (positions P xi,
+    accelerations Pddot xi are formed on the device), or samples ``pos`` / ``acc`` (B, n_p, dim).
+    ``desired``: (n_p, dim) shared or (B, n_p, dim) per member, or None (tracking = 0).
+    Returns numpy arrays (B,): smoothness, tracking, arc_length, worst (max of 1 + margin - dist;
+    -inf without obstacles), success (worst <= 0), min_clearance (+inf without obstacles)."""
+    _lib.require_cuda()
+    lib = _lib.load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    f64 = dict(dtype=torch.float64, device=dev)
+    dim = int(scenario.dim)
+    t = np.asarray(t, dtype=float)
+    n_p = t.size
+    if xi is not None:
+        if basis is None:
+            raise ValueError("coefficient input needs the basis")
+        xi_d = torch.as_tensor(np.ascontiguousarray(xi, dtype=np.float64), device=dev)
+        if xi_d.ndim != 3 or xi_d.shape[1] != dim:
+            raise ValueError("xi must be (B, dim, m)")
+        B, m = int(xi_d.shape[0]), int(xi_d.shape[2])
+        if basis.P.shape != (n_p, m):
+            raise ValueError("basis does not match t / xi")
+        P = torch.as_tensor(np.ascontiguousarray(basis.P), **f64)
+        Pdd = torch.as_tensor(np.ascontiguousarray(basis.Pddot), **f64)
+        pos_d = acc_d = None
+    else:
+        pos_d = torch.as_tensor(np.ascontiguousarray(pos, dtype=np.float64), device=dev)
+        acc_d = torch.as_tensor(np.ascontiguousarray(acc, dtype=np.float64), device=dev)
+        if pos_d.ndim != 3 or pos_d.shape[1:] != (n_p, dim) or acc_d.shape != pos_d.shape:
+            raise ValueError("pos / acc must be (B, n_p, dim)")
+        B, m = int(pos_d.shape[0]), 0
+        xi_d = P = Pdd = None
+    c, v, a, b = _obstacle_arrays(scenario)
+    n_o = a.size
+    consts_t = dict(t=torch.as_tensor(t, **f64), c=torch.as_tensor(c.reshape(-1), **f64),
+                    v=torch.as_tensor(v.reshape(-1), **f64), a=torch.as_tensor(a, **f64), b=torch.as_tensor(b, **f64))
+    per_member = 0
+    des = None
+    if desired is not None:
+        des = torch.as_tensor(np.ascontiguousarray(desired, dtype=np.float64), device=dev)
+        per_member = int(des.ndim == 3)
+        if des.shape != ((B, n_p, dim) if per_member else (n_p, dim)):
+            raise ValueError("desired must be (n_p, dim) or (B, n_p, dim)")
+    out = torch.empty((B, 5), **f64)
+    P_ = _lib.ptr
+    dims = _lib.ValDims(n_members=B, n_obs=n_o, n_p=n_p, m=m, dim=dim, per_member_desired=per_member, reserved=0)
+    consts = _lib.ValConsts(P=P_(P), Pdd=P_(Pdd), t=P_(consts_t["t"]), centers=P_(consts_t["c"]) if n_o else None,
+                            velocities=P_(consts_t["v"]) if n_o else None, shape_a=P_(consts_t["a"]) if n_o else None,
+                            shape_b=P_(consts_t["b"]) if n_o else None, desired=P_(des), margin=float(margin))
+    io = _lib.ValIO(xi=P_(xi_d), pos=P_(pos_d), acc=P_(acc_d), out=out.data_ptr())
+    with torch.cuda.device(dev):
+        rc = lib.tro_validate_f64(ctypes.byref(dims), ctypes.byref(consts), ctypes.byref(io), _lib.stream_handle())
+    _lib.check(rc, "tro_validate_f64")
+    o = out.cpu().numpy()
+    return {"smoothness": o[:, 0], "tracking": o[:, 1], "arc_length": o[:, 2], "worst": o[:, 3],
+            "success": o[:, 3] <= 0.0, "min_clearance": o[:, 4]}
+
+
+def _one(trajectory, scenario, desired=None, margin=0.0) -> dict:
+    return validate_batch(scenario, trajectory.t, pos=np.asarray(trajectory.pos, float)[None],
+                          acc=np.asarray(trajectory.acc, float)[None],
+                          desired=None if desired is None else np.asarray(desired, float), margin=margin)
+
+
+def eval_metrics(trajectory, scenario, desired: np.ndarray | None = None) -> RunMetrics:
+    """Smoothness / tracking / arc-length metrics of a sampled trajectory (metrics.py:26-52)."""
+    r = _one(trajectory, scenario, desired)
+    return RunMetrics(smoothness=float(r["smoothness"][0]), tracking=float(r["tracking"][0]),
+                      arc_length=float(r["arc_length"][0]), success=False, iters=0, residual_final=0.0,
+                      min_clearance=float(r["min_clearance"][0]), wall_time_ms=0.0)
+
+
+def check_collision_free(trajectory, scenario, margin: float = 0.0) -> tuple[bool, float]:
+    """(ok, worst_violation) of the raw quadratic separation constraints (metrics.py:70-82)."""
+    if not scenario.obstacles:
+        return True, -math.inf
+    w = float(_one(trajectory, scenario, margin=margin)["worst"][0])
+    return w <= 0.0, w
+
+
+def clearance_lower_bound(trajectory, scenario) -> float:
+    """Conservative metric clearance in meters (metrics.py:85-95); +inf with no obstacles."""
+    if not scenario.obstacles:
+        return math.inf
+    return float(_one(trajectory, scenario)["min_clearance"][0])

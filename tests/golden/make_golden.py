@@ -454,6 +454,42 @@ def make_batch2d():
           "rho", ranked.state.rho)
 
 
+def make_metrics():
+    """bench/metrics.py on a few trajectories (straight lines, perturbed, a converged C1 solve) against raw
+    scenario geometry (3-D random-static, 2-D dynamic-flow)."""
+    from trajopt.basis import Trajectory, straight_line_coeffs
+    from trajopt.bench import metrics as MT
+
+    out = {}
+    rng = np.random.default_rng(5)
+    for tag, kind, dim, n_o in (("s3", "random-static", 3, 10), ("f2", "dynamic-flow", 2, 12)):
+        sc = gen_scenario(kind, {"dim": dim, "n_o": n_o, "n_p": 100}, seed=2)
+        basis = build_basis(sc.horizon.t0, sc.horizon.tf, sc.horizon.n_p, 10)
+        line = straight_line_coeffs(basis, np.asarray(sc.boundary.start), np.asarray(sc.boundary.goal))
+        xis = [line + s * rng.normal(size=line.shape) for s in (0.0, 0.3, 0.6, 1.0, 1.5)]
+        if tag == "s3":
+            prob = single_problem_from_scenario(sc, basis)
+            xis.append(solver_single.solve_single(prob, solver_single.SingleParams()).state.xi)
+        xis = np.stack(xis)  # (B, dim, m)
+        desired = np.asarray(sc.boundary.start)[None, :] + np.linspace(0, 1, basis.n_p)[:, None] * (
+            np.asarray(sc.boundary.goal) - np.asarray(sc.boundary.start))[None, :]
+        res = []
+        for x in xis:
+            tr = Trajectory(t=basis.grid.timestamps, pos=basis.P @ x.T, vel=basis.Pdot @ x.T, acc=basis.Pddot @ x.T)
+            em = MT.eval_metrics(tr, sc, desired)
+            ok0, w0 = MT.check_collision_free(tr, sc, margin=0.0)
+            ok1, w1 = MT.check_collision_free(tr, sc, margin=0.1)
+            res.append([em.smoothness, em.tracking, em.arc_length, em.min_clearance, w0, float(ok0), w1, float(ok1),
+                        MT.clearance_lower_bound(tr, sc)])
+        out[f"{tag}_xi"] = xis
+        out[f"{tag}_P"], out[f"{tag}_Pdd"], out[f"{tag}_t"] = basis.P, basis.Pddot, basis.grid.timestamps
+        out[f"{tag}_desired"] = desired
+        out[f"{tag}_obs"] = np.array([list(o.center) + list(o.velocity) + [o.a, o.b] for o in sc.obstacles])
+        out[f"{tag}_res"] = np.array(res)
+    np.savez_compressed(os.path.join(OUT, "metrics.npz"), **out)
+    print("metrics written")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
