@@ -46,6 +46,9 @@ CONFIGS["c3"] = (16, 4096, 200, "C3: 4096 joint problems x 16 quadrotors (120 pa
                                 "200 iterations (rho_final 1e3, tol 0: fixed work)")
 CONFIGS["c2alt"] = (50, 1024, 200, "C2-alt (Alg. 2): 1024 members x 50 dyn. circles (dynamic-flow, seed 0) x "
                                    "n_p 100, 1 footprint circle + heading, 200 batch iterations (2-D)")
+CONFIGS["val"] = (100, 131072, 1, "Validation (SURVEY 8(f) row 3): 131072 C5 trajectories x 100 raw dynamic ellipsoids "
+                                  "x n_p 100: smoothness, tracking, arc length, worst incursion, clearance bound")
+VAL_FLOPS_ELEM = 24  # per (member, obstacle, sample): predicted centre 6, offset 3, quad 8, sqrt 1, worst 2, clearance 2
 B2_FLOPS_ELEM = 20  # per (circle, obstacle, sample): deltas, unit vector, num / den / d, targets, residual
 WORDS_3D = 9  # persistent words per (member, obstacle, sample): alpha beta lx ly lz lca lsa lcb lsb
 
@@ -358,6 +361,97 @@ def run_c2alt(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def val_inputs(total: int):
+    """C5 obstacles (raw shapes, no planning inflation) and member trajectories (straight-line coefficients)."""
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200.basis import build_basis, line_basis_vectors
+
+    basis = build_basis(0.0, 10.0, 100, 10)
+    specs = scenarios.flow3d_obstacles(100)
+    starts, goals = scenarios.flow3d_endpoints(range(total))
+    u, v = line_basis_vectors(basis)
+    xi = starts[:, :, None] * u[None, None, :] + (goals - starts)[:, :, None] * v[None, None, :]  # (B, 3, m)
+
+    class Obs:
+        def __init__(self, sp):
+            self.a, self.b, self.center, self.velocity = sp.a, sp.b, list(sp.center), list(sp.velocity)
+
+    class Scene:
+        dim = 3
+        obstacles = [Obs(sp) for sp in specs]
+
+    return basis, Scene(), xi
+
+
+def run_val(args):
+    import torch
+
+    from paper_2408_10731_b200 import metrics as MT
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    n_o, total, _, desc = CONFIGS["val"]
+    if args.members:
+        total = args.members
+    basis, sc, xi = val_inputs(total)
+    t = basis.grid.timestamps
+    dev = torch.device("cuda")
+    xi_dev = torch.as_tensor(xi, device=dev).contiguous()
+    xi_pin = torch.as_tensor(xi).pin_memory()
+    for _ in range(args.warmup):
+        MT.validate_batch(sc, t, xi=xi_dev, basis=basis, return_device=True)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):  # device-resident coefficients and results
+        MT.validate_batch(sc, t, xi=xi_dev, basis=basis, return_device=True)
+    b.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_s = a.elapsed_time(b) / 1e3 / args.steps
+    a.record()
+    for _ in range(args.steps):
+        r = MT.validate_batch(sc, t, xi=xi_pin, basis=basis)  # coefficients from pinned host memory, results back
+    b.record()
+    torch.cuda.synchronize()
+    e2e_s = a.elapsed_time(b) / 1e3 / args.steps
+    flops = VAL_FLOPS_ELEM * total * n_o * 100
+    peak = fp64_peak_tflops()
+    line = {
+        "metric": "trajectories validated/sec (raw-geometry metrics + collision check)", "value": total / step_s,
+        "unit": "traj/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (C5 recipe obstacles, straight-line member trajectories)",
+        "config": {"workload": desc, "members": total, "n_obs": n_o, "n_p": 100},
+        "roofline": {"bound": "fp64", "achieved": flops / step_s / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops / step_s / 1e12 / peak, "traffic": None,
+                     "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)", "kernel": "tro_validate_f64",
+                     "avg_launch_ms": step_s * 1e3, "algorithmic_flops_per_launch": flops,
+                     "note": "per-step time includes validate_batch's host-side argument setup (cached constants)"},
+        "clocks": clk,
+        "e2e": {"value": total / e2e_s, "unit": "traj/s", "h2d_bytes_per_step": int(xi.nbytes),
+                "d2h_bytes_per_step": int(total * 5 * 8)},
+        "gpu_launches": args.steps,
+        "result": {"collision_free": int(r["success"].sum())},
+    }
+    if not args.no_cpu_baseline:
+        from oracle import metrics as OMT
+
+        c = np.array([o.center for o in sc.obstacles])
+        v = np.array([o.velocity for o in sc.obstacles])
+        aa = np.array([o.a for o in sc.obstacles])
+        bb = np.array([o.b for o in sc.obstacles])
+        n_s = 64
+        t0 = time.perf_counter()
+        for k in range(n_s):
+            OMT.metrics(basis.P @ xi[k].T, basis.Pddot @ xi[k].T, t, c, v, aa, bb, 3)
+        wall = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n_s / wall, "unit": "traj/s", "cores": 1, "kind": "port",
+                                "sample": f"{n_s} trajectories x 100 obstacles, oracle port of bench.metrics (1 core)"}
+    print(json.dumps(line), flush=True)
 
 
 def cpu_reference_c2alt(n_iter=3):
@@ -1034,6 +1128,8 @@ def main():
         run_c3(args)
     elif args.config == "c2alt":
         run_c2alt(args)
+    elif args.config == "val":
+        run_val(args)
     else:
         run_b200(args)
 

@@ -15,6 +15,7 @@
 namespace tro {
 
 constexpr int kValWarps = 4;  // members per CTA
+constexpr int kValRec = 9;     // doubles per obstacle record
 
 struct ValArgs {
     tro_val_dims d;
@@ -30,32 +31,43 @@ __global__ void __launch_bounds__(kValWarps * 32) validate_kernel(ValArgs A) {
     double* sP = smem;                         // n_p x m   (coefficient mode)
     double* sPdd = sP + n_p * m;               // n_p x m
     double* sObs = sPdd + n_p * m;             // n_o x 8: c(3) v(3) inv a^2... see below
-    double* sPos = sObs + 8 * (n_o > 0 ? n_o : 1) + kValWarps * 0;  // kValWarps x n_p x DIM
+    double* sPos = sObs + kValRec * (n_o > 0 ? n_o : 1);  // kValWarps x n_p x DIM
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (coeffs)
         for (int k = tid; k < n_p * m; k += blockDim.x) {
             sP[k] = __ldg(A.c.P + k);
             sPdd[k] = __ldg(A.c.Pdd + k);
         }
-    // obstacle record: centre (3), velocity (3), 1/a^2, 1/b^2 ; a / b (for min(a, b)) read from global
+    // obstacle record: centre (3), velocity (3), 1/a^2, 1/b^2, min(a, b)
     for (int j = tid; j < n_o; j += blockDim.x) {
-        double* o = sObs + 8 * j;
+        double* o = sObs + kValRec * j;
         for (int k = 0; k < 3; ++k) {
             o[k] = k < DIM ? __ldg(A.c.centers + j * DIM + k) : 0.0;
             o[3 + k] = k < DIM ? __ldg(A.c.velocities + j * DIM + k) : 0.0;
         }
         const double a = __ldg(A.c.shape_a + j), b = __ldg(A.c.shape_b + j);
-        o[6] = a * a;
-        o[7] = b * b;
+        o[6] = 1.0 / (a * a);
+        o[7] = 1.0 / (b * b);
+        o[8] = a < b ? a : b;
     }
     __syncthreads();
+    // one clearance scale min(a, b) for every obstacle (the common case): then worst and the clearance
+    // bound are monotone functions of the smallest scaled square distance, so one sqrt per member suffices
+    __shared__ int s_uniform;
+    if (tid == 0) {
+        int u = 1;
+        for (int j = 1; j < n_o; ++j) u &= sObs[kValRec * j + 8] == sObs[8];
+        s_uniform = u;
+    }
+    __syncthreads();
+    const bool uniform = s_uniform != 0;
     const int64_t i = (int64_t)blockIdx.x * kValWarps + warp;
     if (i >= A.d.n_members) return;
     double* pw = sPos + (int64_t)warp * n_p * DIM;
     const double* xi = coeffs ? A.io.xi + i * DIM * m : nullptr;
     const double t0 = __ldg(A.c.t);
-    double smooth = 0.0, track = 0.0, worst = -__longlong_as_double(0x7ff0000000000000LL);
-    double clear = __longlong_as_double(0x7ff0000000000000LL);
+    double smooth = 0.0, track = 0.0;
+    double qmin = __longlong_as_double(0x7ff0000000000000LL), clear = qmin;
     for (int t = lane; t < n_p; t += 32) {
         double p[3] = {0, 0, 0}, ac[3] = {0, 0, 0};
         if (coeffs) {
@@ -92,20 +104,20 @@ __global__ void __launch_bounds__(kValWarps * 32) validate_kernel(ValArgs A) {
         }
         const double tau = __ldg(A.c.t + t) - t0;  // predict_obstacles: c + v (t_now + t - t0), t_now = 0
         for (int j = 0; j < n_o; ++j) {
-            const double* o = sObs + 8 * j;
+            const double* o = sObs + kValRec * j;
             double q = 0.0;
 #pragma unroll
             for (int k = 0; k < DIM; ++k) {
-                const double d = p[k] - (o[k] + o[3 + k] * tau);
-                // metrics.py:63-65: the last axis uses b (z in 3-D, y in 2-D), the others a
-                q += d * d / (k == DIM - 1 ? o[7] : o[6]);
+                const double d = p[k] - fma(o[3 + k], tau, o[k]);
+                // metrics.py:63-65: the last axis uses b (z in 3-D, y in 2-D), the others a; multiplied by the
+                // reciprocal squares (<= 1 ulp per term from the reference's divisions)
+                q = fma(d * d, k == DIM - 1 ? o[7] : o[6], q);
             }
-            const double dist = sqrt(q);
-            const double w = 1.0 + A.c.margin - dist;
-            worst = w > worst ? w : worst;
-            const double a = __ldg(A.c.shape_a + j), b = __ldg(A.c.shape_b + j);
-            const double cl = (dist - 1.0) * (a < b ? a : b);
-            clear = cl < clear ? cl : clear;
+            qmin = q < qmin ? q : qmin;
+            if (!uniform) {
+                const double cl = (sqrt(q) - 1.0) * o[8];
+                clear = cl < clear ? cl : clear;
+            }
         }
     }
     __syncwarp();
@@ -124,10 +136,14 @@ __global__ void __launch_bounds__(kValWarps * 32) validate_kernel(ValArgs A) {
     track = warp_sum(track);
     arc = warp_sum(arc);
     for (int o = 16; o > 0; o >>= 1) {
-        const double ow = __shfl_xor_sync(0xffffffffu, worst, o), oc = __shfl_xor_sync(0xffffffffu, clear, o);
-        worst = ow > worst ? ow : worst;
+        const double oq = __shfl_xor_sync(0xffffffffu, qmin, o), oc = __shfl_xor_sync(0xffffffffu, clear, o);
+        qmin = oq < qmin ? oq : qmin;
         clear = oc < clear ? oc : clear;
     }
+    // max(1 + margin - dist) = 1 + margin - sqrt(min q) (sqrt and the affine maps are monotone, also rounded)
+    const double dmin = sqrt(qmin);
+    const double worst = n_o > 0 ? (1.0 + A.c.margin) - dmin : -__longlong_as_double(0x7ff0000000000000LL);
+    if (uniform && n_o > 0) clear = (dmin - 1.0) * sObs[8];
     if (lane == 0) {
         double* out = A.io.out + i * 5;
         out[0] = smooth;
@@ -151,7 +167,7 @@ extern "C" int tro_validate_f64(const tro_val_dims* d, const tro_val_consts* c, 
     A.c = *c;
     A.io = *io;
     const int m = io->xi ? d->m : 0;
-    const size_t smem = sizeof(double) * ((size_t)2 * d->n_p * m + 8 * (d->n_obs > 0 ? d->n_obs : 1) +
+    const size_t smem = sizeof(double) * ((size_t)2 * d->n_p * m + tro::kValRec * (d->n_obs > 0 ? d->n_obs : 1) +
                                           (size_t)tro::kValWarps * d->n_p * d->dim);
     if (smem > 200 * 1024) return TRO_EINVAL;
     const unsigned blocks = (unsigned)((d->n_members + tro::kValWarps - 1) / tro::kValWarps);

@@ -49,15 +49,45 @@ def _obstacle_arrays(scenario):
     return c, v, np.array([float(o.a) for o in obs]), np.array([float(o.b) for o in obs])
 
 
+_CONST_CACHE: dict = {}
+
+
+def _device_consts(t, c, v, a, b, dev) -> dict:
+    """Sample times and obstacle arrays on the device, cached by content (uploaded once per scenario)."""
+    import hashlib
+
+    h = hashlib.blake2b(digest_size=16)
+    for arr in (t, c, v, a, b):
+        h.update(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
+    key = (h.digest(), str(dev))
+    d = _CONST_CACHE.get(key)
+    if d is None:
+        if len(_CONST_CACHE) > 32:
+            _CONST_CACHE.clear()
+        f64 = dict(dtype=torch.float64, device=dev)
+        d = _CONST_CACHE[key] = dict(t=torch.as_tensor(t, **f64), c=torch.as_tensor(c.reshape(-1), **f64),
+                                     v=torch.as_tensor(v.reshape(-1), **f64), a=torch.as_tensor(a, **f64),
+                                     b=torch.as_tensor(b, **f64))
+    return d
+
+
+def _dev_array(x, dev):
+    """numpy or torch (any device; pinned host tensors copy asynchronously) -> contiguous fp64 on dev."""
+    if isinstance(x, torch.Tensor):
+        return x.to(device=dev, dtype=torch.float64, non_blocking=True).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=dev)
+
+
 def validate_batch(scenario, t, *, xi=None, basis=None, pos=None, acc=None, desired=None, margin: float = 0.0,
-                   device=None) -> dict:
+                   device=None, return_device: bool = False) -> dict:
     """Metrics of B trajectories on the sample times ``t`` (n_p) against the raw scenario geometry.
 
     Either coefficients ``xi`` (B, dim, m) with the ``basis`` they refer to (positions P xi,
     accelerations Pddot xi are formed on the device), or samples ``pos`` / ``acc`` (B, n_p, dim).
     ``desired``: (n_p, dim) shared or (B, n_p, dim) per member, or None (tracking = 0).
     Returns numpy arrays (B,): smoothness, tracking, arc_length, worst (max of 1 + margin - dist;
-    -inf without obstacles), success (worst <= 0), min_clearance (+inf without obstacles)."""
+    -inf without obstacles), success (worst <= 0), min_clearance (+inf without obstacles).
+    return_device=True keeps the (B, 5) result on the device (key "out", columns in that order)."""
     _lib.require_cuda()
     lib = _lib.load()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -68,30 +98,29 @@ def validate_batch(scenario, t, *, xi=None, basis=None, pos=None, acc=None, desi
     if xi is not None:
         if basis is None:
             raise ValueError("coefficient input needs the basis")
-        xi_d = torch.as_tensor(np.ascontiguousarray(xi, dtype=np.float64), device=dev)
+        xi_d = _dev_array(xi, dev)
         if xi_d.ndim != 3 or xi_d.shape[1] != dim:
             raise ValueError("xi must be (B, dim, m)")
         B, m = int(xi_d.shape[0]), int(xi_d.shape[2])
         if basis.P.shape != (n_p, m):
             raise ValueError("basis does not match t / xi")
-        P = torch.as_tensor(np.ascontiguousarray(basis.P), **f64)
-        Pdd = torch.as_tensor(np.ascontiguousarray(basis.Pddot), **f64)
+        bk = _device_consts(basis.P.ravel(), basis.Pddot.ravel(), np.zeros(0), np.zeros(0), np.zeros(0), dev)
+        P, Pdd = bk["t"], bk["c"]  # the cached P / Pddot (row-major n_p x m)
         pos_d = acc_d = None
     else:
-        pos_d = torch.as_tensor(np.ascontiguousarray(pos, dtype=np.float64), device=dev)
-        acc_d = torch.as_tensor(np.ascontiguousarray(acc, dtype=np.float64), device=dev)
+        pos_d = _dev_array(pos, dev)
+        acc_d = _dev_array(acc, dev)
         if pos_d.ndim != 3 or pos_d.shape[1:] != (n_p, dim) or acc_d.shape != pos_d.shape:
             raise ValueError("pos / acc must be (B, n_p, dim)")
         B, m = int(pos_d.shape[0]), 0
         xi_d = P = Pdd = None
     c, v, a, b = _obstacle_arrays(scenario)
     n_o = a.size
-    consts_t = dict(t=torch.as_tensor(t, **f64), c=torch.as_tensor(c.reshape(-1), **f64),
-                    v=torch.as_tensor(v.reshape(-1), **f64), a=torch.as_tensor(a, **f64), b=torch.as_tensor(b, **f64))
+    consts_t = _device_consts(t, c, v, a, b, dev)
     per_member = 0
     des = None
     if desired is not None:
-        des = torch.as_tensor(np.ascontiguousarray(desired, dtype=np.float64), device=dev)
+        des = _dev_array(desired, dev)
         per_member = int(des.ndim == 3)
         if des.shape != ((B, n_p, dim) if per_member else (n_p, dim)):
             raise ValueError("desired must be (n_p, dim) or (B, n_p, dim)")
@@ -105,7 +134,9 @@ def validate_batch(scenario, t, *, xi=None, basis=None, pos=None, acc=None, desi
     with torch.cuda.device(dev):
         rc = lib.tro_validate_f64(ctypes.byref(dims), ctypes.byref(consts), ctypes.byref(io), _lib.stream_handle())
     _lib.check(rc, "tro_validate_f64")
-    o = out.cpu().numpy()
+    if return_device:
+        return {"out": out}
+    o = out.cpu().numpy()  # one device-to-host copy of the B x 5 results
     return {"smoothness": o[:, 0], "tracking": o[:, 1], "arc_length": o[:, 2], "worst": o[:, 3],
             "success": o[:, 3] <= 0.0, "min_clearance": o[:, 4]}
 
