@@ -65,9 +65,8 @@ def _device_consts(t, c, v, a, b, dev) -> dict:
         if len(_CONST_CACHE) > 32:
             _CONST_CACHE.clear()
         f64 = dict(dtype=torch.float64, device=dev)
-        d = _CONST_CACHE[key] = dict(t=torch.as_tensor(t, **f64), c=torch.as_tensor(c.reshape(-1), **f64),
-                                     v=torch.as_tensor(v.reshape(-1), **f64), a=torch.as_tensor(a, **f64),
-                                     b=torch.as_tensor(b, **f64))
+        up = lambda x: torch.as_tensor(np.array(x, dtype=np.float64).reshape(-1), **f64)  # noqa: E731 (owned copy)
+        d = _CONST_CACHE[key] = dict(t=up(t), c=up(c), v=up(v), a=up(a), b=up(b))
     return d
 
 
