@@ -174,11 +174,19 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
         }
     }
     __syncthreads();
-    for (int k = tid; k < n_p * n_a * 3; k += blockDim.x) {
-        const int t = k / (n_a * 3), r = k - t * n_a * 3, a = r / 3, ax = r - a * 3;
-        double acc = 0.0;
-        for (int cc = 0; cc < m; ++cc) acc = fma(sP[t * m + cc], sXi[ax * nv + a * m + cc], acc);
-        sPos[k] = acc;
+    for (int k = tid; k < n_p * n_a; k += blockDim.x) {  // one (t, agent) per thread: 3 axes share the P row
+        const int t = k / n_a, a = k - t * n_a;
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+        for (int cc = 0; cc < m; ++cc) {
+            const double pv = sP[t * m + cc];
+            p0 = fma(pv, sXi[a * m + cc], p0);
+            p1 = fma(pv, sXi[nv + a * m + cc], p1);
+            p2 = fma(pv, sXi[2 * nv + a * m + cc], p2);
+        }
+        double* o = sPos + k * 3;
+        o[0] = p0;
+        o[1] = p1;
+        o[2] = p2;
     }
     __syncthreads();
 
@@ -296,13 +304,14 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
                 A.s.export_ab[nplane + e] = atan2(sb, cb);
             }
             // next RHS: recon (+ static centre) and lambda, scattered to the pair's agents below
-            double* sc = sScr + p * 6;
+            // planes [recon x y z | lambda x y z] x pairs: lanes write consecutive pairs (no bank conflicts)
+            double* sc = sScr + p;
             sc[0] = rx + (pj < 0 ? cen[0] : 0.0);
-            sc[1] = ry + (pj < 0 ? cen[1] : 0.0);
-            sc[2] = rz + (pj < 0 ? cen[2] : 0.0);
-            sc[3] = lx;
-            sc[4] = ly;
-            sc[5] = lz;
+            sc[np_] = ry + (pj < 0 ? cen[1] : 0.0);
+            sc[2 * np_] = rz + (pj < 0 ? cen[2] : 0.0);
+            sc[3 * np_] = lx;
+            sc[4 * np_] = ly;
+            sc[5 * np_] = lz;
         }
         __syncwarp();
         // per-agent signed incidence sums (fixed order), contracted with P[t][:]
@@ -312,9 +321,9 @@ __global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
             for (int q = sIncPtr[a]; q < sIncPtr[a + 1]; ++q) {
                 const int pe = sInc[q];
                 const double sgn = pe >= 0 ? 1.0 : -1.0;
-                const double* sc = sScr + (pe >= 0 ? pe : -pe - 1) * 6 + 3 * which;
+                const double* sc = sScr + (pe >= 0 ? pe : -pe - 1) + 3 * which * np_;
 #pragma unroll
-                for (int k = 0; k < 3; ++k) v[k] = fma(sgn, sc[k], v[k]);
+                for (int k = 0; k < 3; ++k) v[k] = fma(sgn, sc[k * np_], v[k]);
             }
             if constexpr (M > 0) {
                 if (task < 32) {  // M > 0 path keeps one task per lane (tasks <= 32)
