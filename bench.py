@@ -48,6 +48,10 @@ CONFIGS["c2alt"] = (50, 1024, 200, "C2-alt (Alg. 2): 1024 members x 50 dyn. circ
                                    "n_p 100, 1 footprint circle + heading, 200 batch iterations (2-D)")
 CONFIGS["val"] = (100, 131072, 1, "Validation (SURVEY 8(f) row 3): 131072 C5 trajectories x 100 raw dynamic ellipsoids "
                                   "x n_p 100: smoothness, tracking, arc length, worst incursion, clearance bound")
+CONFIGS["mpc"] = (50, 1024, 40, "MPC fleet (SURVEY 8(f) row 2): 1024 robots in the C2 field (50 dyn. ellipsoids, "
+                                "n_p 100, 3-D), receding horizon: 30 control steps x 40 warm AM its, 10 samples "
+                                "executed per step")
+MPC_STEPS = 30
 VAL_FLOPS_ELEM = 24  # per (member, obstacle, sample): predicted centre 6, offset 3, quad 8, sqrt 1, worst 2, clearance 2
 B2_FLOPS_ELEM = 20  # per (circle, obstacle, sample): deltas, unit vector, num / den / d, targets, residual
 WORDS_3D = 9  # persistent words per (member, obstacle, sample): alpha beta lx ly lz lca lsa lcb lsb
@@ -438,20 +442,125 @@ def run_val(args):
         "result": {"collision_free": int(r["success"].sum())},
     }
     if not args.no_cpu_baseline:
-        from oracle import metrics as OMT
-
-        c = np.array([o.center for o in sc.obstacles])
-        v = np.array([o.velocity for o in sc.obstacles])
-        aa = np.array([o.a for o in sc.obstacles])
-        bb = np.array([o.b for o in sc.obstacles])
-        n_s = 64
-        t0 = time.perf_counter()
-        for k in range(n_s):
-            OMT.metrics(basis.P @ xi[k].T, basis.Pddot @ xi[k].T, t, c, v, aa, bb, 3)
-        wall = time.perf_counter() - t0
-        line["cpu_baseline"] = {"value": n_s / wall, "unit": "traj/s", "cores": 1, "kind": "port",
-                                "sample": f"{n_s} trajectories x 100 obstacles, oracle port of bench.metrics (1 core)"}
+        v, info = cpu_reference_val()
+        line["cpu_baseline"] = {"value": v, "unit": "traj/s", "cores": 1, "kind": "port", "sample": info}
     print(json.dumps(line), flush=True)
+
+
+def cpu_reference_val(n_s=64):
+    """The oracle port of bench.metrics on a bounded sample of the validation workload (1 core)."""
+    from oracle import metrics as OMT
+
+    basis, sc, xi = val_inputs(n_s)
+    t = basis.grid.timestamps
+    c = np.array([o.center for o in sc.obstacles])
+    v = np.array([o.velocity for o in sc.obstacles])
+    aa = np.array([o.a for o in sc.obstacles])
+    bb = np.array([o.b for o in sc.obstacles])
+    t0 = time.perf_counter()
+    for k in range(n_s):
+        OMT.metrics(basis.P @ xi[k].T, basis.Pddot @ xi[k].T, t, c, v, aa, bb, 3)
+    wall = time.perf_counter() - t0
+    return n_s / wall, f"{n_s} trajectories x 100 obstacles, oracle port of bench.metrics (1 core)"
+
+
+def mpc_inputs(total: int):
+    """The C2 obstacle field as a bench Scenario (3-D, a 0.4 / b 0.3, seeded recipe) + C2 member endpoints."""
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200.bench import scenarios as SC
+
+    specs = scenarios.flow3d_obstacles(CONFIGS["mpc"][0])
+    starts, goals = scenarios.flow3d_endpoints(range(total))
+    sc = SC.Scenario(kind="dynamic-flow", dim=3, horizon=SC.Horizon(t0=0.0, tf=10.0, n_p=100),
+                     robot=SC.RobotSpec(shape=[0.0, 0.0], v_max=3.0, a_max=3.0),
+                     obstacles=[SC.ScenarioObstacle(a=o.a, b=o.b, center=[float(x) for x in o.center],
+                                                    velocity=[float(x) for x in o.velocity]) for o in specs],
+                     boundary=SC.Boundary(start=[0.0, 0.0, 0.0], goal=[12.0, 0.0, 0.0]), seed=0)
+    return sc, starts, goals
+
+
+def run_mpc(args):
+    """One step = one receding-horizon episode of the whole fleet (30 control steps of 40 warm AM iterations
+    + predict / validate / advance per control step), device-resident between control steps."""
+    import torch
+
+    from paper_2408_10731_b200.mpc import MpcFleet
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    n_o, total, budget, desc = CONFIGS["mpc"]
+    if args.members:
+        total = args.members
+    sc, starts, goals = mpc_inputs(total)
+    fleet = MpcFleet(sc, starts, goals, step_budget=budget, layout=args.layout)
+    for _ in range(args.warmup):
+        fleet.run(MPC_STEPS, early_exit=False)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    solve_ms = []
+    a.record()
+    for _ in range(args.steps):
+        fr = fleet.run(MPC_STEPS, early_exit=False)
+        solve_ms.append(float(fr.step_ms.sum()))
+    b.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_s = a.elapsed_time(b) / 1e3 / args.steps
+    robot_steps = total * MPC_STEPS
+    # e2e: the public API from host arrays: fleet construction (uploads) + episode + results to the host
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fr_e = MpcFleet(sc, starts, goals, step_budget=budget, layout=args.layout).run(MPC_STEPS, early_exit=False)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    active = (fr.flags == 0).sum()
+    # roofline of the dominant kernel (the fused AM iteration): algorithmic bytes per launch / per-iteration time
+    it_ms = statistics.mean(solve_ms) / MPC_STEPS / budget
+    bytes_launch = 2 * WORDS_3D * n_o * 100 * 8 * total
+    peak, peak_src = measured_peaks()
+    line = {
+        "metric": "robot control steps/sec (receding horizon, 40 warm AM its per step)",
+        "value": robot_steps / step_s, "unit": "robot-steps/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (C2 recipe obstacle field and endpoints)",
+        "config": {"workload": desc, "robots": total, "n_obs": n_o, "n_p": 100, "control_steps": MPC_STEPS,
+                   "step_budget": budget, "layout": args.layout, "l2": "per-element state 720 MB > L2"},
+        "control_step_ms": step_s * 1e3 / MPC_STEPS,
+        "paper_budget_ms": 40.0,
+        "roofline": {"bound": "hbm", "achieved": bytes_launch / (it_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": bytes_launch / (it_ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                     "kernel": "alg1 fused AM iteration (incl. the per-step prime)",
+                     "avg_launch_ms": it_ms, "algorithmic_bytes_per_launch": bytes_launch},
+        "clocks": clk,
+        "e2e": {"value": robot_steps / e2e_s, "unit": "robot-steps/s",
+                "h2d_bytes_per_step": int(starts.nbytes + goals.nbytes),
+                "d2h_bytes_per_step": int(fr_e.trace.nbytes + fr_e.metrics.nbytes + fr_e.residual.nbytes
+                                          + fr_e.flags.nbytes + fr_e.n_trace.nbytes)},
+        "gpu_launches": args.steps * (2 + MPC_STEPS * (4 + budget)),
+        "result": {"still_driving": int(active), "collided": int((fr.flags == 1).sum()),
+                   "reached": int((fr.flags == 2).sum())},
+    }
+    if not args.no_cpu_baseline:
+        v, info = cpu_reference_mpc()
+        line["cpu_baseline"] = {"value": v, "unit": "robot-steps/s", "cores": 1, "kind": "port",
+                                "sample": info}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_reference_mpc(robots=2, steps=3):
+    """The oracle port of receding_horizon_run (bit-exact with the reference) on a bounded sample."""
+    from oracle import mpc as OM
+    from paper_2408_10731_b200.basis import build_basis
+    from paper_2408_10731_b200.bench.scenarios import obstacle_arrays
+
+    sc, starts, goals = mpc_inputs(robots)
+    b = build_basis(0.0, 10.0, 100, 10)
+    c, v, aa, bb = obstacle_arrays(sc)
+    t0 = time.perf_counter()
+    OM.run(b.P, b.Pdot, b.Pddot, b.grid.timestamps, c, v, aa, bb, starts, goals, step_budget=CONFIGS["mpc"][2],
+           n_steps=steps)
+    wall = time.perf_counter() - t0
+    return robots * steps / wall, f"{robots} robots x {steps} control steps x 40 AM its (oracle port, 1 core)"
 
 
 def cpu_reference_c2alt(n_iter=3):
@@ -1070,6 +1179,26 @@ def run_reference(args):
                           "e2e": {"value": value, "unit": "traj-it/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}), flush=True)
         return
+    if args.config in ("mpc", "val"):
+        vals = []
+        for k in range(args.warmup + args.steps):
+            if args.config == "mpc":
+                v, info = cpu_reference_mpc()
+                unit, metric = "robot-steps/s", "robot control steps/sec (receding horizon, 40 warm AM its per step)"
+            else:
+                v, info = cpu_reference_val()
+                unit, metric = "traj/s", "trajectories validated/sec (raw-geometry metrics + collision check)"
+            if k >= args.warmup:
+                vals.append(v)
+        value = statistics.mean(vals)
+        print(json.dumps({"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": CONFIGS[args.config][3]},
+                          "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "port", "sample": info},
+                          "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return
     if args.config == "c4":
         vals = []
         for k in range(args.warmup + args.steps):
@@ -1130,6 +1259,8 @@ def main():
         run_c2alt(args)
     elif args.config == "val":
         run_val(args)
+    elif args.config == "mpc":
+        run_mpc(args)
     else:
         run_b200(args)
 

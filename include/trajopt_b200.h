@@ -390,6 +390,74 @@ typedef struct tro_val_io {
 
 int tro_validate_f64(const tro_val_dims* dims, const tro_val_consts* c, const tro_val_io* io, void* stream);
 
+/* ---------------- §8(f) row 1: device predict_obstacles (bench/scenarios.py:118-127)
+ * centres c + v (t_now[s] + t[k] - t[0]) of every obstacle of S scenarios (or of one obstacle table at S
+ * prediction times), in the reference's operation order without FMA contraction (bit-exact with numpy). */
+typedef struct tro_track_dims {
+    int32_t n_scen;           /* S */
+    int32_t n_obs;
+    int32_t n_p;
+    int32_t dim;              /* 2 or 3 */
+    int32_t layout;           /* 0: out S x n_obs x n_p x dim (predict_obstacles), 1: S x n_obs x dim x n_p
+                                 (tro_alg1_consts.tracks) */
+    int32_t shared_obstacles; /* 1: centers / velocities are one n_obs x dim table for all S */
+} tro_track_dims;
+
+int tro_predict_tracks_f64(const tro_track_dims* dims, const double* centers, const double* velocities,
+                           const double* t, const double* t_now, double* out, void* stream);
+
+/* ---------------- §8(f) row 2: receding-horizon fleet step (bench/runner.py:326-439)
+ * B robots driving through one scenario with device-resident warm state (an Alg. 1 engine).  After a
+ * control step's solve, mode 1 executes the first n_exec samples of each active member's plan against the
+ * true obstacle motion (collision at t_exec[k], goal proximity; runner.py:406-419), appends them to the
+ * trace, writes the next problem (boundary = executed state, straight desired line to the goal and its
+ * linear term q = -2 w_track P' desired), the warm line-of-sight scales d of the final iterate (read by
+ * the next prime with d_mode 1) and resets the engine's solve-local bookkeeping (runner.py:376-377:
+ * iteration = 0).  Mode 0 starts the episode from bvals' p0 (collision check at t = 0, first problem).
+ * Members that collided or reached the goal are frozen (engine status TRO_CONVERGED). */
+typedef struct tro_mpc_dims {
+    int32_t n_members;
+    int32_t n_obs;
+    int32_t n_p;
+    int32_t m;
+    int32_t dim;
+    int32_t n_exec;      /* samples executed per control step */
+    int32_t trace_cap;   /* trace capacity per member (1 + n_steps * n_exec) */
+    int32_t ring_len;    /* engine stall ring length (2 * stall_window) */
+} tro_mpc_dims;
+
+typedef struct tro_mpc_consts {
+    const double* P;          /* n_p x m */
+    const double* Pdot;
+    const double* Pddot;
+    const double* frac;       /* n_p: linspace(0, 1, n_p) */
+    const double* goal;       /* B x dim */
+    const double* centers;    /* n_obs x dim raw obstacle centres at t = 0 */
+    const double* velocities; /* n_obs x dim */
+    const double* shape_a;    /* n_obs raw semi-axes (collision test) */
+    const double* shape_b;
+    const double* plan_a;     /* n_obs planning semi-axes (the engine's, for d) */
+    const double* plan_b;
+    const double* tracks;     /* n_obs x dim x n_p: the tracks this step's solve used */
+    const double* t_exec;     /* n_exec absolute times of the executed samples (t_abs += dt, in order) */
+    double goal_radius;
+    double w_track;
+} tro_mpc_consts;
+
+typedef struct tro_mpc_io {
+    double* bvals;      /* B x dim x 6: next problem's boundary values (engine bvals) */
+    double* q;          /* B x dim x m: next problem's linear term (engine q) */
+    double* desired;    /* B x n_p x dim: next problem's desired line */
+    double* d;          /* B x n_obs x n_p: warm d for the next prime (NULL: skip) */
+    double* trace;      /* B x trace_cap x dim executed positions */
+    int32_t* n_trace;   /* B */
+    int32_t* flags;     /* B: 1 collided, 2 reached (either: done) */
+    double* res_out;    /* optional B: this step's residual norm (copied from the engine) */
+} tro_mpc_io;
+
+int tro_mpc_advance_f64(int32_t mode, const tro_mpc_dims* dims, const tro_mpc_consts* c,
+                        const tro_alg1_state* engine, const tro_mpc_io* io, void* stream);
+
 /* out (ncols x n) = rhs (ncols x n) * K^-T, i.e. out[c] = K^-1 rhs[c] for every column c.
  * kinv: n x n row-major.  qpcore.solve_batch with the RHS block [-q ; b]. */
 int tro_kkt_apply_f64(const double* kinv, int32_t n, const double* rhs, int64_t ncols,

@@ -44,6 +44,8 @@ EXPORTS = (
     "tro_ma_run",
     "tro_b2_run",
     "tro_validate_f64",
+    "tro_predict_tracks_f64",
+    "tro_mpc_advance_f64",
     "tro_version",
     "tro_error_string",
 )
@@ -202,6 +204,27 @@ class ValIO(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in ("xi", "pos", "acc", "out")]
 
 
+class TrackDims(ctypes.Structure):
+    _fields_ = [(n, c_int32) for n in ("n_scen", "n_obs", "n_p", "dim", "layout", "shared_obstacles")]
+
+
+class MpcDims(ctypes.Structure):
+    _fields_ = [(n, c_int32) for n in ("n_members", "n_obs", "n_p", "m", "dim", "n_exec", "trace_cap", "ring_len")]
+
+
+class MpcConsts(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("P", "Pdot", "Pddot", "frac", "goal", "centers", "velocities", "shape_a",
+                                        "shape_b", "plan_a", "plan_b", "tracks", "t_exec")] + [
+        ("goal_radius", c_double), ("w_track", c_double)]
+
+
+class MpcIO(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("bvals", "q", "desired", "d", "trace", "n_trace", "flags", "res_out")]
+
+
+TRO_MPC_COLLIDED = 1
+TRO_MPC_REACHED = 2
+
 TRO_B2_PSI_IN = 16
 TRO_B2_GIVEN_AD = 32
 TRO_B2_GIVEN_ALPHA = 64
@@ -253,6 +276,12 @@ def load() -> ctypes.CDLL:
     lib.tro_b2_run.restype = c_int32
     lib.tro_validate_f64.argtypes = [POINTER(ValDims), POINTER(ValConsts), POINTER(ValIO), c_void_p]
     lib.tro_validate_f64.restype = c_int32
+    lib.tro_predict_tracks_f64.argtypes = [POINTER(TrackDims), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                           c_void_p]
+    lib.tro_predict_tracks_f64.restype = c_int32
+    lib.tro_mpc_advance_f64.argtypes = [c_int32, POINTER(MpcDims), POINTER(MpcConsts), POINTER(Alg1State),
+                                        POINTER(MpcIO), c_void_p]
+    lib.tro_mpc_advance_f64.restype = c_int32
     lib.tro_fp64_fma_probe.argtypes = [c_int64, c_int32, c_void_p, c_void_p]
     lib.tro_fp64_fma_probe.restype = c_int32
     lib.tro_version.argtypes = []

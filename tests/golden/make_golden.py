@@ -490,6 +490,119 @@ def make_metrics():
     print("metrics written")
 
 
+SCEN_CASES = (
+    ("corridor", {}, 0), ("corridor", {"n_o": 7, "length": 9.0}, 5),
+    ("random-static", {}, 0), ("random-static", {"dim": 3, "n_o": 12}, 3),
+    ("dynamic-flow", {}, 1), ("dynamic-flow", {"n_o": 50, "obstacle_speed": 0.7}, 9),
+    ("square-antipodal", {}, 0), ("square-antipodal", {"n_agents": 16, "side": 8.0}, 4),
+    ("barn-like", {}, 0), ("barn-like", {"n_o": 40, "min_spacing": 0.5}, 6),
+    ("all-infeasible-probe", {}, 0), ("all-infeasible-probe", {"n_p": 30, "length": 8.0}, 2),
+)
+
+
+def make_scenarios():
+    """bench/scenarios.py: gen_scenario JSON text for every kind (default and custom params), and
+    predict_obstacles at a few t_now values (scenarios.json + scenarios.npz)."""
+    import json
+
+    from trajopt.bench import scenarios as SC
+
+    texts, arrays = {}, {}
+    for n, (kind, params, seed) in enumerate(SCEN_CASES):
+        sc = SC.gen_scenario(kind, params, seed=seed)
+        key = f"{n:02d}"
+        texts[key] = {"kind": kind, "params": params, "seed": seed, "json": SC.to_json(sc)}
+        basis_t = np.linspace(sc.horizon.t0, sc.horizon.tf, sc.horizon.n_p)
+        for m, t_now in enumerate((0.0, 1.3, 7.25)):
+            tr = SC.predict_obstacles(sc, basis_t, t_now=t_now)
+            arrays[f"{key}_t{m}"] = np.stack([t.centers for t in tr]) if tr else np.zeros((0, basis_t.size, sc.dim))
+        arrays[f"{key}_tnow"] = np.array([0.0, 1.3, 7.25])
+        arrays[f"{key}_ts"] = basis_t
+        if kind == "square-antipodal":
+            arrays[f"{key}_roster"] = np.array([np.concatenate([s, g]) for s, g in SC.agent_boundaries(sc)])
+    with open(os.path.join(OUT, "scenarios.json"), "w") as fh:
+        json.dump(texts, fh, indent=1)
+    np.savez_compressed(os.path.join(OUT, "scenarios.npz"), **arrays)
+    print("scenarios written")
+
+
+def make_wire():
+    """bench/runner.py wire formats: results CSV (fresh + appended) and trajectory dumps, byte for byte."""
+    from trajopt.basis import Trajectory
+    from trajopt.bench import runner as RN
+    from trajopt.bench.metrics import RunMetrics
+
+    wd = os.path.join(OUT, "wire")
+    os.makedirs(wd, exist_ok=True)
+    vals = [0.1 + 0.2, 1e-300, 12345678.901234567, -0.0, float("inf"), 2.0 ** -1074, 1.0 / 3.0, 7.0]
+    recs = []
+    for k in range(4):
+        m = RunMetrics(smoothness=vals[k], tracking=vals[k + 1], arc_length=vals[k + 2], success=bool(k % 2),
+                       iters=10 * k + 3, residual_final=vals[k + 3], min_clearance=vals[k + 4], wall_time_ms=vals[k + 1])
+        recs.append(RN.RunRecord(scenario_id=f"corridor-{k}", solver=RN.SOLVERS[k], seed=k * 11, metrics=m))
+    path = os.path.join(wd, "results.csv")
+    if os.path.exists(path):
+        os.remove(path)
+    RN.write_results_csv(path, recs[:2])
+    RN.write_results_csv(path, recs[2:])  # appended, no second header
+    rng = np.random.default_rng(3)
+    for dim, with_psi in ((2, True), (3, False)):
+        n = 7
+        tr = Trajectory(t=np.linspace(0.0, 1.0, n), pos=rng.normal(size=(n, dim)) * 3.0, vel=np.zeros((n, dim)),
+                        acc=np.zeros((n, dim)))
+        psi = rng.uniform(-np.pi, np.pi, n) if with_psi else None
+        RN.write_trajectory_csv(os.path.join(wd, f"traj{dim}d.csv"), tr, dim=dim, psi=psi)
+        np.savez(os.path.join(wd, f"traj{dim}d.npz"), t=tr.t, pos=tr.pos, psi=psi if psi is not None else np.zeros(0))
+    np.save(os.path.join(wd, "values.npy"), np.array(vals))
+    print("wire written")
+
+
+def make_mpc():
+    """bench/runner.py receding_horizon_run: the single solver on a 3-D static field and a 2-D moving field
+    (one reaching the goal), and the batch solver on a 2-D moving field; records and executed paths."""
+    from trajopt.bench import runner as RN
+
+    out = {}
+    cases = (("s3", "single", "random-static", {"dim": 3, "n_o": 6}, 2, dict(step_budget=25, n_steps=12)),
+             ("f2", "single", "dynamic-flow", {"n_o": 6}, 4,
+              dict(step_budget=20, n_steps=14, exec_fraction=0.3, goal_radius=1.0)),
+             ("r2", "single", "random-static", {"n_o": 5}, 1,
+              dict(step_budget=30, n_steps=10, exec_fraction=0.5, goal_radius=3.0)),
+             ("b2", "batch", "dynamic-flow", {"n_o": 5, "n_p": 60}, 1, dict(step_budget=15, n_steps=4)))
+    for tag, solver, kind, params, seed, kw in cases:
+        sc = gen_scenario(kind, params, seed=seed)
+        res = RN.receding_horizon_run(sc, solver, seed=0, **kw)
+        rec = [[r.metrics.smoothness, r.metrics.tracking, r.metrics.arc_length, r.metrics.min_clearance,
+                r.metrics.residual_final, float(r.metrics.success), float(r.metrics.iters)] for r in res.records]
+        out[f"{tag}_records"] = np.array(rec)
+        out[f"{tag}_flags"] = np.array([res.success, res.reached_goal, res.collided], dtype=float)
+        out[f"{tag}_pos"] = res.executed.pos
+        out[f"{tag}_t"] = res.executed.t
+        out[f"{tag}_vel"] = res.executed.vel
+        out[f"{tag}_acc"] = res.executed.acc
+        print(tag, "steps", len(res.records), "reached", res.reached_goal, "collided", res.collided)
+    np.savez_compressed(os.path.join(OUT, "mpc.npz"), **out)
+    print("mpc written")
+
+
+def make_runs():
+    """bench/runner.py run_scenario for the single, batch and multiagent solvers (records + trajectories)."""
+    from trajopt.bench import runner as RN
+
+    out = {}
+    for tag, kind, params, solver, iters in (("single", "random-static", {"dim": 3, "n_o": 8}, "single", 120),
+                                             ("batch", "dynamic-flow", {"n_o": 6, "n_p": 60}, "batch", 40),
+                                             ("multi", "square-antipodal", {"n_agents": 4, "n_p": 40}, "multiagent", 25)):
+        sc = gen_scenario(kind, params, seed=1)
+        rec = RN.run_scenario(sc, solver, seed=0, iters=iters)
+        m = rec.metrics
+        out[tag] = np.array([m.smoothness, m.tracking, m.arc_length, float(m.success), float(m.iters),
+                             m.residual_final, m.min_clearance])
+        print(tag, out[tag])
+    np.savez_compressed(os.path.join(OUT, "runs.npz"), **out)
+    print("runs written")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:

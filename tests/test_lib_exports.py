@@ -61,6 +61,8 @@ def test_struct_sizes_match_c_compiler(tmp_path):
         "tro_ma_state": _lib.MaState, "tro_ma_params": _lib.MaParams, "tro_b2_dims": _lib.B2Dims,
         "tro_b2_consts": _lib.B2Consts, "tro_b2_state": _lib.B2State, "tro_b2_params": _lib.B2Params,
         "tro_val_dims": _lib.ValDims, "tro_val_consts": _lib.ValConsts, "tro_val_io": _lib.ValIO,
+        "tro_track_dims": _lib.TrackDims, "tro_mpc_dims": _lib.MpcDims, "tro_mpc_consts": _lib.MpcConsts,
+        "tro_mpc_io": _lib.MpcIO,
     }
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{os.path.abspath(HEADER)}"', "int main(void) {"]
     for cname, ct in pairs.items():
