@@ -507,7 +507,9 @@ def run_mpc(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     step_s = a.elapsed_time(b) / 1e3 / args.steps
-    robot_steps = total * MPC_STEPS
+    # robots that collided or reached the goal are frozen (no further solves): count the control steps solved
+    per_robot = np.array([fr.steps_of(i) for i in range(total)])
+    robot_steps = int(per_robot.sum())
     # e2e: the public API from host arrays: fleet construction (uploads) + episode + results to the host
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -516,7 +518,7 @@ def run_mpc(args):
     active = (fr.flags == 0).sum()
     # roofline of the dominant kernel (the fused AM iteration): algorithmic bytes per launch / per-iteration time
     it_ms = statistics.mean(solve_ms) / MPC_STEPS / budget
-    bytes_launch = 2 * WORDS_3D * n_o * 100 * 8 * total
+    bytes_launch = 2 * WORDS_3D * n_o * 100 * 8 * robot_steps / MPC_STEPS  # mean active robots per launch
     peak, peak_src = measured_peaks()
     line = {
         "metric": "robot control steps/sec (receding horizon, 40 warm AM its per step)",
@@ -538,7 +540,8 @@ def run_mpc(args):
                                           + fr_e.flags.nbytes + fr_e.n_trace.nbytes)},
         "gpu_launches": args.steps * (2 + MPC_STEPS * (4 + budget)),
         "result": {"still_driving": int(active), "collided": int((fr.flags == 1).sum()),
-                   "reached": int((fr.flags == 2).sum())},
+                   "reached": int((fr.flags == 2).sum()), "robot_steps_solved": robot_steps,
+                   "robot_steps_offered": total * MPC_STEPS},
     }
     if not args.no_cpu_baseline:
         v, info = cpu_reference_mpc()
