@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--groups", type=int, default=0)
-    ap.add_argument("--layout", default="unit", choices=["unit", "angle", "half"],
+    ap.add_argument("--layout", default="half", choices=["unit", "angle", "half"],
                     help="per-element state layout (unit: 11 words; angle: the reference's 9 words; half: 9 words, "
                          "angles as folded half-angle tangents)")
     ap.add_argument("--members", type=int, default=0, help="override the member count (testing)")

@@ -44,6 +44,12 @@ __device__ __forceinline__ T max_abs(T acc, T v) {
     v = fabs(v);
     return v > acc ? v : acc;
 }
+// running max of |x| kept as a SIGNED value: |.| is a free operand modifier of the compare, so one
+// step is DSETP + 2 FSEL (max_abs materialises |v| first); the caller takes fabs of the result
+template <typename T>
+__device__ __forceinline__ T max_mag(T acc, T v) {
+    return fabs(v) > fabs(acc) ? v : acc;
+}
 
 // Per-element words of the persistent state.
 //   angle layout (LAY 0, the reference's variables):
@@ -85,6 +91,48 @@ __device__ __forceinline__ void half_decode(T w, T* c, T* s) {
     *s = inner ? ss : -ss;
 }
 
+// Two reciprocals for the price of one (x, y >= 1 here, so x y neither overflows nor underflows):
+// 1/x = y (1/(x y)), 1/y = x (1/(x y)), <= 2 ulp instead of <= 1 ulp each.  The element's independent
+// pairs (the two angle decodes, the two encodes, the alpha- and beta-copy denominators) share one.
+#ifndef TRO_RCP2
+#define TRO_RCP2 1
+#endif
+template <typename T>
+__device__ __forceinline__ void rcp2(T x, T y, T& rx, T& ry) {
+#if TRO_RCP2
+    const T r = rcp_fast(x * y);
+    rx = y * r;
+    ry = x * r;
+#else
+    rx = rcp_fast(x);
+    ry = rcp_fast(y);
+#endif
+}
+template <typename T>
+__device__ __forceinline__ void half_decode2(T w1, T w2, T* c1, T* s1, T* c2, T* s2) {
+    const bool in1 = fabs(w1) <= (T)1, in2 = fabs(w2) <= (T)1;
+    const T t1 = in1 ? w1 : w1 - copysign((T)3, w1);
+    const T t2 = in2 ? w2 : w2 - copysign((T)3, w2);
+    const T u1 = t1 * t1, u2 = t2 * t2;
+    T q1, q2;
+    rcp2((T)1 + u1, (T)1 + u2, q1, q2);
+    const T cc1 = ((T)1 - u1) * q1, ss1 = (T)2 * t1 * q1;
+    const T cc2 = ((T)1 - u2) * q2, ss2 = (T)2 * t2 * q2;
+    *c1 = in1 ? cc1 : -cc1;
+    *s1 = in1 ? ss1 : -ss1;
+    *c2 = in2 ? cc2 : -cc2;
+    *s2 = in2 ? ss2 : -ss2;
+}
+template <typename T>
+__device__ __forceinline__ void half_encode2(T c1, T s1, T c2, T s2, T* w1, T* w2) {
+    const bool p1 = c1 >= (T)0, p2 = c2 >= (T)0;
+    T r1, r2;
+    rcp2(p1 ? (T)1 + c1 : (T)1 - c1, p2 ? (T)1 + c2 : (T)1 - c2, r1, r2);
+    const T t1 = s1 * r1, t2 = s2 * r2;
+    *w1 = p1 ? t1 : copysign((T)3, s1) - t1;
+    *w2 = p2 ? t2 : copysign((T)3, s2) - t2;
+}
+
 // One AM iteration of one element.  v[W]: state words in / out.  d_old: the
 // line-of-sight scale of the previous iterate.  Outputs the new d, the angle
 // copies (for the optional export), and accumulates the residual norm/max and
@@ -101,22 +149,22 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         if constexpr (LAY == kLayUnit) {
             ca = v[0]; sa = v[1]; cb = v[2]; sb = v[3];
         } else if constexpr (LAY == kLayHalf) {
-            half_decode(v[0], &ca, &sa);
-            half_decode(v[1], &cb, &sb);
+            half_decode2(v[0], v[1], &ca, &sa, &cb, &sb);
         } else {
             sincos_fast(v[0], &sa, &ca);  // copy reset (solver_single.py:375-380)
             sincos_fast(v[1], &sb, &cb);
         }
         T lx = v[o], ly = v[o + 1], lz = v[o + 2], lca = v[o + 3], lsa = v[o + 4], lcb = v[o + 5], lsb = v[o + 6];
-        // alpha copies (solver_single.py:223-228)
+        // alpha copies (solver_single.py:223-228) and the beta-copy denominator (:253-266), one reciprocal
         const T coef = a * dold * sb;
-        const T rden = rcp_fast(trho + trho_o * (coef * coef));
+        const T ccb = b * dold;
+        T rden, rbden;
+        rcp2(trho + trho_o * (coef * coef), trho + trho_o * (ccb * ccb), rden, rbden);
         const T Lx = lx + trho_o * dx, Ly = ly + trho_o * dy, Lz = lz + trho_o * dz;
         const T ca2 = (trho * ca - lca + coef * Lx) * rden;
         const T sa2 = (trho * sa - lsa + coef * Ly) * rden;
         // beta copies with the new alpha copies (solver_single.py:253-266)
-        const T ccb = b * dold;
-        const T cb2 = (trho * cb - lcb + ccb * Lz) * rcp_fast(trho + trho_o * (ccb * ccb));
+        const T cb2 = (trho * cb - lcb + ccb * Lz) * rbden;
         const T csb = a * dold;
         const T num = trho * sb - lsb + csb * (ca2 * Lx + sa2 * Ly);
         const T sb2 = num * rcp_fast(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
@@ -128,8 +176,7 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         if constexpr (LAY == kLayUnit) {
             v[0] = cA2; v[1] = sA2; v[2] = cB2; v[3] = sB2;
         } else if constexpr (LAY == kLayHalf) {
-            v[0] = half_encode(cA2, sA2);
-            v[1] = half_encode(cB2, sB2);
+            half_encode2(cA2, sA2, cB2, sB2, &v[0], &v[1]);
         } else {
             v[0] = atan2_fast(sa2, ca2);  // solver_single.py:242
             v[1] = atan2_fast(sb2, cb2);  // solver_single.py:271
@@ -144,9 +191,10 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         ss = fma(ry, ry, ss); ss = fma(rz, rz, ss); ss = fma(rcb, rcb, ss);
         ss = fma(rsb, rsb, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
         sumsq += (double)ss;
-        T ml = fabs(rx);
-        ml = max_abs(ml, ry); ml = max_abs(ml, rz); ml = max_abs(ml, rcb);
-        ml = max_abs(ml, rsb); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
+        T ml = max_mag(rx, ry);
+        ml = max_mag(ml, rz); ml = max_mag(ml, rcb);
+        ml = max_mag(ml, rsb); ml = max_mag(ml, rca); ml = max_mag(ml, rsa);
+        ml = fabs(ml);
         mx = (double)ml > mx ? (double)ml : mx;
         // multiplier ascent (solver_single.py:336-343)
         v[o] = lx + trho_o * rx; v[o + 1] = ly + trho_o * ry; v[o + 2] = lz + trho_o * rz;
@@ -190,8 +238,9 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         T ss = rx * rx;
         ss = fma(ry, ry, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
         sumsq += (double)ss;
-        T ml = fabs(rx);
-        ml = max_abs(ml, ry); ml = max_abs(ml, rca); ml = max_abs(ml, rsa);
+        T ml = max_mag(rx, ry);
+        ml = max_mag(ml, rca); ml = max_mag(ml, rsa);
+        ml = fabs(ml);
         mx = (double)ml > mx ? (double)ml : mx;
         v[o] = lx + trho_o * rx; v[o + 1] = ly + trho_o * ry;
         v[o + 2] = lca + trho * rca; v[o + 3] = lsa + trho * rsa;

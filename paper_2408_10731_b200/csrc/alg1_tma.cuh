@@ -47,7 +47,8 @@ __host__ __device__ inline TmaLayout tma_layout(int stage_bytes, int S, int n_p,
     L.pos_new = off;  off += dim * n_p * 8;
     L.sums_in = off;  off += 2 * dim * n_p * 8;
     L.red = off;      off += G * 2 * dim * n_p * 8;
-    L.shp = off;      off += 4 * (n_o > 0 ? n_o : 1) * 8;
+    off = (off + 15) & ~15;
+    L.shp = off;      off += 4 * (n_o > 0 ? n_o : 1) * 8;  // per obstacle {a, b, 1/a^2, 1/b^2} (two 16-B loads)
     L.qlin = off;     off += dim * 16 * 8;
     L.xi = off;       off += dim * 16 * 8;
     L.warp = off;     off += 2 * (consumers / 32) * 8;
@@ -78,10 +79,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     double* sPosNew = reinterpret_cast<double*>(smraw + L.pos_new);
     double* sSumIn = reinterpret_cast<double*>(smraw + L.sums_in);
     double* sRed = reinterpret_cast<double*>(smraw + L.red);
-    double* sA = reinterpret_cast<double*>(smraw + L.shp);
-    double* sB = sA + n_o;
-    double* sIA2 = sB + n_o;
-    double* sIB2 = sIA2 + n_o;
+    double* sShp = reinterpret_cast<double*>(smraw + L.shp);
     double* sQlin = reinterpret_cast<double*>(smraw + L.qlin);
     double* sXi = reinterpret_cast<double*>(smraw + L.xi);
     double* sWarp = reinterpret_cast<double*>(smraw + L.warp);
@@ -102,35 +100,40 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     for (int k = tid; k < NP * m; k += blockDim.x) sP[k] = ld_const(A.c.P + k);
     for (int k = tid; k < n_o; k += blockDim.x) {
         const double a = ld_const(A.c.shape_a + k), b = ld_const(A.c.shape_b + k);
-        sA[k] = a;
-        sB[k] = b;
-        sIA2[k] = 1.0 / (a * a);
-        sIB2[k] = 1.0 / (b * b);
+        sShp[4 * k + 0] = a;
+        sShp[4 * k + 1] = b;
+        sShp[4 * k + 2] = 1.0 / (a * a);
+        sShp[4 * k + 3] = 1.0 / (b * b);
     }
     __syncthreads();
 
     const int nst = (n_o + G - 1) / G;  // stages per member
+    // ring position: stage s and its phase bit run on across members (no divisions in the loops)
 
     if (warp == NCW) {
         // ======================= producer warp (one elected lane)
         if (lane == 0) {
-            uint32_t kst = 0;
+            int s = 0;
+            uint32_t ph = 0;
+            bool wrapped = false;
             for (int i = blockIdx.x; i < B; i += gridDim.x) {
                 const int st = A.s.status[i];
                 if ((st & (TRO_CONVERGED | TRO_FACTOR_FAILED)) || !A.c.level_ok[A.s.level[i]]) continue;
                 const unsigned char* src = reinterpret_cast<const unsigned char*>(A.s.state) +
                                            (int64_t)i * n_o * C::kRowBytes;
-                for (int k = 0; k < nst; ++k, ++kst) {
-                    const int s = kst % S;
-                    if (kst >= (uint32_t)S) mbar_wait(&empty[s], ((kst / S) - 1) & 1);
-                    const int j0 = k * G;
+                const unsigned char* trk = reinterpret_cast<const unsigned char*>(A.c.tracks);
+                for (int j0 = 0; j0 < n_o; j0 += G) {
+                    if (wrapped) mbar_wait(&empty[s], ph ^ 1u);  // the consumers released this stage
                     const int rows = min(G, n_o - j0);
                     unsigned char* buf = stages + s * C::kStageBytes;
                     mbar_expect_tx(&full[s], rows * (C::kRowBytes + C::kTrkBytes));
                     bulk_g2s(buf, src + (int64_t)j0 * C::kRowBytes, rows * C::kRowBytes, &full[s]);
-                    bulk_g2s(buf + G * C::kRowBytes,
-                             reinterpret_cast<const unsigned char*>(A.c.tracks) + (int64_t)j0 * C::kTrkBytes,
-                             rows * C::kTrkBytes, &full[s]);
+                    bulk_g2s(buf + G * C::kRowBytes, trk + (int64_t)j0 * C::kTrkBytes, rows * C::kTrkBytes, &full[s]);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                        wrapped = true;
+                    }
                 }
             }
         }
@@ -141,7 +144,11 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     const int t = tid % NP;
     const int g = tid / NP;
     const bool act = g < G;
-    uint32_t kst = 0;
+    int s = 0;
+    uint32_t ph = 0;
+    // this thread's offsets inside a stage: its obstacle row of state and of tracks, sample t
+    const int row_off = g * C::kRowBytes + t * (int)sizeof(T);
+    const int trk_off = G * C::kRowBytes + g * C::kTrkBytes + t * 8;
     const int64_t Nel = (int64_t)B * n_o * NP;
     T* dst = reinterpret_cast<T*>(A.s.d);
     T* cop = reinterpret_cast<T*>(A.s.copies);
@@ -209,20 +216,21 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
         const int d_mode = A.p.d_mode;
         T* gbase = reinterpret_cast<T*>(A.s.state) + (int64_t)i * n_o * W * NP + t;
 
-        for (int k = 0; k < nst; ++k, ++kst) {
-            const int s = kst % S;
-            mbar_wait(&full[s], (kst / S) & 1);
-            const int j = k * G + g;
+        T* gp = gbase + (int64_t)g * W * NP;
+        int64_t e = ((int64_t)i * n_o + g) * NP + t;  // index into the optional d / copies planes
+        for (int j = g; j - g < n_o; j += G, gp += G * W * NP, e += G * NP) {
+            mbar_wait(&full[s], ph);
             if (act && j < n_o) {
                 const unsigned char* buf = stages + s * C::kStageBytes;
-                const T* row = reinterpret_cast<const T*>(buf + g * C::kRowBytes) + t;
-                const double* trow = reinterpret_cast<const double*>(buf + G * C::kRowBytes + g * C::kTrkBytes) + t;
+                const T* row = reinterpret_cast<const T*>(buf + row_off);
+                const double* trow = reinterpret_cast<const double*>(buf + trk_off);
                 T v[W];
 #pragma unroll
                 for (int w = 0; w < W; ++w) v[w] = row[w * NP];
                 const double trx = trow[0], trY = trow[NP], trz = DIM == 3 ? trow[2 * NP] : 0.0;
-                const T a = (T)sA[j], b = (T)sB[j], ia2 = (T)sIA2[j], ib2 = (T)sIB2[j];
-                const int64_t e = ((int64_t)i * n_o + j) * NP + t;
+                const double2 ab = *reinterpret_cast<const double2*>(sShp + 4 * j);
+                const double2 iab = *reinterpret_cast<const double2*>(sShp + 4 * j + 2);
+                const T a = (T)ab.x, b = (T)ab.y, ia2 = (T)iab.x, ib2 = (T)iab.y;
                 T dold;
                 if (d_mode == 0) {
                     dold = (T)1;
@@ -242,10 +250,9 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
                 T dn, cp4[4];
                 am_element<DIM, T, LAY>(v, trx, trY, trz, px, py, pz, a, b, ia2, ib2, dold, trho, trho_o, sumsq, mx,
                                    accL, accT, dn, cp4);
-                T* gp = gbase + (int64_t)j * W * NP;
 #pragma unroll
                 for (int w = 0; w < W; ++w) st_stream(gp + w * NP, v[w]);
-                if (dst) dst[e] = dn;
+                if (dst) dst[e] = dn;  // optional exports (tests, warm starts)
                 if (cop) {
 #pragma unroll
                     for (int c = 0; c < 2 * (DIM - 1); ++c) cop[c * Nel + e] = cp4[c];
@@ -253,6 +260,10 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                ph ^= 1u;
+            }
         }
 
         // ---------- epilogue (fixed-order reductions, history, stall rule)

@@ -108,10 +108,10 @@ class MpcFleet:
 
     Defaults follow receding_horizon_run (runner.py:326-334): step_budget 40, exec_fraction 0.1,
     goal_radius 0.5, plan margin 0.05; the basis is the scenario horizon's degree-10 Bernstein basis.
-    ``layout`` selects the engine's word layout ("unit": the fastest)."""
+    ``layout`` selects the engine's word layout ("half": the reference's 9 words, the fastest)."""
 
     def __init__(self, scenario, starts=None, goals=None, *, step_budget: int = 40, exec_fraction: float = 0.1,
-                 goal_radius: float = 0.5, plan_margin: float = 0.05, params=None, layout: str = "unit",
+                 goal_radius: float = 0.5, plan_margin: float = 0.05, params=None, layout: str = "half",
                  record_metrics: bool = True, device=None, solver_label: str = "single", seed: int = 0):
         from .bench.scenarios import obstacle_arrays, predict_obstacles
         from .solver_single import SingleParams

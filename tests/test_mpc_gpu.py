@@ -75,7 +75,7 @@ def test_receding_horizon_single_matches_reference(tag):
     _check_member(res, np.load(os.path.join(GOLD, "mpc.npz")), tag, pos_tol=1e-8)
 
 
-@pytest.mark.parametrize("layout,tol", [("unit", 1e-6), ("angle", 1e-6)])
+@pytest.mark.parametrize("layout,tol", [("unit", 1e-6), ("angle", 1e-6), ("half", 1e-6)])
 def test_fleet_matches_oracle_per_robot(layout, tol):
     """B robots with their own starts / goals in one field: each robot equals the oracle's own run (the unit
     layout computes the angle copies as unit vectors: a different rounding path, 12 steps x 25 iterations)."""
