@@ -48,24 +48,39 @@ struct MpcArgs {
     tro_mpc_io io;
 };
 
-// runner.py:314-323 _in_collision_now: raw shapes, centre c + v t, quad < 1 (3-D: a, a, b; 2-D: a, b)
+// runner.py:314-323 _in_collision_now for ONE obstacle: raw shapes, centre c + v t, quad < 1
+// (3-D: a, a, b; 2-D: a, b); every step rounded once in numpy's order
 template <int DIM>
-__device__ bool in_collision(const MpcArgs& A, const double* p, double t_abs) {
-    for (int j = 0; j < A.d.n_obs; ++j) {
-        const double a = __ldg(A.c.shape_a + j), b = __ldg(A.c.shape_b + j);
-        const double a2 = __dmul_rn(a, a), b2 = __dmul_rn(b, b);
-        double quad = 0.0;
+__device__ __forceinline__ bool hits(const MpcArgs& A, int j, const double* p, double t_abs) {
+    const double a = __ldg(A.c.shape_a + j), b = __ldg(A.c.shape_b + j);
+    const double a2 = __dmul_rn(a, a), b2 = __dmul_rn(b, b);
+    double quad = 0.0;
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) {
-            const double cen = __dadd_rn(__ldg(A.c.centers + j * DIM + ax),
-                                         __dmul_rn(__ldg(A.c.velocities + j * DIM + ax), t_abs));
-            const double dl = __dsub_rn(p[ax], cen);
-            const double term = __ddiv_rn(__dmul_rn(dl, dl), ax == DIM - 1 ? b2 : a2);
-            quad = ax == 0 ? term : __dadd_rn(quad, term);
-        }
-        if (quad < 1.0) return true;
+    for (int ax = 0; ax < DIM; ++ax) {
+        const double cen = __dadd_rn(__ldg(A.c.centers + j * DIM + ax),
+                                     __dmul_rn(__ldg(A.c.velocities + j * DIM + ax), t_abs));
+        const double dl = __dsub_rn(p[ax], cen);
+        const double term = __ddiv_rn(__dmul_rn(dl, dl), ax == DIM - 1 ? b2 : a2);
+        quad = ax == 0 ? term : __dadd_rn(quad, term);
     }
-    return false;
+    return quad < 1.0;
+}
+
+// every (sample, obstacle) pair of the CTA's samples in parallel; bit s of the result: sample s collides
+template <int DIM>
+__device__ unsigned long long collide_mask(const MpcArgs& A, const double* pts, int stride, const double* times,
+                                           int n_s, unsigned long long* sMask) {
+    const int tid = threadIdx.x;
+    if (tid == 0) *sMask = 0ull;
+    __syncthreads();
+    unsigned long long mine = 0ull;
+    for (int o = tid; o < n_s * A.d.n_obs; o += kMpcThreads) {
+        const int smp = o / A.d.n_obs, j = o - smp * A.d.n_obs;
+        if (hits<DIM>(A, j, pts + smp * stride, times[smp])) mine |= 1ull << smp;
+    }
+    if (mine) atomicOr(sMask, mine);
+    __syncthreads();
+    return *sMask;
 }
 
 template <int DIM, int MODE>
@@ -116,8 +131,13 @@ __global__ void __launch_bounds__(kMpcThreads) mpc_advance_kernel(MpcArgs A) {
             sEx[o] = acc;
         }
         __syncthreads();
+        __shared__ double sT[kMpcMaxExec];
+        __shared__ unsigned long long sMask;
+        for (int k = tid; k < n_exec; k += kMpcThreads) sT[k] = __ldg(A.c.t_exec + k);
+        __syncthreads();
+        const unsigned long long coll = collide_mask<DIM>(A, sEx, 3 * DIM, sT, n_exec, &sMask);
         if (tid == 0) {
-            // runner.py:407-419, in order: append, collision at the sample's time, then goal proximity
+            // runner.py:407-419, in order per sample: append, collision at its time, then goal proximity
             int nt = A.io.n_trace[i], fl = 0, stop = n_exec - 1;
             double* tr = A.io.trace + (int64_t)i * A.d.trace_cap * DIM;
             for (int s = 0; s < n_exec; ++s) {
@@ -127,7 +147,7 @@ __global__ void __launch_bounds__(kMpcThreads) mpc_advance_kernel(MpcArgs A) {
                     for (int ax = 0; ax < DIM; ++ax) tr[nt * DIM + ax] = p[ax];
                 }
                 ++nt;
-                if (in_collision<DIM>(A, p, __ldg(A.c.t_exec + s))) {
+                if ((coll >> s) & 1ull) {
                     fl = 1;
                     stop = s;
                     break;
@@ -152,18 +172,21 @@ __global__ void __launch_bounds__(kMpcThreads) mpc_advance_kernel(MpcArgs A) {
         }
     } else {
         // episode start (runner.py:349-358): the robot at rest at the boundary's start
+        __shared__ unsigned long long sMask;
+        __shared__ double sStart[DIM];
+        const double t0 = 0.0;
+        if (tid < DIM) {
+            sStart[tid] = bv[tid * 6 + 0];
+            sNew[tid] = sStart[tid];
+            sNew[DIM + tid] = 0.0;
+            sNew[2 * DIM + tid] = 0.0;
+            A.io.trace[(int64_t)i * A.d.trace_cap * DIM + tid] = sStart[tid];
+        }
+        __syncthreads();
+        const unsigned long long coll = collide_mask<DIM>(A, sStart, DIM, &t0, 1, &sMask);
         if (tid == 0) {
-            double p[DIM];
-#pragma unroll
-            for (int ax = 0; ax < DIM; ++ax) {
-                p[ax] = bv[ax * 6 + 0];
-                sNew[ax] = p[ax];
-                sNew[DIM + ax] = 0.0;
-                sNew[2 * DIM + ax] = 0.0;
-                A.io.trace[(int64_t)i * A.d.trace_cap * DIM + ax] = p[ax];
-            }
             A.io.n_trace[i] = 1;
-            const int fl = in_collision<DIM>(A, p, 0.0) ? 1 : 0;
+            const int fl = (coll & 1ull) ? 1 : 0;
             A.io.flags[i] = fl;
             sFlag = fl;
         }
@@ -192,13 +215,15 @@ __global__ void __launch_bounds__(kMpcThreads) mpc_advance_kernel(MpcArgs A) {
         dg[o] = v;
     }
     __syncthreads();
-    // q = -2 w_track (P' desired)' (solver_single.py:173)
+    // q = -2 w_track (P' desired)' (solver_single.py:173): a warp per output, lanes over samples
     const double w2 = -2.0 * A.c.w_track;
-    for (int o = tid; o < DIM * m; o += kMpcThreads) {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int o = warp; o < DIM * m; o += kMpcThreads / 32) {
         const int ax = o / m, cc = o - ax * m;
         double s = 0.0;
-        for (int t = 0; t < n_p; ++t) s = fma(__ldg(A.c.P + (int64_t)t * m + cc), sDes[t * DIM + ax], s);
-        A.io.q[(int64_t)i * DIM * m + o] = w2 * s;
+        for (int t = lane; t < n_p; t += 32) s = fma(__ldg(A.c.P + (int64_t)t * m + cc), sDes[t * DIM + ax], s);
+        s = warp_sum(s);
+        if (lane == 0) A.io.q[(int64_t)i * DIM * m + o] = w2 * s;
     }
     // a fresh solve_single call on the warm state: iteration = 0 (runner.py:376-377), solve-local history
     if (tid == 0) {
