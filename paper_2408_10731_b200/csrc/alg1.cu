@@ -417,6 +417,9 @@ static int launch_mode(const Alg1Args& A, cudaStream_t st) {
 #ifndef TRO_TMA_S
 #define TRO_TMA_S 3
 #endif
+#ifndef TRO_TMA_DM_SPEC
+#define TRO_TMA_DM_SPEC 1  // steady-state iterations use the d_mode = 2 specialisation
+#endif
 
 static int sm_count() {
     static int cache[64] = {0};
@@ -439,7 +442,9 @@ static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, S, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024 / kTmaMinBlocks);
+        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, S, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024 / kTmaMinBlocks);
         attr_set[dev] = true;
     }
@@ -447,7 +452,12 @@ static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
     B.G = G;
     const int slots = sm_count() * kTmaMinBlocks;
     const int grid = A.d.n_members < slots ? A.d.n_members : slots;
-    alg1_tma_kernel<DIM, T, LAY, 100, G, S><<<grid, C::kThreads, L.total, st>>>(B);
+#if TRO_TMA_DM_SPEC
+    if (A.p.d_mode == 2)
+        alg1_tma_kernel<DIM, T, LAY, 100, G, S, 2><<<grid, C::kThreads, L.total, st>>>(B);
+    else
+#endif
+        alg1_tma_kernel<DIM, T, LAY, 100, G, S, -1><<<grid, C::kThreads, L.total, st>>>(B);
     *rc = (int)cudaGetLastError();
     return 1;
 }

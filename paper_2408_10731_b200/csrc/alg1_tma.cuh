@@ -63,7 +63,9 @@ __host__ __device__ inline TmaLayout tma_layout(int stage_bytes, int S, int n_p,
 #endif
 constexpr int kTmaMinBlocks = TRO_TMA_MINB;  // resident CTAs per SM the kernel is compiled for
 
-template <int DIM, typename T, int LAY, int NP, int G, int S>
+// DM: the previous iterate's d source fixed at compile time (2: recompute, the steady state) or -1 (read
+// A.p.d_mode at run time: the first iteration after an init / prime)
+template <int DIM, typename T, int LAY, int NP, int G, int S, int DM>
 __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaMinBlocks) alg1_tma_kernel(Alg1Args A) {
     using C = TmaCfg<DIM, T, LAY, NP, G, S>;
     constexpr int W = C::W;
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
         const double px = sPosNew[t], py = sPosNew[NP + t], pz = DIM == 3 ? sPosNew[2 * NP + t] : 0.0;
         const double ox = sPosPrev[t], oy = sPosPrev[NP + t], oz = DIM == 3 ? sPosPrev[2 * NP + t] : 0.0;
         const T trho = (T)rho, trho_o = (T)rho_o;
-        const int d_mode = A.p.d_mode;
+        const int d_mode = DM >= 0 ? DM : A.p.d_mode;
         T* gbase = reinterpret_cast<T*>(A.s.state) + (int64_t)i * n_o * W * NP + t;
 
         T* gp = gbase + (int64_t)g * W * NP;
