@@ -646,7 +646,10 @@ def run_c3(args):
     elapsed = float(t.item())
     launch_s = statistics.mean(x.elapsed_time(y) for x, y in runs) / 1e3 / n_iter
     n_pairs = struct.n_pairs
-    alg_bytes = 2 * 3 * n_pairs * 100 * 8 * (hi - lo)  # 3 persistent words (the multipliers) per pair-sample
+    # W = 4 persistent words per pair-sample (lambda x/y/z and d) -> 768 KB per problem-iteration;
+    # this kernel keeps 3 (d is folded into the agent sums), so it moves 3/4 of the algorithmic bytes
+    alg_bytes = 2 * 4 * n_pairs * 100 * 8 * (hi - lo)
+    moved_bytes = 2 * 3 * n_pairs * 100 * 8 * (hi - lo)
     peak, peak_src = measured_peaks()
     # e2e: boundary values from pinned host memory each step, xi / residuals back
     bv_pin = torch.as_tensor(b_eq).pin_memory()
@@ -677,9 +680,10 @@ def run_c3(args):
                      "frac": alg_bytes / launch_s / 1e9 / peak, "traffic": traffic_for("c3") if world == 1 else None,
                      "peak_source": peak_src,
                      "kernel": "tro_ma_run modes 3 + 4 (ma_qp_kernel<11>: DMMA QP; ma_kernel<11, 4>: element pass), per iteration", "avg_launch_ms": launch_s * 1e3,
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "note": "3 words (multipliers) per pair-sample; SURVEY §8(d) counts 4 (d stored): d only "
-                             "feeds the next RHS and is folded into the agent sums"},
+                     "algorithmic_bytes_per_launch": alg_bytes, "state_bytes_moved_per_launch": moved_bytes,
+                     "hbm_frac_of_moved_bytes": moved_bytes / launch_s / 1e9 / peak,
+                     "note": "algorithmic = SURVEY 8(d) W = 4 words per pair-sample (lambda x/y/z, d); the kernel "
+                             "moves 3 (d only feeds the next RHS and is folded into the agent sums)"},
         "clocks": clk,
         "e2e": {"value": total * n_iter * args.steps / float(te.item()), "unit": "problem-it/s",
                 "h2d_bytes_per_step": int(b_eq.nbytes), "d2h_bytes_per_step": int(xi_pin.numel() * 8 + r_pin.numel() * 8)},
