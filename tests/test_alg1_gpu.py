@@ -87,6 +87,23 @@ def test_c1_fixed_100_iterations(golden):
     assert sol.n_factorizations == int(g["fixed_nfact"][0])
 
 
+@pytest.mark.parametrize("layout", ["angle", "unit", "half"])
+def test_c1_fixed_100_iterations_every_layout(golden, layout):
+    """The bench's layouts on the stable C1 problem: the whole 100-iteration history within 1e-9 of the
+    reference, identical rho schedule (the batched entry point, one member)."""
+    from paper_2408_10731_b200.solver_single import SingleBatch, solve_single_batch
+
+    g = golden("c1.npz")
+    prob = problem_from(g)
+    sol = solve_single_batch(SingleBatch.from_problems([prob]), SingleParams(max_iter=100, tol=0.0), history=True,
+                             layout=layout)
+    h = sol.history[0].cpu().numpy()
+    ref = g["fixed_hist"]
+    np.testing.assert_array_equal(h[:, 2], ref[:, 2])
+    np.testing.assert_allclose(h[:, :2], ref[:, :2], rtol=1e-9, atol=0)
+    assert rel(sol.xi[0].cpu().numpy(), g["fixed_xi"]) < 1e-10
+
+
 def test_c1_converged_solve(golden):
     g = golden("c1.npz")
     sol = solve_single(problem_from(g), SingleParams())
