@@ -66,13 +66,16 @@ def parse():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--groups", type=int, default=0)
-    ap.add_argument("--layout", default="half", choices=["unit", "angle", "half"],
+    ap.add_argument("--layout", default=None, choices=["unit", "angle", "half"],
                     help="per-element state layout (unit: 11 words; angle: the reference's 9 words; half: 9 words, "
                          "angles as folded half-angle tangents)")
     ap.add_argument("--members", type=int, default=0, help="override the member count (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.layout is None:  # the measured best per storage type: fp64 half, fp32 unit
+        a.layout = "half" if a.dtype == "f64" else "unit"
+    return a
 
 
 def c4_problem():
