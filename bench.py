@@ -393,15 +393,20 @@ def val_inputs(total: int):
 
 
 def run_val(args):
+    """N > 1: the trajectories shard into contiguous ranges, no collective on the data path."""
     import torch
+    import torch.distributed as dist
 
     from paper_2408_10731_b200 import metrics as MT
+    from paper_2408_10731_b200.distributed import shard_range
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    world, rank, local = _dist_setup()
     n_o, total, _, desc = CONFIGS["val"]
     if args.members:
         total = args.members
-    basis, sc, xi = val_inputs(total)
+    basis, sc, xi_all = val_inputs(total)
+    lo, hi = shard_range(total, rank, world)
+    xi = np.ascontiguousarray(xi_all[lo:hi])
     t = basis.grid.timestamps
     dev = torch.device("cuda")
     xi_dev = torch.as_tensor(xi, device=dev).contiguous()
@@ -409,7 +414,9 @@ def run_val(args):
     for _ in range(args.warmup):
         MT.validate_batch(sc, t, xi=xi_dev, basis=basis, return_device=True)
     torch.cuda.synchronize()
-    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
     clocks.start()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
@@ -418,36 +425,43 @@ def run_val(args):
     b.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    step_s = a.elapsed_time(b) / 1e3 / args.steps
+    step_s = _max_over_ranks(a.elapsed_time(b) / 1e3 / args.steps, world)
+    if world > 1:
+        dist.barrier()
     a.record()
     for _ in range(args.steps):
         r = MT.validate_batch(sc, t, xi=xi_pin, basis=basis)  # coefficients from pinned host memory, results back
     b.record()
     torch.cuda.synchronize()
-    e2e_s = a.elapsed_time(b) / 1e3 / args.steps
+    e2e_s = _max_over_ranks(a.elapsed_time(b) / 1e3 / args.steps, world)
+    n_free = int(_sum_over_ranks(float(r["success"].sum()), world))
     flops = VAL_FLOPS_ELEM * total * n_o * 100
     peak = fp64_peak_tflops()
     line = {
         "metric": "trajectories validated/sec (raw-geometry metrics + collision check)", "value": total / step_s,
-        "unit": "traj/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "unit": "traj/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (C5 recipe obstacles, straight-line member trajectories)",
-        "config": {"workload": desc, "members": total, "n_obs": n_o, "n_p": 100},
-        "roofline": {"bound": "fp64", "achieved": flops / step_s / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": flops / step_s / 1e12 / peak, "traffic": None,
+        "config": {"workload": desc, "members": total, "n_obs": n_o, "n_p": 100,
+                   "parallelism": f"trajectory-shard x{world}"},
+        "roofline": {"bound": "fp64", "achieved": flops / world / step_s / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": flops / world / step_s / 1e12 / peak, "traffic": None,
                      "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)", "kernel": "tro_validate_f64",
                      "avg_launch_ms": step_s * 1e3, "algorithmic_flops_per_launch": flops,
                      "note": "per-step time includes validate_batch's host-side argument setup (cached constants)"},
         "clocks": clk,
-        "e2e": {"value": total / e2e_s, "unit": "traj/s", "h2d_bytes_per_step": int(xi.nbytes),
+        "e2e": {"value": total / e2e_s, "unit": "traj/s", "h2d_bytes_per_step": int(xi_all.nbytes),
                 "d2h_bytes_per_step": int(total * 5 * 8)},
         "gpu_launches": args.steps,
-        "result": {"collision_free": int(r["success"].sum())},
+        "result": {"collision_free": n_free},
     }
-    if not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_val()
         line["cpu_baseline"] = {"value": v, "unit": "traj/s", "cores": 1, "kind": "port", "sample": info}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def cpu_reference_val(n_s=64):
@@ -467,6 +481,42 @@ def cpu_reference_val(n_s=64):
     return n_s / wall, f"{n_s} trajectories x 100 obstacles, oracle port of bench.metrics (1 core)"
 
 
+def _dist_setup():
+    """(world, rank, local) with the NCCL process group initialised for N > 1 (one process per GPU)."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(x: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def mpc_inputs(total: int):
     """The C2 obstacle field as a bench Scenario (3-D, a 0.4 / b 0.3, seeded recipe) + C2 member endpoints."""
     from paper_2408_10731_b200 import scenarios
@@ -484,21 +534,28 @@ def mpc_inputs(total: int):
 
 def run_mpc(args):
     """One step = one receding-horizon episode of the whole fleet (30 control steps of 40 warm AM iterations
-    + predict / validate / advance per control step), device-resident between control steps."""
+    + predict / validate / advance per control step), device-resident between control steps.  N > 1: the
+    robots shard into contiguous ranges (no collective on the data path: robots are independent)."""
     import torch
+    import torch.distributed as dist
 
+    from paper_2408_10731_b200.distributed import shard_range
     from paper_2408_10731_b200.mpc import MpcFleet
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    world, rank, local = _dist_setup()
     n_o, total, budget, desc = CONFIGS["mpc"]
     if args.members:
         total = args.members
-    sc, starts, goals = mpc_inputs(total)
+    sc, starts_all, goals_all = mpc_inputs(total)
+    lo, hi = shard_range(total, rank, world)
+    starts, goals = starts_all[lo:hi], goals_all[lo:hi]
     fleet = MpcFleet(sc, starts, goals, step_budget=budget, layout=args.layout)
     for _ in range(args.warmup):
         fleet.run(MPC_STEPS, early_exit=False)
     torch.cuda.synchronize()
-    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
     clocks.start()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     solve_ms = []
@@ -509,27 +566,30 @@ def run_mpc(args):
     b.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    step_s = a.elapsed_time(b) / 1e3 / args.steps
+    step_s = _max_over_ranks(a.elapsed_time(b) / 1e3 / args.steps, world)
     # robots that collided or reached the goal are frozen (no further solves): count the control steps solved
-    per_robot = np.array([fr.steps_of(i) for i in range(total)])
-    robot_steps = int(per_robot.sum())
+    robot_steps = int(_sum_over_ranks(float(sum(fr.steps_of(i) for i in range(hi - lo))), world))
     # e2e: the public API from host arrays: fleet construction (uploads) + episode + results to the host
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         fr_e = MpcFleet(sc, starts, goals, step_budget=budget, layout=args.layout).run(MPC_STEPS, early_exit=False)
-    e2e_s = (time.perf_counter() - t0) / args.steps
-    active = (fr.flags == 0).sum()
+    e2e_s = _max_over_ranks((time.perf_counter() - t0) / args.steps, world)
+    flags = [int((fr.flags == k).sum()) for k in (0, 1, 2)]
+    flags = [int(_sum_over_ranks(float(f), world)) for f in flags]
     # roofline of the dominant kernel (the fused AM iteration): algorithmic bytes per launch / per-iteration time
-    it_ms = statistics.mean(solve_ms) / MPC_STEPS / budget
-    bytes_launch = 2 * WORDS_3D * n_o * 100 * 8 * robot_steps / MPC_STEPS  # mean active robots per launch
+    it_ms = _max_over_ranks(statistics.mean(solve_ms) / MPC_STEPS / budget, world)
+    bytes_launch = 2 * WORDS_3D * n_o * 100 * 8 * robot_steps / MPC_STEPS / world  # mean active robots per launch
     peak, peak_src = measured_peaks()
     line = {
         "metric": "robot control steps/sec (receding horizon, 40 warm AM its per step)",
-        "value": robot_steps / step_s, "unit": "robot-steps/s", "n_gpus": 1, "steps": args.steps,
+        "value": robot_steps / step_s, "unit": "robot-steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (C2 recipe obstacle field and endpoints)",
         "config": {"workload": desc, "robots": total, "n_obs": n_o, "n_p": 100, "control_steps": MPC_STEPS,
-                   "step_budget": budget, "layout": args.layout, "l2": "per-element state 720 MB > L2"},
+                   "step_budget": budget, "layout": args.layout, "parallelism": f"robot-shard x{world}",
+                   "l2": "per-element state 368 MB > L2"},
         "control_step_ms": step_s * 1e3 / MPC_STEPS,
         "paper_budget_ms": 40.0,
         "roofline": {"bound": "hbm", "achieved": bytes_launch / (it_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
@@ -538,19 +598,21 @@ def run_mpc(args):
                      "avg_launch_ms": it_ms, "algorithmic_bytes_per_launch": bytes_launch},
         "clocks": clk,
         "e2e": {"value": robot_steps / e2e_s, "unit": "robot-steps/s",
-                "h2d_bytes_per_step": int(starts.nbytes + goals.nbytes),
+                "h2d_bytes_per_step": int(starts_all.nbytes + goals_all.nbytes),
                 "d2h_bytes_per_step": int(fr_e.trace.nbytes + fr_e.metrics.nbytes + fr_e.residual.nbytes
                                           + fr_e.flags.nbytes + fr_e.n_trace.nbytes)},
         "gpu_launches": args.steps * (2 + MPC_STEPS * (4 + budget)),
-        "result": {"still_driving": int(active), "collided": int((fr.flags == 1).sum()),
-                   "reached": int((fr.flags == 2).sum()), "robot_steps_solved": robot_steps,
-                   "robot_steps_offered": total * MPC_STEPS},
+        "result": {"still_driving": flags[0], "collided": flags[1], "reached": flags[2],
+                   "robot_steps_solved": robot_steps, "robot_steps_offered": total * MPC_STEPS},
     }
-    if not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_mpc()
         line["cpu_baseline"] = {"value": v, "unit": "robot-steps/s", "cores": 1, "kind": "port",
                                 "sample": info}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def cpu_reference_mpc(robots=2, steps=3):
