@@ -72,20 +72,32 @@ __host__ __device__ inline SmemLayout smem_layout(int n_p, int m, int dim, int n
 }
 
 
+// Solve-local bookkeeping of one member mirrored in shared memory by the in-kernel loop (MODE 3), so
+// thread 0's per-iteration schedule reads no global memory (each read would be a serial L2 round trip).
+struct SchedS {
+    double rho, rho_o;
+    int status, level, iteration, n_hist, last_change, n_changes;
+    double ring[kMaxRing];
+};
+
 // Per-member bookkeeping after an AM iteration (thread 0 of the member's CTA):
 // history, convergence test and the stall / penalty-growth rule
 // (solver_single.py:388, 419-427, 392-404).  nrm / mm: residual norm / max-abs.
+// S != nullptr: the member's bookkeeping is read from (and mirrored into) shared memory; every value is
+// still stored to global memory, so the global state is always current.
 __device__ __forceinline__ void alg1_schedule(const Alg1Args& A, int i, int status0, int level, double rho,
-                                              double rho_o, double nrm, double mm) {
+                                              double rho_o, double nrm, double mm, SchedS* S = nullptr) {
     A.s.res_norm[i] = nrm;
     A.s.res_max[i] = mm;
     if (A.p.flags & TRO_FLAG_NO_SCHEDULE) {
-        A.s.iteration[i] += 1;  // bare am_iteration (solver_single.py:388)
+        const int it = (S ? S->iteration : A.s.iteration[i]) + 1;  // bare am_iteration (solver_single.py:388)
+        A.s.iteration[i] = it;
+        if (S) S->iteration = it;
         return;
     }
-    const int it = A.s.iteration[i] + 1;  // am_iteration: state.iteration += 1
+    const int it = (S ? S->iteration : A.s.iteration[i]) + 1;  // am_iteration: state.iteration += 1
     A.s.iteration[i] = it;
-    const int nh = A.s.n_hist[i];
+    const int nh = S ? S->n_hist : A.s.n_hist[i];
     if (A.s.hist && nh < A.p.max_hist) {
         double* h = A.s.hist + ((int64_t)i * A.p.max_hist + nh) * 3;
         h[0] = nrm;
@@ -97,26 +109,43 @@ __device__ __forceinline__ void alg1_schedule(const Alg1Args& A, int i, int stat
     const int w = A.p.stall_window, w2 = 2 * w;
     double* ring = A.s.ring + (int64_t)i * w2;
     ring[(n - 1) % w2] = mm;
+    if (S) {
+        S->iteration = it;
+        S->n_hist = n;
+        S->ring[(n - 1) % w2] = mm;
+    }
+    const double* rr = S ? S->ring : ring;
     if (mm <= A.p.tol) {  // solver_single.py:424-426 (break before growth)
         A.s.status[i] = status0 | TRO_CONVERGED;
+        if (S) S->status = status0 | TRO_CONVERGED;
         return;
     }
-    const int lc = A.s.last_change[i];
+    const int lc = S ? S->last_change : A.s.last_change[i];
     if (n >= w2 && it - lc >= w) {  // solver_single.py:394
         double sr = 0.0, sp = 0.0;  // np.mean of <8 values: sequential sum / w
-        for (int k = 0; k < w; ++k) sr += ring[(n - w + k) % w2];
-        for (int k = 0; k < w; ++k) sp += ring[(n - w2 + k) % w2];
+        for (int k = 0; k < w; ++k) sr += rr[(n - w + k) % w2];
+        for (int k = 0; k < w; ++k) sp += rr[(n - w2 + k) % w2];
         const double recent = sr / (double)w, previous = sp / (double)w;
         if (!(previous <= fmax(A.p.tol, 0.0)) && (previous - recent) / previous < A.p.stall_improvement) {
             const double nr = fmin(rho * A.p.rho_growth, A.p.rho_cap);
             const double nro = fmin(rho_o * A.p.rho_growth, A.p.rho_cap);
             A.s.rho[i] = nr;
             A.s.rho_o[i] = nro;
+            if (S) {
+                S->rho = nr;
+                S->rho_o = nro;
+            }
             if (nro != rho_o) {
                 A.s.level[i] = level + 1;
-                A.s.n_changes[i] += 1;
+                const int nc = (S ? S->n_changes : A.s.n_changes[i]) + 1;
+                A.s.n_changes[i] = nc;
+                if (S) {
+                    S->level = level + 1;
+                    S->n_changes = nc;
+                }
             }
             A.s.last_change[i] = it;
+            if (S) S->last_change = it;
         }
     }
 }
@@ -163,35 +192,58 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     double* sXi = smem + L.xi;
     double* sWarp = smem + L.warp;
 
-    for (int rep_ = 0; rep_ < (MODE == 3 ? A.n_loop : 1); ++rep_) {
-    if (MODE == 3 && rep_ > 0) __syncthreads();  // the previous iteration's writes (tid 0: status, level, rho)
+    // MODE 3 keeps the member's bookkeeping, the basis, the shapes, the positions and the incoming sums in
+    // shared memory across its iterations: only the first iteration stages them from global memory
+    __shared__ SchedS sS;
+    constexpr bool loop = MODE == 3;
+    for (int rep_ = 0; rep_ < (loop ? A.n_loop : 1); ++rep_) {
+    if (loop && rep_ > 0) __syncthreads();  // the previous iteration's writes (tid 0: sS; all: sums, positions)
     // ---------------- frozen members (converged / failed) do nothing
-    const int status0 = A.s.status[i];
+    if (loop && rep_ == 0 && tid == 0) {
+        sS.status = A.s.status[i];
+        sS.level = A.s.level[i];
+        sS.rho = A.s.rho[i];
+        sS.rho_o = A.s.rho_o[i];
+        sS.iteration = A.s.iteration[i];
+        sS.n_hist = A.s.n_hist[i];
+        sS.last_change = A.s.last_change[i];
+        sS.n_changes = A.s.n_changes[i];
+        const int w2 = 2 * A.p.stall_window;
+        for (int k = 0; k < w2; ++k) sS.ring[k] = A.s.ring[(int64_t)i * w2 + k];
+    }
+    if (loop && rep_ == 0) __syncthreads();
+    const int status0 = loop ? sS.status : A.s.status[i];
     if (!prime && (status0 & (TRO_CONVERGED | TRO_FACTOR_FAILED))) return;
-    const int level = A.s.level[i];
+    const int level = loop ? sS.level : A.s.level[i];
     if (!prime && !A.c.level_ok[level]) {
         // qpcore.factorize raises when the new rho_o's saddle fails the cond guard
         // (qpcore.py:108-110); the member stops here and the host raises.
         if (tid == 0) A.s.status[i] = status0 | TRO_FACTOR_FAILED;
         return;
     }
-    const double rho = A.s.rho[i];
-    const double rho_o = A.s.rho_o[i];
+    const double rho = loop ? sS.rho : A.s.rho[i];
+    const double rho_o = loop ? sS.rho_o : A.s.rho_o[i];
 
     // ---------------- stage constants + previous positions + incoming sums
-    for (int k = tid; k < n_p * m; k += nthr) sP[k] = ld_const(A.c.P + k);
+    if (rep_ == 0) {
+        for (int k = tid; k < n_p * m; k += nthr) sP[k] = ld_const(A.c.P + k);
+        for (int k = tid; k < n_o; k += nthr) {
+            double a = ld_const(A.c.shape_a + k), b = ld_const(A.c.shape_b + k);
+            sA[k] = a;
+            sB[k] = b;
+            sIA2[k] = 1.0 / (a * a);
+            sIB2[k] = 1.0 / (b * b);
+        }
+    }
     const double* posg = A.s.pos + (int64_t)i * DIM * n_p;
     if (!prime) {
-        for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
-        const double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
-        for (int k = tid; k < 2 * DIM * n_p; k += nthr) sSumIn[k] = sg[k];
-    }
-    for (int k = tid; k < n_o; k += nthr) {
-        double a = ld_const(A.c.shape_a + k), b = ld_const(A.c.shape_b + k);
-        sA[k] = a;
-        sB[k] = b;
-        sIA2[k] = 1.0 / (a * a);
-        sIB2[k] = 1.0 / (b * b);
+        if (rep_ == 0) {
+            for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
+            const double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
+            for (int k = tid; k < 2 * DIM * n_p; k += nthr) sSumIn[k] = sg[k];
+        } else {  // the previous iteration's positions; its epilogue left the sums in sSumIn
+            for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = sPosNew[k];
+        }
     }
     __syncthreads();
 
@@ -374,6 +426,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         double acc = 0.0;
         for (int gg = 0; gg < G; ++gg) acc += sRed[gg * 2 * DIM * n_p + k];
         sg[k] = acc;
+        if constexpr (loop) sSumIn[k] = acc;  // the next iteration's position step reads them from here
     }
     if (tid == 0) {
         double ss = 0.0, mm = 0.0;
@@ -385,7 +438,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         const double nrm = sqrt(ss);
         A.s.res_norm[i] = nrm;
         A.s.res_max[i] = mm;
-        if constexpr (!prime) alg1_schedule(A, i, status0, level, rho, rho_o, nrm, mm);
+        if constexpr (!prime) alg1_schedule(A, i, status0, level, rho, rho_o, nrm, mm, loop ? &sS : nullptr);
     }
     }  // rep_
 }
