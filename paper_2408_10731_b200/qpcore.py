@@ -17,7 +17,7 @@ reference) or CUDA tensors (returned as CUDA tensors, no host round trip).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import field, make_dataclass
 
 import numpy as np
 from scipy.linalg import lu_factor, lu_solve
@@ -53,61 +53,45 @@ class FactorizationError(ValueError):
     """Saddle matrix is rank-deficient or too ill-conditioned to trust."""
 
 
-@dataclass(frozen=True)
-class EqQP:
-    Q: np.ndarray
-    q: np.ndarray
-    A: np.ndarray
-    b: np.ndarray
+def _frozen(name, fields, **ns):
+    return make_dataclass(name, fields, frozen=True, namespace={"__module__": __name__, **ns})
 
 
-@dataclass(frozen=True)
-class BatchRHS:
-    """qs (N, n_v) and bs (N, n_eq) stacked right-hand sides."""
-
-    qs: object
-    bs: object
-
-    def __post_init__(self):
-        if self.qs.ndim != 2 or self.bs.ndim != 2:
-            raise ValueError("batch right-hand sides must be 2-D arrays")
-        if self.qs.shape[0] != self.bs.shape[0]:
-            raise ValueError("qs and bs must have the same batch size")
-        if self.qs.shape[0] < 1:
-            raise ValueError("empty batch")
-
-    @property
-    def size(self) -> int:
-        return int(self.qs.shape[0])
+# min 0.5 xi'Q xi + q'xi s.t. A xi = b
+EqQP = _frozen("EqQP", [(k, np.ndarray) for k in ("Q", "q", "A", "b")])
 
 
-@dataclass(frozen=True)
-class KKTFactor:
-    n_v: int
-    n_eq: int
-    cond_estimate: float
-    _lu: tuple = field(repr=False)
-    _kinv: np.ndarray = field(repr=False, default=None)
-    _device: dict = field(repr=False, default_factory=dict, compare=False)
+def _check_rhs(self):
+    if self.qs.ndim != 2 or self.bs.ndim != 2:
+        raise ValueError("batch right-hand sides must be 2-D arrays")
+    if self.qs.shape[0] != self.bs.shape[0]:
+        raise ValueError("qs and bs must have the same batch size")
+    if self.qs.shape[0] < 1:
+        raise ValueError("empty batch")
 
-    @property
-    def size(self) -> int:
-        return self.n_v + self.n_eq
 
-    @property
-    def kinv(self) -> np.ndarray:
-        return self._kinv
+# stacked right-hand sides: qs (N, n_v), bs (N, n_eq); numpy arrays or CUDA tensors
+BatchRHS = _frozen("BatchRHS", [("qs", object), ("bs", object)], __post_init__=_check_rhs,
+                   size=property(lambda r: int(r.qs.shape[0])))
 
-    def kinv_on(self, device):
-        """fp64 K^-1 resident on `device` (uploaded once per device)."""
-        import torch
 
-        key = str(device)
-        t = self._device.get(key)
-        if t is None:
-            t = torch.as_tensor(self._kinv, dtype=torch.float64, device=device).contiguous()
-            self._device[key] = t
-        return t
+def _kinv_on(self, device):
+    """fp64 K^-1 resident on `device` (uploaded once per device)."""
+    import torch
+
+    cache = self._device
+    key = str(device)
+    if key not in cache:
+        cache[key] = torch.as_tensor(self._kinv, dtype=torch.float64, device=device).contiguous()
+    return cache[key]
+
+
+# one saddle's LU (host) and explicit inverse (host + per-device copies)
+KKTFactor = _frozen("KKTFactor", [("n_v", int), ("n_eq", int), ("cond_estimate", float),
+                                  ("_lu", tuple, field(repr=False)),
+                                  ("_kinv", np.ndarray, field(repr=False, default=None)),
+                                  ("_device", dict, field(repr=False, default_factory=dict, compare=False))],
+                    size=property(lambda f: f.n_v + f.n_eq), kinv=property(lambda f: f._kinv), kinv_on=_kinv_on)
 
 
 def saddle_matrix(Q: np.ndarray, A: np.ndarray) -> np.ndarray:
@@ -121,26 +105,24 @@ def saddle_matrix(Q: np.ndarray, A: np.ndarray) -> np.ndarray:
 
 
 def _build(Q, A, cond_limit: float) -> KKTFactor:
-    """factorize without touching the process-wide counter (engines count levels they use)."""
+    """factorize without touching the process-wide counter (engines count the levels they use)."""
     Q = np.asarray(Q, dtype=float)
     A = np.atleast_2d(np.asarray(A, dtype=float))
-    n_v = Q.shape[0]
+    n_v, n_eq = Q.shape[0], A.shape[0]
     if Q.shape != (n_v, n_v):
         raise ValueError(f"Q must be square, got {Q.shape}")
     if not np.allclose(Q, Q.T, rtol=1e-10, atol=1e-12):
         raise ValueError("Q must be symmetric")
-    n_eq = A.shape[0]
     if A.shape[1] != n_v:
         raise ValueError(f"A has {A.shape[1]} columns, expected {n_v}")
-    if n_eq > 0 and np.linalg.matrix_rank(A) < n_eq:
+    if n_eq and np.linalg.matrix_rank(A) < n_eq:  # qpcore.py:98-100
         raise FactorizationError(f"equality matrix A is rank-deficient (rank < {n_eq})")
     K = saddle_matrix(Q, A)
-    cond = float(np.linalg.cond(K))
-    if not np.isfinite(cond) or cond > cond_limit:
+    cond = float(np.linalg.cond(K))  # qpcore.py:108-110
+    if not (np.isfinite(cond) and cond <= cond_limit):
         raise FactorizationError(f"saddle matrix is near-singular (cond estimate {cond:.3e})")
     lu = lu_factor(K)
-    kinv = lu_solve(lu, np.eye(K.shape[0]))
-    return KKTFactor(n_v=n_v, n_eq=n_eq, cond_estimate=cond, _lu=lu, _kinv=kinv)
+    return KKTFactor(n_v=n_v, n_eq=n_eq, cond_estimate=cond, _lu=lu, _kinv=lu_solve(lu, np.eye(K.shape[0])))
 
 
 def factorize(Q: np.ndarray, A: np.ndarray, *, cond_limit: float = 1e12) -> KKTFactor:
