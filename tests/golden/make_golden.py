@@ -603,6 +603,24 @@ def make_runs():
     print("runs written")
 
 
+def make_acceptance5():
+    """Acceptance criterion 5 (test_acceptance.py:123-139): solve_batch_opt on random-static n_o 10, seeds 0-9,
+    n_batch 100, 100 iterations: best-member history norms / max and the best index per seed."""
+    from trajopt import solver_batch
+    from trajopt.bench.runner import batch_problem_from_scenario as bp
+
+    out = {}
+    for seed in range(10):
+        sc = gen_scenario("random-static", {"n_o": 10}, seed=seed)
+        basis = build_basis(sc.horizon.t0, sc.horizon.tf, sc.horizon.n_p, 10)
+        ranked = solver_batch.solve_batch_opt(bp(sc, basis, n_batch=100), solver_batch.BatchParams(max_iter=100),
+                                              seed=seed)
+        out[f"s{seed}_norm"] = np.array([h["norm"] for h in ranked.best_history])
+        out[f"s{seed}_best"] = np.array([-1 if ranked.best_index is None else ranked.best_index])
+    np.savez_compressed(os.path.join(OUT, "acceptance5.npz"), **out)
+    print("acceptance5 written")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
