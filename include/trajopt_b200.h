@@ -289,12 +289,15 @@ typedef struct tro_b2_consts {
     const double* q;             /* 4m linear cost (_Structure.q, solver_batch.py:170-177) */
     const double* b;             /* 12 boundary values [x(6) | y(6)] */
     const double* b_psi;         /* 2 heading boundary values */
-    const double* kinvT_xi;      /* n_levels x (4m + 12) x 4m: rows 0..4m-1 of K_xi^-1, transposed */
+    const double* kinvT_xi;      /* n_levels x (4m + 12) x (4m + 12): K_xi^-1, transposed (all rows) */
     const double* kinvT_psi;     /* n_levels x (m + 2) x m: rows 0..m-1 of K_psi^-1, transposed */
     const double* rho_chain;     /* n_levels: rho per level (min(rho * growth, cap) chain) */
     const double* rho_psi_chain; /* n_levels: rho_psi per level */
     const double* desired;       /* n_p x 2 (member costs, mode 3) */
     double v_max, a_max, w_smooth, w_track;
+    const double* k_xi;          /* n_levels x (4m + 12) x (4m + 12): K_xi itself (symmetric); the xi step
+                                    refines K^-1 rhs once (r = rhs - K sol, xi += (K^-1 r)[:4m]) so xi carries
+                                    the LU solve's rounding floor, not the explicit inverse's */
 } tro_b2_consts;
 
 typedef struct tro_b2_state {

@@ -175,7 +175,7 @@ class B2Dims(ctypes.Structure):
 class B2Consts(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in ("PT", "Pr", "obs", "obs_ab", "offsets", "q", "b", "b_psi", "kinvT_xi",
                                         "kinvT_psi", "rho_chain", "rho_psi_chain", "desired")] + [
-        (n, c_double) for n in ("v_max", "a_max", "w_smooth", "w_track")]
+        (n, c_double) for n in ("v_max", "a_max", "w_smooth", "w_track")] + [("k_xi", c_void_p)]
 
 
 class B2State(ctypes.Structure):

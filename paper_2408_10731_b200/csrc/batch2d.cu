@@ -241,6 +241,21 @@ __global__ void __launch_bounds__(32) b2_merge_kernel(B2Args A) {
 
 enum { kModeIter = 0, kModePrime = 1, kModeMaterialise = 2, kModeRank = 3, kModeXi = 4, kModeHeading = 5 };
 
+// sum_j M[j * ld + col] * v[j] over j < n (v in shared memory), four independent FMA chains
+__device__ __forceinline__ double b2_gemv_col(const double* M, int ld, int col, const double* v, int n) {
+    const double* p = M + col;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {
+        a0 = fma(__ldg(p + (int64_t)j * ld), v[j], a0);
+        a1 = fma(__ldg(p + (int64_t)(j + 1) * ld), v[j + 1], a1);
+        a2 = fma(__ldg(p + (int64_t)(j + 2) * ld), v[j + 2], a2);
+        a3 = fma(__ldg(p + (int64_t)(j + 3) * ld), v[j + 3], a3);
+    }
+    for (; j < n; ++j) a0 = fma(__ldg(p + (int64_t)j * ld), v[j], a0);
+    return (a0 + a1) + (a2 + a3);
+}
+
 template <int NC, int MODE, bool CIRC>
 __global__ void __launch_bounds__(kB2Threads, B2_MINB) b2_kernel(B2Args A) {
     constexpr bool iter = MODE == kModeIter;
@@ -306,18 +321,19 @@ __global__ void __launch_bounds__(kB2Threads, B2_MINB) b2_kernel(B2Args A) {
             sRhs[tid] = A.c.b[tid - nv];
         }
         __syncthreads();
+        // [xi; nu] = K^-1 [-q; b] (qpcore.py:141-143), then one step of iterative refinement:
+        // r = rhs - K [xi; nu], xi += (K^-1 r)[:4m].  The explicit inverse alone leaves xi ~1e-11 from the
+        // LU solve; the refined xi sits at the LU solve's rounding floor.
+        double* sSol = smem + L.part;  // the contraction partials' space is free during the prologue
+        double* sRes = sSol + nk;
+        const double* Ki = A.c.kinvT_xi + (int64_t)level * nk * nk;
+        if (tid < nk) sSol[tid] = b2_gemv_col(Ki, nk, tid, sRhs, nk);
+        __syncthreads();
+        if (tid < nk)  // K is symmetric: its column tid is row tid, read coalesced across threads
+            sRes[tid] = sRhs[tid] - b2_gemv_col(A.c.k_xi + (int64_t)level * nk * nk, nk, tid, sSol, nk);
+        __syncthreads();
         if (tid < nv) {
-            const double* K = A.c.kinvT_xi + (int64_t)level * nk * nv + tid;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int j = 0;
-            for (; j + 4 <= nk; j += 4) {
-                a0 = fma(__ldg(K + (int64_t)j * nv), sRhs[j], a0);
-                a1 = fma(__ldg(K + (int64_t)(j + 1) * nv), sRhs[j + 1], a1);
-                a2 = fma(__ldg(K + (int64_t)(j + 2) * nv), sRhs[j + 2], a2);
-                a3 = fma(__ldg(K + (int64_t)(j + 3) * nv), sRhs[j + 3], a3);
-            }
-            for (; j < nk; ++j) a0 = fma(__ldg(K + (int64_t)j * nv), sRhs[j], a0);
-            const double acc = (a0 + a1) + (a2 + a3);
+            const double acc = sSol[tid] + b2_gemv_col(Ki, nk, tid, sRes, nk);
             sXi[tid] = acc;
             if (MODE == kModeXi) g_xi[tid] = acc;
         }
@@ -808,6 +824,7 @@ static int b2_dispatch(const B2Args& A, int mode, size_t smem, cudaStream_t st) 
 extern "C" int tro_b2_run(int32_t mode, const tro_b2_dims* d, const tro_b2_consts* c, const tro_b2_state* s,
                           const tro_b2_params* p, void* stream) {
     if (!d || !c || !s || !p || mode < 0 || mode > 6) return TRO_EINVAL;
+    if (!c->k_xi || !c->kinvT_xi) return TRO_EINVAL;  // the xi step solves with K^-1 and refines with K
     if ((p->flags & TRO_B2_SHARD) && mode == 0 && !s->shard) return TRO_EINVAL;
     if (mode == 6) {
         if (!s->shards_in || p->n_shards < 1 || !s->ring || p->stall_window < 1 ||

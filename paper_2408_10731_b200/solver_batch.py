@@ -349,7 +349,8 @@ class _Levels:
         chain_p += [chain_p[-1]] * (n - len(chain_p))
         self.rho, self.rho_psi = chain, chain_p
         nv, nk = 4 * m, 4 * m + 12
-        self.kinvT_xi = np.zeros((n, nk, nv))
+        self.kinvT_xi = np.zeros((n, nk, nk))
+        self.k_xi = np.zeros((n, nk, nk))
         self.kinvT_psi = np.zeros((n, m + 2, m))
         PtP = basis.P.T @ basis.P
         self.error: list = [None] * n
@@ -362,7 +363,8 @@ class _Levels:
                     raise
                 self.error[k] = exc  # a level the schedule may never reach: fail when it does
                 continue
-            self.kinvT_xi[k] = fx.kinv[:nv, :].T
+            self.kinvT_xi[k] = fx.kinv.T
+            self.k_xi[k] = qpcore.saddle_matrix(struct.Q + chain[k] * struct.FtF, struct.A)
             self.kinvT_psi[k] = fp.kinv[:m, :].T
         self._dev = {}
 
@@ -372,6 +374,7 @@ class _Levels:
         if t is None:
             f64 = dict(dtype=torch.float64, device=dev)
             t = dict(kinvT_xi=torch.as_tensor(self.kinvT_xi, **f64).contiguous(),
+                     k_xi=torch.as_tensor(self.k_xi, **f64).contiguous(),
                      kinvT_psi=torch.as_tensor(self.kinvT_psi, **f64).contiguous(),
                      rho=torch.as_tensor(self.rho, **f64), rho_psi=torch.as_tensor(self.rho_psi, **f64))
             self._dev[key] = t
@@ -448,7 +451,7 @@ class _Engine:
             q=P(c["q"]), b=P(c["b"]), b_psi=P(c["b_psi"]), kinvT_xi=P(lv["kinvT_xi"]),
             kinvT_psi=P(lv["kinvT_psi"]), rho_chain=P(lv["rho"]), rho_psi_chain=P(lv["rho_psi"]),
             desired=P(c["desired"]), v_max=float(pb.v_max), a_max=float(pb.a_max), w_smooth=float(pb.w_smooth),
-            w_track=float(pb.w_track))
+            w_track=float(pb.w_track), k_xi=P(lv["k_xi"]))
         self._state_struct()
 
     def _alloc_geo(self):
