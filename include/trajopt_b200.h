@@ -114,6 +114,12 @@ typedef struct tro_alg1_state {
     int32_t* n_hist;      /* B: iterations recorded in this solve */
     int32_t* status;      /* B: TRO_CONVERGED | TRO_FACTOR_FAILED */
     int32_t* n_changes;   /* B: rho_o changes in this solve (new factorizations) */
+    /* optional tail balancing of the persistent TMA kernel (NULL: off).  When B is not a multiple of the
+     * grid, the last partial round's members are split into two obstacle halves run by two CTAs; the halves'
+     * partial sums meet here and the second finisher (ticket) combines them in a fixed order:
+     * split_scratch >= 2 x 2 x (2 dim n_p + 2) doubles per grid slot, split_ticket >= 1 zeroed uint32 per slot */
+    double* split_scratch;
+    uint32_t* split_ticket;
 } tro_alg1_state;
 
 /* Sums for the first position step + positions of the current xi + residual of the

@@ -101,7 +101,7 @@ class Alg1Engine:
     def __init__(self, basis: BasisSet, tracks, shape_a, shape_b, bvals, q, *, params, rho0=None,
                  w_smooth: float = 1.0, w_track: float = 1.0, dtype=torch.float64, device=None, groups: int = 0,
                  max_hist: int = 0, export: bool = False, keep_d: bool = False, cond_limit: float = 1e12,
-                 use_tma: bool = True, layout: str = "angle"):
+                 use_tma: bool = True, layout: str = "angle", tail_split: bool = True):
         _lib.require_cuda()
         self.lib = _lib.load()
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -177,6 +177,10 @@ class Alg1Engine:
         self.n_hist = torch.zeros(B, **i32)
         self.status = torch.zeros(B, **i32)
         self.n_changes = torch.zeros(B, **i32)
+        # tail balancing of the persistent kernel: per grid slot two halves' partial sums + a ticket
+        slots = 2 * torch.cuda.get_device_properties(dev).multi_processor_count
+        self.split_scratch = torch.zeros((slots, 2, 2 * dim * n_p + 2), **f64) if tail_split else None
+        self.split_ticket = torch.zeros(slots, **i32) if tail_split else None
 
         self._dims = _lib.Alg1Dims(B, n_o, n_p, m, dim, self.n_eq, len(self.table.rhos), int(groups),
                                    {"unit": _lib.TRO_LAYOUT_UNIT, "half": _lib.TRO_LAYOUT_HALF}.get(
@@ -190,7 +194,7 @@ class Alg1Engine:
             p(self.state), p(self.d), p(self.copies), p(self.xi), p(self.pos),
             p(self.sums), p(self.rho), p(self.rho_o), p(self.ring), p(self.res_norm), p(self.res_max), p(self.hist),
             p(self.level), p(self.iteration), p(self.last_change), p(self.n_hist), p(self.status),
-            p(self.n_changes))
+            p(self.n_changes), p(self.split_scratch), p(self.split_ticket))
         self._graph = None
         self._graph_n = 0
         # TMA-pipelined persistent kernel for the iteration unless disabled (flags bit 2)

@@ -115,6 +115,8 @@ class Alg1State(ctypes.Structure):
         ("n_hist", c_void_p),
         ("status", c_void_p),
         ("n_changes", c_void_p),
+        ("split_scratch", c_void_p),
+        ("split_ticket", c_void_p),
     ]
 
 

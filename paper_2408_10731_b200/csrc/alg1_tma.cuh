@@ -63,6 +63,28 @@ __host__ __device__ inline TmaLayout tma_layout(int stage_bytes, int S, int n_p,
 #endif
 constexpr int kTmaMinBlocks = TRO_TMA_MINB;  // resident CTAs per SM the kernel is compiled for
 
+// Work unit u of this CTA: a member and the stage range [st0, st1) of its obstacle rows (half: -1 = whole
+// member, 0 / 1 = the first / second half of a tail member)
+struct WorkUnit {
+    int member, st0, st1, half;
+};
+__device__ __forceinline__ WorkUnit work_unit(int u, int rounds, int split_tail, int nst) {
+    WorkUnit w;
+    if (split_tail && u == rounds) {
+        const int h = (int)blockIdx.x & 1, mid = nst / 2;
+        w.member = rounds * (int)gridDim.x + (int)blockIdx.x / 2;
+        w.st0 = h ? mid : 0;
+        w.st1 = h ? nst : mid;
+        w.half = h;
+    } else {
+        w.member = (int)blockIdx.x + u * (int)gridDim.x;
+        w.st0 = 0;
+        w.st1 = nst;
+        w.half = -1;
+    }
+    return w;
+}
+
 // DM: the previous iterate's d source fixed at compile time (2: recompute, the steady state) or -1 (read
 // A.p.d_mode at run time: the first iteration after an init / prime)
 template <int DIM, typename T, int LAY, int NP, int G, int S, int DM>
@@ -111,6 +133,11 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
 
     const int nst = (n_o + G - 1) / G;  // stages per member
     // ring position: stage s and its phase bit run on across members (no divisions in the loops)
+    // work units of this CTA: members blockIdx.x + u gridDim.x, or with tail balancing (A.split_tail = M > 0)
+    // `rounds` full rounds and then, for the first 2 M CTAs, one half (of the stages) of a tail member
+    const int rounds = B / (int)gridDim.x;
+    const int n_units = A.split_tail ? rounds + ((int)blockIdx.x < 2 * A.split_tail ? 1 : 0)
+                                     : (B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
     if (warp == NCW) {
         // ======================= producer warp (one elected lane)
@@ -118,13 +145,15 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             int s = 0;
             uint32_t ph = 0;
             bool wrapped = false;
-            for (int i = blockIdx.x; i < B; i += gridDim.x) {
+            for (int u = 0; u < n_units; ++u) {
+                const WorkUnit wu = work_unit(u, rounds, A.split_tail, nst);
+                const int i = wu.member;
                 const int st = A.s.status[i];
                 if ((st & (TRO_CONVERGED | TRO_FACTOR_FAILED)) || !A.c.level_ok[A.s.level[i]]) continue;
                 const unsigned char* src = reinterpret_cast<const unsigned char*>(A.s.state) +
                                            (int64_t)i * n_o * C::kRowBytes;
                 const unsigned char* trk = reinterpret_cast<const unsigned char*>(A.c.tracks);
-                for (int j0 = 0; j0 < n_o; j0 += G) {
+                for (int j0 = wu.st0 * G; j0 < n_o && j0 < wu.st1 * G; j0 += G) {
                     if (wrapped) mbar_wait(&empty[s], ph ^ 1u);  // the consumers released this stage
                     const int rows = min(G, n_o - j0);
                     unsigned char* buf = stages + s * C::kStageBytes;
@@ -155,7 +184,10 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     T* dst = reinterpret_cast<T*>(A.s.d);
     T* cop = reinterpret_cast<T*>(A.s.copies);
 
-    for (int i = blockIdx.x; i < B; i += gridDim.x) {
+    for (int u = 0; u < n_units; ++u) {
+        const WorkUnit wu = work_unit(u, rounds, A.split_tail, nst);
+        const int i = wu.member;
+        const bool split = wu.half >= 0;
         const int status0 = A.s.status[i];
         if (status0 & (TRO_CONVERGED | TRO_FACTOR_FAILED)) continue;
         const int level = A.s.level[i];
@@ -195,7 +227,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             for (int cc = 0; cc < m; ++cc) acc += ld_const(Kr + cc) * (-sQlin[ax * m + cc]);
             for (int e = 0; e < ne; ++e) acc += ld_const(Kr + m + e) * bg[ax * ne + e];
             sXi[o] = acc;
-            A.s.xi[(int64_t)i * DIM * m + o] = acc;
+            if (!split) A.s.xi[(int64_t)i * DIM * m + o] = acc;  // split: written by the combining half
         }
         consumer_sync(NC);
         for (int k = tid; k < DIM * NP; k += NC) {
@@ -203,7 +235,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             double acc = 0.0;
             for (int cc = 0; cc < m; ++cc) acc += sP[tt * m + cc] * sXi[ax * m + cc];
             sPosNew[k] = acc;
-            A.s.pos[(int64_t)i * DIM * NP + k] = acc;
+            if (!split) A.s.pos[(int64_t)i * DIM * NP + k] = acc;
         }
         consumer_sync(NC);
 
@@ -218,9 +250,10 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
         const int d_mode = DM >= 0 ? DM : A.p.d_mode;
         T* gbase = reinterpret_cast<T*>(A.s.state) + (int64_t)i * n_o * W * NP + t;
 
-        T* gp = gbase + (int64_t)g * W * NP;
-        int64_t e = ((int64_t)i * n_o + g) * NP + t;  // index into the optional d / copies planes
-        for (int j = g; j - g < n_o; j += G, gp += G * W * NP, e += G * NP) {
+        const int j_first = wu.st0 * G + g, j_end = wu.st1 * G + g;  // this unit's stages
+        T* gp = gbase + (int64_t)j_first * W * NP;
+        int64_t e = ((int64_t)i * n_o + j_first) * NP + t;  // index into the optional d / copies planes
+        for (int j = j_first; j < j_end && j - g < n_o; j += G, gp += G * W * NP, e += G * NP) {
             mbar_wait(&full[s], ph);
             if (act && j < n_o) {
                 const unsigned char* buf = stages + s * C::kStageBytes;
@@ -283,20 +316,65 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             sWarp[NCW + warp] = mx;
         }
         consumer_sync(NC);
-        double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
-        for (int k = tid; k < 2 * DIM * NP; k += NC) {
-            double acc = 0.0;
-            for (int gg = 0; gg < G; ++gg) acc += sRed[gg * 2 * DIM * NP + k];
-            sg[k] = acc;
-        }
-        if (tid == 0) {
-            double ss = 0.0, mm = 0.0;
-            for (int w = 0; w < NCW; ++w) {
-                ss += sWarp[w];
-                mm = fmax(mm, sWarp[NCW + w]);
+        if (!split) {
+            double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
+            for (int k = tid; k < 2 * DIM * NP; k += NC) {
+                double acc = 0.0;
+                for (int gg = 0; gg < G; ++gg) acc += sRed[gg * 2 * DIM * NP + k];
+                sg[k] = acc;
             }
-            if (ss != ss) mm = ss;  // np.max propagates NaN
-            alg1_schedule(A, i, status0, level, rho, rho_o, sqrt(ss), mm);
+            if (tid == 0) {
+                double ss = 0.0, mm = 0.0;
+                for (int w = 0; w < NCW; ++w) {
+                    ss += sWarp[w];
+                    mm = fmax(mm, sWarp[NCW + w]);
+                }
+                if (ss != ss) mm = ss;  // np.max propagates NaN
+                alg1_schedule(A, i, status0, level, rho, rho_o, sqrt(ss), mm);
+            }
+        } else {
+            // this half's sums over its groups, residual sum of squares and max into the scratch; the
+            // second half to finish combines (half 0 + half 1: a fixed order whichever finishes last)
+            constexpr int kPart = 2 * DIM * NP + 2;
+            const int tk = i - rounds * (int)gridDim.x;  // tail member index
+            double* part = A.s.split_scratch + ((int64_t)tk * 2 + wu.half) * kPart;
+            for (int k = tid; k < 2 * DIM * NP; k += NC) {
+                double acc = 0.0;
+                for (int gg = 0; gg < G; ++gg) acc += sRed[gg * 2 * DIM * NP + k];
+                part[k] = acc;
+            }
+            __shared__ int sLast;
+            if (tid == 0) {
+                double ss = 0.0, mm = 0.0;
+                for (int w = 0; w < NCW; ++w) {
+                    ss += sWarp[w];
+                    mm = fmax(mm, sWarp[NCW + w]);
+                }
+                part[2 * DIM * NP] = ss;
+                part[2 * DIM * NP + 1] = mm;
+            }
+            consumer_sync(NC);
+            if (tid == 0) {
+                __threadfence();
+                sLast = atomicAdd(A.s.split_ticket + tk, 1u) == 1u;
+            }
+            consumer_sync(NC);
+            if (sLast) {
+                __threadfence();
+                const double* p0 = A.s.split_scratch + (int64_t)tk * 2 * kPart;
+                const double* p1 = p0 + kPart;
+                double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
+                for (int k = tid; k < 2 * DIM * NP; k += NC) sg[k] = __ldcg(p0 + k) + __ldcg(p1 + k);
+                for (int k = tid; k < DIM * NP; k += NC) A.s.pos[(int64_t)i * DIM * NP + k] = sPosNew[k];
+                for (int k = tid; k < DIM * m; k += NC) A.s.xi[(int64_t)i * DIM * m + k] = sXi[k];
+                if (tid == 0) {
+                    const double ss = __ldcg(p0 + 2 * DIM * NP) + __ldcg(p1 + 2 * DIM * NP);
+                    double mm = fmax(__ldcg(p0 + 2 * DIM * NP + 1), __ldcg(p1 + 2 * DIM * NP + 1));
+                    if (ss != ss) mm = ss;  // np.max propagates NaN
+                    alg1_schedule(A, i, status0, level, rho, rho_o, sqrt(ss), mm);
+                    A.s.split_ticket[tk] = 0u;  // ready for the next launch
+                }
+            }
         }
         consumer_sync(NC);  // sRed / sWarp / sPos* are reused by the next member
     }

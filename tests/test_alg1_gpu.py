@@ -373,3 +373,30 @@ def test_topk_stable_bitexact(n, k):
         keys[rng.integers(0, n, size=3)] = -np.inf
     ref = np.argsort(keys, kind="stable")[:k]
     np.testing.assert_array_equal(_topk(keys, k), ref)
+
+
+def test_tail_split_matches_unsplit_batch(golden):
+    """Tail balancing of the persistent kernel (B not a multiple of the grid: the last round's members run
+    as two obstacle halves on two CTAs, combined in a fixed order) vs the same batch without it: equal up to
+    the association of the obstacle sums (1e-10 over 20 iterations), identical schedules."""
+    bs = basis_from(golden("flow3d_hist.npz"))
+    slots = 2 * torch.cuda.get_device_properties(0).multi_processor_count
+    B = slots + 5  # 5 tail members -> 10 half-units
+    batch = scenarios.flow3d_batch(50, range(B), basis=bs)
+    params = SingleParams(max_iter=20, tol=0.0)
+    out = {}
+    for split in (True, False):
+        eng = Alg1Engine(bs, np.stack([o.centers for o in batch.obstacles]), [o.shape.a for o in batch.obstacles],
+                         [o.shape.b for o in batch.obstacles], batch.bvals, batch.linear_terms(), params=params,
+                         max_hist=20, layout="half", tail_split=split)
+        eng.cold_init()
+        eng.run(20, use_graph=False, loop=False)
+        torch.cuda.synchronize()
+        out[split] = (eng.hist.cpu().numpy(), eng.xi.cpu().numpy(), eng.rho_o.cpu().numpy())
+    hs, xs, rs = out[True]
+    hu, xu, ru = out[False]
+    np.testing.assert_array_equal(hs[:, :, 2], hu[:, :, 2])
+    np.testing.assert_array_equal(rs, ru)
+    assert rel(hs[:, :, :2], hu[:, :, :2]) < 1e-10
+    assert rel(xs, xu) < 1e-10
+    np.testing.assert_array_equal(xs[:slots], xu[:slots])  # members of the full round: bitwise
