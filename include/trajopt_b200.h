@@ -120,6 +120,10 @@ typedef struct tro_alg1_state {
      * split_scratch >= 2 x 2 x (2 dim n_p + 2) doubles per grid slot, split_ticket >= 1 zeroed uint32 per slot */
     double* split_scratch;
     uint32_t* split_ticket;
+    /* optional member order of the persistent TMA kernel (NULL: members 0..B-1): it works through
+     * order[0 .. *n_order) only (e.g. the robots of a fleet still driving; tro_mpc_compact builds it) */
+    const int32_t* order;
+    const int32_t* n_order;
 } tro_alg1_state;
 
 /* Sums for the first position step + positions of the current xi + residual of the
@@ -466,6 +470,9 @@ typedef struct tro_mpc_io {
 
 int tro_mpc_advance_f64(int32_t mode, const tro_mpc_dims* dims, const tro_mpc_consts* c,
                         const tro_alg1_state* engine, const tro_mpc_io* io, void* stream);
+
+/* order[0 .. *n_order) = the members with flags == 0 in increasing index (one CTA; n_members <= 2^31). */
+int tro_mpc_compact(int32_t n_members, const int32_t* flags, int32_t* order, int32_t* n_order, void* stream);
 
 /* out (ncols x n) = rhs (ncols x n) * K^-T, i.e. out[c] = K^-1 rhs[c] for every column c.
  * kinv: n x n row-major.  qpcore.solve_batch with the RHS block [-q ; b]. */

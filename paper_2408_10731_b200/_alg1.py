@@ -194,7 +194,7 @@ class Alg1Engine:
             p(self.state), p(self.d), p(self.copies), p(self.xi), p(self.pos),
             p(self.sums), p(self.rho), p(self.rho_o), p(self.ring), p(self.res_norm), p(self.res_max), p(self.hist),
             p(self.level), p(self.iteration), p(self.last_change), p(self.n_hist), p(self.status),
-            p(self.n_changes), p(self.split_scratch), p(self.split_ticket))
+            p(self.n_changes), p(self.split_scratch), p(self.split_ticket), None, None)
         self._graph = None
         self._graph_n = 0
         # TMA-pipelined persistent kernel for the iteration unless disabled (flags bit 2)

@@ -46,6 +46,7 @@ EXPORTS = (
     "tro_validate_f64",
     "tro_predict_tracks_f64",
     "tro_mpc_advance_f64",
+    "tro_mpc_compact",
     "tro_version",
     "tro_error_string",
 )
@@ -117,6 +118,8 @@ class Alg1State(ctypes.Structure):
         ("n_changes", c_void_p),
         ("split_scratch", c_void_p),
         ("split_ticket", c_void_p),
+        ("order", c_void_p),
+        ("n_order", c_void_p),
     ]
 
 
@@ -284,6 +287,8 @@ def load() -> ctypes.CDLL:
     lib.tro_mpc_advance_f64.argtypes = [c_int32, POINTER(MpcDims), POINTER(MpcConsts), POINTER(Alg1State),
                                         POINTER(MpcIO), c_void_p]
     lib.tro_mpc_advance_f64.restype = c_int32
+    lib.tro_mpc_compact.argtypes = [c_int32, c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.tro_mpc_compact.restype = c_int32
     lib.tro_fp64_fma_probe.argtypes = [c_int64, c_int32, c_void_p, c_void_p]
     lib.tro_fp64_fma_probe.restype = c_int32
     lib.tro_version.argtypes = []

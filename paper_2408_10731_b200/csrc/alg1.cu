@@ -48,7 +48,7 @@ struct Alg1Args {
     tro_alg1_params p;
     int32_t G;
     int32_t n_loop;      // MODE 3: AM iterations per launch
-    int32_t split_tail;  // TMA kernel: members of the last partial round run as two obstacle halves (0: off)
+    int32_t split_tail;  // TMA kernel: 1 = the last partial round may run as obstacle halves (scratch given)
 };
 
 struct SmemLayout {
@@ -506,9 +506,13 @@ static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
     B.G = G;
     const int slots = sm_count() * kTmaMinBlocks;
     const int grid = A.d.n_members < slots ? A.d.n_members : slots;
-    // tail balancing: B = R grid + M with 0 < 2 M <= grid -> the last round's M members become 2 M halves
-    const int tail = A.d.n_members % grid;
-    B.split_tail = (A.s.split_scratch && A.s.split_ticket && tail > 0 && 2 * tail <= grid) ? tail : 0;
+    // tail balancing (decided in the kernel from the work-list length): when it is R grid + M with
+    // 0 < 2 M <= grid, the last round's M members become 2 M halves
+    B.split_tail = (A.s.split_scratch && A.s.split_ticket) ? 1 : 0;
+    if ((A.s.order == nullptr) != (A.s.n_order == nullptr)) {
+        *rc = TRO_EINVAL;
+        return 1;
+    }
 #if TRO_TMA_DM_SPEC
     if (A.p.d_mode == 2)
         alg1_tma_kernel<DIM, T, LAY, 100, G, S, 2><<<grid, C::kThreads, L.total, st>>>(B);

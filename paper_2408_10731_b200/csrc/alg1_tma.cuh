@@ -66,22 +66,23 @@ constexpr int kTmaMinBlocks = TRO_TMA_MINB;  // resident CTAs per SM the kernel 
 // Work unit u of this CTA: a member and the stage range [st0, st1) of its obstacle rows (half: -1 = whole
 // member, 0 / 1 = the first / second half of a tail member)
 struct WorkUnit {
-    int member, st0, st1, half;
+    int pos, member, st0, st1, half;  // pos: index into the work list (order, or the members themselves)
 };
-__device__ __forceinline__ WorkUnit work_unit(int u, int rounds, int split_tail, int nst) {
+__device__ __forceinline__ WorkUnit work_unit(int u, int rounds, int split_tail, int nst, const int32_t* order) {
     WorkUnit w;
     if (split_tail && u == rounds) {
         const int h = (int)blockIdx.x & 1, mid = nst / 2;
-        w.member = rounds * (int)gridDim.x + (int)blockIdx.x / 2;
+        w.pos = rounds * (int)gridDim.x + (int)blockIdx.x / 2;
         w.st0 = h ? mid : 0;
         w.st1 = h ? nst : mid;
         w.half = h;
     } else {
-        w.member = (int)blockIdx.x + u * (int)gridDim.x;
+        w.pos = (int)blockIdx.x + u * (int)gridDim.x;
         w.st0 = 0;
         w.st1 = nst;
         w.half = -1;
     }
+    w.member = order ? __ldg(order + w.pos) : w.pos;
     return w;
 }
 
@@ -135,9 +136,14 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     // ring position: stage s and its phase bit run on across members (no divisions in the loops)
     // work units of this CTA: members blockIdx.x + u gridDim.x, or with tail balancing (A.split_tail = M > 0)
     // `rounds` full rounds and then, for the first 2 M CTAs, one half (of the stages) of a tail member
-    const int rounds = B / (int)gridDim.x;
-    const int n_units = A.split_tail ? rounds + ((int)blockIdx.x < 2 * A.split_tail ? 1 : 0)
-                                     : (B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    // the work list: order[0 .. *n_order) when given (e.g. the robots still driving), else members 0..B-1
+    const int32_t* order = A.s.order;
+    const int n_work = order ? *A.s.n_order : B;
+    const int rounds = n_work / (int)gridDim.x;
+    const int tail = n_work - rounds * (int)gridDim.x;
+    const int split_tail = (A.split_tail && tail > 0 && 2 * tail <= (int)gridDim.x) ? tail : 0;
+    const int n_units = split_tail ? rounds + ((int)blockIdx.x < 2 * split_tail ? 1 : 0)
+                                   : (n_work - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
     if (warp == NCW) {
         // ======================= producer warp (one elected lane)
@@ -146,7 +152,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             uint32_t ph = 0;
             bool wrapped = false;
             for (int u = 0; u < n_units; ++u) {
-                const WorkUnit wu = work_unit(u, rounds, A.split_tail, nst);
+                const WorkUnit wu = work_unit(u, rounds, split_tail, nst, order);
                 const int i = wu.member;
                 const int st = A.s.status[i];
                 if ((st & (TRO_CONVERGED | TRO_FACTOR_FAILED)) || !A.c.level_ok[A.s.level[i]]) continue;
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     T* cop = reinterpret_cast<T*>(A.s.copies);
 
     for (int u = 0; u < n_units; ++u) {
-        const WorkUnit wu = work_unit(u, rounds, A.split_tail, nst);
+        const WorkUnit wu = work_unit(u, rounds, split_tail, nst, order);
         const int i = wu.member;
         const bool split = wu.half >= 0;
         const int status0 = A.s.status[i];
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             // this half's sums over its groups, residual sum of squares and max into the scratch; the
             // second half to finish combines (half 0 + half 1: a fixed order whichever finishes last)
             constexpr int kPart = 2 * DIM * NP + 2;
-            const int tk = i - rounds * (int)gridDim.x;  // tail member index
+            const int tk = wu.pos - rounds * (int)gridDim.x;  // tail index in the work list
             double* part = A.s.split_scratch + ((int64_t)tk * 2 + wu.half) * kPart;
             for (int k = tid; k < 2 * DIM * NP; k += NC) {
                 double acc = 0.0;

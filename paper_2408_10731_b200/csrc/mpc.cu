@@ -290,3 +290,42 @@ extern "C" int tro_mpc_advance_f64(int32_t mode, const tro_mpc_dims* d, const tr
 #undef TRO_MPC_LAUNCH
     return (int)cudaGetLastError();
 }
+
+namespace tro {
+// order[] = indices with flags == 0, increasing (a single CTA: block-wide exclusive scan per 1024-chunk)
+__global__ void __launch_bounds__(1024) mpc_compact_kernel(int n, const int32_t* __restrict__ flags,
+                                                            int32_t* __restrict__ order, int32_t* n_order) {
+    __shared__ int sWarpSum[32];
+    __shared__ int sBase;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) sBase = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < n; c0 += 1024) {
+        const int k = c0 + tid;
+        const int keep = (k < n && __ldg(flags + k) == 0) ? 1 : 0;
+        const unsigned ball = __ballot_sync(0xffffffffu, keep);
+        const int before = __popc(ball & ((1u << lane) - 1u));
+        if (lane == 0) sWarpSum[warp] = __popc(ball);
+        __syncthreads();
+        int wbase = 0;
+        for (int w = 0; w < warp; ++w) wbase += sWarpSum[w];
+        if (keep) order[sBase + wbase + before] = k;
+        __syncthreads();
+        if (tid == 0) {
+            int tot = 0;
+            for (int w = 0; w < 32; ++w) tot += sWarpSum[w];
+            sBase += tot;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) *n_order = sBase;
+}
+}  // namespace tro
+
+extern "C" int tro_mpc_compact(int32_t n_members, const int32_t* flags, int32_t* order, int32_t* n_order,
+                               void* stream) {
+    if (n_members < 0 || !n_order || (n_members > 0 && (!flags || !order))) return TRO_EINVAL;
+    tro::mpc_compact_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(n_members, flags, order,
+                                                                                     n_order);
+    return (int)cudaGetLastError();
+}

@@ -160,6 +160,12 @@ class MpcFleet:
         self.desired = torch.empty((B, basis.n_p, dim), **f64)
         self.flags = torch.zeros(B, **i32)
         self.n_trace = torch.zeros(B, **i32)
+        # the robots still driving, compacted on the device after every control step: the persistent
+        # iteration kernel works through this list only (frozen robots cost nothing, the rest stay balanced)
+        self.order = torch.arange(B, **i32)
+        self.n_order = torch.full((1,), B, **i32)
+        self.eng._state.order = self.order.data_ptr()
+        self.eng._state.n_order = self.n_order.data_ptr()
         self._i32 = i32
         self._f64 = f64
         self._mdims = None
@@ -184,6 +190,13 @@ class MpcFleet:
             rc = self.lib.tro_mpc_advance_f64(int(mode), ctypes.byref(self._mdims), ctypes.byref(consts),
                                               ctypes.byref(e._state), ctypes.byref(io), _lib.stream_handle())
         _lib.check(rc, "tro_mpc_advance_f64")
+        self._compact()
+
+    def _compact(self):
+        with torch.cuda.device(self.device):
+            rc = self.lib.tro_mpc_compact(self.B, self.flags.data_ptr(), self.order.data_ptr(),
+                                          self.n_order.data_ptr(), _lib.stream_handle())
+        _lib.check(rc, "tro_mpc_compact")
 
     def _predict(self, t_now_dev, k: int):
         if not self.n_o:

@@ -157,3 +157,23 @@ def test_run_scenario_other_solvers_structural():
     for solver in ("priest", "cem"):
         r = RN.run_scenario(SC.gen_scenario("barn-like", {"n_o": 6, "n_p": 40}, seed=2), solver, 0, 2)
         assert r.metrics.iters == 2 and np.isfinite(r.metrics.smoothness) and isinstance(r.metrics.success, bool)
+
+
+def test_compact_active_members():
+    """tro_mpc_compact: the indices with flags == 0, increasing, and their count (several 1024-chunks)."""
+    import ctypes  # noqa: F401
+
+    from paper_2408_10731_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(3)
+    for n in (1, 1023, 1024, 5000):
+        flags = rng.integers(0, 3, n).astype(np.int32)
+        f = torch.as_tensor(flags, device="cuda")
+        order = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.check(lib.tro_mpc_compact(n, f.data_ptr(), order.data_ptr(), cnt.data_ptr(), _lib.stream_handle()),
+                   "tro_mpc_compact")
+        ref = np.nonzero(flags == 0)[0]
+        assert int(cnt.item()) == ref.size
+        np.testing.assert_array_equal(order.cpu().numpy()[:ref.size], ref)
