@@ -34,6 +34,9 @@ constexpr int kB2MaxM = 16;
 #ifndef B2_UNROLL_BASIS
 #define B2_UNROLL_BASIS 1
 #endif
+#ifndef B2_OBS_BATCH
+#define B2_OBS_BATCH 5  // obstacles whose track loads are issued before the first use (element pass; 8 spilled more: 49.8 vs 47.0 us per C2-alt iteration)
+#endif
 #ifndef B2_MINB
 #define B2_MINB 7  // 7 CTAs / SM (72 registers, some spills): C2-alt's 1024 members in one wave; 6 % faster than 4 CTAs / 128 registers at 1024 and 8192 members (tools/tune_b2.sh)
 #endif
@@ -532,7 +535,7 @@ __global__ void __launch_bounds__(kB2Threads, B2_MINB) b2_kernel(B2Args A) {
                     ss = fma(rx, rx, ss);
                     ss = fma(ry, ry, ss);
                 };
-                constexpr int kBatch = 8;  // all loads of a batch in flight before the first use
+                constexpr int kBatch = B2_OBS_BATCH;  // all loads of a batch in flight before the first use
                 const int stride = 2 * n_p;
                 int o = 0;
                 for (; o + kBatch <= n_o; o += kBatch) {
