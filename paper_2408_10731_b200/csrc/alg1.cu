@@ -36,7 +36,7 @@ constexpr int kMaxRing = 64;
 #define TRO_MIN_BLOCKS 1
 #endif
 #ifndef TRO_UNROLL
-#define TRO_UNROLL 2
+#define TRO_UNROLL 1  // C1 in-kernel loop: 0.848 -> 0.82 ms per 100 iterations vs 2 (4: 0.83)
 #endif
 constexpr int kMaxThreads = TRO_MAX_THREADS;
 constexpr int kUnroll = TRO_UNROLL;
