@@ -14,7 +14,10 @@
 
 namespace tro {
 
-constexpr int kValWarps = 4;  // members per CTA
+#ifndef VAL_WARPS
+#define VAL_WARPS 8  // members per CTA: 2 -> 51 M, 4 -> 60 M, 8 -> 61.5 M, 16 -> 60 M traj/s (val config)
+#endif
+constexpr int kValWarps = VAL_WARPS;  // members per CTA (fewer when the sample buffers would not fit)
 constexpr int kValRec = 9;     // doubles per obstacle record
 
 struct ValArgs {
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(kValWarps * 32) validate_kernel(ValArgs A) {
     }
     __syncthreads();
     const bool uniform = s_uniform != 0;
-    const int64_t i = (int64_t)blockIdx.x * kValWarps + warp;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;  // one member per warp
     if (i >= A.d.n_members) return;
     double* pw = sPos + (int64_t)warp * n_p * DIM;
     const double* xi = coeffs ? A.io.xi + i * DIM * m : nullptr;
@@ -167,17 +170,23 @@ extern "C" int tro_validate_f64(const tro_val_dims* d, const tro_val_consts* c, 
     A.c = *c;
     A.io = *io;
     const int m = io->xi ? d->m : 0;
-    const size_t smem = sizeof(double) * ((size_t)2 * d->n_p * m + tro::kValRec * (d->n_obs > 0 ? d->n_obs : 1) +
-                                          (size_t)tro::kValWarps * d->n_p * d->dim);
+    // members (warps) per CTA: kValWarps, halved while the per-warp sample buffers do not fit
+    int wpc = tro::kValWarps;
+    auto smem_for = [&](int w) {
+        return sizeof(double) * ((size_t)2 * d->n_p * m + tro::kValRec * (d->n_obs > 0 ? d->n_obs : 1) +
+                                 (size_t)w * d->n_p * d->dim);
+    };
+    while (wpc > 1 && smem_for(wpc) > 200 * 1024) wpc >>= 1;
+    const size_t smem = smem_for(wpc);
     if (smem > 200 * 1024) return TRO_EINVAL;
-    const unsigned blocks = (unsigned)((d->n_members + tro::kValWarps - 1) / tro::kValWarps);
+    const unsigned blocks = (unsigned)((d->n_members + wpc - 1) / wpc);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (d->dim == 3) {
         cudaFuncSetAttribute(tro::validate_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tro::validate_kernel<3><<<blocks, tro::kValWarps * 32, smem, st>>>(A);
+        tro::validate_kernel<3><<<blocks, wpc * 32, smem, st>>>(A);
     } else {
         cudaFuncSetAttribute(tro::validate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tro::validate_kernel<2><<<blocks, tro::kValWarps * 32, smem, st>>>(A);
+        tro::validate_kernel<2><<<blocks, wpc * 32, smem, st>>>(A);
     }
     return (int)cudaGetLastError();
 }
