@@ -22,7 +22,10 @@
 
 namespace tro {
 
-constexpr int kPrWarps = 8;
+#ifndef PR_WARPS
+#define PR_WARPS 8
+#endif
+constexpr int kPrWarps = PR_WARPS;  // samples (warps) per CTA
 #ifndef PR_MINB
 #define PR_MINB 2  // 2 CTAs / SM at the 128-register cap (3 spills heavily)
 #endif
