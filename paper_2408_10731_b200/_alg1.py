@@ -195,6 +195,16 @@ class Alg1Engine:
             p(self.sums), p(self.rho), p(self.rho_o), p(self.ring), p(self.res_norm), p(self.res_max), p(self.hist),
             p(self.level), p(self.iteration), p(self.last_change), p(self.n_hist), p(self.status),
             p(self.n_changes), p(self.split_scratch), p(self.split_ticket), None, None)
+        # the persistent kernel's work list (batches above the in-kernel-loop size): run() compacts it to the
+        # members still iterating before every chunk, so converged members cost nothing and the rest stay
+        # balanced over the CTAs; outside run() it is the identity
+        self.order = self.n_order = None
+        if B > LOOP_MAX_MEMBERS:
+            self._identity = torch.arange(B, **i32)
+            self.order = self._identity.clone()
+            self.n_order = torch.full((1,), B, **i32)
+            self._state.order = self.order.data_ptr()
+            self._state.n_order = self.n_order.data_ptr()
         self._graph = None
         self._graph_n = 0
         # TMA-pipelined persistent kernel for the iteration unless disabled (flags bit 2)
@@ -310,6 +320,20 @@ class Alg1Engine:
         self.ring.zero_()
         self.status.zero_()
 
+    def compact_active(self):
+        """Work list = the members whose status is 0 (not converged / failed), on the device."""
+        if not self._state.order:
+            return
+        with torch.cuda.device(self.device):
+            rc = self.lib.tro_mpc_compact(self.B, self.status.data_ptr(), self._state.order, self._state.n_order,
+                                          _lib.stream_handle())
+        _lib.check(rc, "tro_mpc_compact")
+
+    def _restore_order(self):
+        if self.order is not None and self._state.order == self.order.data_ptr():
+            self.order.copy_(self._identity)
+            self.n_order.fill_(self.B)
+
     def _capture(self, n: int):
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(device=self.device)
@@ -319,6 +343,7 @@ class Alg1Engine:
             pass
         torch.cuda.current_stream(self.device).wait_stream(s)
         with torch.cuda.graph(g):
+            self.compact_active()
             for _ in range(n):
                 self.iterate(2)
         self._graph, self._graph_n = g, n
@@ -353,12 +378,14 @@ class Alg1Engine:
             if use_graph and n == chunk:
                 if self._graph is None or self._graph_n != chunk:
                     self._capture(chunk)
-                self._graph.replay()
+                self._graph.replay()  # compacts the work list, then n iterations
             else:
+                self.compact_active()
                 for _ in range(n):
                     self.iterate(2)
             done += n
             since_check += n
+        self._restore_order()
         return done
 
     # ------------------------------------------------------------ host transfer

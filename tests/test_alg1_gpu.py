@@ -400,3 +400,36 @@ def test_tail_split_matches_unsplit_batch(golden):
     assert rel(hs[:, :, :2], hu[:, :, :2]) < 1e-10
     assert rel(xs, xu) < 1e-10
     np.testing.assert_array_equal(xs[:slots], xu[:slots])  # members of the full round: bitwise
+
+
+def test_converged_members_leave_the_work_list(golden):
+    """run() compacts the persistent kernel's work list to the members still iterating: a tol > 0 batch above
+    the in-kernel-loop size gives the same results as the same batch run one launch per iteration without
+    a work list (members converge at different iterations)."""
+    from paper_2408_10731_b200 import _alg1
+
+    bs = basis_from(golden("flow3d_hist.npz"))
+    B = 200
+    batch = scenarios.flow3d_batch(20, range(B), basis=bs)
+    params = SingleParams(max_iter=150, tol=0.1)  # 77 of 200 members converge along the way
+    res = {}
+    for compact in (True, False):
+        eng = Alg1Engine(bs, np.stack([o.centers for o in batch.obstacles]), [o.shape.a for o in batch.obstacles],
+                         [o.shape.b for o in batch.obstacles], batch.bvals, batch.linear_terms(), params=params,
+                         layout="half", tail_split=False)
+        if not compact:
+            eng._state.order = None
+            eng._state.n_order = None
+        eng.cold_init()
+        eng.run(150, use_graph=compact, loop=False)
+        torch.cuda.synchronize()
+        res[compact] = (eng.xi.cpu().numpy(), eng.iteration.cpu().numpy(), eng.status.cpu().numpy())
+        if compact:
+            assert int(eng.n_order.item()) == B and np.array_equal(eng.order.cpu().numpy(), np.arange(B))
+    (xa, ia, sa), (xb, ib, sb) = res[True], res[False]
+    n_conv = int(((sa & _lib.TRO_CONVERGED) > 0).sum())
+    assert 0 < n_conv < B, n_conv  # some members converged early, some did not
+    np.testing.assert_array_equal(ia, ib)
+    np.testing.assert_array_equal(sa, sb)
+    np.testing.assert_array_equal(xa, xb)  # same kernel arithmetic per member, only the CTA assignment moved
+    assert _alg1.LOOP_MAX_MEMBERS < B
