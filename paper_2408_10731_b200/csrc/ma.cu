@@ -23,6 +23,9 @@
 
 namespace tro {
 
+#ifndef MA_MINB
+#define MA_MINB 2  // resident CTAs per SM the element kernel is compiled for (128 registers)
+#endif
 constexpr int kMaWarps = 8;
 constexpr int kMaMaxAgents = 32;
 constexpr int kMaMaxRing = 64;
@@ -63,7 +66,7 @@ __host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs
 }
 
 template <int M, int MODE>
-__global__ void __launch_bounds__(kMaWarps * 32, 2) ma_kernel(MaArgs A) {
+__global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     // MODE 0: iteration; 1: prime (sums of a given state: lambda in `state`, d / alpha / beta in
     // the export planes); 2: cold init (straight lines, angles, d = 1, lambda = 0) + sums;
     // 4: iteration whose QP step already ran (ma_qp_kernel wrote xi): the element pass alone
