@@ -445,7 +445,8 @@ def run_val(args):
         "config": {"workload": desc, "members": total, "n_obs": n_o, "n_p": 100,
                    "parallelism": f"trajectory-shard x{world}"},
         "roofline": {"bound": "fp64", "achieved": flops / world / step_s / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": flops / world / step_s / 1e12 / peak, "traffic": None,
+                     "frac": flops / world / step_s / 1e12 / peak,
+                     "traffic": traffic_for("val") if world == 1 else None,
                      "peak_source": "measured (tro_fp64_fma_probe, DFMA chains)", "kernel": "tro_validate_f64",
                      "avg_launch_ms": step_s * 1e3, "algorithmic_flops_per_launch": flops,
                      "note": "per-step time includes validate_batch's host-side argument setup (cached constants)"},
@@ -593,7 +594,8 @@ def run_mpc(args):
         "control_step_ms": step_s * 1e3 / MPC_STEPS,
         "paper_budget_ms": 40.0,
         "roofline": {"bound": "hbm", "achieved": bytes_launch / (it_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": bytes_launch / (it_ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": bytes_launch / (it_ms * 1e-3) / 1e9 / peak,
+                     "traffic": traffic_for("mpc") if world == 1 else None, "peak_source": peak_src,
                      "kernel": "alg1 fused AM iteration (incl. the per-step prime)",
                      "avg_launch_ms": it_ms, "algorithmic_bytes_per_launch": bytes_launch},
         "clocks": clk,

@@ -471,6 +471,12 @@ static int launch_mode(const Alg1Args& A, cudaStream_t st) {
 #ifndef TRO_TMA_S
 #define TRO_TMA_S 3
 #endif
+#ifndef TRO_TMA_S32
+#define TRO_TMA_S32 (TRO_TMA_S + 1)  // fp32 stages are half as large: one more keeps more bytes in flight
+#endif
+#ifndef TRO_TMA_G32
+#define TRO_TMA_G32 TRO_TMA_G
+#endif
 #ifndef TRO_TMA_DM_SPEC
 #define TRO_TMA_DM_SPEC 1  // steady-state iterations use the d_mode = 2 specialisation
 #endif
@@ -487,8 +493,8 @@ static int sm_count() {
 // persistent TMA-pipelined AM iteration (n_p == 100); returns 1 if it launched
 template <int DIM, typename T, int LAY>
 static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
-    constexpr int G = TRO_TMA_G;
-    constexpr int S = (sizeof(T) == 8 && DIM == 3) ? TRO_TMA_S : TRO_TMA_S + 1;
+    constexpr int G = sizeof(T) == 8 ? TRO_TMA_G : TRO_TMA_G32;
+    constexpr int S = (sizeof(T) == 8 && DIM == 3) ? TRO_TMA_S : TRO_TMA_S32;
     using C = TmaCfg<DIM, T, LAY, 100, G, S>;
     const TmaLayout L = tma_layout(C::kStageBytes, S, 100, A.d.m, DIM, A.d.n_obs, G, C::kConsumers);
     if (L.total * kTmaMinBlocks > 227 * 1024) return 0;
