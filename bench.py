@@ -426,6 +426,9 @@ def run_val(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     step_s = _max_over_ranks(a.elapsed_time(b) / 1e3 / args.steps, world)
+    for _ in range(args.warmup):  # the e2e path's own warm-up (pinned result buffer, copy stream)
+        MT.validate_batch(sc, t, xi=xi_pin, basis=basis)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     a.record()

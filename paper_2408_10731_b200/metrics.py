@@ -77,6 +77,18 @@ def _dev_array(x, dev):
     return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=dev)
 
 
+_PIPE_MIN_CHUNK = 16384  # members per chunk of the pipelined host-input path (a chunk still fills every SM)
+_PIPE_MAX_CHUNKS = 4
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev):
+    s = _COPY_STREAMS.get(str(dev))
+    if s is None:
+        s = _COPY_STREAMS[str(dev)] = torch.cuda.Stream(device=dev)
+    return s
+
+
 def validate_batch(scenario, t, *, xi=None, basis=None, pos=None, acc=None, desired=None, margin: float = 0.0,
                    device=None, return_device: bool = False) -> dict:
     """Metrics of B trajectories on the sample times ``t`` (n_p) against the raw scenario geometry.
@@ -94,10 +106,19 @@ def validate_batch(scenario, t, *, xi=None, basis=None, pos=None, acc=None, desi
     dim = int(scenario.dim)
     t = np.asarray(t, dtype=float)
     n_p = t.size
+    # coefficients in pinned host memory, results to the host: chunks whose upload (copy stream), validation
+    # and result download overlap; members are independent, so the results are those of one launch
+    n_chunks = 0
+    if (xi is not None and isinstance(xi, torch.Tensor) and xi.device.type == "cpu" and xi.is_pinned()
+            and xi.dtype == torch.float64 and xi.is_contiguous() and not return_device):
+        n_chunks = min(_PIPE_MAX_CHUNKS, int(xi.shape[0]) // _PIPE_MIN_CHUNK)
     if xi is not None:
         if basis is None:
             raise ValueError("coefficient input needs the basis")
-        xi_d = _dev_array(xi, dev)
+        if n_chunks >= 2:
+            xi_d = torch.empty(tuple(xi.shape), **f64)
+        else:
+            xi_d = _dev_array(xi, dev)
         if xi_d.ndim != 3 or xi_d.shape[1] != dim:
             raise ValueError("xi must be (B, dim, m)")
         B, m = int(xi_d.shape[0]), int(xi_d.shape[2])
@@ -129,15 +150,56 @@ def validate_batch(scenario, t, *, xi=None, basis=None, pos=None, acc=None, desi
     consts = _lib.ValConsts(P=P_(P), Pdd=P_(Pdd), t=P_(consts_t["t"]), centers=P_(consts_t["c"]) if n_o else None,
                             velocities=P_(consts_t["v"]) if n_o else None, shape_a=P_(consts_t["a"]) if n_o else None,
                             shape_b=P_(consts_t["b"]) if n_o else None, desired=P_(des), margin=float(margin))
-    io = _lib.ValIO(xi=P_(xi_d), pos=P_(pos_d), acc=P_(acc_d), out=out.data_ptr())
-    with torch.cuda.device(dev):
-        rc = lib.tro_validate_f64(ctypes.byref(dims), ctypes.byref(consts), ctypes.byref(io), _lib.stream_handle())
-    _lib.check(rc, "tro_validate_f64")
-    if return_device:
-        return {"out": out}
-    o = out.cpu().numpy()  # one device-to-host copy of the B x 5 results
+    if n_chunks >= 2:
+        o = _validate_pipelined(lib, dims, consts, xi, xi_d, out, des if per_member else None, n_chunks, dev)
+    else:
+        io = _lib.ValIO(xi=P_(xi_d), pos=P_(pos_d), acc=P_(acc_d), out=out.data_ptr())
+        with torch.cuda.device(dev):
+            rc = lib.tro_validate_f64(ctypes.byref(dims), ctypes.byref(consts), ctypes.byref(io),
+                                      _lib.stream_handle())
+        _lib.check(rc, "tro_validate_f64")
+        if return_device:
+            return {"out": out}
+        o = out.cpu().numpy()  # one device-to-host copy of the B x 5 results
     return {"smoothness": o[:, 0], "tracking": o[:, 1], "arc_length": o[:, 2], "worst": o[:, 3],
             "success": o[:, 3] <= 0.0, "min_clearance": o[:, 4]}
+
+
+def _validate_pipelined(lib, dims, consts, xi_host, xi_d, out, des_pm, n_chunks, dev):
+    """Chunked tro_validate_f64: chunk k's upload on a copy stream overlaps chunk k-1's validation and
+    result download (pinned host buffer) on the current stream."""
+    B = int(xi_host.shape[0])
+    per = xi_d[0].numel()
+    bounds = [(B * k // n_chunks, B * (k + 1) // n_chunks) for k in range(n_chunks)]
+    host = torch.empty((B, 5), dtype=torch.float64, pin_memory=True)
+    with torch.cuda.device(dev):
+        cur = torch.cuda.current_stream(dev)
+        cp = _copy_stream(dev)
+        cp.wait_stream(cur)  # the fresh device buffers are ordered on the current stream
+        xi_d.record_stream(cp)
+        ready = []
+        with torch.cuda.stream(cp):
+            for lo, hi in bounds:
+                xi_d[lo:hi].copy_(xi_host[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cp)
+                ready.append(ev)
+        base_xi, base_out = xi_d.data_ptr(), out.data_ptr()
+        for (lo, hi), ev in zip(bounds, ready):
+            cur.wait_event(ev)
+            d = _lib.ValDims(n_members=hi - lo, n_obs=dims.n_obs, n_p=dims.n_p, m=dims.m, dim=dims.dim,
+                             per_member_desired=dims.per_member_desired, reserved=0)
+            c = consts
+            if des_pm is not None:  # per-member desired rows follow the chunk
+                c = _lib.ValConsts(P=consts.P, Pdd=consts.Pdd, t=consts.t, centers=consts.centers,
+                                   velocities=consts.velocities, shape_a=consts.shape_a, shape_b=consts.shape_b,
+                                   desired=des_pm[lo].data_ptr(), margin=consts.margin)
+            io = _lib.ValIO(xi=base_xi + lo * per * 8, pos=None, acc=None, out=base_out + lo * 5 * 8)
+            rc = lib.tro_validate_f64(ctypes.byref(d), ctypes.byref(c), ctypes.byref(io), cur.cuda_stream)
+            _lib.check(rc, "tro_validate_f64")
+            host[lo:hi].copy_(out[lo:hi], non_blocking=True)
+        cur.synchronize()
+    return host.numpy()
 
 
 def _one(trajectory, scenario, desired=None, margin=0.0) -> dict:

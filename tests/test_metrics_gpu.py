@@ -102,3 +102,27 @@ def test_large_batch_matches_oracle_on_a_sample():
         ref = OMT.metrics(pos[i], acc[i], t, c, v, a, b, 3, des, 0.05)
         got = [r["smoothness"][i], r["tracking"][i], r["arc_length"][i], r["worst"][i], r["min_clearance"][i]]
         assert rel(got, ref) <= 1e-12, i
+
+
+@pytest.mark.parametrize("per_member_desired", [False, True])
+def test_pinned_host_input_pipelined_matches_one_launch(golden, per_member_desired):
+    """Coefficients in pinned host memory take the chunked upload/validate/download path (metrics.py
+    _validate_pipelined): bitwise the results of one launch over device-resident coefficients."""
+    import torch
+
+    g = golden("metrics.npz")
+    sc, bs = scene(g, "s3", 3), basis_of(g, "s3")
+    xi0 = g["s3_xi"]
+    B = 3 * MT._PIPE_MIN_CHUNK + 17  # 3 ragged chunks
+    rng = np.random.default_rng(5)
+    xi = xi0[rng.integers(0, xi0.shape[0], B)] + rng.normal(scale=0.05, size=(B,) + xi0.shape[1:])
+    des = g["s3_desired"]
+    if per_member_desired:
+        des = des[None] + rng.normal(scale=0.1, size=(B,) + des.shape)
+    xi_pin = torch.as_tensor(xi).pin_memory()
+    r = MT.validate_batch(sc, g["s3_t"], xi=xi_pin, basis=bs, desired=des, margin=0.05)
+    ref = MT.validate_batch(sc, g["s3_t"], xi=torch.as_tensor(xi, device="cuda"), basis=bs, desired=des,
+                            margin=0.05, return_device=True)["out"].cpu().numpy()
+    got = np.stack([r["smoothness"], r["tracking"], r["arc_length"], r["worst"], r["min_clearance"]], axis=1)
+    np.testing.assert_array_equal(got, ref)
+    np.testing.assert_array_equal(r["success"], ref[:, 3] <= 0.0)
