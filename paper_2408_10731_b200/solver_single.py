@@ -187,17 +187,42 @@ def _upload(eng: Alg1Engine, state: SingleState):
                    rho_o=[state.rho_o], iteration=[state.iteration])
 
 
-def _download(eng: Alg1Engine, into: SingleState | None = None) -> SingleState:
+_SCALARS = ("status", "level", "n_changes", "iteration", "n_hist", "rho", "rho_o", "res_norm", "res_max")
+
+
+def _snapshot(eng: Alg1Engine) -> dict:
+    """Member 0's state, bookkeeping scalars and residual history in ONE device-to-host copy (one sync
+    instead of one per field); integer scalars travel as exact fp64."""
+    parts = [("xi", eng.xi[0])]
+    if eng.n_o:
+        parts += [("lam", eng.lam[:, 0]), ("alpha", eng.alpha[0]), ("beta", eng.beta[0] if eng.dim == 3 else None),
+                  ("d", eng.d[0] if eng.d is not None else None), ("copies", eng.copies[:, 0])]
+    parts.append(("scal", torch.stack([getattr(eng, k)[0].double() for k in _SCALARS])))
+    if eng.hist is not None:
+        parts.append(("hist", eng.hist[0]))
+    parts = [(k, t) for k, t in parts if t is not None]
+    flat = torch.cat([t.reshape(-1).double() for _, t in parts]).cpu().numpy()
+    out, o = {}, 0
+    for k, t in parts:
+        out[k] = flat[o:o + t.numel()].reshape(tuple(t.shape))
+        o += t.numel()
+    for j, k in enumerate(_SCALARS):
+        out[k] = float(out["scal"][j])
+    return out
+
+
+def _download(eng: Alg1Engine, into: SingleState | None = None, snap: dict | None = None) -> SingleState:
     """Member 0 of a device engine -> numpy SingleState (copies exported by the last iteration)."""
     dim, n_o, n_p = eng.dim, eng.n_o, eng.n_p
-    f = lambda t: t[0].double().cpu().numpy().copy() if t is not None else None  # noqa: E731
-    xi = eng.xi[0].cpu().numpy().copy()
+    snap = snap if snap is not None else _snapshot(eng)
+    f = lambda k: snap[k].copy() if k in snap else None  # noqa: E731
+    xi = f("xi")
     if n_o:
-        lam = eng.lam[:, 0].double().cpu().numpy()
-        alpha = f(eng.alpha)
-        beta = f(eng.beta) if dim == 3 else None
-        d = f(eng.d)
-        cop = eng.copies[:, 0].double().cpu().numpy()
+        lam = snap["lam"]
+        alpha = f("alpha")
+        beta = f("beta") if dim == 3 else None
+        d = f("d")
+        cop = snap["copies"]
         lam_pos = lam[:dim].copy()
         lca, lsa = lam[dim].copy(), lam[dim + 1].copy()
         lcb = lam[dim + 2].copy() if dim == 3 else None
@@ -216,13 +241,17 @@ def _download(eng: Alg1Engine, into: SingleState | None = None) -> SingleState:
     st.xi, st.d, st.alpha, st.beta = xi, d, alpha, beta
     st.cos_a, st.sin_a, st.cos_b, st.sin_b = ca, sa, cb, sb
     st.lam_pos, st.lam_cos_a, st.lam_sin_a, st.lam_cos_b, st.lam_sin_b = lam_pos, lca, lsa, lcb, lsb
-    st.rho = float(eng.rho[0].item())
-    st.rho_o = float(eng.rho_o[0].item())
-    st.iteration = int(eng.iteration[0].item())
+    st.rho = snap["rho"]
+    st.rho_o = snap["rho_o"]
+    st.iteration = int(snap["iteration"])
     return st
 
 
-def _raise_if_failed(eng: Alg1Engine):
+def _raise_if_failed(eng: Alg1Engine, snap: dict | None = None):
+    if snap is not None and eng.B == 1:  # member 0 is the batch
+        if int(snap["status"]) & _lib.TRO_FACTOR_FAILED:
+            raise eng.table.error_for(int(snap["level"]))
+        return
     st = eng.status.cpu().numpy()
     bad = np.nonzero(st & _lib.TRO_FACTOR_FAILED)[0]
     if bad.size:
@@ -243,10 +272,10 @@ def init_state(problem: SingleProblem, seed: int | None = None, params: SinglePa
     return st
 
 
-def _factor_bookkeeping(state: SingleState, eng: Alg1Engine) -> int:
+def _factor_bookkeeping(state: SingleState, eng: Alg1Engine, snap: dict | None = None) -> int:
     """New factorizations the reference would have performed in this call (solver_single.py:198-202)."""
     fresh = 1 if (state._factor is None or state._factor_rho_o != state.rho_o) else 0
-    return fresh + int(eng.n_changes[0].item())
+    return fresh + int(snap["n_changes"] if snap is not None else eng.n_changes[0].item())
 
 
 def am_iteration(state: SingleState, problem: SingleProblem) -> SingleState:
@@ -286,21 +315,22 @@ def solve_single(problem: SingleProblem, params: SingleParams | None = None,
         eng.prime(1)
     ran = eng.run(params.max_iter, use_graph=params.max_iter > 50, chunk=25,
                   check_every=50 if params.max_iter > 50 else 0)
-    _raise_if_failed(eng)
-    new = _factor_bookkeeping(state, eng) if ran > 0 else 0
+    snap = _snapshot(eng)
+    _raise_if_failed(eng, snap)
+    new = _factor_bookkeeping(state, eng, snap) if ran > 0 else 0
     if ran > 0 or state.xi is None:
-        _download(eng, into=state)
+        _download(eng, into=state, snap=snap)
     if new:
         qpcore._bump(new)
     state.n_factorizations += new
-    lv = int(eng.level[0].item())
+    lv = int(snap["level"])
     state._factor = eng.table.factors[lv]
     state._factor_rho_o = state.rho_o
 
-    nh = int(eng.n_hist[0].item())
-    hist = eng.hist[0, :nh].cpu().numpy() if eng.hist is not None else np.zeros((0, 3))
+    nh = int(snap["n_hist"])
+    hist = snap["hist"][:nh] if "hist" in snap else np.zeros((0, 3))
     history = [{"norm": float(h[0]), "max_abs": float(h[1]), "rho_o": float(h[2])} for h in hist]
-    converged = bool(eng.status[0].item() & _lib.TRO_CONVERGED)
+    converged = bool(int(snap["status"]) & _lib.TRO_CONVERGED)
     basis = problem.basis
     traj = Trajectory(t=basis.grid.timestamps, pos=basis.P @ state.xi.T, vel=basis.Pdot @ state.xi.T,
                       acc=basis.Pddot @ state.xi.T)
@@ -308,8 +338,8 @@ def solve_single(problem: SingleProblem, params: SingleParams | None = None,
         trajectory=traj,
         converged=converged,
         iterations=state.iteration,
-        residual_norm=float(eng.res_norm[0].item()),
-        residual_max=float(eng.res_max[0].item()),
+        residual_norm=snap["res_norm"],
+        residual_max=snap["res_max"],
         residual_history=history,
         smoothness_cost=float(np.sum(traj.acc**2)),
         tracking_cost=float(np.sum((traj.pos - problem.desired) ** 2)),
