@@ -364,6 +364,14 @@ def _draw_z(rng, n: int, d: int) -> np.ndarray:
     return rng.standard_normal((n, d))
 
 
+def _z_round(z, dev):
+    """One round's standard normals on the device: pinned host rows upload asynchronously (the host does
+    not wait for the previous round's kernels before queueing this round)."""
+    if isinstance(z, torch.Tensor) and z.device.type == "cpu" and z.is_pinned():
+        return z.to(device=dev, dtype=torch.float64, non_blocking=True).contiguous()
+    return torch.as_tensor(z, device=dev).contiguous()
+
+
 def priest_optimize(setup: ProjectionSetup, c1, distribution: SamplingDistribution,
                     params: PriestParams | None = None, *, z_rounds=None) -> PriestResult:
     """Projection-guided sampling loop (solver_priest.py:336-382), one device pass per round.
@@ -386,7 +394,7 @@ def priest_optimize(setup: ProjectionSetup, c1, distribution: SamplingDistributi
         d["L"].copy_(torch.as_tensor(_draw_factor(sig_h)))
         d["mu"].copy_(mu)
         if z_rounds is not None:
-            z = torch.as_tensor(z_rounds[r], device=dev).contiguous()
+            z = _z_round(z_rounds[r], dev)
         else:
             z = torch.as_tensor(_draw_z(rng, params.n_batch, dm), device=dev)
         xi, scores, _, smp = _run_project(setup, z=z, n_inner=params.n_inner, keep_samples=True)
@@ -567,7 +575,7 @@ def priest_optimize_sharded(setup: ProjectionSetup, c1, distribution: SamplingDi
         d["L"].copy_(torch.as_tensor(_draw_factor(sig_h)))
         d["mu"].copy_(mu)
         if z_rounds is not None:
-            z = torch.as_tensor(z_rounds[r][lo:hi], device=dev).contiguous()
+            z = _z_round(z_rounds[r][lo:hi], dev)
         else:  # every rank draws the whole round (the shared stream) and keeps its rows
             z = torch.as_tensor(_draw_z(rng, params.n_batch, mu.numel())[lo:hi], device=dev).contiguous()
         mine = rnd.local(z, lo)
