@@ -212,3 +212,21 @@ def test_sharded_rounds_are_bitwise_the_single_gpu_rounds(golden, n_ce):
     np.testing.assert_array_equal(one.mu, ref.mu)
     np.testing.assert_array_equal(one.best.projected, ref.best.projected)
     np.testing.assert_array_equal(one.best.original, ref.best.original)
+
+
+def test_pinned_host_normals_match_device_normals(golden):
+    """z_rounds from pinned host memory (asynchronous per-round upload, solver_priest._z_round), from
+    numpy and from the device give the same rounds bit for bit."""
+    g = golden("priest.npz")
+    st = setup_from(g, "p3")
+    dist = SP.SamplingDistribution(g["p3_mu0"], g["p3_sigma0"])
+    params = SP.PriestParams(n_outer=3, n_batch=96, n_constraint_elite=48, n_elite=12, n_inner=30, seed=0)
+    c1 = SP.BarnCost(np.zeros(3), np.array([12.0, 0.0, 0.0]))
+    z = np.random.default_rng(7).standard_normal((params.n_outer, params.n_batch, dist.mu.size))
+    runs = [SP.priest_optimize(st, c1, dist, params, z_rounds=zr)
+            for zr in (torch.as_tensor(z, device="cuda"), torch.as_tensor(z).pin_memory(), z)]
+    for r in runs[1:]:
+        np.testing.assert_array_equal(r.mu, runs[0].mu)
+        np.testing.assert_array_equal(r.sigma_mat, runs[0].sigma_mat)
+        np.testing.assert_array_equal(r.best.projected, runs[0].best.projected)
+        assert r.history == runs[0].history
