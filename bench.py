@@ -1011,7 +1011,7 @@ def run_b200(args):
     from paper_2408_10731_b200 import scenarios
     from paper_2408_10731_b200.basis import build_basis
     from paper_2408_10731_b200.distributed import gather_summaries, shard_range, shard_summary
-    from paper_2408_10731_b200.solver_single import SingleParams, make_batch_engine
+    from paper_2408_10731_b200.solver_single import SingleBatch, SingleParams, make_batch_engine
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -1029,8 +1029,6 @@ def run_b200(args):
 
     basis = build_basis(0.0, 10.0, 100, 10)
     if args.config == "c1":
-        from paper_2408_10731_b200.solver_single import SingleBatch
-
         batch = SingleBatch.from_problems([scenarios.c1_problem()])
     else:
         batch = scenarios.flow3d_batch(n_o, range(lo, hi), basis=basis)
@@ -1039,9 +1037,7 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
 
     def solve_device():
-        eng.reset_schedule()
-        eng.level.copy_(eng.level0)
-        eng.cold_init()
+        eng.cold_init()  # complete cold start on the device: rho, rho_o, level, iteration, schedule reset
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -1101,37 +1097,56 @@ def run_b200(args):
             prof = json.load(fh)
         traffic = prof.get("dram_bytes_per_element_launch", 0) * B * n_o * 100 or None
 
-    # e2e through the public API with host buffers
+    # the last timed solve must be a cold solve: its first members equal a fresh engine's solve bitwise
+    # (members are independent and run whole on one CTA; the fresh engine has no tail split)
+    n_chk = min(B, 512)
+    xi_last = eng.xi[:n_chk].clone()
+    res_last = eng.res_max[:n_chk].clone()
+    chk_batch = (SingleBatch.from_problems([scenarios.c1_problem()]) if args.config == "c1"
+                 else scenarios.flow3d_batch(n_o, range(lo, lo + n_chk), basis=basis))
+    chk = make_batch_engine(chk_batch, params, dtype=dtype, groups=args.groups, layout=args.layout,
+                            tail_split=False)
+    chk.cold_init()
+    chk.run(n_iter, use_graph=True)
+    fresh_equal = bool(torch.equal(chk.xi, xi_last) and torch.equal(chk.res_max, res_last))
+    del chk
+    torch.cuda.empty_cache()
+    if not fresh_equal:
+        raise SystemExit("bench: the last timed solve differs from a fresh-engine solve (stale state)")
+
+    # e2e through the public API (solve_single_batch) with host numpy in and out: each step uploads the
+    # members' boundary values, computes the linear terms on the device, cold-starts, runs the AM loop and
+    # copies every per-member result back (xi, residuals, rho_o, flags, counters) in one D2H copy
     e2e = None
     if not args.no_e2e:
-        bv_host = torch.as_tensor(batch.bvals, dtype=torch.float64).pin_memory()
-        q_host = torch.as_tensor(batch.linear_terms(), dtype=torch.float64).pin_memory()
-        xi_host = torch.empty(eng.xi.shape, dtype=torch.float64).pin_memory()
-        res_host = torch.empty((2, B), dtype=torch.float64).pin_memory()
-        st_host = torch.empty(B, dtype=torch.int32).pin_memory()  # same dtype: a plain async D2H copy
-        h2d = (bv_host.numel() + q_host.numel()) * 8
-        d2h = (xi_host.numel() + res_host.numel()) * 8 + st_host.numel() * 4
+        from paper_2408_10731_b200.solver_single import solve_single_batch
+
+        host_batch = SingleBatch(batch.basis, np.ascontiguousarray(batch.bvals), list(batch.obstacles),
+                                 batch.desired, batch.w_smooth, batch.w_track)
+        res = solve_single_batch(host_batch, params, engine=eng, use_graph=True).numpy()  # warm (graph built)
+        h2d = host_batch.bvals.nbytes
+        d2h = B * (eng.xi[0].numel() + 6) * 8
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
         a.record(stream)
         for _ in range(args.steps):
-            eng.bvals.copy_(bv_host, non_blocking=True)
-            eng.q.copy_(q_host, non_blocking=True)
-            solve_device()
-            xi_host.copy_(eng.xi, non_blocking=True)
-            res_host[0].copy_(eng.res_max, non_blocking=True)
-            res_host[1].copy_(eng.res_norm, non_blocking=True)
-            st_host.copy_(eng.status, non_blocking=True)
+            res = solve_single_batch(host_batch, params, engine=eng, use_graph=True).numpy()
         b.record(stream)
         torch.cuda.synchronize()
+        wall_e2e = time.perf_counter() - w0
         te = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        if not np.array_equal(res.xi[:n_chk], xi_last.cpu().numpy()):
+            raise SystemExit("bench: the public-API solve differs from the device-timed solve")
         e2e = {"value": members_total * n_iter * args.steps / float(te.item()), "unit": "traj-it/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "api": "solver_single.solve_single_batch(SingleBatch numpy in, engine=cached).numpy()",
+               "wall_s": wall_e2e}
         if args.config == "c1" and world == 1:
             # C1 is the reference's single-problem case: the call a user makes is solve_single (numpy in,
             # SingleSolution out: trajectory, histories, state), timed on the stream around the call
@@ -1324,8 +1339,31 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return int(sk.getsockname()[1])
+
+
+def _spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under torch.distributed.run with one rank
+    per GPU (NCCL over NVLink; rendezvous on 127.0.0.1) and return its exit code."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the NCCL init lines (transport, NVLS) land on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        raise SystemExit(_spawn_ranks(args.gpus))
+    if world and world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but the launcher started {world} ranks")
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "c4":

@@ -74,6 +74,11 @@ typedef struct tro_alg1_consts {
     const double* bvals;     /* B x dim x n_eq boundary values */
     const double* line_u;    /* m: lstsq(P, 1)      straight-line init xi = u p0 + v (p1 - p0) */
     const double* line_v;    /* m: lstsq(P, tau)    (basis.py:207-217, used by tro_alg1_init) */
+    const int32_t* level0;   /* B: each member's cold-start level (the K^-1 table entry built at rho_start).
+                                Non-NULL: tro_alg1_init is a complete cold start (solver_single.py:115-166):
+                                it also sets rho = rho_o = level_rho[level0[i]], level = level0[i] and zeroes
+                                iteration, last_change, n_hist, n_changes, status and the stall ring.
+                                NULL: tro_alg1_init leaves that bookkeeping to the caller (the MPC fleet). */
 } tro_alg1_consts;
 
 typedef struct tro_alg1_params {
@@ -146,6 +151,14 @@ int tro_alg1_iterate(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_co
  * pipeline fills; large batches keep the TMA-pipelined tro_alg1_iterate. */
 int tro_alg1_iterate_n(int32_t dtype, const tro_alg1_dims* dims, const tro_alg1_consts* c,
                        const tro_alg1_state* s, const tro_alg1_params* p, int32_t n_iter, void* stream);
+
+/* Per-member linear cost terms q = -2 w_track (P' desired_i)' (solver_single.py:173), B x dim x m, on the
+ * device.  desired: B x n_p x dim member paths, or NULL for each member's straight start -> goal line
+ * desired[t] = p0 + frac[t] (p1 - p0) with p0 = bvals[i][ax][0], p1 = bvals[i][ax][3] (bench/runner.py:88-94;
+ * frac = linspace(0, 1, n_p), bitwise numpy's line).  The sum over samples runs in sample order. */
+int tro_alg1_linear_terms(int64_t n_members, int32_t n_p, int32_t m, int32_t dim, int32_t n_eq, const double* P,
+                          const double* frac, const double* bvals, const double* desired, double w_track, double* q,
+                          void* stream);
 
 /* ------------------------------------------------------------------ PRIEST / CEM (Alg. 3) */
 typedef struct tro_priest_dims {

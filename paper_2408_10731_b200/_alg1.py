@@ -98,7 +98,7 @@ class LevelTable:
 class Alg1Engine:
     """B members on one device.  All per-member inputs may be numpy or torch."""
 
-    def __init__(self, basis: BasisSet, tracks, shape_a, shape_b, bvals, q, *, params, rho0=None,
+    def __init__(self, basis: BasisSet, tracks, shape_a, shape_b, bvals, q=None, *, params, desired=None, rho0=None,
                  w_smooth: float = 1.0, w_track: float = 1.0, dtype=torch.float64, device=None, groups: int = 0,
                  max_hist: int = 0, export: bool = False, keep_d: bool = False, cond_limit: float = 1e12,
                  use_tma: bool = True, layout: str = "angle", tail_split: bool = True):
@@ -137,9 +137,15 @@ class Alg1Engine:
         self.kinv = torch.as_tensor(self.table.kinv, **f64).contiguous()
         self.level_rho = torch.as_tensor(np.asarray(self.table.rhos), **f64)
         self.level_ok = torch.as_tensor(self.table.ok, **i32)
-        self.q = torch.as_tensor(q, **f64).reshape(B, dim, m).contiguous()
         self.bvals = torch.as_tensor(bvals, **f64).reshape(B, dim, -1).contiguous()
         self.n_eq = int(self.bvals.shape[2])
+        self.w_track = float(w_track)
+        self.frac = torch.as_tensor(np.linspace(0.0, 1.0, n_p), **f64)
+        self.q = torch.empty((B, dim, m), **f64)
+        if q is not None:
+            self.q.copy_(torch.as_tensor(q, **f64).reshape(B, dim, m))
+        else:
+            self.compute_linear_terms(desired)
         u, v = line_basis_vectors(basis)
         self.line_u = torch.as_tensor(u, **f64)
         self.line_v = torch.as_tensor(v, **f64)
@@ -188,7 +194,7 @@ class Alg1Engine:
         self._consts = _lib.Alg1Consts(
             self.P.data_ptr(), self.tracks.data_ptr(), self.shape_a.data_ptr(), self.shape_b.data_ptr(),
             self.kinv.data_ptr(), self.level_rho.data_ptr(), self.level_ok.data_ptr(), self.q.data_ptr(),
-            self.bvals.data_ptr(), self.line_u.data_ptr(), self.line_v.data_ptr())
+            self.bvals.data_ptr(), self.line_u.data_ptr(), self.line_v.data_ptr(), self.level0.data_ptr())
         p = _lib.ptr
         self._state = _lib.Alg1State(
             p(self.state), p(self.d), p(self.copies), p(self.xi), p(self.pos),
@@ -209,6 +215,28 @@ class Alg1Engine:
         self._graph_n = 0
         # TMA-pipelined persistent kernel for the iteration unless disabled (flags bit 2)
         self.base_flags = 0 if use_tma else _lib.TRO_FLAG_NO_TMA
+
+    def compute_linear_terms(self, desired=None):
+        """q = -2 w_track (P' desired_i)' on the device (tro_alg1_linear_terms, solver_single.py:173);
+        desired None: each member's straight start -> goal line from the current bvals."""
+        des = None
+        if desired is not None:
+            des = torch.as_tensor(desired, dtype=torch.float64, device=self.device).reshape(
+                self.B, self.n_p, self.dim).contiguous()
+        with torch.cuda.device(self.device):
+            rc = self.lib.tro_alg1_linear_terms(self.B, self.n_p, self.m, self.dim, self.n_eq, self.P.data_ptr(),
+                                                self.frac.data_ptr(), self.bvals.data_ptr(), _lib.ptr(des),
+                                                self.w_track, self.q.data_ptr(), _lib.stream_handle())
+        _lib.check(rc, "tro_alg1_linear_terms")
+
+    def set_members(self, bvals, desired=None):
+        """New members' boundary values (and desired paths; None = straight lines) for the next cold solve on
+        this engine (same obstacles, basis and batch size)."""
+        bv = torch.as_tensor(bvals, dtype=torch.float64)
+        if tuple(bv.shape) != tuple(self.bvals.shape):
+            raise ValueError(f"boundary values must be {tuple(self.bvals.shape)}, got {tuple(bv.shape)}")
+        self.bvals.copy_(bv, non_blocking=bv.is_pinned())
+        self.compute_linear_terms(desired)
 
     # ------------------------------------------------------------ angle views
     @staticmethod
@@ -284,7 +312,9 @@ class Alg1Engine:
         _lib.check(rc, name)
 
     def cold_init(self):
-        """init_state (solver_single.py:115-166) for every member, on device; d == 1."""
+        """init_state (solver_single.py:115-166) for every member, on device; d == 1.  A complete cold start:
+        the launch also resets rho, rho_o, level, iteration and the solve-local schedule to rho_start
+        (unless the engine's consts.level0 is NULL, as in the MPC fleet)."""
         self._call("tro_alg1_init", 0)
         self.first_d_mode = 0
 

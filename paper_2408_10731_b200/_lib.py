@@ -33,6 +33,7 @@ EXPORTS = (
     "tro_alg1_init",
     "tro_alg1_iterate",
     "tro_alg1_iterate_n",
+    "tro_alg1_linear_terms",
     "tro_kkt_apply_f64",
     "tro_topk_stable_f64",
     "tro_topk_workspace_bytes",
@@ -80,6 +81,7 @@ class Alg1Consts(ctypes.Structure):
         ("bvals", c_void_p),
         ("line_u", c_void_p),
         ("line_v", c_void_p),
+        ("level0", c_void_p),
     ]
 
 
@@ -257,6 +259,9 @@ def load() -> ctypes.CDLL:
         f.restype = c_int32
     lib.tro_alg1_iterate_n.argtypes = [c_int32] + sig[:4] + [c_int32, c_void_p]
     lib.tro_alg1_iterate_n.restype = c_int32
+    lib.tro_alg1_linear_terms.argtypes = [c_int64, c_int32, c_int32, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_double, c_void_p, c_void_p]
+    lib.tro_alg1_linear_terms.restype = c_int32
     lib.tro_kkt_apply_f64.argtypes = [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p]
     lib.tro_kkt_apply_f64.restype = c_int32
     lib.tro_topk_stable_f64.argtypes = [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_int64, c_void_p]

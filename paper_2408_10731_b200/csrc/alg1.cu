@@ -252,6 +252,22 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         // positions of the current xi; d recompute (d_mode 2) uses these too
         double* xg = A.s.xi + (int64_t)i * DIM * m;
         if constexpr (init) {
+            if (tid == 0 && A.c.level0) {
+                // complete cold start (init_state, solver_single.py:115-166 + the solve-local bookkeeping
+                // solve_single starts from, :407-418): penalties back to rho_start, counters and ring zeroed
+                const int lv = A.c.level0[i];
+                const double r0 = A.c.level_rho[lv];
+                A.s.level[i] = lv;
+                A.s.rho[i] = r0;
+                A.s.rho_o[i] = r0;
+                A.s.iteration[i] = 0;
+                A.s.last_change[i] = 0;
+                A.s.n_hist[i] = 0;
+                A.s.n_changes[i] = 0;
+                A.s.status[i] = 0;
+                const int w2 = 2 * A.p.stall_window;
+                for (int k = 0; k < w2; ++k) A.s.ring[(int64_t)i * w2 + k] = 0.0;
+            }
             // straight-line coefficients (solver_single.py:127, basis.py:207-217)
             const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
             for (int k = tid; k < DIM * m; k += nthr) {
@@ -649,5 +665,46 @@ extern "C" int tro_fastmath_eval(int32_t fn, const double* x, const double* y, i
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     tro::fastmath_eval_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(fn, x, y, n, out);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- per-member linear terms
+namespace tro {
+// q[i][ax][c] = (-2 w_track) * sum_t P[t][c] * desired_i[t][ax]  (solver_single.py:173), the sum in sample
+// order.  desired == NULL: each member's straight start -> goal line (bench/runner.py:88-94)
+// desired[t] = p0 + frac[t] * (p1 - p0), each operation explicitly rounded, so the line is bitwise numpy's.
+__global__ void alg1_linear_terms_kernel(int64_t B, int n_p, int m, int dim, int ne, const double* __restrict__ P,
+                                         const double* __restrict__ frac, const double* __restrict__ bvals,
+                                         const double* __restrict__ desired, double scale, double* __restrict__ q) {
+    const int64_t n = B * dim * m;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = k / (dim * m);
+        const int r = (int)(k - i * dim * m);
+        const int ax = r / m, c = r - ax * m;
+        double acc = 0.0;
+        if (desired) {
+            const double* dp = desired + i * n_p * dim + ax;
+            for (int t = 0; t < n_p; ++t) acc = fma(P[t * m + c], dp[(int64_t)t * dim], acc);
+        } else {
+            const double p0 = bvals[(i * dim + ax) * ne + 0], p1 = bvals[(i * dim + ax) * ne + 3];
+            const double dl = __dsub_rn(p1, p0);
+            for (int t = 0; t < n_p; ++t) acc = fma(P[t * m + c], __dadd_rn(p0, __dmul_rn(frac[t], dl)), acc);
+        }
+        q[k] = scale * acc;
+    }
+}
+}  // namespace tro
+
+extern "C" int tro_alg1_linear_terms(int64_t n_members, int32_t n_p, int32_t m, int32_t dim, int32_t n_eq,
+                                     const double* P, const double* frac, const double* bvals, const double* desired,
+                                     double w_track, double* q, void* stream) {
+    if (n_members < 0 || n_p < 1 || m < 1 || (dim != 2 && dim != 3) || n_eq < 4 || !P || !q) return TRO_EINVAL;
+    if (!desired && (!frac || !bvals)) return TRO_EINVAL;
+    if (n_members == 0) return 0;
+    const int64_t n = n_members * dim * m;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    tro::alg1_linear_terms_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        n_members, n_p, m, dim, n_eq, P, frac, bvals, desired, -2.0 * w_track, q);
     return (int)cudaGetLastError();
 }

@@ -10,6 +10,7 @@ NVLink/NVSwitch on a B200 box, gloo in the CPU tests).
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -47,13 +48,66 @@ def merge_summaries(parts: list[torch.Tensor]) -> dict:
     return {"best_residual_max": best, "best_member": best_idx, "converged": conv, "members": members}
 
 
-def gather_summaries(summary: torch.Tensor) -> dict:
-    """All-gather the per-shard summaries (one tiny collective per solve) and merge them."""
-    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+def gather_summaries(summary: torch.Tensor, group=None) -> dict:
+    """All-gather the per-shard summaries (one tiny collective per solve) and merge them.  NCCL gathers the
+    device tensor; gloo (CPU tests, or ranks sharing one GPU) gathers a host copy."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return merge_summaries([summary])
-    out = [torch.empty_like(summary) for _ in range(dist.get_world_size())]
-    dist.all_gather(out, summary)
+    if dist.get_backend(group) != "nccl":
+        summary = summary.cpu()
+    out = [torch.empty_like(summary) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, summary, group=group)
     return merge_summaries(out)
+
+
+def _world(group=None) -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def shard_batch(batch, rank: int, world: int):
+    """This rank's contiguous member range of a solver_single.SingleBatch (shared basis and obstacles)."""
+    from .solver_single import SingleBatch
+
+    lo, hi = shard_range(batch.B, rank, world)
+    des = None if batch.desired is None else np.asarray(batch.desired)[lo:hi]
+    return lo, hi, SingleBatch(batch.basis, np.asarray(batch.bvals)[lo:hi], list(batch.obstacles), des,
+                               batch.w_smooth, batch.w_track)
+
+
+def solve_single_batch_sharded(batch, params=None, *, group=None, gather_results: bool = False, solve=None, **kw):
+    """solve_single_batch over all ranks of `group` (one process per GPU): rank r solves members
+    [shard_range(B, r, world)) with NO per-iteration communication (members are independent,
+    solver_single.py:407-450), then ONE all-gather of the per-shard summaries.
+
+    Returns (local BatchResult, merged summary, full results or None).  gather_results=True also
+    all-gathers every rank's per-member results (xi, residuals, counters) into member order, which the
+    bitwise shard-vs-single tests use; `solve` substitutes the per-shard solve (host-logic tests)."""
+    from .solver_single import solve_single_batch
+
+    rank, world = _world(group)
+    if batch.B < world:
+        raise ValueError("fewer members than ranks")
+    lo, hi, sub = shard_batch(batch, rank, world)
+    sol = (solve or solve_single_batch)(sub, params, **kw)
+    local = sol.numpy()
+    dev = sol.residual_max.device
+    summary = shard_summary(torch.as_tensor(local.residual_max, device=dev),
+                            torch.as_tensor(local.residual_norm, device=dev),
+                            torch.as_tensor(local.converged, device=dev), lo)
+    merged = gather_summaries(summary, group)
+    full = None
+    if gather_results:
+        parts = [None] * world
+        if world > 1:
+            dist.all_gather_object(parts, local, group=group)
+        else:
+            parts = [local]
+        full = {k: np.concatenate([getattr(p, k) for p in parts])
+                for k in ("xi", "residual_norm", "residual_max", "rho_o", "converged", "iterations",
+                          "n_factorizations")}
+    return local, merged, full
 
 
 # ------------------------------------------------------------------ Alg. 2 (batch-global rho)

@@ -147,6 +147,9 @@ class MpcFleet:
         self.params = params or SingleParams(max_iter=self.step_budget)
         self.eng = Alg1Engine(basis, tracks0, pa, pb, bvals, np.zeros((B, dim, self.m)), params=self.params,
                               layout=layout, device=dev)
+        # the fleet owns its solve-local bookkeeping (tro_mpc_advance resets it per control step and freezes
+        # finished robots through status): the init launch must not reset it
+        self.eng._consts.level0 = None
         f64 = dict(dtype=torch.float64, device=dev)
         i32 = dict(dtype=torch.int32, device=dev)
         up = lambda x: torch.as_tensor(np.array(x, dtype=float, copy=True), **f64)  # noqa: E731

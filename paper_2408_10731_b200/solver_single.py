@@ -15,7 +15,11 @@ used at solve boundaries.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass, field
+
+import hashlib
+import threading
 
 import numpy as np
 import torch
@@ -32,6 +36,8 @@ __all__ = [
     "SingleSolution",
     "SingleBatch",
     "BatchSolution",
+    "BatchResult",
+    "make_batch_engine",
     "init_state",
     "am_iteration",
     "solve_single",
@@ -142,10 +148,16 @@ def _engine_for(problem: SingleProblem, params: SingleParams, *, rho0=None, expo
                 dtype=torch.float64) -> Alg1Engine:
     a, b = _shapes(problem)
     bvals = np.stack([bc.values() for bc in problem.boundary])[None]
-    q = _linear_term(problem.basis, problem.desired, problem.w_track)[None]
-    return Alg1Engine(problem.basis, _tracks(problem), a, b, bvals, q, params=params, rho0=rho0,
-                      w_smooth=problem.w_smooth, w_track=problem.w_track, dtype=dtype, max_hist=max_hist,
+    return Alg1Engine(problem.basis, _tracks(problem), a, b, bvals, desired=problem.desired[None], params=params,
+                      rho0=rho0, w_smooth=problem.w_smooth, w_track=problem.w_track, dtype=dtype, max_hist=max_hist,
                       export=export, keep_d=True)
+
+
+def _owner_key():
+    """Cached engines are single-owner: one per (thread, device, stream), so concurrent solver
+    calls from different threads or streams never share device buffers or captured graphs."""
+    dev = torch.cuda.current_device()
+    return (threading.get_ident(), dev, torch.cuda.current_stream(dev).cuda_stream)
 
 
 _ENGINE_CACHE: dict = {}
@@ -154,15 +166,13 @@ _ENGINE_CACHE: dict = {}
 def _cached_engine(problem: SingleProblem, params: SingleParams, *, max_hist: int) -> Alg1Engine:
     """Cold-start engines reused across solve_single calls on the same problem content and parameters:
     the device buffers, constants and level table are built once (one solver per stream)."""
-    import hashlib
-
     h = hashlib.blake2b(digest_size=20)
     b = problem.basis
     for arr in (b.P, b.Pdot, b.Pddot, problem.desired, _tracks(problem), *_shapes(problem),
                 np.stack([bc.values() for bc in problem.boundary])):
         h.update(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
     key = (h.digest(), problem.w_smooth, problem.w_track, params.rho_start, params.rho_growth, params.rho_cap,
-           params.tol, params.stall_window, params.stall_improvement, int(max_hist), torch.cuda.current_device())
+           params.tol, params.stall_window, params.stall_improvement, int(max_hist), _owner_key())
     eng = _ENGINE_CACHE.get(key)
     if eng is None:
         if len(_ENGINE_CACHE) > 16:
@@ -304,8 +314,7 @@ def solve_single(problem: SingleProblem, params: SingleParams | None = None,
     params = params or SingleParams()
     if state is None:
         eng = _cached_engine(problem, params, max_hist=max(params.max_iter, 1))
-        eng.reset_cold()
-        eng.cold_init()
+        eng.cold_init()  # complete cold start: penalties, counters and schedule back to rho_start
         state = SingleState(xi=None, d=None, alpha=None, beta=None, cos_a=None, sin_a=None, cos_b=None,
                             sin_b=None, lam_pos=None, lam_cos_a=None, lam_sin_a=None, lam_cos_b=None,
                             lam_sin_b=None, rho=params.rho_start, rho_o=params.rho_start)
@@ -409,7 +418,10 @@ class SingleBatch:
 
 @dataclass
 class BatchSolution:
-    """Device-resident results of solve_single_batch (torch tensors on the solve device)."""
+    """Device-resident results of solve_single_batch (torch tensors on the solve device).
+
+    The tensors alias the engine's buffers: the next solve on the same engine overwrites them
+    (use ``numpy()`` / ``clone`` to keep a result)."""
 
     xi: torch.Tensor
     converged: torch.Tensor
@@ -426,36 +438,113 @@ class BatchSolution:
         xi = self.xi[i].cpu().numpy()
         return Trajectory(t=b.grid.timestamps, pos=b.P @ xi.T, vel=b.Pdot @ xi.T, acc=b.Pddot @ xi.T)
 
+    def numpy(self) -> "BatchResult":
+        """Every per-member result in ONE device-to-host copy (integers travel as exact fp64)."""
+        B = int(self.xi.shape[0])
+        parts = [self.xi.reshape(B, -1), self.residual_norm[:, None], self.residual_max[:, None],
+                 self.rho_o[:, None], self.converged[:, None].double(), self.iterations[:, None].double(),
+                 self.n_factorizations[:, None].double()]
+        flat = torch.cat(parts, dim=1).cpu().numpy()
+        k = self.xi[0].numel()
+        return BatchResult(xi=flat[:, :k].reshape(tuple(self.xi.shape)), residual_norm=flat[:, k],
+                           residual_max=flat[:, k + 1], rho_o=flat[:, k + 2], converged=flat[:, k + 3] != 0,
+                           iterations=flat[:, k + 4].astype(np.int64),
+                           n_factorizations=flat[:, k + 5].astype(np.int64),
+                           history=None if self.history is None else self.history.cpu().numpy())
+
+
+@dataclass
+class BatchResult:
+    """Host (numpy) copy of a BatchSolution."""
+
+    xi: np.ndarray
+    residual_norm: np.ndarray
+    residual_max: np.ndarray
+    rho_o: np.ndarray
+    converged: np.ndarray
+    iterations: np.ndarray
+    n_factorizations: np.ndarray
+    history: np.ndarray | None
+
+
+def _obstacle_key(batch: SingleBatch) -> bytes:
+    h = hashlib.blake2b(digest_size=20)
+    b = batch.basis
+    h.update(np.asarray([batch.B, batch.dim, len(batch.obstacles), batch.w_smooth, batch.w_track]).tobytes())
+    for arr in (b.P, b.Pdot, b.Pddot):
+        h.update(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
+    if batch.obstacles:
+        h.update(np.ascontiguousarray(np.stack([o.centers for o in batch.obstacles]), dtype=np.float64).tobytes())
+        h.update(np.array([[o.shape.a, o.shape.b] for o in batch.obstacles], dtype=np.float64).tobytes())
+    return h.digest()
+
 
 def make_batch_engine(batch: SingleBatch, params: SingleParams, *, dtype=torch.float64, device=None,
                       history: bool = False, groups: int = 0, export: bool = False, layout: str = "angle",
-                      use_tma: bool = True) -> Alg1Engine:
+                      use_tma: bool = True, tail_split: bool = True) -> Alg1Engine:
+    """An Alg. 1 engine for the batch; the linear terms are computed on the device from the members' boundary
+    values (straight-line desired paths) or from the given desired paths."""
     a = np.array([o.shape.a for o in batch.obstacles], dtype=float)
     b = np.array([o.shape.b for o in batch.obstacles], dtype=float)
     tracks = (np.stack([o.centers for o in batch.obstacles]) if batch.obstacles
               else np.zeros((0, batch.basis.n_p, batch.dim)))
-    return Alg1Engine(batch.basis, tracks, a, b, batch.bvals, batch.linear_terms(), params=params,
-                      w_smooth=batch.w_smooth, w_track=batch.w_track, dtype=dtype, device=device, groups=groups,
-                      max_hist=params.max_iter if history else 0, export=export, layout=layout, use_tma=use_tma)
+    eng = Alg1Engine(batch.basis, tracks, a, b, batch.bvals, desired=batch.desired, params=params,
+                     w_smooth=batch.w_smooth, w_track=batch.w_track, dtype=dtype, device=device, groups=groups,
+                     max_hist=params.max_iter if history else 0, export=export, layout=layout, use_tma=use_tma,
+                     tail_split=tail_split)
+    eng.obstacle_key = _obstacle_key(batch)
+    eng.solve_params = dataclasses.astuple(params)
+    return eng
+
+
+_BATCH_CACHE: dict = {}
+
+
+def _batch_engine(batch: SingleBatch, params: SingleParams, **kw) -> Alg1Engine:
+    """Engines reused across solve_single_batch calls with the same shape, obstacles and parameters (one per
+    thread / device / stream: cached engines are single-owner)."""
+    key = (_obstacle_key(batch), dataclasses.astuple(params), tuple(sorted(kw.items())), _owner_key())
+    eng = _BATCH_CACHE.get(key)
+    if eng is None:
+        if len(_BATCH_CACHE) >= 4:  # batch engines can hold tens of GB: keep few alive
+            _BATCH_CACHE.clear()
+            torch.cuda.empty_cache()
+        eng = _BATCH_CACHE[key] = make_batch_engine(batch, params, **kw)
+    return eng
 
 
 def solve_single_batch(batch: SingleBatch | list, params: SingleParams | None = None, *, dtype=torch.float64,
                        device=None, history: bool = False, groups: int = 0, use_graph: bool = True,
-                       engine: Alg1Engine | None = None, layout: str = "angle") -> BatchSolution:
-    """Solve B independent members (each = solve_single of its problem) in one device pass.
+                       engine: Alg1Engine | None = None, layout: str = "angle", cache: bool = False) -> BatchSolution:
+    """Solve B independent members (each = solve_single of its problem, cold start) in one device pass.
 
     dtype: storage of the per-element state (float64, or float32 with the QP step and all
     per-member reductions kept in fp64).
     layout: "angle" keeps the reference's angle variables (9 words / element in 3-D); "unit"
-    keeps each angle as its unit vector (11 words) and skips the atan2/sincos round trip."""
+    keeps each angle as its unit vector (11 words) and skips the atan2/sincos round trip; "half" keeps the
+    reference's 9 words with each angle as a folded half-angle tangent.
+    engine: reuse this engine (built by make_batch_engine for a batch with the same size, obstacles and
+    basis; ValueError otherwise): the new batch's boundary values and desired paths are uploaded and the
+    linear terms recomputed on the device before the cold start.
+    cache: reuse an engine cached by shape, obstacles and parameters (per thread and stream)."""
     params = params or SingleParams()
     if isinstance(batch, list):
         batch = SingleBatch.from_problems(batch)
-    eng = engine or make_batch_engine(batch, params, dtype=dtype, device=device, history=history, groups=groups,
-                                      layout=layout)
-    eng.reset_schedule()
-    eng.level.copy_(eng.level0)
-    eng.cold_init()
+    if engine is not None:
+        if getattr(engine, "obstacle_key", None) != _obstacle_key(batch):
+            raise ValueError("engine was built for a different batch size, basis or obstacle set")
+        if getattr(engine, "solve_params", None) not in (None, dataclasses.astuple(params)):
+            raise ValueError("engine was built with different SingleParams")
+        eng = engine
+        eng.set_members(batch.bvals, batch.desired)
+    elif cache:
+        eng = _batch_engine(batch, params, dtype=dtype, device=device, history=history, groups=groups,
+                            layout=layout)
+        eng.set_members(batch.bvals, batch.desired)
+    else:
+        eng = make_batch_engine(batch, params, dtype=dtype, device=device, history=history, groups=groups,
+                                layout=layout)
+    eng.cold_init()  # complete cold start (rho, rho_o, level, iteration, schedule reset on the device)
     eng.run(params.max_iter, use_graph=use_graph, check_every=50 if params.tol > 0 else 0)
     _raise_if_failed(eng)
     # one shared factorization per distinct rho_o level any member reached

@@ -158,3 +158,64 @@ def test_priest_candidate_gather_is_the_global_stable_topk(k):
         p.join(timeout=60)
     for _, idx in got:
         np.testing.assert_array_equal(idx, np.argsort(scores, kind="stable")[:k])
+
+
+# ------------------------------------------------------------------ Alg. 1: sharded public entry point
+class _FakeSol:
+    """Stands in for a BatchSolution in the host-logic test (deterministic per-member values)."""
+
+    def __init__(self, sub):
+        from paper_2408_10731_b200.solver_single import BatchResult
+
+        bv = np.asarray(sub.bvals)
+        B = bv.shape[0]
+        xi = np.repeat(bv[:, :, :1], 11, axis=2) * np.arange(11)[None, None, :]
+        rmax = np.round(np.abs(bv[:, 1, 0]) + np.abs(bv[:, 2, 3]), 1)
+        self._r = BatchResult(xi=xi, residual_norm=2 * rmax, residual_max=rmax, rho_o=np.ones(B),
+                              converged=rmax <= 0.5, iterations=np.full(B, 7), n_factorizations=np.ones(B, int),
+                              history=None)
+        self.residual_max = torch.as_tensor(rmax)
+
+    def numpy(self):
+        return self._r
+
+
+def _fake_solve(sub, params=None, **kw):
+    return _FakeSol(sub)
+
+
+def _sharded_worker(rank, world, port, out_q):
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200.basis import build_basis
+    from paper_2408_10731_b200.distributed import solve_single_batch_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    batch = scenarios.flow3d_batch(5, range(23), basis=build_basis(0.0, 10.0, 100, 10))
+    local, merged, full = solve_single_batch_sharded(batch, None, gather_results=True, solve=_fake_solve)
+    out_q.put((rank, local.xi.shape[0], merged, {k: v.tolist() for k, v in full.items()}))
+    dist.destroy_process_group()
+
+
+def test_alg1_sharded_entry_point_two_ranks_gloo():
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200.basis import build_basis
+    from paper_2408_10731_b200.distributed import solve_single_batch_sharded
+
+    batch = scenarios.flow3d_batch(5, range(23), basis=build_basis(0.0, 10.0, 100, 10))
+    _, single, full1 = solve_single_batch_sharded(batch, None, gather_results=True, solve=_fake_solve)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=180) for _ in procs])
+    for p in procs:
+        p.join(timeout=60)
+    assert [g[1] for g in got] == [11, 12]  # contiguous ranges [0, 11) and [11, 23)
+    for _, _, merged, full in got:
+        assert merged == single
+        for k, v in full1.items():
+            np.testing.assert_array_equal(np.asarray(full[k]), v)
