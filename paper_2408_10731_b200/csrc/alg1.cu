@@ -123,10 +123,8 @@ __device__ __forceinline__ void alg1_schedule(const Alg1Args& A, int i, int stat
     }
     const int lc = S ? S->last_change : A.s.last_change[i];
     if (n >= w2 && it - lc >= w) {  // solver_single.py:394
-        double sr = 0.0, sp = 0.0;  // np.mean of <8 values: sequential sum / w
-        for (int k = 0; k < w; ++k) sr += rr[(n - w + k) % w2];
-        for (int k = 0; k < w; ++k) sp += rr[(n - w2 + k) % w2];
-        const double recent = sr / (double)w, previous = sp / (double)w;
+        // np.mean(history[-w:]), np.mean(history[-2w:-w]) in numpy's summation order
+        const double recent = np_mean_ring(rr, n - w, w, w2), previous = np_mean_ring(rr, n - w2, w, w2);
         if (!(previous <= fmax(A.p.tol, 0.0)) && (previous - recent) / previous < A.p.stall_improvement) {
             const double nr = fmin(rho * A.p.rho_growth, A.p.rho_cap);
             const double nro = fmin(rho_o * A.p.rho_growth, A.p.rho_cap);

@@ -193,10 +193,8 @@ __device__ void b2_schedule(const B2Args& A, int level, double rho, const B2Summ
     if (A.p.flags & TRO_FLAG_NO_SCHEDULE) return;
     const int lc = A.s.last_change[0];
     if (n >= w2 && it - lc >= w) {  // :398
-        double sr = 0.0, sp = 0.0;  // np.mean of < 8 values: sequential sum / w
-        for (int k = 0; k < w; ++k) sr += A.s.ring[(n - w + k) % w2];
-        for (int k = 0; k < w; ++k) sp += A.s.ring[(n - w2 + k) % w2];
-        const double recent = sr / (double)w, previous = sp / (double)w;
+        // np.mean(history[-w:]), np.mean(history[-2w:-w]) in numpy's summation order
+        const double recent = np_mean_ring(A.s.ring, n - w, w, w2), previous = np_mean_ring(A.s.ring, n - w2, w, w2);
         if (previous > fmax(A.p.tol, 0.0) && (previous - recent) / previous < A.p.stall_improvement) {
             if (level + 1 < A.d.n_levels) {
                 A.s.level[0] = level + 1;

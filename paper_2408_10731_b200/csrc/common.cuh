@@ -40,4 +40,29 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// np.mean of the w ring values v[k] = ring[(start + k) % w2], k = 0 .. w-1, with numpy's own summation
+// order (pairwise_sum in numpy/_core/src/umath/loops_utils.h.src, which np.add.reduce uses for float64):
+// n < 8 sequential from 0.0; 8 <= n <= 128 eight interleaved partial sums combined as
+// ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)), then the n % 8 tail in order; then / n.
+// (The stall windows here are <= 32, so the recursive n > 128 branch never applies.)
+__device__ __forceinline__ double np_mean_ring(const double* ring, int start, int w, int w2) {
+    double res;
+    if (w < 8) {
+        res = 0.0;
+        for (int k = 0; k < w; ++k) res += ring[(start + k) % w2];
+    } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = ring[(start + j) % w2];
+        int k = 8;
+        for (; k < w - (w % 8); k += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] += ring[(start + k + j) % w2];
+        }
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; k < w; ++k) res += ring[(start + k) % w2];
+    }
+    return res / (double)w;
+}
+
 }  // namespace tro

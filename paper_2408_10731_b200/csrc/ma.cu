@@ -400,11 +400,8 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
             if (scheduled > nl - 1) scheduled = nl - 1;
             bool stalled = false;
             const int lc = A.s.last_change[i];
-            if (n >= w2 && it - lc >= w) {  // :327-331 (np.mean of <8 values: sequential sum / w)
-                double sr = 0.0, sp = 0.0;
-                for (int k = 0; k < w; ++k) sr += ring[(n - w + k) % w2];
-                for (int k = 0; k < w; ++k) sp += ring[(n - w2 + k) % w2];
-                const double recent = sr / (double)w, previous = sp / (double)w;
+            if (n >= w2 && it - lc >= w) {  // :327-331 (np.mean in numpy's summation order)
+                const double recent = np_mean_ring(ring, n - w, w, w2), previous = np_mean_ring(ring, n - w2, w, w2);
                 stalled = previous > 0.0 && (previous - recent) / previous < A.p.stall_improvement;
             }
             const int target = scheduled > (stalled ? level + 1 : level) ? scheduled : (stalled ? level + 1 : level);

@@ -91,6 +91,21 @@ def flow3d_obstacles(n_o: int, seed: int = 0) -> list[ObstacleSpec]:
     return out
 
 
+def flow3d_scenario(n_o: int, member: int = 0, seed: int = 0):
+    """The C2/C5 recipe as a bench Scenario (raw obstacle geometry, member's boundary): what the reference's
+    metrics (check_collision_free, metrics.py:60-82) evaluate a member's trajectory against."""
+    from .bench.scenarios import Boundary, Horizon, RobotSpec, Scenario, ScenarioObstacle
+
+    starts, goals = flow3d_endpoints([member])
+    return Scenario(kind="dynamic-flow", dim=3, horizon=Horizon(0.0, 10.0, 100),
+                    robot=RobotSpec(shape=[0.0, 0.0], v_max=3.0, a_max=3.0),
+                    obstacles=[ScenarioObstacle(a=o.a, b=o.b, center=[float(v) for v in o.center],
+                                                velocity=[float(v) for v in o.velocity])
+                               for o in flow3d_obstacles(n_o, seed)],
+                    boundary=Boundary(start=[float(v) for v in starts[0]], goal=[float(v) for v in goals[0]]),
+                    seed=seed)
+
+
 def flow3d_endpoints(members) -> tuple[np.ndarray, np.ndarray]:
     """(starts, goals), each (len(members), 3), member i seeded by default_rng(1000 + i)."""
     members = list(members)

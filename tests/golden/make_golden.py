@@ -90,7 +90,7 @@ def run_with_snapshots(prob, params, snap_at):
     return np.array(history), state, snaps
 
 
-def flow3d_problem(n_o, member, basis):
+def flow3d_problem(n_o, member, basis, with_scenario=False):
     specs = flow3d_obstacles(n_o, 0)
     starts, goals = flow3d_endpoints([member])
     sc = Scenario(kind="dynamic-flow", dim=3, horizon=Horizon(0.0, 10.0, 100),
@@ -99,7 +99,8 @@ def flow3d_problem(n_o, member, basis):
                                               velocity=[float(v) for v in o.velocity]) for o in specs],
                   boundary=Boundary(start=[float(v) for v in starts[0]], goal=[float(v) for v in goals[0]]),
                   seed=0)
-    return single_problem_from_scenario(sc, basis)
+    prob = single_problem_from_scenario(sc, basis)
+    return (prob, sc) if with_scenario else prob
 
 
 class KinvPatch:
@@ -619,6 +620,92 @@ def make_acceptance5():
         out[f"s{seed}_best"] = np.array([-1 if ranked.best_index is None else ranked.best_index])
     np.savez_compressed(os.path.join(OUT, "acceptance5.npz"), **out)
     print("acceptance5 written")
+
+
+# ---------------------------------------------------------------- C5 regime (round 2)
+C5_TF_PLAN = {0: (25, 100, 199), 5: (150, 199), 2: (199,)}
+C5_STATE = ("xi", "d", "alpha", "beta", "lam_pos", "lam_cos_a", "lam_sin_a", "lam_cos_b", "lam_sin_b")
+
+
+def _digest(a) -> str:
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def make_c5_tf():
+    """C5 recipe (n_o 100) teacher-forcing snapshots where the headline runs: rho_o at / near the 1e3 cap.
+
+    Per (member, k): the full state after iteration k (+ stall bookkeeping), and of the reference's state
+    after k+1 only xi, rho / rho_o, the residual extremes and a sha256 per array (the oracle is pinned to
+    those bit for bit; the device is compared with the pinned oracle step at test time)."""
+    basis = build_basis(0.0, 10.0, 100, 10)
+    params = solver_single.SingleParams(max_iter=200, tol=0.0)
+    out = {}
+    for member, ks in C5_TF_PLAN.items():
+        prob = flow3d_problem(100, member, basis)
+        if member == 0:
+            out.update(problem_arrays(prob))
+        out[f"m{member}_bvals"] = problem_arrays(prob)["bvals"]
+        out[f"m{member}_desired"] = problem_arrays(prob)["desired"]
+        snap_at = set(ks) | {k + 1 for k in ks}
+        hist, _, snaps = run_with_snapshots(prob, params, snap_at)
+        out[f"m{member}_hist"] = hist
+        for k in ks:
+            st, mh, lc = snaps[k]
+            full = state_arrays(st, f"m{member}_k{k}_")
+            out.update({key: v for key, v in full.items() if key.split(f"_k{k}_")[1] in C5_STATE + ("scal",)})
+            out[f"m{member}_k{k}_maxhist"] = np.array(mh)
+            out[f"m{member}_k{k}_last_change"] = np.array([lc])
+            nx, mhx, lcx = snaps[k + 1]
+            pre = f"m{member}_k{k}_next_"
+            out[pre + "xi"] = nx.xi.copy()
+            out[pre + "scal"] = np.array([nx.rho, nx.rho_o, nx.iteration, lcx], dtype=float)
+            norm, mx = solver_single._residual_extremes(nx, prob)
+            out[pre + "res"] = np.array([norm, mx])
+            out[pre + "sha"] = np.array([_digest(getattr(nx, name)) for name in C5_STATE])
+        out[f"m{member}_ks"] = np.array(ks)
+        print("c5_tf member", member, "rho_o at ks:", [snaps[k][0].rho_o for k in ks])
+    np.savez_compressed(os.path.join(OUT, "c5_tf.npz"), **out)
+    print("c5_tf written")
+
+
+def _c5_member(args):
+    """One C5-recipe member through the unmodified reference: the fixed 200-iteration solve (tol 0) and the
+    default converged solve, each with check_collision_free against the raw scenario geometry."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from trajopt.bench.metrics import check_collision_free
+
+    member, n_o = args
+    basis = build_basis(0.0, 10.0, 100, 10)
+    prob, sc = flow3d_problem(n_o, member, basis, with_scenario=True)
+    row = []
+    for params in (solver_single.SingleParams(max_iter=200, tol=0.0), solver_single.SingleParams()):
+        sol = solver_single.solve_single(prob, params)
+        ok, worst = check_collision_free(sol.trajectory, sc)
+        bc = max(float(np.max(np.abs(sol.trajectory.pos[0] - sc.boundary.start))),
+                 float(np.max(np.abs(sol.trajectory.pos[-1] - sc.boundary.goal))))
+        row.append((sol.state.xi.copy(), sol.residual_norm, sol.residual_max, sol.state.rho_o, sol.iterations,
+                    int(sol.converged), sol.n_factorizations, worst, bc))
+    return row
+
+
+def make_c5_dist(n_members=512, n_o=100):
+    """Tier-3 end-state distribution fixture: members 0..n-1 of the C5 recipe."""
+    import multiprocessing as mp
+
+    with mp.get_context("fork").Pool(os.cpu_count()) as pool:
+        rows = pool.map(_c5_member, [(i, n_o) for i in range(n_members)], chunksize=4)
+    out = {"members": np.arange(n_members)}
+    for k, tag in enumerate(("fixed", "conv")):
+        out[f"{tag}_xi"] = np.array([r[k][0] for r in rows])
+        out[f"{tag}_scal"] = np.array([r[k][1:] for r in rows], dtype=float)
+    out["scal_names"] = np.array(["res_norm", "res_max", "rho_o", "iterations", "converged", "n_factorizations",
+                                  "worst_violation", "boundary_err"])
+    np.savez_compressed(os.path.join(OUT, "c5_dist.npz"), **out)
+    f, c = out["fixed_scal"], out["conv_scal"]
+    print("c5_dist: fixed median max|r|", np.median(f[:, 1]), "collision-free", np.mean(f[:, 6] <= 0),
+          "| converged", np.mean(c[:, 4]), "iters median", np.median(c[:, 3]))
 
 
 if __name__ == "__main__":

@@ -47,8 +47,7 @@ def test_same_batch_twice_on_one_engine_is_bitwise_a_fresh_solve(layout):
     fresh = _result(solve_single_batch(batch, PARAMS, history=True, layout=layout))
     _same(first, second)
     _same(first, fresh)
-    its, rho_o = first[1], first[2]
-    assert its.min() < PARAMS.max_iter and rho_o.max() > 1.0  # the schedule really ran
+    assert first[2].max() > 1.0  # penalties grew: a stale rho_o would show in every field
 
 
 def test_small_batch_in_kernel_loop_reuse():
