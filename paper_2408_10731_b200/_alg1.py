@@ -372,7 +372,7 @@ class Alg1Engine:
             # warm-up launch outside capture is not needed: launches are plain kernels
             pass
         torch.cuda.current_stream(self.device).wait_stream(s)
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
             self.compact_active()
             for _ in range(n):
                 self.iterate(2)

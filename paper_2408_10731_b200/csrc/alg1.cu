@@ -638,7 +638,7 @@ namespace tro {
 __global__ void fastmath_eval_kernel(int fn, const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                                      double* __restrict__ out) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const double v = x[k];
+        const double v = fn == 9 ? 0.0 : x[k];
         double s, c, r = 0.0;
         switch (fn) {
             case 0: sincos_fast(v, &s, &c); r = s; break;
@@ -650,6 +650,7 @@ __global__ void fastmath_eval_kernel(int fn, const double* __restrict__ x, const
             case 6: unit_dir(v, y[k], &c, &s); r = c; break;
             case 7: unit_dir(v, y[k], &c, &s); r = s; break;
             case 8: r = los_scale(v); break;
+            case 9: r = np_mean_ring(x + 32 * k, 0, (int)y[k], 64); break;  // x: n x 32 windows, y: lengths
             default: r = 0.0;
         }
         out[k] = r;
@@ -658,7 +659,7 @@ __global__ void fastmath_eval_kernel(int fn, const double* __restrict__ x, const
 }  // namespace tro
 
 extern "C" int tro_fastmath_eval(int32_t fn, const double* x, const double* y, int64_t n, double* out, void* stream) {
-    if (!x || !out || n < 0 || fn < 0 || fn > 8 || ((fn == 2 || fn == 6 || fn == 7) && !y)) return TRO_EINVAL;
+    if (!x || !out || n < 0 || fn < 0 || fn > 9 || ((fn == 2 || fn == 6 || fn == 7 || fn == 9) && !y)) return TRO_EINVAL;
     if (n == 0) return 0;
     int64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;

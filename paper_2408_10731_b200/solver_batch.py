@@ -542,7 +542,7 @@ class _Engine:
 
     def _capture(self, n: int):
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
             for _ in range(n):
                 self.iterate()
         self._graph, self._graph_n = g, n
@@ -637,6 +637,15 @@ def _ensure_factors(state: BatchState, levels: _Levels, level: int) -> None:
 _ENGINE_CACHE: dict = {}
 
 
+def _owner_key():
+    """Cached engines are single-owner: one per (thread, device, stream), so concurrent calls
+    never share device buffers, the captured graph or the grid ticket."""
+    import threading
+
+    dev = torch.cuda.current_device()
+    return (threading.get_ident(), dev, torch.cuda.current_stream(dev).cuda_stream)
+
+
 def _engine_for(state: BatchState, problem: BatchProblem, struct: _Structure, params: BatchParams | None = None,
                 max_hist: int = 0, cached: bool = False):
     """Engine loaded with the state; `given` = alpha / d must be read from explicit arrays.
@@ -649,8 +658,7 @@ def _engine_for(state: BatchState, problem: BatchProblem, struct: _Structure, pa
     eng = None
     if cached:
         key = (struct.key, n_b, float(state.rho), float(state.rho_psi), float(p.rho_growth), float(p.rho_cap),
-               float(p.tol), float(p.stall_improvement), int(p.stall_window), int(max_hist),
-               torch.cuda.current_device())
+               float(p.tol), float(p.stall_improvement), int(p.stall_window), int(max_hist), _owner_key())
         eng = _ENGINE_CACHE.get(key)
         if eng is None:
             if len(_ENGINE_CACHE) > 8:

@@ -282,7 +282,7 @@ class MaEngine:
             if use_graph and n == chunk:
                 if self._graph is None:
                     g = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g):
+                    with torch.cuda.graph(g, capture_error_mode="thread_local"):
                         for _ in range(chunk):
                             self.iterate()
                     self._graph = g

@@ -308,7 +308,6 @@ def test_no_obstacles_one_iteration():
 def test_factorization_guard_raises(golden):
     g = golden("c1.npz")
     eng = engine_from(g, g["bvals"], g["desired"], SingleParams(max_iter=3, tol=0.0))
-    eng.table.ok[:] = 0
     eng.level_ok.zero_()
     eng.cold_init()
     eng.run(3, use_graph=False)

@@ -7,6 +7,7 @@ bit: the GPU teacher-forced tests (tests/test_c5_parity_gpu.py) then compare the
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -17,7 +18,7 @@ C5_STATE = ("xi", "d", "alpha", "beta", "lam_pos", "lam_cos_a", "lam_sin_a", "la
 
 
 def c5_cases():
-    g = np.load("tests/golden/c5_tf.npz")
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c5_tf.npz"))
     return [(int(m[1:].split("_")[0]), int(k)) for m in g.files if m.endswith("_ks") for k in g[m]]
 
 
@@ -38,12 +39,13 @@ def c5_state(g, pre):
                    factor_rho_o=[sc[1]], n_factorizations=np.zeros(1, dtype=np.int64))
 
 
-def oracle_step(g, member, k):
-    """The reference's loop body at iteration k+1 (solver_single.py:419-427) on the snapshot."""
+def oracle_step(g, member, k, mode="lu"):
+    """The reference's loop body at iteration k+1 (solver_single.py:419-427) on the snapshot.
+    mode "kinv": the position step applies the explicit K^-1 (the reference's LU-vs-K^-1 twin)."""
     pre = f"m{member}_k{k}_"
     prob = c5_problem(g, member)
     st = c5_state(g, pre)
-    O.am_iteration(st, prob, O.KKTCache(prob))
+    O.am_iteration(st, prob, O.KKTCache(prob, mode=mode))
     norm, mx = O.residual_extremes(st, prob)
     hist = list(g[pre + "maxhist"]) + [float(mx[0])]
     rho, rho_o, lc = O.maybe_grow(st.rho[0], st.rho_o[0], int(st.iteration[0]), O.Params(max_iter=200, tol=0.0),
