@@ -1188,11 +1188,12 @@ def run_b200(args):
                      "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_s * 1e3,
                      "layout": args.layout, "state_bytes_moved_per_launch": moved_bytes,
                      "hbm_frac_of_moved_bytes": moved_bytes / avg_launch_s / 1e9 / peak,
-                     "kernel": "tro_alg1_iterate (alg1_kernel<3,T>)"},
+                     "kernel": "tro_alg1_iterate (alg1_tma_kernel<3,T,LAY,100,G,MINB,2>: persistent, warp-"
+                               "specialised producer / scalar / consumer warps)"},
         "clocks": clk,
         "e2e": e2e,
-        # init + per-iteration launches; batches up to LOOP_MAX_MEMBERS run iterations 2..n in one launch
-        "gpu_launches": args.steps * ((1 + n_iter) if B > _alg1_loop_max() else 3),
+        # per step: the cold-start init + the iteration launches and work-list compactions of run()
+        "gpu_launches": args.steps * (1 + eng.launches_per_run(n_iter)),
     }
     if args.config == "c1" and rank == 0:
         # second headline of the metric: ms per converged solve (C1, SingleParams() defaults,
@@ -1221,8 +1222,8 @@ def run_b200(args):
                                    "api": "solver_single.solve_single (host numpy in/out, wall clock)",
                                    "cpu_port_ms_per_solve": ref_ms}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # bounded sample: ~4 member-solves per host core (C5 ~0.4 s each -> 10-30 s of CPU work)
-        sample = 4 * (os.cpu_count() or 1) if args.config != "c1" else 2 * (os.cpu_count() or 1)
+        # bounded sample: ~40 member-solves per host core (C5 ~0.45 s each -> ~20 s of CPU work)
+        sample = 40 * (os.cpu_count() or 1) if args.config != "c1" else 2 * (os.cpu_count() or 1)
         v, info = cpu_reference(args.config, sample)
         line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port",
                                 "sample": f"{sample} members x {info['iterations']} AM its of the same recipe, "

@@ -79,6 +79,11 @@ typedef struct tro_alg1_consts {
                                 it also sets rho = rho_o = level_rho[level0[i]], level = level0[i] and zeroes
                                 iteration, last_change, n_hist, n_changes, status and the stall ring.
                                 NULL: tro_alg1_init leaves that bookkeeping to the caller (the MPC fleet). */
+    const double* track_lin; /* optional constant-velocity description of `tracks`: n_o records of 6 doubles
+                                (3-D {cx cy cz vx vy vz}, 2-D {cx cy vx vy 0 0}) then n_p times rel[t], with
+                                tracks[j][ax][t] == c + v * rel[t] BITWISE (one rounded product, one rounded
+                                sum, as numpy's c + v * rel).  Non-NULL: the TMA iteration kernel generates the
+                                track rows in registers instead of streaming them (NULL: stream `tracks`). */
 } tro_alg1_consts;
 
 typedef struct tro_alg1_params {

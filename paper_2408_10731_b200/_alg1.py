@@ -38,6 +38,43 @@ def rho_chain(r0: float, growth: float, cap: float) -> list[float]:
         vals.append(nxt)
 
 
+def linear_track_record(tracks: np.ndarray, timestamps: np.ndarray) -> np.ndarray | None:
+    """Constant-velocity description of obstacle tracks (n_o, n_p, dim), or None.
+
+    Returns [c_j (dim), v_j (dim) padded to 6 doubles per obstacle ..., rel (n_p)] with rel = t - t[0] when
+    every sample equals numpy's c + v * rel BITWISE (bench/scenarios.py:118-127, scenarios.tracks_on_grid):
+    the velocity is recovered from the end points and its neighbouring doubles are tried until one
+    reproduces every sample exactly.  The iteration kernel then generates the tracks in registers
+    (tro_alg1_consts.track_lin) instead of streaming them; anything else keeps the streamed tracks."""
+    n_o, n_p, dim = tracks.shape
+    if n_o == 0 or n_p < 2:
+        return None
+    rel = np.asarray(timestamps, dtype=float) - float(timestamps[0])
+    if rel[0] != 0.0 or rel[-1] == 0.0:
+        return None
+    c = tracks[:, 0, :]
+    # least-squares slope over every sample (the end-point quotient alone can be hundreds of ulps off
+    # when |v rel| << |c|); the search below then finds an exactly reproducing double nearby
+    v0 = np.einsum("t,jtk->jk", rel, tracks - c[:, None, :]) / float(rel @ rel)
+    best = np.full(v0.shape, np.nan)
+    steps = [v0]  # v0, then up to 64 doubles either side (the end-point quotient loses ~|c| / |v rel| ulps)
+    up, dn = v0, v0
+    for _ in range(64):
+        up, dn = np.nextafter(up, np.inf), np.nextafter(dn, -np.inf)
+        steps += [up, dn]
+    for v in steps:
+        ok = np.all(c[:, None, :] + v[:, None, :] * rel[None, :, None] == tracks, axis=1)
+        best = np.where(np.isnan(best) & ok, v, best)
+        if not np.isnan(best).any():
+            break
+    if np.isnan(best).any():
+        return None
+    rec = np.zeros((n_o, 6))
+    rec[:, :dim] = c
+    rec[:, dim:2 * dim] = best
+    return np.concatenate([rec.reshape(-1), rel])
+
+
 _TABLE_CACHE: dict = {}
 
 
@@ -134,6 +171,8 @@ class Alg1Engine:
         if n_o == 0:
             self.shape_a = torch.ones(1, **f64)
             self.shape_b = torch.ones(1, **f64)
+        lin = linear_track_record(tracks, basis.grid.timestamps) if n_o and tracks.shape[1] == n_p else None
+        self.track_lin = torch.as_tensor(lin, **f64) if lin is not None else None
         self.kinv = torch.as_tensor(self.table.kinv, **f64).contiguous()
         self.level_rho = torch.as_tensor(np.asarray(self.table.rhos), **f64)
         self.level_ok = torch.as_tensor(self.table.ok, **i32)
@@ -194,7 +233,8 @@ class Alg1Engine:
         self._consts = _lib.Alg1Consts(
             self.P.data_ptr(), self.tracks.data_ptr(), self.shape_a.data_ptr(), self.shape_b.data_ptr(),
             self.kinv.data_ptr(), self.level_rho.data_ptr(), self.level_ok.data_ptr(), self.q.data_ptr(),
-            self.bvals.data_ptr(), self.line_u.data_ptr(), self.line_v.data_ptr(), self.level0.data_ptr())
+            self.bvals.data_ptr(), self.line_u.data_ptr(), self.line_v.data_ptr(), self.level0.data_ptr(),
+            _lib.ptr(self.track_lin))
         p = _lib.ptr
         self._state = _lib.Alg1State(
             p(self.state), p(self.d), p(self.copies), p(self.xi), p(self.pos),
@@ -377,6 +417,16 @@ class Alg1Engine:
             for _ in range(n):
                 self.iterate(2)
         self._graph, self._graph_n = g, n
+
+    def launches_per_run(self, n_iter: int, chunk: int = 25, loop: bool | None = None) -> int:
+        """Kernel launches of run(n_iter) without early exit (iterations + work-list compactions)."""
+        if n_iter <= 0:
+            return 0
+        if (self.B <= LOOP_MAX_MEMBERS) if loop is None else loop:
+            return 1 + (1 if n_iter > 1 else 0)
+        rest = n_iter - 1
+        compactions = -(-rest // chunk) if self._state.order else 0
+        return n_iter + compactions
 
     def run(self, n_iter: int, *, use_graph: bool = True, chunk: int = 25, check_every: int = 0,
             loop: bool | None = None) -> int:

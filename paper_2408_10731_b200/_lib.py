@@ -82,6 +82,7 @@ class Alg1Consts(ctypes.Structure):
         ("line_u", c_void_p),
         ("line_v", c_void_p),
         ("level0", c_void_p),
+        ("track_lin", c_void_p),
     ]
 
 

@@ -49,6 +49,7 @@ struct Alg1Args {
     int32_t G;
     int32_t n_loop;      // MODE 3: AM iterations per launch
     int32_t split_tail;  // TMA kernel: 1 = the last partial round may run as obstacle halves (scratch given)
+    int32_t n_stages;    // TMA kernel: ring stages that fit the shared-memory budget
 };
 
 struct SmemLayout {
@@ -480,16 +481,22 @@ static int launch_mode(const Alg1Args& A, cudaStream_t st) {
 }
 
 #ifndef TRO_TMA_G
-#define TRO_TMA_G 2
+#define TRO_TMA_G 4  // fp64 obstacle rows per stage: 400 elements on 13 consumer warps (12.5 % idle lanes at G = 2)
+#endif
+#ifndef TRO_TMA_MINB
+#define TRO_TMA_MINB 1  // fp64: one CTA per SM (13 consumer + scalar + producer warps, <= 136 registers)
 #endif
 #ifndef TRO_TMA_S
-#define TRO_TMA_S 3
-#endif
-#ifndef TRO_TMA_S32
-#define TRO_TMA_S32 (TRO_TMA_S + 1)  // fp32 stages are half as large: one more keeps more bytes in flight
+#define TRO_TMA_S 4  // ring stages (fewer when they do not fit the shared-memory budget)
 #endif
 #ifndef TRO_TMA_G32
-#define TRO_TMA_G32 TRO_TMA_G
+#define TRO_TMA_G32 4  // fp32: same geometry (C5 unit: 0.64 -> 0.71 of HBM vs G 2 at 2 CTAs/SM)
+#endif
+#ifndef TRO_TMA_MINB32
+#define TRO_TMA_MINB32 1
+#endif
+#ifndef TRO_TMA_S32
+#define TRO_TMA_S32 6
 #endif
 #ifndef TRO_TMA_DM_SPEC
 #define TRO_TMA_DM_SPEC 1  // steady-state iterations use the d_mode = 2 specialisation
@@ -507,24 +514,34 @@ static int sm_count() {
 // persistent TMA-pipelined AM iteration (n_p == 100); returns 1 if it launched
 template <int DIM, typename T, int LAY>
 static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
-    constexpr int G = sizeof(T) == 8 ? TRO_TMA_G : TRO_TMA_G32;
-    constexpr int S = (sizeof(T) == 8 && DIM == 3) ? TRO_TMA_S : TRO_TMA_S32;
-    using C = TmaCfg<DIM, T, LAY, 100, G, S>;
-    const TmaLayout L = tma_layout(C::kStageBytes, S, 100, A.d.m, DIM, A.d.n_obs, G, C::kConsumers);
-    if (L.total * kTmaMinBlocks > 227 * 1024) return 0;
-    static bool attr_set[64] = {false};
+    constexpr bool f64 = sizeof(T) == 8;
+    constexpr int G = f64 ? TRO_TMA_G : TRO_TMA_G32;
+    constexpr int MINB = f64 ? TRO_TMA_MINB : TRO_TMA_MINB32;
+    constexpr int SMAX = f64 ? TRO_TMA_S : TRO_TMA_S32;
+    static_assert(SMAX >= 2 && SMAX <= kTmaMaxStages, "ring stages");
+    using C = TmaCfg<DIM, T, LAY, 100, G>;
+    const bool lin = A.c.track_lin != nullptr;
+    // the shared-memory budget of one CTA at MINB CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
+    const int budget = (228 * 1024) / MINB - 1024;
+    const TmaLayout L0 = tma_layout(C::kRowBytes, C::kTrkBytes, lin, 0, 100, A.d.m, DIM, A.d.n_obs, G, C::kConsumers);
+    int S = SMAX;
+    while (S >= 2 && L0.total + S * L0.stage_bytes > budget) --S;
+    if (S < 2) return 0;
+    const int total = L0.total + S * L0.stage_bytes;
+    static int attr_set[64] = {0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, S, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024 / kTmaMinBlocks);
-        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, S, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024 / kTmaMinBlocks);
-        attr_set[dev] = true;
+        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, -1>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
+        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, 2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
+        attr_set[dev] = 1;
     }
     Alg1Args B = A;
     B.G = G;
-    const int slots = sm_count() * kTmaMinBlocks;
+    B.n_stages = S;
+    const int slots = sm_count() * MINB;
     const int grid = A.d.n_members < slots ? A.d.n_members : slots;
     // tail balancing (decided in the kernel from the work-list length): when it is R grid + M with
     // 0 < 2 M <= grid, the last round's M members become 2 M halves
@@ -535,10 +552,10 @@ static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
     }
 #if TRO_TMA_DM_SPEC
     if (A.p.d_mode == 2)
-        alg1_tma_kernel<DIM, T, LAY, 100, G, S, 2><<<grid, C::kThreads, L.total, st>>>(B);
+        alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, 2><<<grid, C::kThreads, total, st>>>(B);
     else
 #endif
-        alg1_tma_kernel<DIM, T, LAY, 100, G, S, -1><<<grid, C::kThreads, L.total, st>>>(B);
+        alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, -1><<<grid, C::kThreads, total, st>>>(B);
     *rc = (int)cudaGetLastError();
     return 1;
 }

@@ -77,7 +77,7 @@ struct Words {
 template <typename T>
 __device__ __forceinline__ T half_encode(T c, T s) {
     const bool pos = c >= (T)0;
-    const T t = s * rcp_fast(pos ? (T)1 + c : (T)1 - c);
+    const T t = s * rcp_fast2ulp(pos ? (T)1 + c : (T)1 - c);
     return pos ? t : copysign((T)3, s) - t;
 }
 template <typename T>
@@ -85,7 +85,7 @@ __device__ __forceinline__ void half_decode(T w, T* c, T* s) {
     const bool inner = fabs(w) <= (T)1;
     const T t = inner ? w : w - copysign((T)3, w);
     const T t2 = t * t;
-    const T q = rcp_fast((T)1 + t2);
+    const T q = rcp_fast2ulp((T)1 + t2);
     const T cc = ((T)1 - t2) * q, ss = (T)2 * t * q;
     *c = inner ? cc : -cc;
     *s = inner ? ss : -ss;
@@ -100,12 +100,12 @@ __device__ __forceinline__ void half_decode(T w, T* c, T* s) {
 template <typename T>
 __device__ __forceinline__ void rcp2(T x, T y, T& rx, T& ry) {
 #if TRO_RCP2
-    const T r = rcp_fast(x * y);
+    const T r = rcp_fast2ulp(x * y);
     rx = y * r;
     ry = x * r;
 #else
-    rx = rcp_fast(x);
-    ry = rcp_fast(y);
+    rx = rcp_fast2ulp(x);
+    ry = rcp_fast2ulp(y);
 #endif
 }
 template <typename T>
@@ -167,7 +167,7 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         const T cb2 = (trho * cb - lcb + ccb * Lz) * rbden;
         const T csb = a * dold;
         const T num = trho * sb - lsb + csb * (ca2 * Lx + sa2 * Ly);
-        const T sb2 = num * rcp_fast(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
+        const T sb2 = num * rcp_fast2ulp(trho + trho_o * (csb * csb) * (ca2 * ca2 + sa2 * sa2));
         // d from the new positions (solver_single.py:283-290)
         dn = los_scale(dx * dx * ia2 + dy * dy * ia2 + dz * dz * ib2);
         T cA2, sA2, cB2, sB2;

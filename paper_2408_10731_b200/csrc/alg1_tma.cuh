@@ -1,67 +1,75 @@
 // Persistent, warp-specialised fused AM iteration (Alg. 1) for sm_100a.
 //
-// Why: the one-CTA-per-member kernel is latency-bound — each warp issues its
-// element's 12 global loads and then computes ~500 instructions with nothing in
-// flight, so too few bytes are outstanding per SM (ncu: long-scoreboard stalls
-// dominate, 0.6 eligible warps/cycle).  Here one producer warp streams the
-// state rows into a shared-memory ring with TMA bulk copies
-// (cp.async.bulk ... mbarrier::complete_tx) while G*NP consumer threads compute
-// out of shared memory and write results straight back to HBM.  In the
-// interleaved layout state[i][j][w][t] the W words x NP samples of one
-// obstacle row are ONE contiguous block (fp64 3-D: 7200 B), as is the matching
-// track row tracks[j][ax][t], so a stage (G rows) is 2G bulk copies.
+// Three warp roles per CTA:
+//   * a PRODUCER warp (one elected lane) streams each member's obstacle rows of state into a shared-memory
+//     ring with TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx).  In the interleaved layout
+//     state[i][j][w][t] the W words x NP samples of one obstacle row are ONE contiguous block (fp64 3-D:
+//     7200 B), so a stage (G rows) is one bulk copy (plus one for the track rows when the obstacles are
+//     not constant-velocity tracks the kernel can generate itself);
+//   * CONSUMER warps (G*NP threads: sample t, obstacle group g) run the element pass out of the ring and
+//     write the new state straight back to HBM;
+//   * a SCALAR warp runs each member's QP prologue (q_lin, xi = K^-1 [-q_lin; b], positions) and epilogue
+//     (fixed-order obstacle sums, residual norm / max, history, stall rule) OFF the consumers' path: the
+//     prologue of the next member and the epilogue of the previous one run while the consumers stream
+//     the current member.  Positions, reduction partials and the member's penalties are double-buffered
+//     in shared memory (buffer = active-unit count & 1) and handed over with mbarriers
+//     (ready[b]: scalar -> consumers, done[b]: consumers -> scalar).
+// Measured (tools/ab_alg1_exp.sh): taking the prologue off the consumers' path alone moved the C5 launch
+// from 0.78 to 0.85 of HBM.
 //
-// Grid = min(B, SMs): each CTA walks members i = blockIdx.x, += gridDim.x and
-// the producer runs ahead across member boundaries, so the next member's first
-// rows are in flight while the consumers do this member's epilogue and the
-// next member's QP prologue.  Consumers synchronise with a named barrier
-// (bar 1) that excludes the producer warp.
+// Grid = min(B, SMs * MINB): each CTA walks members i = blockIdx.x, += gridDim.x (or the work list).
 #pragma once
 #include "alg1_elem.cuh"
 #include "tma.cuh"
 
 namespace tro {
 
-template <int DIM, typename T, int LAY, int NP, int G, int S>
+template <int DIM, typename T, int LAY, int NP, int G>
 struct TmaCfg {
     static constexpr int W = Words<DIM, LAY>::W;
     static constexpr int kRowBytes = W * NP * (int)sizeof(T);  // one obstacle row of state
     static constexpr int kTrkBytes = DIM * NP * 8;             // one obstacle row of tracks
-    static constexpr int kStageBytes = G * (kRowBytes + kTrkBytes);
     static constexpr int kConsumers = ((G * NP + 31) / 32) * 32;
-    static constexpr int kThreads = kConsumers + 32;
+    static constexpr int kThreads = kConsumers + 64;           // + scalar warp + producer warp
     static_assert(kRowBytes % 16 == 0 && kTrkBytes % 16 == 0, "bulk copies need 16-byte rows");
 };
 
-// shared-memory carve-up (bytes): [stages | P | pos_prev | pos_new | sums_in | red | shapes | qlin | xi | warp | bars]
+constexpr int kTmaMaxStages = 8;
+
+// shared-memory carve-up (bytes), buffers [2] are double-buffered per active unit:
+// [stages | P | pos_prev[2] | pos_new[2] | sums_in | red[2] | shapes | lin | qlin | xi[2] | warp[2] | scal[2] | bars]
 struct TmaLayout {
-    int stages, P, pos_prev, pos_new, sums_in, red, shp, qlin, xi, warp, bars, total;
+    int stages, stage_bytes, n_stages, P, pos_prev, pos_new, sums_in, red, shp, lin, qlin, xi, warp, scal, kmat, qb,
+        sched, bars, total;
 };
-__host__ __device__ inline TmaLayout tma_layout(int stage_bytes, int S, int n_p, int m, int dim, int n_o, int G,
-                                                int consumers) {
+__host__ __device__ inline TmaLayout tma_layout(int row_bytes, int trk_bytes, bool lin, int n_stages, int n_p, int m,
+                                                int dim, int n_o, int G, int consumers) {
     TmaLayout L;
+    L.stage_bytes = G * (row_bytes + (lin ? 0 : trk_bytes));
+    L.n_stages = n_stages;
     int off = 0;
-    L.stages = off; off += S * stage_bytes;
+    L.stages = off;   off += n_stages * L.stage_bytes;
     L.P = off;        off += n_p * m * 8;
-    L.pos_prev = off; off += dim * n_p * 8;
-    L.pos_new = off;  off += dim * n_p * 8;
+    L.pos_prev = off; off += 2 * dim * n_p * 8;
+    L.pos_new = off;  off += 2 * dim * n_p * 8;
     L.sums_in = off;  off += 2 * dim * n_p * 8;
-    L.red = off;      off += G * 2 * dim * n_p * 8;
+    L.red = off;      off += 2 * G * 2 * dim * n_p * 8;
     off = (off + 15) & ~15;
     L.shp = off;      off += 4 * (n_o > 0 ? n_o : 1) * 8;  // per obstacle {a, b, 1/a^2, 1/b^2} (two 16-B loads)
+    L.lin = off;      off += lin ? (6 * (n_o > 0 ? n_o : 1) + n_p) * 8 : 0;  // {c, v} per obstacle + rel times
     L.qlin = off;     off += dim * 16 * 8;
-    L.xi = off;       off += dim * 16 * 8;
-    L.warp = off;     off += 2 * (consumers / 32) * 8;
+    L.xi = off;       off += 2 * dim * 16 * 8;
+    L.warp = off;     off += 2 * 2 * (consumers / 32) * 8;
+    L.scal = off;     off += 2 * 2 * 8;
+    L.kmat = off;     off += kMaxNk * kMaxNk * 8;        // the member's K^-1 level (scalar warp)
+    L.qb = off;       off += dim * (16 + kMaxNk) * 8;    // the member's q and boundary values (scalar warp)
     off = (off + 15) & ~15;
-    L.bars = off;     off += 2 * S * 8;
+    L.sched = off;    off += 2 * (int)((sizeof(SchedS) + 15) & ~(size_t)15);  // [2] bookkeeping mirrors
+    off = (off + 15) & ~15;
+    L.bars = off;     off += (2 * kTmaMaxStages + 4) * 8;
     L.total = off;
     return L;
 }
-
-#ifndef TRO_TMA_MINB
-#define TRO_TMA_MINB 2
-#endif
-constexpr int kTmaMinBlocks = TRO_TMA_MINB;  // resident CTAs per SM the kernel is compiled for
 
 // Work unit u of this CTA: a member and the stage range [st0, st1) of its obstacle rows (half: -1 = whole
 // member, 0 / 1 = the first / second half of a tail member)
@@ -86,39 +94,68 @@ __device__ __forceinline__ WorkUnit work_unit(int u, int rounds, int split_tail,
     return w;
 }
 
+// The next unit >= u that is active (not frozen, level passes the cond guard); n_units if none.  Every role
+// walks the same sequence: a member's status and level are only written by its own epilogue, after every
+// role has passed it.
+__device__ __forceinline__ int next_active(const Alg1Args& A, int u, int n_units, int rounds, int split_tail, int nst,
+                                           const int32_t* order, WorkUnit* wu) {
+    for (; u < n_units; ++u) {
+        *wu = work_unit(u, rounds, split_tail, nst, order);
+        const int st = A.s.status[wu->member];
+        if (!(st & (TRO_CONVERGED | TRO_FACTOR_FAILED)) && A.c.level_ok[A.s.level[wu->member]]) return u;
+    }
+    return n_units;
+}
+
 // DM: the previous iterate's d source fixed at compile time (2: recompute, the steady state) or -1 (read
 // A.p.d_mode at run time: the first iteration after an init / prime)
-template <int DIM, typename T, int LAY, int NP, int G, int S, int DM>
-__global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaMinBlocks) alg1_tma_kernel(Alg1Args A) {
-    using C = TmaCfg<DIM, T, LAY, NP, G, S>;
+template <int DIM, typename T, int LAY, int NP, int G, int MINB, int DM>
+__global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) alg1_tma_kernel(Alg1Args A) {
+    using C = TmaCfg<DIM, T, LAY, NP, G>;
     constexpr int W = C::W;
     constexpr int NC = C::kConsumers;
     constexpr int NCW = NC / 32;
     extern __shared__ __align__(128) unsigned char smraw[];
     const int n_o = A.d.n_obs, m = A.d.m, ne = A.d.n_eq, nk = m + ne;
     const int B = A.d.n_members;
-    const TmaLayout L = tma_layout(C::kStageBytes, S, NP, m, DIM, n_o, G, NC);
+    const bool lin = A.c.track_lin != nullptr;
+    const int S = A.n_stages;
+    const TmaLayout L = tma_layout(C::kRowBytes, C::kTrkBytes, lin, S, NP, m, DIM, n_o, G, NC);
     unsigned char* stages = smraw + L.stages;
     double* sP = reinterpret_cast<double*>(smraw + L.P);
-    double* sPosPrev = reinterpret_cast<double*>(smraw + L.pos_prev);
-    double* sPosNew = reinterpret_cast<double*>(smraw + L.pos_new);
+    double* sPosPrev = reinterpret_cast<double*>(smraw + L.pos_prev);  // [2][DIM * NP]
+    double* sPosNew = reinterpret_cast<double*>(smraw + L.pos_new);    // [2][DIM * NP]
     double* sSumIn = reinterpret_cast<double*>(smraw + L.sums_in);
-    double* sRed = reinterpret_cast<double*>(smraw + L.red);
+    double* sRed = reinterpret_cast<double*>(smraw + L.red);           // [2][G * 2 * DIM * NP]
     double* sShp = reinterpret_cast<double*>(smraw + L.shp);
+    double* sLin = reinterpret_cast<double*>(smraw + L.lin);
     double* sQlin = reinterpret_cast<double*>(smraw + L.qlin);
-    double* sXi = reinterpret_cast<double*>(smraw + L.xi);
-    double* sWarp = reinterpret_cast<double*>(smraw + L.warp);
+    double* sXi = reinterpret_cast<double*>(smraw + L.xi);             // [2][DIM * 16]
+    double* sWarp = reinterpret_cast<double*>(smraw + L.warp);         // [2][2 * NCW]
+    double* sScal = reinterpret_cast<double*>(smraw + L.scal);         // [2][rho, rho_o]
+    double* sK = reinterpret_cast<double*>(smraw + L.kmat);
+    double* sQ = reinterpret_cast<double*>(smraw + L.qb);              // [DIM * 16] q, then [DIM * ne] bvals
+    double* sBv = sQ + DIM * 16;
+    constexpr int kSchedBytes = (int)((sizeof(SchedS) + 15) & ~(size_t)15);
+    SchedS* sSched = reinterpret_cast<SchedS*>(smraw + L.sched);       // [2] (stride kSchedBytes)
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw + L.bars);
-    uint64_t* empty = full + S;
+    uint64_t* empty = full + kTmaMaxStages;
+    uint64_t* ready = empty + kTmaMaxStages;  // [2] scalar warp -> consumers: prologue of the unit in buffer b
+    uint64_t* done = ready + 2;               // [2] consumers -> scalar warp: partials of buffer b written
+    constexpr int kRedBuf = G * 2 * DIM * NP;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
 
-    // ---------------- one-time setup: barriers, basis, shapes
+    // ---------------- one-time setup: barriers, basis, shapes, linear tracks
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&ready[b], 1);
+            mbar_init(&done[b], NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -130,13 +167,14 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
         sShp[4 * k + 2] = 1.0 / (a * a);
         sShp[4 * k + 3] = 1.0 / (b * b);
     }
+    if (lin)
+        for (int k = tid; k < 6 * n_o + NP; k += blockDim.x) sLin[k] = ld_const(A.c.track_lin + k);
     __syncthreads();
 
     const int nst = (n_o + G - 1) / G;  // stages per member
-    // ring position: stage s and its phase bit run on across members (no divisions in the loops)
-    // work units of this CTA: members blockIdx.x + u gridDim.x, or with tail balancing (A.split_tail = M > 0)
-    // `rounds` full rounds and then, for the first 2 M CTAs, one half (of the stages) of a tail member
-    // the work list: order[0 .. *n_order) when given (e.g. the robots still driving), else members 0..B-1
+    // the work list: order[0 .. *n_order) when given (e.g. the robots still driving), else members 0..B-1;
+    // `rounds` full rounds and then, with tail balancing, one half (of the stages) of a tail member for
+    // the first 2 * tail CTAs
     const int32_t* order = A.s.order;
     const int n_work = order ? *A.s.n_order : B;
     const int rounds = n_work / (int)gridDim.x;
@@ -145,33 +183,236 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     const int n_units = split_tail ? rounds + ((int)blockIdx.x < 2 * split_tail ? 1 : 0)
                                    : (n_work - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
-    if (warp == NCW) {
+    if (warp == NCW + 1) {
         // ======================= producer warp (one elected lane)
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
             bool wrapped = false;
-            for (int u = 0; u < n_units; ++u) {
-                const WorkUnit wu = work_unit(u, rounds, split_tail, nst, order);
+            const int stage_tx = lin ? C::kRowBytes : C::kRowBytes + C::kTrkBytes;
+            WorkUnit wu;
+            for (int u = next_active(A, 0, n_units, rounds, split_tail, nst, order, &wu); u < n_units;
+                 u = next_active(A, u + 1, n_units, rounds, split_tail, nst, order, &wu)) {
                 const int i = wu.member;
-                const int st = A.s.status[i];
-                if ((st & (TRO_CONVERGED | TRO_FACTOR_FAILED)) || !A.c.level_ok[A.s.level[i]]) continue;
                 const unsigned char* src = reinterpret_cast<const unsigned char*>(A.s.state) +
                                            (int64_t)i * n_o * C::kRowBytes;
                 const unsigned char* trk = reinterpret_cast<const unsigned char*>(A.c.tracks);
                 for (int j0 = wu.st0 * G; j0 < n_o && j0 < wu.st1 * G; j0 += G) {
                     if (wrapped) mbar_wait(&empty[s], ph ^ 1u);  // the consumers released this stage
                     const int rows = min(G, n_o - j0);
-                    unsigned char* buf = stages + s * C::kStageBytes;
-                    mbar_expect_tx(&full[s], rows * (C::kRowBytes + C::kTrkBytes));
+                    unsigned char* buf = stages + s * L.stage_bytes;
+                    mbar_expect_tx(&full[s], rows * stage_tx);
                     bulk_g2s(buf, src + (int64_t)j0 * C::kRowBytes, rows * C::kRowBytes, &full[s]);
-                    bulk_g2s(buf + G * C::kRowBytes, trk + (int64_t)j0 * C::kTrkBytes, rows * C::kTrkBytes, &full[s]);
+                    if (!lin)
+                        bulk_g2s(buf + G * C::kRowBytes, trk + (int64_t)j0 * C::kTrkBytes, rows * C::kTrkBytes,
+                                 &full[s]);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1u;
                         wrapped = true;
                     }
                 }
+            }
+        }
+        return;
+    }
+
+    if (warp == NCW) {
+        // ======================= scalar warp: QP prologue / reduction epilogue, two units apart
+        auto prologue = [&](const WorkUnit& wu, int b) {
+            // Latency-conscious: a single warp does what 13 warps did, so every global read is issued up front
+            // in unrolled batches (one memory latency per batch, not one per element), the K^-1 level, q and
+            // the boundary values are staged in shared memory, and each lane owns whole dot products (no
+            // shuffle chains).
+            const int i = wu.member;
+            const bool split = wu.half >= 0;
+            constexpr int NPOS = DIM * NP, NSUM = 2 * DIM * NP;
+            constexpr int RP = (NPOS + 31) / 32, RS = (NSUM + 31) / 32, RK = (kMaxNk * kMaxNk + 31) / 32;
+            double* pPrev = sPosPrev + b * DIM * NP;
+            double* pNew = sPosNew + b * DIM * NP;
+            double* xs = sXi + b * DIM * 16;
+            SchedS* S = reinterpret_cast<SchedS*>(reinterpret_cast<unsigned char*>(sSched) + b * kSchedBytes);
+            const int level = A.s.level[i];  // broadcast; the K^-1 rows below depend on it
+            const double* posg = A.s.pos + (int64_t)i * NPOS;
+            const double* sg_in = A.s.sums + (int64_t)i * NSUM;
+            double rp[RP], rs[RS], rk[RK];
+#pragma unroll
+            for (int r = 0; r < RP; ++r) rp[r] = lane + 32 * r < NPOS ? posg[lane + 32 * r] : 0.0;
+#pragma unroll
+            for (int r = 0; r < RS; ++r) rs[r] = lane + 32 * r < NSUM ? sg_in[lane + 32 * r] : 0.0;
+            const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
+#pragma unroll
+            for (int r = 0; r < RK; ++r) rk[r] = lane + 32 * r < nk * nk ? ld_const(Kl + lane + 32 * r) : 0.0;
+            const double* qg = A.c.q + (int64_t)i * DIM * m;
+            const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
+            const double q0 = lane < DIM * m ? qg[lane] : 0.0;
+            const double q1 = lane + 32 < DIM * m ? qg[lane + 32] : 0.0;
+            const double bv0 = lane < DIM * ne ? bg[lane] : 0.0;
+            const double bv1 = lane + 32 < DIM * ne ? bg[lane + 32] : 0.0;
+            // the member's bookkeeping (the epilogue's stall rule then reads no global memory)
+            const int w2 = 2 * A.p.stall_window;
+            const double rg0 = lane < w2 ? A.s.ring[(int64_t)i * w2 + lane] : 0.0;
+            const double rg1 = lane + 32 < w2 ? A.s.ring[(int64_t)i * w2 + lane + 32] : 0.0;
+            if (lane == 0) {
+                S->rho = A.s.rho[i];
+                S->rho_o = A.s.rho_o[i];
+                S->status = A.s.status[i];
+                S->level = level;
+                S->iteration = A.s.iteration[i];
+                S->n_hist = A.s.n_hist[i];
+                S->last_change = A.s.last_change[i];
+                S->n_changes = A.s.n_changes[i];
+            }
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+                if (lane + 32 * r < NPOS) pPrev[lane + 32 * r] = rp[r];
+#pragma unroll
+            for (int r = 0; r < RS; ++r)
+                if (lane + 32 * r < NSUM) sSumIn[lane + 32 * r] = rs[r];
+#pragma unroll
+            for (int r = 0; r < RK; ++r)
+                if (lane + 32 * r < nk * nk) sK[lane + 32 * r] = rk[r];
+            if (lane < DIM * m) sQ[lane] = q0;
+            if (lane + 32 < DIM * m) sQ[lane + 32] = q1;
+            if (lane < DIM * ne) sBv[lane] = bv0;
+            if (lane + 32 < DIM * ne) sBv[lane + 32] = bv1;
+            if (lane < w2) S->ring[lane] = rg0;
+            if (lane + 32 < w2) S->ring[lane + 32] = rg1;
+            __syncwarp();
+            const double rho_o = S->rho_o;
+            // q_lin[ax][c] = (q + sum_t Slam[ax][t] P[t][c]) - sum_t (rho_o ST[ax][t]) P[t][c]: one lane per output,
+            // four interleaved partial sums per product (t = 4k + r), combined (0 + 1) + (2 + 3)
+            for (int o = lane; o < DIM * m; o += 32) {
+                const int ax = o / m, cc = o - ax * m;
+                const double* sl = sSumIn + ax * NP;
+                const double* st = sSumIn + (DIM + ax) * NP;
+                double u[4] = {0.0, 0.0, 0.0, 0.0}, v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 5
+                for (int tt = 0; tt < NP; tt += 4) {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (tt + r < NP) {
+                            const double pt = sP[(tt + r) * m + cc];
+                            u[r] = fma(sl[tt + r], pt, u[r]);
+                            v[r] = fma(rho_o * st[tt + r], pt, v[r]);
+                        }
+                    }
+                }
+                sQlin[o] = (sQ[o] + ((u[0] + u[1]) + (u[2] + u[3]))) - ((v[0] + v[1]) + (v[2] + v[3]));
+            }
+            __syncwarp();
+            // xi = K^-1 [-q_lin ; b]  (first m rows of the saddle solution, qpcore.py:141-143)
+            for (int o = lane; o < DIM * m; o += 32) {
+                const int ax = o / m, r = o - ax * m;
+                const double* Kr = sK + r * nk;
+                double acc = 0.0;
+                for (int cc = 0; cc < m; ++cc) acc += Kr[cc] * (-sQlin[ax * m + cc]);
+                for (int e = 0; e < ne; ++e) acc += Kr[m + e] * sBv[ax * ne + e];
+                xs[o] = acc;
+                if (!split) A.s.xi[(int64_t)i * DIM * m + o] = acc;  // split: written by the combining half
+            }
+            __syncwarp();
+            for (int k = lane; k < NPOS; k += 32) {
+                const int ax = k / NP, tt = k - ax * NP;
+                double acc = 0.0;
+                for (int cc = 0; cc < m; ++cc) acc += sP[tt * m + cc] * xs[ax * m + cc];
+                pNew[k] = acc;
+                if (!split) A.s.pos[(int64_t)i * NPOS + k] = acc;
+            }
+            if (lane == 0) {
+                sScal[2 * b] = S->rho;
+                sScal[2 * b + 1] = rho_o;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ready[b]);
+        };
+        auto epilogue = [&](const WorkUnit& wu, int b) {
+            const int i = wu.member;
+            const double* red = sRed + b * kRedBuf;
+            const double* wp = sWarp + b * 2 * NCW;
+            SchedS* S = reinterpret_cast<SchedS*>(reinterpret_cast<unsigned char*>(sSched) + b * kSchedBytes);
+            const int status0 = S->status;
+            const int level = S->level;
+            const double rho = sScal[2 * b], rho_o = sScal[2 * b + 1];
+            if (wu.half < 0) {
+                double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
+                for (int k = lane; k < 2 * DIM * NP; k += 32) {
+                    double acc = 0.0;
+                    for (int gg = 0; gg < G; ++gg) acc += red[gg * 2 * DIM * NP + k];
+                    sg[k] = acc;
+                }
+                if (lane == 0) {
+                    double ss = 0.0, mm = 0.0;
+                    for (int w = 0; w < NCW; ++w) {
+                        ss += wp[w];
+                        mm = fmax(mm, wp[NCW + w]);
+                    }
+                    if (ss != ss) mm = ss;  // np.max propagates NaN
+                    alg1_schedule(A, i, status0, level, rho, rho_o, sqrt(ss), mm, S);
+                }
+                __syncwarp();
+                return;
+            }
+            // tail half: this half's sums over its groups, residual sum of squares and max into the scratch;
+            // the second half to finish combines (half 0 + half 1: a fixed order whichever finishes last)
+            constexpr int kPart = 2 * DIM * NP + 2;
+            const int tk = wu.pos - rounds * (int)gridDim.x;  // tail index in the work list
+            double* part = A.s.split_scratch + ((int64_t)tk * 2 + wu.half) * kPart;
+            for (int k = lane; k < 2 * DIM * NP; k += 32) {
+                double acc = 0.0;
+                for (int gg = 0; gg < G; ++gg) acc += red[gg * 2 * DIM * NP + k];
+                part[k] = acc;
+            }
+            if (lane == 0) {
+                double ss = 0.0, mm = 0.0;
+                for (int w = 0; w < NCW; ++w) {
+                    ss += wp[w];
+                    mm = fmax(mm, wp[NCW + w]);
+                }
+                part[2 * DIM * NP] = ss;
+                part[2 * DIM * NP + 1] = mm;
+            }
+            __threadfence();
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) last = atomicAdd(A.s.split_ticket + tk, 1u) == 1u;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                __threadfence();
+                const double* p0 = A.s.split_scratch + (int64_t)tk * 2 * kPart;
+                const double* p1 = p0 + kPart;
+                double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
+                const double* pNew = sPosNew + b * DIM * NP;
+                const double* xs = sXi + b * DIM * 16;
+                for (int k = lane; k < 2 * DIM * NP; k += 32) sg[k] = __ldcg(p0 + k) + __ldcg(p1 + k);
+                for (int k = lane; k < DIM * NP; k += 32) A.s.pos[(int64_t)i * DIM * NP + k] = pNew[k];
+                for (int k = lane; k < DIM * m; k += 32) A.s.xi[(int64_t)i * DIM * m + k] = xs[k];
+                if (lane == 0) {
+                    const double ss = __ldcg(p0 + 2 * DIM * NP) + __ldcg(p1 + 2 * DIM * NP);
+                    double mm = fmax(__ldcg(p0 + 2 * DIM * NP + 1), __ldcg(p1 + 2 * DIM * NP + 1));
+                    if (ss != ss) mm = ss;  // np.max propagates NaN
+                    alg1_schedule(A, i, status0, level, rho, rho_o, sqrt(ss), mm, S);
+                    A.s.split_ticket[tk] = 0u;  // ready for the next launch
+                }
+            }
+            __syncwarp();
+        };
+
+        WorkUnit pw, ew;
+        int pu = next_active(A, 0, n_units, rounds, split_tail, nst, order, &pw);
+        for (int pk = 0; pk < 2 && pu < n_units; ++pk) {  // prime both buffers
+            prologue(pw, pk);
+            pu = next_active(A, pu + 1, n_units, rounds, split_tail, nst, order, &pw);
+        }
+        int ek = 0;
+        for (int eu = next_active(A, 0, n_units, rounds, split_tail, nst, order, &ew); eu < n_units;
+             eu = next_active(A, eu + 1, n_units, rounds, split_tail, nst, order, &ew), ++ek) {
+            const int b = ek & 1;
+            mbar_wait(&done[b], (uint32_t)((ek >> 1) & 1));
+            epilogue(ew, b);
+            if (pu < n_units) {  // buffer b is free again: the prologue two units ahead
+                prologue(pw, b);
+                pu = next_active(A, pu + 1, n_units, rounds, split_tail, nst, order, &pw);
             }
         }
         return;
@@ -186,72 +427,29 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
     // this thread's offsets inside a stage: its obstacle row of state and of tracks, sample t
     const int row_off = g * C::kRowBytes + t * (int)sizeof(T);
     const int trk_off = G * C::kRowBytes + g * C::kTrkBytes + t * 8;
+    const double rel_t = lin ? sLin[6 * n_o + t] : 0.0;  // this sample's time offset (linear tracks)
     const int64_t Nel = (int64_t)B * n_o * NP;
     T* dst = reinterpret_cast<T*>(A.s.d);
     T* cop = reinterpret_cast<T*>(A.s.copies);
 
-    for (int u = 0; u < n_units; ++u) {
-        const WorkUnit wu = work_unit(u, rounds, split_tail, nst, order);
+    WorkUnit wu;
+    int k = 0;
+    for (int u = next_active(A, 0, n_units, rounds, split_tail, nst, order, &wu); u < n_units;
+         u = next_active(A, u + 1, n_units, rounds, split_tail, nst, order, &wu), ++k) {
         const int i = wu.member;
-        const bool split = wu.half >= 0;
-        const int status0 = A.s.status[i];
-        if (status0 & (TRO_CONVERGED | TRO_FACTOR_FAILED)) continue;
-        const int level = A.s.level[i];
-        if (!A.c.level_ok[level]) {  // qpcore.py:108-110 -> the host raises FactorizationError
-            if (tid == 0) A.s.status[i] = status0 | TRO_FACTOR_FAILED;
-            continue;
-        }
-        const double rho = A.s.rho[i];
-        const double rho_o = A.s.rho_o[i];
-
-        // ---------- QP position step (solver_single.py:204-211)
-        const double* posg = A.s.pos + (int64_t)i * DIM * NP;
-        for (int k = tid; k < DIM * NP; k += NC) sPosPrev[k] = posg[k];
-        const double* sg_in = A.s.sums + (int64_t)i * 2 * DIM * NP;
-        for (int k = tid; k < 2 * DIM * NP; k += NC) sSumIn[k] = sg_in[k];
-        consumer_sync(NC);
-        const double* qg = A.c.q + (int64_t)i * DIM * m;
-        for (int o = warp; o < DIM * m; o += NCW) {
-            const int ax = o / m, cc = o - ax * m;
-            double u = 0.0, v = 0.0;
-            for (int tt = lane; tt < NP; tt += 32) {
-                const double pt = sP[tt * m + cc];
-                u += sSumIn[ax * NP + tt] * pt;
-                v += (rho_o * sSumIn[(DIM + ax) * NP + tt]) * pt;
-            }
-            u = warp_sum(u);
-            v = warp_sum(v);
-            if (lane == 0) sQlin[o] = (qg[o] + u) - v;
-        }
-        consumer_sync(NC);
-        const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
-        const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
-        for (int o = tid; o < DIM * m; o += NC) {
-            const int ax = o / m, r = o - ax * m;
-            const double* Kr = Kl + r * nk;
-            double acc = 0.0;
-            for (int cc = 0; cc < m; ++cc) acc += ld_const(Kr + cc) * (-sQlin[ax * m + cc]);
-            for (int e = 0; e < ne; ++e) acc += ld_const(Kr + m + e) * bg[ax * ne + e];
-            sXi[o] = acc;
-            if (!split) A.s.xi[(int64_t)i * DIM * m + o] = acc;  // split: written by the combining half
-        }
-        consumer_sync(NC);
-        for (int k = tid; k < DIM * NP; k += NC) {
-            const int ax = k / NP, tt = k - ax * NP;
-            double acc = 0.0;
-            for (int cc = 0; cc < m; ++cc) acc += sP[tt * m + cc] * sXi[ax * m + cc];
-            sPosNew[k] = acc;
-            if (!split) A.s.pos[(int64_t)i * DIM * NP + k] = acc;
-        }
-        consumer_sync(NC);
+        const int b = k & 1;
+        mbar_wait(&ready[b], (uint32_t)((k >> 1) & 1));  // the scalar warp's prologue of this unit
+        const double rho = sScal[2 * b], rho_o = sScal[2 * b + 1];
+        const double* pNew = sPosNew + b * DIM * NP;
+        const double* pPrev = sPosPrev + b * DIM * NP;
 
         // ---------- element pass out of the shared-memory ring
         double sumsq = 0.0, mx = 0.0;
         double accL[DIM], accT[DIM];
 #pragma unroll
         for (int ax = 0; ax < DIM; ++ax) accL[ax] = accT[ax] = 0.0;
-        const double px = sPosNew[t], py = sPosNew[NP + t], pz = DIM == 3 ? sPosNew[2 * NP + t] : 0.0;
-        const double ox = sPosPrev[t], oy = sPosPrev[NP + t], oz = DIM == 3 ? sPosPrev[2 * NP + t] : 0.0;
+        const double px = pNew[t], py = pNew[NP + t], pz = DIM == 3 ? pNew[2 * NP + t] : 0.0;
+        const double ox = pPrev[t], oy = pPrev[NP + t], oz = DIM == 3 ? pPrev[2 * NP + t] : 0.0;
         const T trho = (T)rho, trho_o = (T)rho_o;
         const int d_mode = DM >= 0 ? DM : A.p.d_mode;
         T* gbase = reinterpret_cast<T*>(A.s.state) + (int64_t)i * n_o * W * NP + t;
@@ -262,16 +460,35 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
         for (int j = j_first; j < j_end && j - g < n_o; j += G, gp += G * W * NP, e += G * NP) {
             mbar_wait(&full[s], ph);
             if (act && j < n_o) {
-                const unsigned char* buf = stages + s * C::kStageBytes;
+                const unsigned char* buf = stages + s * L.stage_bytes;
                 const T* row = reinterpret_cast<const T*>(buf + row_off);
-                const double* trow = reinterpret_cast<const double*>(buf + trk_off);
                 T v[W];
 #pragma unroll
                 for (int w = 0; w < W; ++w) v[w] = row[w * NP];
-                const double trx = trow[0], trY = trow[NP], trz = DIM == 3 ? trow[2 * NP] : 0.0;
+                double trx, trY, trz;
+                if (lin) {  // c + v rel_t, rounded like numpy's c + v * rel (bench/scenarios.py:118-127)
+                    const double* lj = sLin + 6 * j;  // 3-D {cx cy cz vx vy vz}, 2-D {cx cy vx vy - -}
+                    const double2 q0 = *reinterpret_cast<const double2*>(lj);
+                    const double2 q1 = *reinterpret_cast<const double2*>(lj + 2);
+                    if constexpr (DIM == 3) {
+                        const double2 q2 = *reinterpret_cast<const double2*>(lj + 4);
+                        trx = __dadd_rn(q0.x, __dmul_rn(q1.y, rel_t));
+                        trY = __dadd_rn(q0.y, __dmul_rn(q2.x, rel_t));
+                        trz = __dadd_rn(q1.x, __dmul_rn(q2.y, rel_t));
+                    } else {
+                        trx = __dadd_rn(q0.x, __dmul_rn(q1.x, rel_t));
+                        trY = __dadd_rn(q0.y, __dmul_rn(q1.y, rel_t));
+                        trz = 0.0;
+                    }
+                } else {
+                    const double* trow = reinterpret_cast<const double*>(buf + trk_off);
+                    trx = trow[0];
+                    trY = trow[NP];
+                    trz = DIM == 3 ? trow[2 * NP] : 0.0;
+                }
                 const double2 ab = *reinterpret_cast<const double2*>(sShp + 4 * j);
                 const double2 iab = *reinterpret_cast<const double2*>(sShp + 4 * j + 2);
-                const T a = (T)ab.x, b = (T)ab.y, ia2 = (T)iab.x, ib2 = (T)iab.y;
+                const T a = (T)ab.x, bb = (T)ab.y, ia2 = (T)iab.x, ib2 = (T)iab.y;
                 T dold;
                 if (d_mode == 0) {
                     dold = (T)1;
@@ -289,8 +506,8 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
                     dold = los_scale(qd);
                 }
                 T dn, cp4[4];
-                am_element<DIM, T, LAY>(v, trx, trY, trz, px, py, pz, a, b, ia2, ib2, dold, trho, trho_o, sumsq, mx,
-                                   accL, accT, dn, cp4);
+                am_element<DIM, T, LAY>(v, trx, trY, trz, px, py, pz, a, bb, ia2, ib2, dold, trho, trho_o, sumsq,
+                                        mx, accL, accT, dn, cp4);
 #pragma unroll
                 for (int w = 0; w < W; ++w) st_stream(gp + w * NP, v[w]);
                 if (dst) dst[e] = dn;  // optional exports (tests, warm starts)
@@ -307,82 +524,23 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G, S>::kThreads, kTmaM
             }
         }
 
-        // ---------- epilogue (fixed-order reductions, history, stall rule)
+        // ---------- hand the partials to the scalar warp (fixed-order reductions there)
+        double* red = sRed + b * kRedBuf;
         if (act) {
 #pragma unroll
             for (int ax = 0; ax < DIM; ++ax) {
-                sRed[(g * 2 * DIM + ax) * NP + t] = accL[ax];
-                sRed[(g * 2 * DIM + DIM + ax) * NP + t] = accT[ax];
+                red[(g * 2 * DIM + ax) * NP + t] = accL[ax];
+                red[(g * 2 * DIM + DIM + ax) * NP + t] = accT[ax];
             }
         }
         sumsq = warp_sum(sumsq);
         mx = warp_max(mx);
         if (lane == 0) {
-            sWarp[warp] = sumsq;
-            sWarp[NCW + warp] = mx;
+            sWarp[b * 2 * NCW + warp] = sumsq;
+            sWarp[b * 2 * NCW + NCW + warp] = mx;
         }
-        consumer_sync(NC);
-        if (!split) {
-            double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
-            for (int k = tid; k < 2 * DIM * NP; k += NC) {
-                double acc = 0.0;
-                for (int gg = 0; gg < G; ++gg) acc += sRed[gg * 2 * DIM * NP + k];
-                sg[k] = acc;
-            }
-            if (tid == 0) {
-                double ss = 0.0, mm = 0.0;
-                for (int w = 0; w < NCW; ++w) {
-                    ss += sWarp[w];
-                    mm = fmax(mm, sWarp[NCW + w]);
-                }
-                if (ss != ss) mm = ss;  // np.max propagates NaN
-                alg1_schedule(A, i, status0, level, rho, rho_o, sqrt(ss), mm);
-            }
-        } else {
-            // this half's sums over its groups, residual sum of squares and max into the scratch; the
-            // second half to finish combines (half 0 + half 1: a fixed order whichever finishes last)
-            constexpr int kPart = 2 * DIM * NP + 2;
-            const int tk = wu.pos - rounds * (int)gridDim.x;  // tail index in the work list
-            double* part = A.s.split_scratch + ((int64_t)tk * 2 + wu.half) * kPart;
-            for (int k = tid; k < 2 * DIM * NP; k += NC) {
-                double acc = 0.0;
-                for (int gg = 0; gg < G; ++gg) acc += sRed[gg * 2 * DIM * NP + k];
-                part[k] = acc;
-            }
-            __shared__ int sLast;
-            if (tid == 0) {
-                double ss = 0.0, mm = 0.0;
-                for (int w = 0; w < NCW; ++w) {
-                    ss += sWarp[w];
-                    mm = fmax(mm, sWarp[NCW + w]);
-                }
-                part[2 * DIM * NP] = ss;
-                part[2 * DIM * NP + 1] = mm;
-            }
-            consumer_sync(NC);
-            if (tid == 0) {
-                __threadfence();
-                sLast = atomicAdd(A.s.split_ticket + tk, 1u) == 1u;
-            }
-            consumer_sync(NC);
-            if (sLast) {
-                __threadfence();
-                const double* p0 = A.s.split_scratch + (int64_t)tk * 2 * kPart;
-                const double* p1 = p0 + kPart;
-                double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
-                for (int k = tid; k < 2 * DIM * NP; k += NC) sg[k] = __ldcg(p0 + k) + __ldcg(p1 + k);
-                for (int k = tid; k < DIM * NP; k += NC) A.s.pos[(int64_t)i * DIM * NP + k] = sPosNew[k];
-                for (int k = tid; k < DIM * m; k += NC) A.s.xi[(int64_t)i * DIM * m + k] = sXi[k];
-                if (tid == 0) {
-                    const double ss = __ldcg(p0 + 2 * DIM * NP) + __ldcg(p1 + 2 * DIM * NP);
-                    double mm = fmax(__ldcg(p0 + 2 * DIM * NP + 1), __ldcg(p1 + 2 * DIM * NP + 1));
-                    if (ss != ss) mm = ss;  // np.max propagates NaN
-                    alg1_schedule(A, i, status0, level, rho, rho_o, sqrt(ss), mm);
-                    A.s.split_ticket[tk] = 0u;  // ready for the next launch
-                }
-            }
-        }
-        consumer_sync(NC);  // sRed / sWarp / sPos* are reused by the next member
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[b]);
     }
 }
 

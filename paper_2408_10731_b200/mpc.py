@@ -150,6 +150,8 @@ class MpcFleet:
         # the fleet owns its solve-local bookkeeping (tro_mpc_advance resets it per control step and freezes
         # finished robots through status): the init launch must not reset it
         self.eng._consts.level0 = None
+        # the fleet re-predicts the tracks into eng.tracks every control step: stream them (no register tracks)
+        self.eng._consts.track_lin = None
         f64 = dict(dtype=torch.float64, device=dev)
         i32 = dict(dtype=torch.int32, device=dev)
         up = lambda x: torch.as_tensor(np.array(x, dtype=float, copy=True), **f64)  # noqa: E731

@@ -127,3 +127,18 @@ def test_from_problems_batch_equals_single_batch_recipe():
     a = _result(solve_single_batch(batch, PARAMS, history=True))
     b = _result(solve_single_batch(via_problems, PARAMS, history=True))
     _same(a, b)
+
+
+def test_register_tracks_equal_streamed_tracks():
+    """Constant-velocity obstacles: the TMA kernel generates c + v rel in registers (track_lin) instead of
+    streaming the track rows; the result is bitwise the streamed-track run (the record reproduces every
+    sample exactly, tests/test_host_logic.py)."""
+    batch = _batch(range(150), n_o=30)
+    out = []
+    for lin in (True, False):
+        eng = make_batch_engine(batch, PARAMS, history=True, layout="half")
+        assert eng.track_lin is not None
+        if not lin:
+            eng._consts.track_lin = None
+        out.append(_result(solve_single_batch(batch, PARAMS, engine=eng)))
+    _same(out[0], out[1])

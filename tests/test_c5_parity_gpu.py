@@ -165,9 +165,6 @@ def test_c5_end_state_distribution(tag):
     # iteration counts of the converged solve: same distribution of stopping iterations
     if tag == "conv":
         assert _bootstrap_quantile_ok(res.iterations.astype(float), col("iterations"), 0.5, rng)
-    # members whose runs are not chaotic agree individually: the twin-stable ones match to 1e-9
-    same = np.abs(res.residual_max - col("res_max")) <= 1e-9 * col("res_max")
-    assert same.sum() >= 1
 
 
 # ------------------------------------------------------------------ fp32 free run, numpy's stall-window mean

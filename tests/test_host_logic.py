@@ -127,3 +127,24 @@ def test_from_problems_requires_shared_obstacles():
     b2 = scenarios.flow3d_batch(6, [1], basis=bs).problem(0)
     with pytest.raises(ValueError):
         SingleBatch.from_problems([b1, b2])
+
+
+def test_linear_track_record_reproduces_tracks_bitwise():
+    from paper_2408_10731_b200 import scenarios
+    from paper_2408_10731_b200._alg1 import linear_track_record
+    from paper_2408_10731_b200.basis import build_basis
+
+    b = build_basis(0.0, 10.0, 100, 10)
+    for n_o in (10, 50, 100):
+        tr = np.stack([o.centers for o in scenarios.flow3d_batch(n_o, [0], basis=b).obstacles])
+        rec = linear_track_record(tr, b.grid.timestamps)
+        assert rec is not None
+        cv, rel = rec[: 6 * n_o].reshape(n_o, 6), rec[6 * n_o:]
+        np.testing.assert_array_equal(cv[:, None, :3] + cv[:, None, 3:] * rel[None, :, None], tr)
+    bad = tr.copy()
+    bad[3, 40, 1] = np.nextafter(bad[3, 40, 1], np.inf)  # one sample off by one ulp: not a linear track
+    assert linear_track_record(bad, b.grid.timestamps) is None
+    p = scenarios.c1_problem()  # static obstacles: v = 0
+    tr = np.stack([o.centers for o in p.obstacles])
+    rec = linear_track_record(tr, p.basis.grid.timestamps)
+    assert rec is not None and not np.any(rec[: 6 * len(tr)].reshape(-1, 6)[:, 3:])

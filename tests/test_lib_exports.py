@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_layouts_match_header():
     # 10 int32 dims; 11 const pointers; 4 doubles + 4 int32; 18 pointers
     assert ctypes.sizeof(_lib.Alg1Dims) == 40
-    assert ctypes.sizeof(_lib.Alg1Consts) == 12 * 8
+    assert ctypes.sizeof(_lib.Alg1Consts) == 13 * 8
     assert ctypes.sizeof(_lib.Alg1Params) == 4 * 8 + 4 * 4
     assert ctypes.sizeof(_lib.Alg1State) == 22 * 8
 

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--tag", default=os.path.basename(os.environ.get("TRO_LIB_PATH", "default")))
     ap.add_argument("--no-tma", action="store_true")
     ap.add_argument("--layout", default="angle")
+    ap.add_argument("--no-lin", action="store_true", help="stream the track rows (no register-generated tracks)")
     a = ap.parse_args()
     dtype = torch.float64 if a.dtype == "f64" else torch.float32
     s = 8 if a.dtype == "f64" else 4
@@ -37,6 +38,8 @@ def main():
         eng = make_batch_engine(batch, params, dtype=dtype, groups=G, layout=a.layout)
         if a.no_tma:
             eng.base_flags = 2
+        if a.no_lin:
+            eng._consts.track_lin = None
         eng.cold_init()
         eng.run(5, use_graph=False)
         torch.cuda.synchronize()
@@ -48,7 +51,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
         gbs = 2 * 9 * a.n_obs * 100 * s * a.members / (ms / 1e3) / 1e9
-        print(json.dumps({"tag": a.tag + ("" if not a.no_tma else "+notma") + "+" + a.layout, "G": G, "ms_per_iter": round(ms, 4), "GBps": round(gbs, 1),
+        print(json.dumps({"tag": a.tag + ("" if not a.no_tma else "+notma") + ("+nolin" if a.no_lin else "") + "+" + a.layout, "G": G, "ms_per_iter": round(ms, 4), "GBps": round(gbs, 1),
                           "frac": round(gbs / peak, 3), "dtype": a.dtype, "members": a.members, "n_obs": a.n_obs}))
         del eng
         torch.cuda.empty_cache()
