@@ -22,7 +22,7 @@ __device__ __forceinline__ void unit_dir(double c, double s, double* cu, double*
 __device__ __forceinline__ void unit_dir(float c, float s, float* cu, float* su) {
     const float h2 = fmaf(c, c, s * s);
     if (h2 > 0.0f) {
-        const float r = rsqrtf(h2);
+        const float r = rsqrt_fast(h2);
         *cu = c * r;
         *su = s * r;
     } else {

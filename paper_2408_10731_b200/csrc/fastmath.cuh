@@ -151,10 +151,30 @@ __device__ __forceinline__ void unit2(double x, double y, double* c, double* s) 
 }
 
 // ---------------------------------------------------------------- fp32
+// fp32 storage builds are held to 1e-4 (north_star): the hardware approximations (one MUFU each, <= 2 ulp)
+// replace the correctly rounded IEEE sequences, which cost ~10 instructions apiece
+#ifndef TRO_F32_IEEE
+__device__ __forceinline__ float rcp_fast(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rsqrt_fast(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_fast(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+#else
 __device__ __forceinline__ float rcp_fast(float x) { return __frcp_rn(x); }
-__device__ __forceinline__ float rcp_fast2ulp(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ float rsqrt_fast(float x) { return rsqrtf(x); }
 __device__ __forceinline__ float sqrt_fast(float x) { return sqrtf(x); }
+#endif
+__device__ __forceinline__ float rcp_fast2ulp(float x) { return rcp_fast(x); }
 
 __device__ __forceinline__ void sincos_fast(float x, float* s, float* c) {
     if (fabsf(x) > 1.0e4f) {
@@ -181,7 +201,7 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
     const bool swap = ay > ax;
     const float mx = swap ? ay : ax, mn = swap ? ax : ay;
     const bool big = mn > 0.414213562f * mx;
-    const float t = (big ? mn - mx : mn) * __frcp_rn((big ? mn + mx : mx) + 1e-37f);
+    const float t = (big ? mn - mx : mn) * rcp_fast((big ? mn + mx : mx) + 1e-37f);
     const float z = t * t;
     // t - t z (1/3 - z/5 + z^2/7 - z^3/9 + z^4/11 - z^5/13 + z^6/15)
     const float p = fmaf(z, fmaf(z, fmaf(z, fmaf(z, fmaf(z, fmaf(z, 0.0666666667f, -0.0769230769f), 0.0909090909f),
