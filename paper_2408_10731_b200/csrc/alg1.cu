@@ -407,9 +407,20 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                     }
                 }
             } else {
-                T dn, cp4[4];
-                am_element<DIM, T, LAY>(v, trx, trY, trz, px, py, pz, (T)sA[j], (T)sB[j], ia2, ib2, dold, trho,
-                                         trho_o, sumsq, mx, accL, accT, dn, cp4);
+                T dn, cp4[4], ss, ml, off[DIM];
+                am_element<DIM, T, LAY>(v, (T)(px - trx), (T)(py - trY), (T)(pz - trz), (T)sA[j], (T)sB[j], ia2, ib2,
+                                        dold, trho, trho_o, ss, ml, off, dn, cp4);
+                sumsq += (double)ss;
+                mx = (double)ml > mx ? (double)ml : mx;
+                constexpr int o = Words<DIM, LAY>::NV;
+                accL[0] += (double)v[o];
+                accL[1] += (double)v[o + 1];
+                accT[0] += trx + (double)off[0];
+                accT[1] += trY + (double)off[1];
+                if constexpr (DIM == 3) {
+                    accL[2] += (double)v[o + 2];
+                    accT[2] += trz + (double)off[2];
+                }
 #pragma unroll
                 for (int w = 0; w < W; ++w) st_stream(sp + w * n_p, v[w]);
                 if (dst) dst[e] = dn;
@@ -534,7 +545,7 @@ static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
     if (dev >= 0 && dev < 64 && !attr_set[dev]) {
         cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, -1>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
-        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, 2>,
+        cudaFuncSetAttribute(alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, 2, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
         attr_set[dev] = 1;
     }
@@ -551,8 +562,8 @@ static int launch_tma(const Alg1Args& A, cudaStream_t st, int* rc) {
         return 1;
     }
 #if TRO_TMA_DM_SPEC
-    if (A.p.d_mode == 2)
-        alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, 2><<<grid, C::kThreads, total, st>>>(B);
+    if (A.p.d_mode == 2 && !A.s.d && !A.s.copies)
+        alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, 2, false><<<grid, C::kThreads, total, st>>>(B);
     else
 #endif
         alg1_tma_kernel<DIM, T, LAY, 100, G, MINB, -1><<<grid, C::kThreads, total, st>>>(B);

@@ -133,17 +133,16 @@ __device__ __forceinline__ void half_encode2(T c1, T s1, T c2, T s2, T* w1, T* w
     *w2 = p2 ? t2 : copysign((T)3, s2) - t2;
 }
 
-// One AM iteration of one element.  v[W]: state words in / out.  d_old: the
-// line-of-sight scale of the previous iterate.  Outputs the new d, the angle
-// copies (for the optional export), and accumulates the residual norm/max and
-// the sums the next position step needs.
+// One AM iteration of one element.  v[W]: state words in / out.  (dx, dy, dz): the new position minus the
+// obstacle centre.  d_old: the line-of-sight scale of the previous iterate.  Outputs the new d, the angle
+// copies (for the optional export), the element's residual sum of squares `ss` and max-abs `ml`, and the
+// target offsets off[] = target - obstacle centre the next position step sums (solver_single.py:177-189);
+// the new position multipliers are v[o .. o + DIM).  The caller accumulates (in double, or in the storage
+// type inside a thread for the fp32 build).
 template <int DIM, typename T, int LAY>
-__device__ __forceinline__ void am_element(T* v, double trx, double trY, double trz, double px, double py, double pz,
-                                           T a, T b, T ia2, T ib2, T dold, T trho, T trho_o, double& sumsq,
-                                           double& mx, double* accL, double* accT, T& dn, T* copies) {
-    const T dx = (T)(px - trx), dy = (T)(py - trY);
+__device__ __forceinline__ void am_element(T* v, T dx, T dy, T dz, T a, T b, T ia2, T ib2, T dold, T trho, T trho_o,
+                                           T& ss_out, T& ml_out, T* off, T& dn, T* copies) {
     if constexpr (DIM == 3) {
-        const T dz = (T)(pz - trz);
         constexpr int o = LAY == kLayUnit ? 4 : 2;  // first multiplier word
         T sa, ca, sb, cb;
         if constexpr (LAY == kLayUnit) {
@@ -190,23 +189,21 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         T ss = rx * rx;
         ss = fma(ry, ry, ss); ss = fma(rz, rz, ss); ss = fma(rcb, rcb, ss);
         ss = fma(rsb, rsb, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
-        sumsq += (double)ss;
+        ss_out = ss;
         T ml = max_mag(rx, ry);
         ml = max_mag(ml, rz); ml = max_mag(ml, rcb);
         ml = max_mag(ml, rsb); ml = max_mag(ml, rca); ml = max_mag(ml, rsa);
-        ml = fabs(ml);
-        mx = (double)ml > mx ? (double)ml : mx;
+        ml_out = fabs(ml);
         // multiplier ascent (solver_single.py:336-343)
         v[o] = lx + trho_o * rx; v[o + 1] = ly + trho_o * ry; v[o + 2] = lz + trho_o * rz;
         v[o + 3] = lca + trho * rca; v[o + 4] = lsa + trho * rsa;
         v[o + 5] = lcb + trho * rcb; v[o + 6] = lsb + trho * rsb;
         copies[0] = ca2; copies[1] = sa2; copies[2] = cb2; copies[3] = sb2;
-        // sums for the next position step with the reset copies cos/sin of the new angles
-        // (solver_single.py:177-189, 204-207)
-        accL[0] += (double)v[o]; accL[1] += (double)v[o + 1]; accL[2] += (double)v[o + 2];
-        accT[0] += trx + (double)(adn * cA2 * sB2);
-        accT[1] += trY + (double)(adn * sA2 * sB2);
-        accT[2] += trz + (double)(b * dn * cB2);
+        // the next position step's targets use the reset copies cos/sin of the new angles (solver_single.py:
+        // 177-189, 204-207)
+        off[0] = adn * cA2 * sB2;
+        off[1] = adn * sA2 * sB2;
+        off[2] = b * dn * cB2;
     } else {
         constexpr int o = LAY == kLayUnit ? 2 : 1;
         T sa, ca;
@@ -237,17 +234,15 @@ __device__ __forceinline__ void am_element(T* v, double trx, double trY, double 
         const T rca = ca2 - cA2, rsa = sa2 - sA2;
         T ss = rx * rx;
         ss = fma(ry, ry, ss); ss = fma(rca, rca, ss); ss = fma(rsa, rsa, ss);
-        sumsq += (double)ss;
+        ss_out = ss;
         T ml = max_mag(rx, ry);
         ml = max_mag(ml, rca); ml = max_mag(ml, rsa);
-        ml = fabs(ml);
-        mx = (double)ml > mx ? (double)ml : mx;
+        ml_out = fabs(ml);
         v[o] = lx + trho_o * rx; v[o + 1] = ly + trho_o * ry;
         v[o + 2] = lca + trho * rca; v[o + 3] = lsa + trho * rsa;
         copies[0] = ca2; copies[1] = sa2;
-        accL[0] += (double)v[o]; accL[1] += (double)v[o + 1];
-        accT[0] += trx + (double)(a * dn * cA2);
-        accT[1] += trY + (double)(b * dn * sA2);
+        off[0] = a * dn * cA2;
+        off[1] = b * dn * sA2;
     }
 }
 

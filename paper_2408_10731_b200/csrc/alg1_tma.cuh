@@ -39,8 +39,8 @@ constexpr int kTmaMaxStages = 8;
 // shared-memory carve-up (bytes), buffers [2] are double-buffered per active unit:
 // [stages | P | pos_prev[2] | pos_new[2] | sums_in | red[2] | shapes | lin | qlin | xi[2] | warp[2] | scal[2] | bars]
 struct TmaLayout {
-    int stages, stage_bytes, n_stages, P, pos_prev, pos_new, sums_in, red, shp, lin, qlin, xi, warp, scal, kmat, qb,
-        sched, bars, total;
+    int stages, stage_bytes, n_stages, P, pos_prev, pos_new, sums_in, red, shp, lin, shpT, linT, trks, qlin, xi, warp,
+        scal, kmat, qb, sched, bars, total;
 };
 __host__ __device__ inline TmaLayout tma_layout(int row_bytes, int trk_bytes, bool lin, int n_stages, int n_p, int m,
                                                 int dim, int n_o, int G, int consumers) {
@@ -57,6 +57,11 @@ __host__ __device__ inline TmaLayout tma_layout(int row_bytes, int trk_bytes, bo
     off = (off + 15) & ~15;
     L.shp = off;      off += 4 * (n_o > 0 ? n_o : 1) * 8;  // per obstacle {a, b, 1/a^2, 1/b^2} (two 16-B loads)
     L.lin = off;      off += lin ? (6 * (n_o > 0 ? n_o : 1) + n_p) * 8 : 0;  // {c, v} per obstacle + rel times
+    L.shpT = off;     off += 4 * (n_o > 0 ? n_o : 1) * 4;  // fp32 builds: the shape records in float
+    off = (off + 15) & ~15;
+    L.linT = off;     off += lin ? (6 * (n_o > 0 ? n_o : 1) + n_p) * 4 : 0;  // fp32 builds: the track records
+    off = (off + 15) & ~15;
+    L.trks = off;     off += dim * n_p * 8;  // sum over obstacles of the track centres per (axis, sample)
     L.qlin = off;     off += dim * 16 * 8;
     L.xi = off;       off += 2 * dim * 16 * 8;
     L.warp = off;     off += 2 * 2 * (consumers / 32) * 8;
@@ -108,8 +113,9 @@ __device__ __forceinline__ int next_active(const Alg1Args& A, int u, int n_units
 }
 
 // DM: the previous iterate's d source fixed at compile time (2: recompute, the steady state) or -1 (read
-// A.p.d_mode at run time: the first iteration after an init / prime)
-template <int DIM, typename T, int LAY, int NP, int G, int MINB, int DM>
+// A.p.d_mode at run time: the first iteration after an init / prime).  EXP: the optional d / copies exports
+// exist (false: compiled out, the steady state of the benchmarks)
+template <int DIM, typename T, int LAY, int NP, int G, int MINB, int DM, bool EXP = true>
 __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) alg1_tma_kernel(Alg1Args A) {
     using C = TmaCfg<DIM, T, LAY, NP, G>;
     constexpr int W = C::W;
@@ -129,6 +135,9 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
     double* sRed = reinterpret_cast<double*>(smraw + L.red);           // [2][G * 2 * DIM * NP]
     double* sShp = reinterpret_cast<double*>(smraw + L.shp);
     double* sLin = reinterpret_cast<double*>(smraw + L.lin);
+    float* sShpF = reinterpret_cast<float*>(smraw + L.shpT);
+    float* sLinF = reinterpret_cast<float*>(smraw + L.linT);
+    double* sTrk = reinterpret_cast<double*>(smraw + L.trks);  // [DIM * NP]
     double* sQlin = reinterpret_cast<double*>(smraw + L.qlin);
     double* sXi = reinterpret_cast<double*>(smraw + L.xi);             // [2][DIM * 16]
     double* sWarp = reinterpret_cast<double*>(smraw + L.warp);         // [2][2 * NCW]
@@ -169,6 +178,30 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
     }
     if (lin)
         for (int k = tid; k < 6 * n_o + NP; k += blockDim.x) sLin[k] = ld_const(A.c.track_lin + k);
+    if constexpr (sizeof(T) == 4) {
+        for (int k = tid; k < 4 * n_o; k += blockDim.x) {
+            const double a = ld_const(A.c.shape_a + k / 4), b = ld_const(A.c.shape_b + k / 4);
+            const int c = k & 3;
+            sShpF[k] = (float)(c == 0 ? a : c == 1 ? b : c == 2 ? 1.0 / (a * a) : 1.0 / (b * b));
+        }
+        if (lin)
+            for (int k = tid; k < 6 * n_o + NP; k += blockDim.x) sLinF[k] = (float)ld_const(A.c.track_lin + k);
+    }
+    __syncthreads();  // sLin complete
+    // the obstacle-summed track centres of every sample: the target sums the next position step needs are
+    // sum_j (centre_j + offset_j); the consumers accumulate only the offsets and the epilogue adds these
+    for (int k = tid; k < DIM * NP; k += blockDim.x) {
+        const int ax = k / NP, tt = k - ax * NP;
+        double acc = 0.0;
+        if (lin) {
+            const double rel = sLin[6 * n_o + tt];
+            for (int j = 0; j < n_o; ++j)
+                acc += __dadd_rn(sLin[6 * j + ax], __dmul_rn(sLin[6 * j + DIM + ax], rel));
+        } else {
+            for (int j = 0; j < n_o; ++j) acc += ld_const(A.c.tracks + ((int64_t)j * DIM + ax) * NP + tt);
+        }
+        sTrk[k] = acc;
+    }
     __syncthreads();
 
     const int nst = (n_o + G - 1) / G;  // stages per member
@@ -339,7 +372,7 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
                 for (int k = lane; k < 2 * DIM * NP; k += 32) {
                     double acc = 0.0;
                     for (int gg = 0; gg < G; ++gg) acc += red[gg * 2 * DIM * NP + k];
-                    sg[k] = acc;
+                    sg[k] = k < DIM * NP ? acc : acc + sTrk[k - DIM * NP];
                 }
                 if (lane == 0) {
                     double ss = 0.0, mm = 0.0;
@@ -384,7 +417,10 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
                 double* sg = A.s.sums + (int64_t)i * 2 * DIM * NP;
                 const double* pNew = sPosNew + b * DIM * NP;
                 const double* xs = sXi + b * DIM * 16;
-                for (int k = lane; k < 2 * DIM * NP; k += 32) sg[k] = __ldcg(p0 + k) + __ldcg(p1 + k);
+                for (int k = lane; k < 2 * DIM * NP; k += 32) {
+                    const double h = __ldcg(p0 + k) + __ldcg(p1 + k);
+                    sg[k] = k < DIM * NP ? h : h + sTrk[k - DIM * NP];
+                }
                 for (int k = lane; k < DIM * NP; k += 32) A.s.pos[(int64_t)i * DIM * NP + k] = pNew[k];
                 for (int k = lane; k < DIM * m; k += 32) A.s.xi[(int64_t)i * DIM * m + k] = xs[k];
                 if (lane == 0) {
@@ -429,8 +465,8 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
     const int trk_off = G * C::kRowBytes + g * C::kTrkBytes + t * 8;
     const double rel_t = lin ? sLin[6 * n_o + t] : 0.0;  // this sample's time offset (linear tracks)
     const int64_t Nel = (int64_t)B * n_o * NP;
-    T* dst = reinterpret_cast<T*>(A.s.d);
-    T* cop = reinterpret_cast<T*>(A.s.copies);
+    T* dst = EXP ? reinterpret_cast<T*>(A.s.d) : nullptr;
+    T* cop = EXP ? reinterpret_cast<T*>(A.s.copies) : nullptr;
 
     WorkUnit wu;
     int k = 0;
@@ -444,12 +480,13 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
         const double* pPrev = sPosPrev + b * DIM * NP;
 
         // ---------- element pass out of the shared-memory ring
-        double sumsq = 0.0, mx = 0.0;
-        double accL[DIM], accT[DIM];
+        // per-thread accumulation in the storage type (fp32 builds: no double conversions per element; the
+        // partials are widened once per member)
+        T sumsq = (T)0, mx = (T)0, accL[DIM], accO[DIM];
 #pragma unroll
-        for (int ax = 0; ax < DIM; ++ax) accL[ax] = accT[ax] = 0.0;
-        const double px = pNew[t], py = pNew[NP + t], pz = DIM == 3 ? pNew[2 * NP + t] : 0.0;
-        const double ox = pPrev[t], oy = pPrev[NP + t], oz = DIM == 3 ? pPrev[2 * NP + t] : 0.0;
+        for (int ax = 0; ax < DIM; ++ax) accL[ax] = accO[ax] = (T)0;
+        const T px = (T)pNew[t], py = (T)pNew[NP + t], pz = DIM == 3 ? (T)pNew[2 * NP + t] : (T)0;
+        const T ox = (T)pPrev[t], oy = (T)pPrev[NP + t], oz = DIM == 3 ? (T)pPrev[2 * NP + t] : (T)0;
         const T trho = (T)rho, trho_o = (T)rho_o;
         const int d_mode = DM >= 0 ? DM : A.p.d_mode;
         T* gbase = reinterpret_cast<T*>(A.s.state) + (int64_t)i * n_o * W * NP + t;
@@ -465,55 +502,87 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
                 T v[W];
 #pragma unroll
                 for (int w = 0; w < W; ++w) v[w] = row[w * NP];
-                double trx, trY, trz;
-                if (lin) {  // c + v rel_t, rounded like numpy's c + v * rel (bench/scenarios.py:118-127)
-                    const double* lj = sLin + 6 * j;  // 3-D {cx cy cz vx vy vz}, 2-D {cx cy vx vy - -}
-                    const double2 q0 = *reinterpret_cast<const double2*>(lj);
-                    const double2 q1 = *reinterpret_cast<const double2*>(lj + 2);
-                    if constexpr (DIM == 3) {
-                        const double2 q2 = *reinterpret_cast<const double2*>(lj + 4);
-                        trx = __dadd_rn(q0.x, __dmul_rn(q1.y, rel_t));
-                        trY = __dadd_rn(q0.y, __dmul_rn(q2.x, rel_t));
-                        trz = __dadd_rn(q1.x, __dmul_rn(q2.y, rel_t));
-                    } else {
-                        trx = __dadd_rn(q0.x, __dmul_rn(q1.x, rel_t));
-                        trY = __dadd_rn(q0.y, __dmul_rn(q1.y, rel_t));
-                        trz = 0.0;
+                T trx, trY, trz;
+                if (lin) {
+                    if constexpr (sizeof(T) == 8) {  // c + v rel_t rounded like numpy's c + v * rel (bitwise)
+                        const double* lj = sLin + 6 * j;  // 3-D {cx cy cz vx vy vz}, 2-D {cx cy vx vy - -}
+                        const double2 q0 = *reinterpret_cast<const double2*>(lj);
+                        const double2 q1 = *reinterpret_cast<const double2*>(lj + 2);
+                        if constexpr (DIM == 3) {
+                            const double2 q2 = *reinterpret_cast<const double2*>(lj + 4);
+                            trx = __dadd_rn(q0.x, __dmul_rn(q1.y, rel_t));
+                            trY = __dadd_rn(q0.y, __dmul_rn(q2.x, rel_t));
+                            trz = __dadd_rn(q1.x, __dmul_rn(q2.y, rel_t));
+                        } else {
+                            trx = __dadd_rn(q0.x, __dmul_rn(q1.x, rel_t));
+                            trY = __dadd_rn(q0.y, __dmul_rn(q1.y, rel_t));
+                            trz = 0.0;
+                        }
+                    } else {  // fp32 build: the track in float (1e-4 contract)
+                        const float* lj = sLinF + 6 * j;
+                        const float relf = (float)rel_t;
+                        const float2 q0 = *reinterpret_cast<const float2*>(lj);
+                        const float2 q1 = *reinterpret_cast<const float2*>(lj + 2);
+                        const float2 q2 = *reinterpret_cast<const float2*>(lj + 4);
+                        if constexpr (DIM == 3) {
+                            trx = fmaf(q1.y, relf, q0.x);
+                            trY = fmaf(q2.x, relf, q0.y);
+                            trz = fmaf(q2.y, relf, q1.x);
+                        } else {
+                            trx = fmaf(q1.x, relf, q0.x);
+                            trY = fmaf(q1.y, relf, q0.y);
+                            trz = 0.0f;
+                        }
                     }
                 } else {
                     const double* trow = reinterpret_cast<const double*>(buf + trk_off);
-                    trx = trow[0];
-                    trY = trow[NP];
-                    trz = DIM == 3 ? trow[2 * NP] : 0.0;
+                    trx = (T)trow[0];
+                    trY = (T)trow[NP];
+                    trz = DIM == 3 ? (T)trow[2 * NP] : (T)0;
                 }
-                const double2 ab = *reinterpret_cast<const double2*>(sShp + 4 * j);
-                const double2 iab = *reinterpret_cast<const double2*>(sShp + 4 * j + 2);
-                const T a = (T)ab.x, bb = (T)ab.y, ia2 = (T)iab.x, ib2 = (T)iab.y;
+                T a, bb, ia2, ib2;
+                if constexpr (sizeof(T) == 8) {
+                    const double2 ab = *reinterpret_cast<const double2*>(sShp + 4 * j);
+                    const double2 iab = *reinterpret_cast<const double2*>(sShp + 4 * j + 2);
+                    a = ab.x; bb = ab.y; ia2 = iab.x; ib2 = iab.y;
+                } else {
+                    const float4 sh = *reinterpret_cast<const float4*>(sShpF + 4 * j);
+                    a = sh.x; bb = sh.y; ia2 = sh.z; ib2 = sh.w;
+                }
                 T dold;
                 if (d_mode == 0) {
                     dold = (T)1;
-                } else if (d_mode == 1) {
+                } else if (EXP && d_mode == 1) {
                     dold = dst[e];
                 } else {
-                    const T ex = (T)(ox - trx), ey = (T)(oy - trY);
+                    const T ex = ox - trx, ey = oy - trY;
                     T qd;
                     if constexpr (DIM == 3) {
-                        const T ez = (T)(oz - trz);
+                        const T ez = oz - trz;
                         qd = ex * ex * ia2 + ey * ey * ia2 + ez * ez * ib2;
                     } else {
                         qd = ex * ex * ia2 + ey * ey * ib2;
                     }
                     dold = los_scale(qd);
                 }
-                T dn, cp4[4];
-                am_element<DIM, T, LAY>(v, trx, trY, trz, px, py, pz, a, bb, ia2, ib2, dold, trho, trho_o, sumsq,
-                                        mx, accL, accT, dn, cp4);
+                T dn, cp4[4], ss, ml, off[DIM];
+                am_element<DIM, T, LAY>(v, px - trx, py - trY, pz - trz, a, bb, ia2, ib2, dold, trho, trho_o, ss, ml,
+                                        off, dn, cp4);
+                sumsq += ss;
+                mx = ml > mx ? ml : mx;
+#pragma unroll
+                for (int ax = 0; ax < DIM; ++ax) {
+                    accL[ax] += v[Words<DIM, LAY>::NV + ax];
+                    accO[ax] += off[ax];
+                }
 #pragma unroll
                 for (int w = 0; w < W; ++w) st_stream(gp + w * NP, v[w]);
-                if (dst) dst[e] = dn;  // optional exports (tests, warm starts)
-                if (cop) {
+                if constexpr (EXP) {
+                    if (dst) dst[e] = dn;  // optional exports (tests, warm starts)
+                    if (cop) {
 #pragma unroll
-                    for (int c = 0; c < 2 * (DIM - 1); ++c) cop[c * Nel + e] = cp4[c];
+                        for (int c = 0; c < 2 * (DIM - 1); ++c) cop[c * Nel + e] = cp4[c];
+                    }
                 }
             }
             __syncwarp();
@@ -529,15 +598,15 @@ __global__ void __launch_bounds__(TmaCfg<DIM, T, LAY, NP, G>::kThreads, MINB) al
         if (act) {
 #pragma unroll
             for (int ax = 0; ax < DIM; ++ax) {
-                red[(g * 2 * DIM + ax) * NP + t] = accL[ax];
-                red[(g * 2 * DIM + DIM + ax) * NP + t] = accT[ax];
+                red[(g * 2 * DIM + ax) * NP + t] = (double)accL[ax];
+                red[(g * 2 * DIM + DIM + ax) * NP + t] = (double)accO[ax];
             }
         }
-        sumsq = warp_sum(sumsq);
-        mx = warp_max(mx);
+        const double wss = warp_sum((double)sumsq);
+        const double wmx = warp_max((double)mx);
         if (lane == 0) {
-            sWarp[b * 2 * NCW + warp] = sumsq;
-            sWarp[b * 2 * NCW + NCW + warp] = mx;
+            sWarp[b * 2 * NCW + warp] = wss;
+            sWarp[b * 2 * NCW + NCW + warp] = wmx;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&done[b]);
