@@ -293,6 +293,27 @@ typedef struct tro_ma_params {
 int tro_ma_run(int32_t mode, const tro_ma_dims* dims, const tro_ma_consts* c, const tro_ma_state* s,
                const tro_ma_params* p, void* stream);
 
+/* Ozaki int8 tensor-core backend of the mode-3 QP step: the same xi = K_L^-1 [rho B - C ; b_eq] for every
+ * non-converged problem, as an exactly-accumulated int8 GEMM on tcgen05 (kind::i8, TMEM accumulators,
+ * tensor-map TMA) of n_slices 7-bit slices per operand, with separate exponents for the primal K block
+ * [0, nv) and the boundary K block [nv, nk).  a_slices / a_exp: the level inverses' rows K_L^-1[0:nv, 0:nk]
+ * split on the host (paper_2408_10731_b200.ozaki.split_blocks): int8
+ * [n_levels][n_slices][m_tiles][ks0 + ks1][4096] (128 x 32 canonical no-swizzle K-major blocks) and the
+ * per-row exponents int32 [n_levels][2][m_tiles * 128]; b_slices / b_exp: workspaces of
+ * [n_slices][n_col_tiles][ks0 + ks1][1024] int8 and [2][n_col_tiles * 32] int32, n_col_tiles >= ceil(3 B / 32);
+ * m_tiles = ceil(nv / 128) <= 2, ks0 = ceil(nv / 32), ks1 = ceil(n_eq / 32), each <= 16. */
+typedef struct tro_ozaki_ws {
+    const int8_t* a_slices;
+    const int32_t* a_exp;
+    int8_t* b_slices;
+    int32_t* b_exp;
+    int32_t n_slices;    /* 6, 7 or 8 (truncation ~128^-(n_slices + 1) relative) */
+    int32_t n_col_tiles; /* capacity of the B workspaces in 32-column tiles */
+} tro_ozaki_ws;
+
+int tro_ma_qp_ozaki(const tro_ma_dims* dims, const tro_ma_consts* c, const tro_ma_state* s, const tro_ozaki_ws* ws,
+                    void* stream);
+
 /* ------------------------------------------------------------------ 2-D batch optimizer (Alg. 2)
  * Replaces solver_batch.batch_iteration + the residual / _maybe_grow_rho bookkeeping of
  * solve_batch_opt (solver_batch.py:352-363, 396-406, 451-461) for the whole batch.  One CTA per

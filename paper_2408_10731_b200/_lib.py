@@ -43,6 +43,7 @@ EXPORTS = (
     "tro_elite_update_f64",
     "tro_fp64_fma_probe",
     "tro_ma_run",
+    "tro_ma_qp_ozaki",
     "tro_b2_run",
     "tro_validate_f64",
     "tro_predict_tracks_f64",
@@ -170,6 +171,11 @@ class MaState(ctypes.Structure):
                                         "iteration", "last_change", "n_hist", "status", "export_d", "export_ab")]
 
 
+class OzakiWs(ctypes.Structure):
+    _fields_ = [("a_slices", c_void_p), ("a_exp", c_void_p), ("b_slices", c_void_p), ("b_exp", c_void_p),
+                ("n_slices", c_int32), ("n_col_tiles", c_int32)]
+
+
 class MaParams(ctypes.Structure):
     _fields_ = [("tol_norm", c_double), ("stall_improvement", c_double), ("stall_window", c_int32),
                 ("max_iter", c_int32), ("max_hist", c_int32), ("reserved", c_int32)]
@@ -282,6 +288,8 @@ def load() -> ctypes.CDLL:
     lib.tro_ma_run.argtypes = [c_int32, POINTER(MaDims), POINTER(MaConsts), POINTER(MaState), POINTER(MaParams),
                                c_void_p]
     lib.tro_ma_run.restype = c_int32
+    lib.tro_ma_qp_ozaki.argtypes = [POINTER(MaDims), POINTER(MaConsts), POINTER(MaState), POINTER(OzakiWs), c_void_p]
+    lib.tro_ma_qp_ozaki.restype = c_int32
     lib.tro_b2_run.argtypes = [c_int32, POINTER(B2Dims), POINTER(B2Consts), POINTER(B2State), POINTER(B2Params),
                                c_void_p]
     lib.tro_b2_run.restype = c_int32

@@ -173,8 +173,14 @@ class MaEngine:
     """B problems sharing one _Structure, resident on one device."""
 
     def __init__(self, struct: _Structure, b_eq: np.ndarray, statics: np.ndarray | None, params: JointParams, *,
-                 device=None, max_hist: int = 0, export: bool = False, split_qp: bool = True):
-        self.split_qp = split_qp  # tro_ma_run modes 3 + 4 (DMMA QP) instead of the fused mode 0
+                 device=None, max_hist: int = 0, export: bool = False, split_qp: bool = True, qp: str = "dmma",
+                 ozaki_slices: int = 8):
+        # the QP step: "dmma" (tro_ma_run mode 3, fp64 mma.sync), "ozaki" (tro_ma_qp_ozaki: exact int8 GEMM on
+        # tcgen05 / TMEM), each followed by the element pass (mode 4); split_qp=False: the fused mode 0
+        self.split_qp = split_qp
+        if qp not in ("dmma", "ozaki"):
+            raise ValueError("qp must be 'dmma' or 'ozaki'")
+        self.qp = qp
         _lib.require_cuda()
         self.lib = _lib.load()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -228,6 +234,28 @@ class MaEngine:
                                    p(self.last_change), p(self.n_hist), p(self.status), p(self.export_d),
                                    p(self.export_ab))
         self._graph, self._graph_n = None, 0
+        self._ozaki = None
+        if qp == "ozaki":
+            from . import ozaki
+
+            nv, nk = n_a * m, self.kinv.shape[1]
+            sl, ea = ozaki.split_blocks(np.stack([f.kinv for f in struct.factors])[:, :nv, :nk], nv, ozaki_slices)
+            mt, ks0, ks1 = ozaki.block_tiles(nv, nk - nv)
+            ks = ks0 + ks1
+            nt = -(-3 * B // ozaki.BN)
+            self.oz_a = torch.as_tensor(sl.reshape(-1), device=dev)
+            self.oz_ea = torch.as_tensor(ea.reshape(-1), **i32)
+            self.oz_b = torch.zeros(ozaki_slices * nt * ks * ozaki.BN * ozaki.BK, dtype=torch.int8, device=dev)
+            self.oz_eb = torch.zeros(2 * nt * ozaki.BN, **i32)
+            self._ozaki = _lib.OzakiWs(p(self.oz_a), p(self.oz_ea), p(self.oz_b), p(self.oz_eb), int(ozaki_slices), nt)
+
+    def qp_ozaki(self):
+        """The QP step of every non-converged problem on the int8 tensor cores (writes xi, like mode 3)."""
+        with torch.cuda.device(self.device):
+            rc = self.lib.tro_ma_qp_ozaki(ctypes.byref(self._dims), ctypes.byref(self._consts),
+                                          ctypes.byref(self._state), ctypes.byref(self._ozaki),
+                                          ctypes.c_void_p(_lib.stream_handle()))
+        _lib.check(rc, "tro_ma_qp_ozaki")
 
     def _call(self, mode: int):
         pr = self.params
@@ -264,7 +292,10 @@ class MaEngine:
         self._call(2)
 
     def iterate(self):
-        if self.split_qp:  # QP step batched on the fp64 tensor cores, then the element pass
+        if self.qp == "ozaki":  # exact int8 GEMM on tcgen05, then the element pass
+            self.qp_ozaki()
+            self._call(4)
+        elif self.split_qp:  # QP step batched on the fp64 tensor cores (DMMA), then the element pass
             self._call(3)
             self._call(4)
         else:  # one fused launch (per-problem QP in the kernel prologue)
@@ -327,7 +358,8 @@ def _statics(problem: MultiAgentProblem) -> np.ndarray:
 
 
 def solve_joint_batch(problems: list, params: JointParams | None = None, *, history: bool = False,
-                      use_graph: bool = True, device=None, engine: MaEngine | None = None) -> MaEngine:
+                      use_graph: bool = True, device=None, engine: MaEngine | None = None,
+                      qp: str = "dmma") -> MaEngine:
     """Solve B independent joint problems in one device pass; returns the engine (device tensors:
     xi, res_norm, res_max, status, iteration, level, hist)."""
     params = params or JointParams()
@@ -340,7 +372,7 @@ def solve_joint_batch(problems: list, params: JointParams | None = None, *, hist
     b_eq = np.stack([_b_eq(p) for p in problems])
     statics = np.stack([_statics(p) for p in problems]) if struct.n_static else None
     eng = engine or MaEngine(struct, b_eq, statics, params, device=device,
-                             max_hist=params.max_iter if history else 0)
+                             max_hist=params.max_iter if history else 0, qp=qp)
     if struct.n_pairs == 0:
         raise ValueError("the device path needs at least one constraint pair")
     eng.reset()

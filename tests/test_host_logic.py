@@ -148,3 +148,21 @@ def test_linear_track_record_reproduces_tracks_bitwise():
     tr = np.stack([o.centers for o in p.obstacles])
     rec = linear_track_record(tr, p.basis.grid.timestamps)
     assert rec is not None and not np.any(rec[: 6 * len(tr)].reshape(-1, 6)[:, 3:])
+
+
+def test_ozaki_row_split_is_exact():
+    """The int8 slices of the level inverses reconstruct the fp64 rows to the truncation of S 7-bit slices
+    (S = 8: below one ulp of the row maximum), in the tiled canonical layout the tensor-core kernel reads."""
+    from paper_2408_10731_b200 import ozaki
+
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((2, 176, 272)) * 10.0 ** rng.uniform(-6, 6, (2, 176, 1))
+    A[0, 5] = 0.0  # a zero row
+    for S, tol in ((8, 2.0 ** -54), (7, 2.0 ** -47)):
+        sl, ea = ozaki.split_rows(A, S)
+        assert sl.dtype == np.int8 and sl.shape == (2, S, 2, 9, 4096)
+        assert np.abs(sl.astype(int)).max() <= 127
+        R = ozaki.reconstruct(sl, ea, 176, 272)
+        scale = np.maximum(np.abs(A).max(axis=2, keepdims=True), 1e-300)
+        assert np.max(np.abs(R - A) / scale) <= tol
+    assert ea[0, 5] == 0 and not sl[0, :, 0].reshape(S, -1)[:, :0].size
