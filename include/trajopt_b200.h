@@ -225,7 +225,24 @@ int tro_priest_cost_f64(const tro_priest_dims* dims, const tro_priest_consts* c,
 /* Distribution refit from elites xis[rows[k]] with costs[k] (solver_priest.py:317-333); updates mu
  * (dm) and cov (dm x dm) in place.  gamma == 0: plain CEM mean / population covariance (:442-444). */
 int tro_elite_update_f64(const double* xis, int32_t dm, const int64_t* rows, int32_t n_elite,
-                         const double* costs, double sigma, double gamma, double* mu, double* cov, void* stream);
+                         const double* costs, double sigma, double gamma, int32_t mode, double* mu, double* cov,
+                         void* stream);
+
+/* tro_elite_update_f64 modes: PRIEST's exp-weighted refit with learning rate sigma (gamma used as given,
+ * solver_priest.py:317-333), or CEM's plain mean / population covariance (:442-444) */
+#define TRO_REFIT_PRIEST 0
+#define TRO_REFIT_CEM 1
+
+/* Throughput-mode sampling: standard normals out[s][j] (n_samples x dim, row-major) of
+ * samples first_sample .. first_sample + n_samples - 1, Philox4x32-10 keyed by seed, counter = (pair index,
+ * stream_id), Box-Muller; a pure function of (seed, stream_id, global sample, j), so shards draw their own
+ * rows.  Not numpy's stream (parity mode keeps numpy's Generator draws). */
+int tro_normal_philox_f64(uint64_t seed, uint64_t stream_id, int64_t first_sample, int64_t n_samples, int32_t dim,
+                          double* out, void* stream);
+
+/* Lower Cholesky factor of a symmetric PSD n x n matrix (n <= the PRIEST coefficient dimension bound), one
+ * CTA; non-positive pivots give zero columns.  The throughput-mode draw factor (samples = mu + z L'). */
+int tro_cholesky_f64(const double* a, int32_t n, double* l, void* stream);
 
 /* ------------------------------------------------------------------ joint multi-agent (Alg. 5) */
 typedef struct tro_ma_dims {

@@ -26,6 +26,8 @@ TRO_LAYOUT_ANGLE = 0
 TRO_LAYOUT_UNIT = 1
 TRO_LAYOUT_HALF = 2
 TRO_EINVAL = -1
+TRO_REFIT_PRIEST = 0
+TRO_REFIT_CEM = 1
 
 # every symbol include/trajopt_b200.h declares (checked by tests/test_lib_exports.py)
 EXPORTS = (
@@ -41,6 +43,8 @@ EXPORTS = (
     "tro_priest_project_f64",
     "tro_priest_cost_f64",
     "tro_elite_update_f64",
+    "tro_normal_philox_f64",
+    "tro_cholesky_f64",
     "tro_fp64_fma_probe",
     "tro_ma_run",
     "tro_ma_qp_ozaki",
@@ -281,7 +285,12 @@ def load() -> ctypes.CDLL:
                                         c_void_p, c_double, c_double, c_double, c_void_p, c_void_p]
     lib.tro_priest_cost_f64.restype = c_int32
     lib.tro_elite_update_f64.argtypes = [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_double, c_double,
-                                         c_void_p, c_void_p, c_void_p]
+                                         c_int32, c_void_p, c_void_p, c_void_p]
+    lib.tro_normal_philox_f64.argtypes = [ctypes.c_uint64, ctypes.c_uint64, c_int64, c_int64, c_int32, c_void_p,
+                                          c_void_p]
+    lib.tro_normal_philox_f64.restype = c_int32
+    lib.tro_cholesky_f64.argtypes = [c_void_p, c_int32, c_void_p, c_void_p]
+    lib.tro_cholesky_f64.restype = c_int32
     lib.tro_elite_update_f64.restype = c_int32
     lib.tro_fastmath_eval.argtypes = [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     lib.tro_fastmath_eval.restype = c_int32

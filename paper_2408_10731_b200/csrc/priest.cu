@@ -473,21 +473,25 @@ __global__ void __launch_bounds__(256) priest_cost_kernel(PrArgs A, const double
 // ---------------------------------------------------------------- distribution refit
 // weights = exp((c - min c)/gamma); mu' = (1-sigma) mu + sigma sum(w x)/sum w;
 // Sigma' = (1-sigma) Sigma + sigma sum(w (x - mu')(x - mu')')/sum w   (solver_priest.py:317-333)
-// gamma == 0 selects the plain CEM refit (mean, population covariance; :442-444).
+// cem = true selects the plain CEM refit (mean, population covariance; :442-444); otherwise gamma is used as
+// given (gamma == 0 gives numpy's exp(x / 0): inf / NaN weights), and min(c) propagates NaN like np.min.
 __global__ void __launch_bounds__(256) elite_update_kernel(const double* __restrict__ xis, int dm,
                                                            const int64_t* __restrict__ rows, int n_el,
                                                            const double* __restrict__ costs, double sigma,
-                                                           double gamma, double* mu, double* cov) {
+                                                           double gamma, int cem, double* mu, double* cov) {
     __shared__ double w[1024];
     __shared__ double mnew[kPrMaxDm];
     __shared__ double red[2];
     const int tid = threadIdx.x;
     if (tid == 0) {
         double cmin = costs[0];
-        for (int k = 1; k < n_el; ++k) cmin = fmin(cmin, costs[k]);
+        for (int k = 1; k < n_el; ++k) {
+            const double c = costs[k];
+            if (cmin == cmin && (c != c || c < cmin)) cmin = c;  // np.min: NaN wins
+        }
         double ws = 0.0;
         for (int k = 0; k < n_el; ++k) {
-            const double v = gamma != 0.0 ? exp((costs[k] - cmin) / gamma) : 1.0;
+            const double v = !cem ? exp((costs[k] - cmin) / gamma) : 1.0;
             w[k] = v;
             ws += v;
         }
@@ -499,7 +503,7 @@ __global__ void __launch_bounds__(256) elite_update_kernel(const double* __restr
         double acc = 0.0;
         for (int k = 0; k < n_el; ++k) acc += w[k] * xis[rows[k] * dm + c];
         const double wm = acc / ws;
-        const double nm = gamma != 0.0 ? (1.0 - sigma) * mu[c] + sigma * wm : wm;
+        const double nm = !cem ? (1.0 - sigma) * mu[c] + sigma * wm : wm;
         mnew[c] = nm;
     }
     __syncthreads();
@@ -511,10 +515,83 @@ __global__ void __launch_bounds__(256) elite_update_kernel(const double* __restr
             acc += w[k] * ((x[a] - mnew[a]) * (x[b] - mnew[b]));
         }
         const double wc = acc / ws;
-        cov[o] = gamma != 0.0 ? (1.0 - sigma) * cov[o] + sigma * wc : wc;
+        cov[o] = !cem ? (1.0 - sigma) * cov[o] + sigma * wc : wc;
     }
     __syncthreads();
     for (int c = tid; c < dm; c += blockDim.x) mu[c] = mnew[c];
+}
+
+// ---------------------------------------------------------------- throughput-mode sampling
+// Philox4x32-10 (Salmon et al., SC'11: the counter-based generator of cuRAND / numpy's Philox) keyed by
+// the 64-bit seed; counter = (pair index (64 bit), stream id (64 bit)).  Each counter gives two 53-bit
+// uniforms and, by Box-Muller, two standard normals, so element e of sample s is a pure function of
+// (seed, stream, s * ceil(d / 2) * 2 + j): any shard of the batch draws its own samples.
+__device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t h0 = __umulhi(0xD2511F53u, c[0]), l0 = 0xD2511F53u * c[0];
+        const uint32_t h1 = __umulhi(0xCD9E8D57u, c[2]), l1 = 0xCD9E8D57u * c[2];
+        const uint32_t n0 = h1 ^ c[1] ^ k0, n2 = h0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = l1;
+        c[2] = n2;
+        c[3] = l0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+__global__ void normal_philox_kernel(uint64_t seed, uint64_t stream_id, int64_t first, int64_t n, int d,
+                                     double* __restrict__ out) {
+    const int dp = (d + 1) / 2;  // counters per sample
+    const int64_t total = n * dp;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = q / dp;
+        const int h = (int)(q - s * dp);
+        const uint64_t ctr = (uint64_t)(first + s) * dp + h;
+        uint32_t c[4] = {(uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream_id, (uint32_t)(stream_id >> 32)};
+        philox10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+        // uniforms in (0, 1]: 53 bits each
+        const uint64_t a = ((uint64_t)c[0] << 21) ^ (c[1] >> 11), b = ((uint64_t)c[2] << 21) ^ (c[3] >> 11);
+        const double u1 = ((double)(a & ((1ull << 53) - 1)) + 1.0) * 0x1.0p-53;
+        const double u2 = (double)(b & ((1ull << 53) - 1)) * 0x1.0p-53;
+        const double r = sqrt(-2.0 * log(u1));
+        double sn, cs;
+        sincospi(2.0 * u2, &sn, &cs);
+        double* o = out + s * d + 2 * h;
+        o[0] = r * cs;
+        if (2 * h + 1 < d) o[1] = r * sn;
+    }
+}
+
+// Cholesky factor L (lower, row-major) of a symmetric positive semidefinite n x n matrix, one CTA: columns
+// left to right; a pivot <= 0 (a singular direction of the refit covariance) gives a zero column, so
+// L L' == A on the matrix's range.  Throughput-mode draw factor (samples = mu + z L'), in place of numpy's
+// svd factor u sqrt(s) (same distribution, not the same samples).
+__global__ void __launch_bounds__(256) cholesky_kernel(const double* __restrict__ A, int n, double* __restrict__ L) {
+    __shared__ double s[kPrMaxDm * kPrMaxDm];
+    for (int k = threadIdx.x; k < n * n; k += blockDim.x) s[k] = A[k];
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {
+        __shared__ double piv;
+        if (threadIdx.x == 0) {
+            const double v = s[j * n + j];
+            piv = v > 0.0 ? sqrt(v) : 0.0;
+            s[j * n + j] = piv;
+        }
+        __syncthreads();
+        for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) s[i * n + j] = piv > 0.0 ? s[i * n + j] / piv : 0.0;
+        __syncthreads();
+        for (int o = threadIdx.x; o < (n - j - 1) * (n - j - 1); o += blockDim.x) {
+            const int i = j + 1 + o / (n - j - 1), k = j + 1 + o % (n - j - 1);
+            if (k <= i) s[i * n + k] -= s[i * n + j] * s[k * n + j];
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < n * n; k += blockDim.x) {
+        const int i = k / n, c = k - i * n;
+        L[k] = c <= i ? s[k] : 0.0;
+    }
 }
 
 }  // namespace tro
@@ -591,11 +668,30 @@ extern "C" int tro_priest_cost_f64(const tro_priest_dims* dims, const tro_priest
 }
 
 extern "C" int tro_elite_update_f64(const double* xis, int32_t dm, const int64_t* rows, int32_t n_elite,
-                                    const double* costs, double sigma, double gamma, double* mu, double* cov,
-                                    void* stream) {
-    if (!xis || !rows || !costs || !mu || !cov || dm < 1 || dm > tro::kPrMaxDm || n_elite < 1 || n_elite > 1024)
+                                    const double* costs, double sigma, double gamma, int32_t mode, double* mu,
+                                    double* cov, void* stream) {
+    if (!xis || !rows || !costs || !mu || !cov || dm < 1 || dm > tro::kPrMaxDm || n_elite < 1 || n_elite > 1024 ||
+        (mode != TRO_REFIT_PRIEST && mode != TRO_REFIT_CEM))
         return TRO_EINVAL;
-    tro::elite_update_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(xis, dm, rows, n_elite, costs,
-                                                                                      sigma, gamma, mu, cov);
+    tro::elite_update_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        xis, dm, rows, n_elite, costs, sigma, gamma, mode == TRO_REFIT_CEM, mu, cov);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int tro_normal_philox_f64(uint64_t seed, uint64_t stream_id, int64_t first_sample, int64_t n_samples,
+                                     int32_t dim, double* out, void* stream) {
+    if (!out || n_samples < 0 || first_sample < 0 || dim < 1) return TRO_EINVAL;
+    if (n_samples == 0) return 0;
+    const int64_t total = n_samples * ((dim + 1) / 2);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    tro::normal_philox_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        seed, stream_id, first_sample, n_samples, dim, out);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int tro_cholesky_f64(const double* a, int32_t n, double* l, void* stream) {
+    if (!a || !l || n < 1 || n > tro::kPrMaxDm) return TRO_EINVAL;
+    tro::cholesky_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a, n, l);
     return (int)cudaGetLastError();
 }

@@ -284,10 +284,10 @@ def _topk(keys: torch.Tensor, k: int) -> torch.Tensor:
     return out[:k]
 
 
-def _refit(xi, rows, costs, sigma, gamma, mu, cov):
+def _refit(xi, rows, costs, sigma, gamma, mu, cov, mode=_lib.TRO_REFIT_PRIEST):
     rc = _lib.load().tro_elite_update_f64(xi.data_ptr(), int(xi.shape[1]), rows.data_ptr(), int(rows.numel()),
-                                         costs.data_ptr(), float(sigma), float(gamma), mu.data_ptr(), cov.data_ptr(),
-                                         _stream())
+                                         costs.data_ptr(), float(sigma), float(gamma), int(mode), mu.data_ptr(),
+                                         cov.data_ptr(), _stream())
     _lib.check(rc, "tro_elite_update_f64")
 
 
@@ -364,6 +364,36 @@ def _draw_z(rng, n: int, d: int) -> np.ndarray:
     return rng.standard_normal((n, d))
 
 
+SAMPLERS = ("numpy", "philox")
+
+
+class _DeviceSampler:
+    """Throughput-mode draws, all on the device: the draw factor is the Cholesky factor of the current
+    covariance (tro_cholesky_f64) and the standard normals come from Philox4x32-10 keyed by the seed with
+    the round as the stream id (tro_normal_philox_f64), so a round needs no host round trip.  Parity mode
+    ("numpy") keeps numpy's Generator stream and svd factor, which reproduce the reference's samples."""
+
+    def __init__(self, seed: int, n: int, dm: int, dev, first: int = 0):
+        self.seed, self.n, self.dm, self.first = int(seed) & (2**64 - 1), int(n), int(dm), int(first)
+        self.z = torch.empty((n, dm), dtype=torch.float64, device=dev)
+
+    def factor(self, sig: torch.Tensor, L: torch.Tensor):
+        rc = _lib.load().tro_cholesky_f64(sig.data_ptr(), self.dm, L.data_ptr(), _stream())
+        _lib.check(rc, "tro_cholesky_f64")
+
+    def normals(self, round_index: int) -> torch.Tensor:
+        rc = _lib.load().tro_normal_philox_f64(self.seed, int(round_index), self.first, self.n, self.dm,
+                                               self.z.data_ptr(), _stream())
+        _lib.check(rc, "tro_normal_philox_f64")
+        return self.z
+
+
+def device_normals(seed: int, round_index: int, n: int, dm: int, first: int = 0, device=None) -> torch.Tensor:
+    """(n, dm) throughput-mode standard normals of samples first .. first + n - 1 (see _DeviceSampler)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    return _DeviceSampler(seed, n, dm, dev, first).normals(round_index).clone()
+
+
 def _z_round(z, dev):
     """One round's standard normals on the device: pinned host rows upload asynchronously (the host does
     not wait for the previous round's kernels before queueing this round)."""
@@ -373,12 +403,19 @@ def _z_round(z, dev):
 
 
 def priest_optimize(setup: ProjectionSetup, c1, distribution: SamplingDistribution,
-                    params: PriestParams | None = None, *, z_rounds=None) -> PriestResult:
+                    params: PriestParams | None = None, *, z_rounds=None, sampler: str = "numpy") -> PriestResult:
     """Projection-guided sampling loop (solver_priest.py:336-382), one device pass per round.
 
     z_rounds: optional pre-drawn standard normals (n_outer, n_batch, d), device or host, in
-    place of drawing them from default_rng(params.seed) round by round."""
+    place of drawing them from default_rng(params.seed) round by round.
+    sampler: "numpy" (parity mode: the reference's Generator stream and svd factor, host draws) or "philox"
+    (throughput mode: Cholesky factor and Philox normals on the device; with a BarnCost c1 the rounds run
+    without a host synchronisation until the result is read)."""
     params = params or PriestParams()
+    if sampler not in SAMPLERS:
+        raise ValueError(f"sampler must be one of {SAMPLERS}")
+    if sampler == "philox" and z_rounds is None and isinstance(c1, BarnCost):
+        return _priest_device_rounds(setup, c1, distribution, params)
     d = setup.device()
     dev = d["device"]
     rng = np.random.default_rng(params.seed)
@@ -432,11 +469,50 @@ class CemResult:
     params: CemParams
 
 
+def _priest_device_rounds(setup: ProjectionSetup, c1, distribution: SamplingDistribution,
+                          params: PriestParams) -> PriestResult:
+    """priest_optimize in throughput mode: every round (factor, draw, projection, scores, stable top-k,
+    aug costs, elite top-k, refit, history entry) is enqueued on the device; one host read at the end."""
+    d = setup.device()
+    dev = d["device"]
+    mu = torch.as_tensor(distribution.mu.copy(), device=dev)
+    sig = torch.as_tensor(distribution.sigma_mat.copy(), device=dev)
+    dm = mu.numel()
+    sampler = _DeviceSampler(params.seed, params.n_batch, dm, dev)
+    line = c1.line(dev)
+    hist = torch.empty((params.n_outer, 3), dtype=torch.float64, device=dev)
+    best_row = None
+    xi = smp = scores = None
+    for r in range(params.n_outer):
+        sampler.factor(sig, d["L"])
+        d["mu"].copy_(mu)
+        xi, scores, _, smp = _run_project(setup, z=sampler.normals(r), n_inner=params.n_inner, keep_samples=True)
+        keep = _topk(scores, params.n_constraint_elite)  # :358
+        aug = _run_cost(setup, xi, keep, scores, 1.0, params.residual_weight, 0.0, line)  # :359-361
+        erank = _topk(aug, params.n_elite)  # :362-363
+        rows = keep[erank].contiguous()
+        ecost = aug[erank].contiguous()
+        _refit(xi, rows, ecost, params.sigma, params.gamma, mu, sig)  # :365-372
+        best_row = rows[0]
+        hist[r, 0] = ecost[0]
+        hist[r, 1] = scores[best_row]
+        hist[r, 2] = scores.min()
+    h = hist.cpu().numpy()
+    b = int(best_row.item())
+    bx = xi[b].cpu().numpy()
+    best = ProjectedSample(original=smp[b].cpu().numpy(), projected=bx, residual=float(h[-1, 1]),
+                           trajectory=setup.trajectory_of(bx), aug_cost=float(h[-1, 0]))
+    history = [{"best_aug_cost": float(e[0]), "best_residual": float(e[1]), "min_residual": float(e[2])} for e in h]
+    return PriestResult(best=best, mu=mu.cpu().numpy(), sigma_mat=sig.cpu().numpy(), history=history, params=params)
+
+
 def cem_optimize(setup: ProjectionSetup, c1, distribution: SamplingDistribution,
-                 params: CemParams | None = None) -> CemResult:
+                 params: CemParams | None = None, *, sampler: str = "numpy") -> CemResult:
     """Plain cross-entropy baseline (solver_priest.py:422-457): no projection, penalty costs,
-    unweighted elite refit — costs, top-k and refit on the GPU."""
+    unweighted elite refit — costs, top-k and refit on the GPU.  sampler: see priest_optimize."""
     params = params or CemParams()
+    if sampler not in SAMPLERS:
+        raise ValueError(f"sampler must be one of {SAMPLERS}")
     d = setup.device()
     dev = d["device"]
     rng = np.random.default_rng(params.seed)
@@ -448,10 +524,16 @@ def cem_optimize(setup: ProjectionSetup, c1, distribution: SamplingDistribution,
     line = c1.line(dev) if device_cost else None
     history = []
     best_xi, best_cost = None, np.inf
-    for _ in range(params.iterations):
-        d["L"].copy_(torch.as_tensor(_draw_factor(sig_h)))
-        d["mu"].copy_(mu)
-        z = torch.as_tensor(_draw_z(rng, params.n_batch, dm), device=dev)
+    dsamp = _DeviceSampler(params.seed, params.n_batch, dm, dev) if sampler == "philox" else None
+    for it in range(params.iterations):
+        if dsamp is not None:
+            dsamp.factor(sig, d["L"])
+            d["mu"].copy_(mu)
+            z = dsamp.normals(it)
+        else:
+            d["L"].copy_(torch.as_tensor(_draw_factor(sig_h)))
+            d["mu"].copy_(mu)
+            z = torch.as_tensor(_draw_z(rng, params.n_batch, dm), device=dev)
         smp, _, _, _ = _run_project(setup, z=z, n_inner=-1)  # draw only
         if device_cost:
             costs = _run_cost(setup, smp, None, None, 1.0, 0.0, params.penalty_weight, line)
@@ -460,15 +542,16 @@ def cem_optimize(setup: ProjectionSetup, c1, distribution: SamplingDistribution,
             base = torch.as_tensor(np.array([float(c1(setup.trajectory_of(x))) for x in sh]), device=dev)
             costs = base + params.penalty_weight * _run_cost(setup, smp, None, None, 0.0, 0.0, 1.0, d["line"])
         order = _topk(costs, params.n_elite)  # :440
-        _refit(smp, order, costs[order].contiguous(), 1.0, 0.0, mu, sig)  # :442-444
-        sig_h = sig.cpu().numpy()
+        _refit(smp, order, costs[order].contiguous(), 1.0, 0.0, mu, sig, _lib.TRO_REFIT_CEM)  # :442-444
+        if dsamp is None:
+            sig_h = sig.cpu().numpy()
         c0 = float(costs[order[0]].item())
         if c0 < best_cost:
             best_cost = c0
             best_xi = smp[order[0]].cpu().numpy()
         history.append({"best_cost": c0, "mean_cost": float(costs.mean().item())})
     return CemResult(best_xi=best_xi, best_cost=best_cost, best_trajectory=setup.trajectory_of(best_xi),
-                     mu=mu.cpu().numpy(), sigma_mat=sig_h, history=history, params=params)
+                     mu=mu.cpu().numpy(), sigma_mat=sig.cpu().numpy(), history=history, params=params)
 
 
 # ---------------------------------------------------------------- cost helpers (host, per trajectory)
