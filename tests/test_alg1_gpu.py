@@ -360,7 +360,9 @@ def _topk(keys, k):
     return out[:k].cpu().numpy()
 
 
-@pytest.mark.parametrize("n,k", [(1, 1), (7, 3), (1000, 1000), (16384, 8192), (16384, 256), (50000, 17)])
+@pytest.mark.parametrize("n,k", [(1, 1), (7, 3), (1000, 1000), (4096, 4096), (4097, 4097), (16384, 8192),
+                                 (16384, 256), (50000, 17), (20000, 1), (131072, 65536), (131072, 256),
+                                 (131072, 131072), (262144, 5000)])
 def test_topk_stable_bitexact(n, k):
     rng = np.random.default_rng(n + k)
     keys = np.round(rng.normal(size=n), 2)  # many exact ties
@@ -372,6 +374,14 @@ def test_topk_stable_bitexact(n, k):
         keys[rng.integers(0, n, size=3)] = -np.inf
     ref = np.argsort(keys, kind="stable")[:k]
     np.testing.assert_array_equal(_topk(keys, k), ref)
+
+
+@pytest.mark.parametrize("n,k", [(10000, 5000), (10000, 1), (10000, 10000)])
+def test_topk_all_ties_and_sorted_inputs(n, k):
+    """Radix select edge cases: every key equal (all ties: index order), ascending and descending inputs."""
+    for keys in (np.full(n, 0.25), np.arange(n, dtype=float), -np.arange(n, dtype=float),
+                 np.repeat(np.array([3.0, -1.0, 2.0, -1.0]), n // 4)):
+        np.testing.assert_array_equal(_topk(keys, k), np.argsort(keys, kind="stable")[:k])
 
 
 def test_tail_split_matches_unsplit_batch(golden):
