@@ -53,7 +53,7 @@ struct Alg1Args {
 };
 
 struct SmemLayout {
-    int P, pos_prev, pos_new, sums_in, red, shp, qlin, xi, warp;
+    int P, pos_prev, pos_new, sums_in, red, shp, qlin, xi, warp, kx, bq;
     int total;  // doubles
 };
 
@@ -69,6 +69,8 @@ __host__ __device__ inline SmemLayout smem_layout(int n_p, int m, int dim, int n
     L.qlin = off;     off += dim * kMaxM;
     L.xi = off;       off += dim * kMaxM;
     L.warp = off;     off += 2 * 32;
+    L.kx = off;       off += kMaxM * kMaxNk;          // MODE 3: the first m rows of the level's K^-1
+    L.bq = off;       off += dim * (kMaxNk + kMaxM);  // MODE 3: the member's boundary values and q
     L.total = off;
     return L;
 }
@@ -191,11 +193,37 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     double* sQlin = smem + L.qlin;
     double* sXi = smem + L.xi;
     double* sWarp = smem + L.warp;
+    double* sKx = smem + L.kx;
+    double* sBq = smem + L.bq;
+    __shared__ int sKLevel;
 
     // MODE 3 keeps the member's bookkeeping, the basis, the shapes, the positions and the incoming sums in
     // shared memory across its iterations: only the first iteration stages them from global memory
     __shared__ SchedS sS;
     constexpr bool loop = MODE == 3;
+    // MODE 3 with few obstacles per thread (C1: 10 obstacles, 5 groups): the thread's elements and their
+    // track samples stay in REGISTERS across the in-kernel iterations (no L2 round trip per iteration);
+    // they are written back once, when the member stops or the launch's iterations are done
+    constexpr int kRegJ = loop ? 2 : 1;
+    T vc[kRegJ][Words<DIM, LAY>::W];
+    double tc[kRegJ][3];
+#ifndef TRO_C1_REGCACHE
+#define TRO_C1_REGCACHE 1
+#endif
+    const bool cached = TRO_C1_REGCACHE && loop && n_o <= A.G * kRegJ;
+    auto flush = [&]() {
+        const int t_ = tid % n_p, g_ = tid / n_p;
+        if (!cached || g_ >= A.G) return;
+        T* sb = reinterpret_cast<T*>(A.s.state) + (int64_t)i * n_o * Words<DIM, LAY>::W * n_p + t_;
+#pragma unroll
+        for (int q = 0; q < kRegJ; ++q) {
+            const int j = g_ + A.G * q;
+            if (j < n_o) {
+#pragma unroll
+                for (int w = 0; w < Words<DIM, LAY>::W; ++w) st_stream(sb + (j * Words<DIM, LAY>::W + w) * n_p, vc[q][w]);
+            }
+        }
+    };
     for (int rep_ = 0; rep_ < (loop ? A.n_loop : 1); ++rep_) {
     if (loop && rep_ > 0) __syncthreads();  // the previous iteration's writes (tid 0: sS; all: sums, positions)
     // ---------------- frozen members (converged / failed) do nothing
@@ -213,12 +241,16 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     }
     if (loop && rep_ == 0) __syncthreads();
     const int status0 = loop ? sS.status : A.s.status[i];
-    if (!prime && (status0 & (TRO_CONVERGED | TRO_FACTOR_FAILED))) return;
+    if (!prime && (status0 & (TRO_CONVERGED | TRO_FACTOR_FAILED))) {
+        if (rep_ > 0) flush();
+        return;
+    }
     const int level = loop ? sS.level : A.s.level[i];
     if (!prime && !A.c.level_ok[level]) {
         // qpcore.factorize raises when the new rho_o's saddle fails the cond guard
         // (qpcore.py:108-110); the member stops here and the host raises.
         if (tid == 0) A.s.status[i] = status0 | TRO_FACTOR_FAILED;
+        if (rep_ > 0) flush();
         return;
     }
     const double rho = loop ? sS.rho : A.s.rho[i];
@@ -233,6 +265,16 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
             sB[k] = b;
             sIA2[k] = 1.0 / (a * a);
             sIB2[k] = 1.0 / (b * b);
+        }
+    }
+    if (loop) {  // the level's K^-1 rows (first m), the boundary values and q, staged once per level / launch
+        if (rep_ == 0 || level != sKLevel) {
+            const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
+            for (int k = tid; k < m * nk; k += nthr) sKx[k] = ld_const(Kl + k);
+        }
+        if (rep_ == 0) {
+            for (int k = tid; k < DIM * ne; k += nthr) sBq[k] = A.c.bvals[(int64_t)i * DIM * ne + k];
+            for (int k = tid; k < DIM * m; k += nthr) sBq[DIM * kMaxNk + k] = A.c.q[(int64_t)i * DIM * m + k];
         }
     }
     const double* posg = A.s.pos + (int64_t)i * DIM * n_p;
@@ -303,20 +345,34 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
             }
             u = warp_sum(u);
             v = warp_sum(v);
-            if (lane == 0) sQlin[o] = (qg[o] + u) - v;
+            if (lane == 0) sQlin[o] = ((loop ? sBq[DIM * kMaxNk + o] : qg[o]) + u) - v;
         }
+        if (loop && tid == 0) sKLevel = level;  // the staged K^-1 rows' level (read again after the next sync)
         __syncthreads();
         // xi = K^-1 [-q_lin ; b]  (first m rows of the saddle solution, qpcore.py:141-143)
         const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
         const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
-        for (int o = tid; o < DIM * m; o += nthr) {
-            const int ax = o / m, r = o - ax * m;
-            const double* Kr = Kl + r * nk;
-            double acc = 0.0;
-            for (int cc = 0; cc < m; ++cc) acc += ld_const(Kr + cc) * (-sQlin[ax * m + cc]);
-            for (int e = 0; e < ne; ++e) acc += ld_const(Kr + m + e) * bg[ax * ne + e];
-            sXi[o] = acc;
-            A.s.xi[(int64_t)i * DIM * m + o] = acc;
+        if (loop) {  // shared-memory copies (the level's rows are re-staged when the level changes)
+            for (int o = tid; o < DIM * m; o += nthr) {
+                const int ax = o / m, r = o - ax * m;
+                const double* Kr = sKx + r * nk;
+                const double* bq = sBq + ax * ne;
+                double acc = 0.0;
+                for (int cc = 0; cc < m; ++cc) acc += Kr[cc] * (-sQlin[ax * m + cc]);
+                for (int e = 0; e < ne; ++e) acc += Kr[m + e] * bq[e];
+                sXi[o] = acc;
+                A.s.xi[(int64_t)i * DIM * m + o] = acc;
+            }
+        } else {
+            for (int o = tid; o < DIM * m; o += nthr) {
+                const int ax = o / m, r = o - ax * m;
+                const double* Kr = Kl + r * nk;
+                double acc = 0.0;
+                for (int cc = 0; cc < m; ++cc) acc += ld_const(Kr + cc) * (-sQlin[ax * m + cc]);
+                for (int e = 0; e < ne; ++e) acc += ld_const(Kr + m + e) * bg[ax * ne + e];
+                sXi[o] = acc;
+                A.s.xi[(int64_t)i * DIM * m + o] = acc;
+            }
         }
         __syncthreads();
         for (int k = tid; k < DIM * n_p; k += nthr) {
@@ -351,14 +407,9 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         const T trho = (T)rho, trho_o = (T)rho_o;
         const int d_mode = init ? 0 : A.p.d_mode;
 
-#pragma unroll kUnroll
-        for (int j = g; j < n_o; j += G) {
-            T* sp = sbase + j * (W * n_p);
-            const double* tp = tbase + j * (DIM * n_p);
+        // one element (member i, obstacle j, sample t): v in / out, tracks given; loads / stores by the caller
+        auto elem = [&](int j, T* v, double trx, double trY, double trz) {
             const int64_t e = ((int64_t)i * n_o + j) * n_p + t;  // index into d / copies planes
-            const double trx = ld_const(tp);
-            const double trY = ld_const(tp + n_p);
-            const double trz = (DIM == 3) ? ld_const(tp + 2 * n_p) : 0.0;
             const T ia2 = (T)sIA2[j], ib2 = (T)sIB2[j];
 
             // line-of-sight scale of the previous iterate (solver_single.py:274-291)
@@ -378,17 +429,10 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                 }
                 dold = los_scale(qd);
             }
-            T v[W];
-            if constexpr (!init) {
-#pragma unroll
-                for (int w = 0; w < W; ++w) v[w] = ld_stream(sp + w * n_p);
-            }
             if constexpr (prime) {
                 prime_element<DIM, T, LAY, init>(v, trx, trY, trz, px, py, pz, sA[j], sB[j], dold, sumsq, mx,
                                                   accL, accT);
                 if constexpr (init) {
-#pragma unroll
-                    for (int w = 0; w < W; ++w) st_stream(sp + w * n_p, v[w]);
                     if (dst) dst[e] = dold;
                     if (cop) {
                         T c4[4];
@@ -421,13 +465,46 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
                     accL[2] += (double)v[o + 2];
                     accT[2] += trz + (double)off[2];
                 }
-#pragma unroll
-                for (int w = 0; w < W; ++w) st_stream(sp + w * n_p, v[w]);
                 if (dst) dst[e] = dn;
                 if (cop) {
 #pragma unroll
                     for (int c = 0; c < 2 * (DIM - 1); ++c) cop[c * Nel + e] = cp4[c];
                 }
+            }
+        };
+        if (cached) {
+#pragma unroll
+            for (int q = 0; q < kRegJ; ++q) {
+                const int j = g + G * q;
+                if (j < n_o) {
+                    if (rep_ == 0) {
+                        const T* sp = sbase + j * (W * n_p);
+                        const double* tp = tbase + j * (DIM * n_p);
+#pragma unroll
+                        for (int w = 0; w < W; ++w) vc[q][w] = ld_stream(sp + w * n_p);
+                        tc[q][0] = ld_const(tp);
+                        tc[q][1] = ld_const(tp + n_p);
+                        tc[q][2] = (DIM == 3) ? ld_const(tp + 2 * n_p) : 0.0;
+                    }
+                    elem(j, vc[q], tc[q][0], tc[q][1], tc[q][2]);
+                }
+            }
+        } else {
+#pragma unroll kUnroll
+            for (int j = g; j < n_o; j += G) {
+                T* sp = sbase + j * (W * n_p);
+                const double* tp = tbase + j * (DIM * n_p);
+                const double trx = ld_const(tp);
+                const double trY = ld_const(tp + n_p);
+                const double trz = (DIM == 3) ? ld_const(tp + 2 * n_p) : 0.0;
+                T v[W];
+                if constexpr (!init) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) v[w] = ld_stream(sp + w * n_p);
+                }
+                elem(j, v, trx, trY, trz);
+#pragma unroll
+                for (int w = 0; w < W; ++w) st_stream(sp + w * n_p, v[w]);
             }
         }
     }
@@ -468,6 +545,9 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         if constexpr (!prime) alg1_schedule(A, i, status0, level, rho, rho_o, nrm, mm, loop ? &sS : nullptr);
     }
     }  // rep_
+    if constexpr (loop) {
+        if (cached) flush();
+    }
 }
 
 template <int DIM, typename T, int LAY, int MODE, int NP>

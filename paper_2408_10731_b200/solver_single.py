@@ -197,27 +197,51 @@ def _upload(eng: Alg1Engine, state: SingleState):
                    rho_o=[state.rho_o], iteration=[state.iteration])
 
 
-_SCALARS = ("status", "level", "n_changes", "iteration", "n_hist", "rho", "rho_o", "res_norm", "res_max")
+_FSCALARS = ("rho", "rho_o", "res_norm", "res_max")
+_ISCALARS = ("status", "level", "n_changes", "iteration", "n_hist")
+
+
+def _host_angles(eng: Alg1Engine, words: np.ndarray, k: int) -> np.ndarray:
+    """Angle k (0: alpha, 1: beta) of member 0 from its raw state words (n_o, W, n_p), on the host."""
+    if eng.layout == "angle":
+        return words[:, k].astype(float)
+    if eng.layout == "unit":
+        return np.arctan2(words[:, 2 * k + 1].astype(float), words[:, 2 * k].astype(float))
+    w = words[:, k].astype(float)  # folded half-angle tangent (half_decode in alg1_elem.cuh)
+    inner = np.abs(w) <= 1
+    sg = np.where(np.signbit(w), -1.0, 1.0)
+    ang = 2.0 * np.arctan(np.where(inner, w, w - 3.0 * sg))
+    return np.where(inner, ang, ang + np.pi * sg)
 
 
 def _snapshot(eng: Alg1Engine) -> dict:
-    """Member 0's state, bookkeeping scalars and residual history in ONE device-to-host copy (one sync
-    instead of one per field); integer scalars travel as exact fp64."""
-    parts = [("xi", eng.xi[0])]
+    """Member 0's state, bookkeeping scalars and residual history in TWO device-to-host copies (float64 and
+    int32 groups, raw state words: the angles are decoded on the host), instead of one small kernel per
+    field."""
+    fparts = [("xi", eng.xi[0])]
     if eng.n_o:
-        parts += [("lam", eng.lam[:, 0]), ("alpha", eng.alpha[0]), ("beta", eng.beta[0] if eng.dim == 3 else None),
-                  ("d", eng.d[0] if eng.d is not None else None), ("copies", eng.copies[:, 0])]
-    parts.append(("scal", torch.stack([getattr(eng, k)[0].double() for k in _SCALARS])))
+        fparts += [("words", eng.state[0]), ("d", eng.d[0] if eng.d is not None else None),
+                   ("copies", eng.copies[:, 0] if eng.copies is not None else None)]
+    fparts += [(k, getattr(eng, k)[:1]) for k in _FSCALARS]
     if eng.hist is not None:
-        parts.append(("hist", eng.hist[0]))
-    parts = [(k, t) for k, t in parts if t is not None]
-    flat = torch.cat([t.reshape(-1).double() for _, t in parts]).cpu().numpy()
+        fparts.append(("hist", eng.hist[0]))
+    fparts = [(k, t) for k, t in fparts if t is not None]
+    flat = torch.cat([t.reshape(-1).to(torch.float64) for _, t in fparts]).cpu().numpy()
+    ints = torch.cat([getattr(eng, k)[:1] for k in _ISCALARS]).cpu().numpy()
     out, o = {}, 0
-    for k, t in parts:
+    for k, t in fparts:
         out[k] = flat[o:o + t.numel()].reshape(tuple(t.shape))
         o += t.numel()
-    for j, k in enumerate(_SCALARS):
-        out[k] = float(out["scal"][j])
+    for k in _FSCALARS:
+        out[k] = float(out[k][0])
+    for j, k in enumerate(_ISCALARS):
+        out[k] = int(ints[j])
+    if eng.n_o:
+        words = out.pop("words")  # (n_o, W, n_p)
+        out["lam"] = np.ascontiguousarray(np.transpose(words[:, eng.NV:], (1, 0, 2)))
+        out["alpha"] = _host_angles(eng, words, 0)
+        if eng.dim == 3:
+            out["beta"] = _host_angles(eng, words, 1)
     return out
 
 
