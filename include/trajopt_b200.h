@@ -134,6 +134,10 @@ typedef struct tro_alg1_state {
      * order[0 .. *n_order) only (e.g. the robots of a fleet still driving; tro_mpc_compact builds it) */
     const int32_t* order;
     const int32_t* n_order;
+    /* optional B (NULL: not written): the level of the latest iteration's position step.  Levels only grow by
+     * one per change, so a solve factorized levels level0 .. level_used (solver_single.py:198-202): a growth
+     * on the final iteration of a run that then stops is not followed by a factorization */
+    int32_t* level_used;
 } tro_alg1_state;
 
 /* Sums for the first position step + positions of the current xi + residual of the

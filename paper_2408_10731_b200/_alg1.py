@@ -21,6 +21,15 @@ import math
 import numpy as np
 import torch
 
+
+def _graphs_allowed() -> bool:
+    """CUDA-graph capture only on the main thread: a capture is invalidated by launches other threads make on
+    the legacy default stream at the same time, so solver instances running in other threads launch their
+    iterations directly (same kernels, same results)."""
+    import threading
+
+    return threading.current_thread() is threading.main_thread()
+
 from . import _lib, qpcore
 from .basis import BasisSet, boundary_matrix, line_basis_vectors
 
@@ -222,6 +231,7 @@ class Alg1Engine:
         self.n_hist = torch.zeros(B, **i32)
         self.status = torch.zeros(B, **i32)
         self.n_changes = torch.zeros(B, **i32)
+        self.level_used = torch.zeros(B, **i32)
         # tail balancing of the persistent kernel: per grid slot two halves' partial sums + a ticket
         slots = 2 * torch.cuda.get_device_properties(dev).multi_processor_count
         self.split_scratch = torch.zeros((slots, 2, 2 * dim * n_p + 2), **f64) if tail_split else None
@@ -240,7 +250,7 @@ class Alg1Engine:
             p(self.state), p(self.d), p(self.copies), p(self.xi), p(self.pos),
             p(self.sums), p(self.rho), p(self.rho_o), p(self.ring), p(self.res_norm), p(self.res_max), p(self.hist),
             p(self.level), p(self.iteration), p(self.last_change), p(self.n_hist), p(self.status),
-            p(self.n_changes), p(self.split_scratch), p(self.split_ticket), None, None)
+            p(self.n_changes), p(self.split_scratch), p(self.split_ticket), None, None, p(self.level_used))
         # the persistent kernel's work list (batches above the in-kernel-loop size): run() compacts it to the
         # members still iterating before every chunk, so converged members cost nothing and the rest stay
         # balanced over the CTAs; outside run() it is the identity
@@ -455,7 +465,7 @@ class Alg1Engine:
             n = min(chunk, n_iter - done)
             if check_every:
                 n = min(n, check_every - since_check)
-            if use_graph and n == chunk:
+            if use_graph and n == chunk and _graphs_allowed():
                 if self._graph is None or self._graph_n != chunk:
                     self._capture(chunk)
                 self._graph.replay()  # compacts the work list, then n iterations

@@ -128,6 +128,7 @@ class Alg1State(ctypes.Structure):
         ("split_ticket", c_void_p),
         ("order", c_void_p),
         ("n_order", c_void_p),
+        ("level_used", c_void_p),
     ]
 
 

@@ -93,6 +93,7 @@ __device__ __forceinline__ void alg1_schedule(const Alg1Args& A, int i, int stat
                                               double rho_o, double nrm, double mm, SchedS* S = nullptr) {
     A.s.res_norm[i] = nrm;
     A.s.res_max[i] = mm;
+    if (A.s.level_used) A.s.level_used[i] = level;  // this iteration's position step used `level`
     if (A.p.flags & TRO_FLAG_NO_SCHEDULE) {
         const int it = (S ? S->iteration : A.s.iteration[i]) + 1;  // bare am_iteration (solver_single.py:388)
         A.s.iteration[i] = it;

@@ -25,6 +25,15 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+
+def _graphs_allowed() -> bool:
+    """CUDA-graph capture only on the main thread: a capture is invalidated by launches other threads make on
+    the legacy default stream at the same time, so solver instances running in other threads launch their
+    iterations directly (same kernels, same results)."""
+    import threading
+
+    return threading.current_thread() is threading.main_thread()
+
 from . import _lib, qpcore
 from ._alg1 import rho_chain
 from .basis import AxisBoundary, BasisSet, Trajectory, boundary_matrix
@@ -551,7 +560,7 @@ class _Engine:
         done = 0
         while done < n_iter:
             n = min(chunk, n_iter - done)
-            if use_graph and n == chunk:
+            if use_graph and n == chunk and _graphs_allowed():
                 if self._graph is None or self._graph_n != chunk:
                     self._capture(chunk)
                 self._graph.replay()

@@ -22,6 +22,15 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+
+def _graphs_allowed() -> bool:
+    """CUDA-graph capture only on the main thread: a capture is invalidated by launches other threads make on
+    the legacy default stream at the same time, so solver instances running in other threads launch their
+    iterations directly (same kernels, same results)."""
+    import threading
+
+    return threading.current_thread() is threading.main_thread()
+
 from . import _lib, qpcore
 from .basis import AxisBoundary, BasisSet, Trajectory, boundary_matrix, line_basis_vectors  # noqa: F401
 from .geometry import D_CAP, EllipsoidShape  # noqa: F401
@@ -310,7 +319,7 @@ class MaEngine:
                 if bool((self.status == 0).sum().item() == 0):
                     break
             n = min(chunk, n_iter - done)
-            if use_graph and n == chunk:
+            if use_graph and n == chunk and _graphs_allowed():
                 if self._graph is None:
                     g = torch.cuda.CUDAGraph()
                     with torch.cuda.graph(g, capture_error_mode="thread_local"):

@@ -198,7 +198,7 @@ def _upload(eng: Alg1Engine, state: SingleState):
 
 
 _FSCALARS = ("rho", "rho_o", "res_norm", "res_max")
-_ISCALARS = ("status", "level", "n_changes", "iteration", "n_hist")
+_ISCALARS = ("status", "level", "n_changes", "iteration", "n_hist", "level_used")
 
 
 def _host_angles(eng: Alg1Engine, words: np.ndarray, k: int) -> np.ndarray:
@@ -339,6 +339,7 @@ def solve_single(problem: SingleProblem, params: SingleParams | None = None,
     if state is None:
         eng = _cached_engine(problem, params, max_hist=max(params.max_iter, 1))
         eng.cold_init()  # complete cold start: penalties, counters and schedule back to rho_start
+        level_start = int(eng.table.level_of(params.rho_start))
         state = SingleState(xi=None, d=None, alpha=None, beta=None, cos_a=None, sin_a=None, cos_b=None,
                             sin_b=None, lam_pos=None, lam_cos_a=None, lam_sin_a=None, lam_cos_b=None,
                             lam_sin_b=None, rho=params.rho_start, rho_o=params.rho_start)
@@ -346,19 +347,25 @@ def solve_single(problem: SingleProblem, params: SingleParams | None = None,
         eng = _engine_for(problem, params, rho0=[state.rho_o], max_hist=max(params.max_iter, 1))
         _upload(eng, state)
         eng.prime(1)
+        level_start = eng._level_for(state.rho_o)
     ran = eng.run(params.max_iter, use_graph=params.max_iter > 50, chunk=25,
                   check_every=50 if params.max_iter > 50 else 0)
     snap = _snapshot(eng)
     _raise_if_failed(eng, snap)
-    new = _factor_bookkeeping(state, eng, snap) if ran > 0 else 0
+    # the reference factorizes at a position step whose rho_o differs from the cached factor's
+    # (solver_single.py:198-202): levels level_start .. level_used, the first only if not already cached; a
+    # growth on the final iteration is not followed by a position step
+    fresh = 1 if (state._factor is None or state._factor_rho_o != state.rho_o) else 0
+    lv = int(snap["level_used"]) if ran > 0 else level_start
+    new = fresh + (lv - level_start) if ran > 0 else 0
     if ran > 0 or state.xi is None:
         _download(eng, into=state, snap=snap)
     if new:
         qpcore._bump(new)
     state.n_factorizations += new
-    lv = int(snap["level"])
-    state._factor = eng.table.factors[lv]
-    state._factor_rho_o = state.rho_o
+    if ran > 0:
+        state._factor = eng.table.factors[lv]
+        state._factor_rho_o = eng.table.rhos[lv]
 
     nh = int(snap["n_hist"])
     hist = snap["hist"][:nh] if "hist" in snap else np.zeros((0, 3))
@@ -571,11 +578,13 @@ def solve_single_batch(batch: SingleBatch | list, params: SingleParams | None = 
     eng.cold_init()  # complete cold start (rho, rho_o, level, iteration, schedule reset on the device)
     eng.run(params.max_iter, use_graph=use_graph, check_every=50 if params.tol > 0 else 0)
     _raise_if_failed(eng)
-    # one shared factorization per distinct rho_o level any member reached
-    qpcore._bump(int((eng.level - eng.level0).max().item()) + 1)
+    # one shared factorization per distinct rho_o level any member's position steps used
+    # (levels level0 .. level_used: a growth on a member's final iteration is not followed by one)
+    nf = (eng.level_used - eng.level0 + 1) if params.max_iter > 0 else torch.zeros_like(eng.level0)
+    qpcore._bump(int(nf.max().item()) if params.max_iter > 0 else 0)
     return BatchSolution(xi=eng.xi, converged=(eng.status & _lib.TRO_CONVERGED) != 0, iterations=eng.iteration,
                          residual_norm=eng.res_norm, residual_max=eng.res_max, rho_o=eng.rho_o,
-                         n_factorizations=eng.n_changes + 1, history=eng.hist, engine=eng)
+                         n_factorizations=nf, history=eng.hist, engine=eng)
 
 
 # ---------------------------------------------------------------- diagnostics (host, small arrays)

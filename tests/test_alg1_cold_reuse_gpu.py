@@ -142,3 +142,27 @@ def test_register_tracks_equal_streamed_tracks():
             eng._consts.track_lin = None
         out.append(_result(solve_single_batch(batch, PARAMS, engine=eng)))
     _same(out[0], out[1])
+
+
+def test_factorization_count_when_the_final_iteration_grows_the_penalty():
+    """A run that stops right after a penalty growth never factorizes the new level (the reference factorizes
+    in the NEXT position step, solver_single.py:198-202): n_factorizations counts the levels used."""
+    from oracle import alg1 as O
+
+    prob = scenarios.c1_problem()
+    op = O.Problem(P=prob.basis.P, Pd=prob.basis.Pdot, Pdd=prob.basis.Pddot,
+                   bvals=np.stack([bc.values() for bc in prob.boundary])[None], desired=prob.desired[None],
+                   tracks=np.stack([o.centers for o in prob.obstacles]),
+                   a=np.array([o.shape.a for o in prob.obstacles]), b=np.array([o.shape.b for o in prob.obstacles]))
+    prm = dict(tol=0.0, stall_improvement=0.5)  # frequent growths
+    full = O.solve(op, O.Params(max_iter=120, **prm))
+    rho = np.array(full.rho_hist[0])  # rho_o used by each iteration's position step
+    grow_after = [k + 1 for k in range(len(rho) - 1) if rho[k + 1] != rho[k]]  # iterations ending in a growth
+    assert len(grow_after) >= 2
+    for n in (grow_after[0], grow_after[1], grow_after[0] + 1):
+        ref = O.solve(op, O.Params(max_iter=n, **prm))
+        want = int(ref.state.n_factorizations[0])
+        sol = solve_single(prob, SingleParams(max_iter=n, **prm))
+        assert sol.n_factorizations == want, (n, sol.n_factorizations, want)
+        bs = solve_single_batch(SingleBatch.from_problems([prob] * 70), SingleParams(max_iter=n, **prm))
+        assert set(bs.n_factorizations.cpu().numpy().tolist()) == {want}, n

@@ -30,7 +30,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.Alg1Dims) == 40
     assert ctypes.sizeof(_lib.Alg1Consts) == 13 * 8
     assert ctypes.sizeof(_lib.Alg1Params) == 4 * 8 + 4 * 4
-    assert ctypes.sizeof(_lib.Alg1State) == 22 * 8
+    assert ctypes.sizeof(_lib.Alg1State) == 23 * 8
 
 
 def test_host_only_calls():
