@@ -1,5 +1,6 @@
 #!/bin/bash
 # every bench config once (1 GPU), JSON lines into gpurun_out/final_<cfg>.json, then the reference arms
+cd $GRAFT_REPO_ROOT 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 for cfg in c5 c2 c1 c2alt c3 c4 val mpc; do
   timeout 900 python bench.py --config $cfg --steps 3 --warmup 3 > gpurun_out/final_$cfg.json 2> gpurun_out/final_$cfg.err
