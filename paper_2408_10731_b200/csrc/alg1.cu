@@ -41,6 +41,17 @@ constexpr int kMaxRing = 64;
 constexpr int kMaxThreads = TRO_MAX_THREADS;
 constexpr int kUnroll = TRO_UNROLL;
 
+// phase timing of the in-kernel loop (diagnostic build only: -DTRO_PHASE_PROF; tools/c1_phases.py)
+#ifdef TRO_PHASE_PROF
+__device__ long long g_phase[1024 * 8];
+#define TRO_PHASE(k)                                                                                    \
+    if (loop && tid == 0 && rep_ < 1024) g_phase[rep_ * 8 + (k)] = clock64() - ph_t0;
+#define TRO_PHASE0() long long ph_t0 = (loop && tid == 0) ? clock64() : 0;
+#else
+#define TRO_PHASE(k)
+#define TRO_PHASE0()
+#endif
+
 struct Alg1Args {
     tro_alg1_dims d;
     tro_alg1_consts c;
@@ -64,7 +75,8 @@ __host__ __device__ inline SmemLayout smem_layout(int n_p, int m, int dim, int n
     L.pos_prev = off; off += dim * n_p;
     L.pos_new = off;  off += dim * n_p;
     L.sums_in = off;  off += 2 * dim * n_p;
-    L.red = off;      off += G * 2 * dim * n_p;
+    L.red = off;      // group partial sums; MODE 3 also uses it for the q_lin chunk partials
+    off += (G * 2 * dim * n_p > 2 * dim * kMaxM * 15) ? G * 2 * dim * n_p : 2 * dim * kMaxM * 15;
     L.shp = off;      off += 4 * (n_o > 0 ? n_o : 1);
     L.qlin = off;     off += dim * kMaxM;
     L.xi = off;       off += dim * kMaxM;
@@ -183,8 +195,8 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     const int G = A.G;
     const SmemLayout L = smem_layout(n_p, m, DIM, n_o, G);
     double* sP = smem + L.P;
-    double* sPosPrev = smem + L.pos_prev;
-    double* sPosNew = smem + L.pos_new;
+    double* const sPosA = smem + L.pos_prev;
+    double* const sPosB = smem + L.pos_new;
     double* sSumIn = smem + L.sums_in;
     double* sRed = smem + L.red;
     double* sA = smem + L.shp;
@@ -227,6 +239,11 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
     };
     for (int rep_ = 0; rep_ < (loop ? A.n_loop : 1); ++rep_) {
     if (loop && rep_ > 0) __syncthreads();  // the previous iteration's writes (tid 0: sS; all: sums, positions)
+    TRO_PHASE0()
+    // MODE 3 alternates the two position buffers (this iteration's new positions become the next one's
+    // previous positions without a copy)
+    double* sPosPrev = (loop && (rep_ & 1)) ? sPosB : sPosA;
+    double* sPosNew = (loop && (rep_ & 1)) ? sPosA : sPosB;
     // ---------------- frozen members (converged / failed) do nothing
     if (loop && rep_ == 0 && tid == 0) {
         sS.status = A.s.status[i];
@@ -284,11 +301,10 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
             for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = posg[k];
             const double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
             for (int k = tid; k < 2 * DIM * n_p; k += nthr) sSumIn[k] = sg[k];
-        } else {  // the previous iteration's positions; its epilogue left the sums in sSumIn
-            for (int k = tid; k < DIM * n_p; k += nthr) sPosPrev[k] = sPosNew[k];
-        }
+        }  // rep_ > 0: sPosPrev is the previous iteration's sPosNew; its epilogue left the sums in sSumIn
     }
     __syncthreads();
+    TRO_PHASE(1)
 
     if constexpr (prime) {
         // positions of the current xi; d recompute (d_mode 2) uses these too
@@ -336,20 +352,49 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         // ---------- QP position step (solver_single.py:204-211)
         // q_lin[ax][c] = (q + sum_t Slam[ax][t] P[t][c]) - sum_t (rho_o ST[ax][t]) P[t][c]
         const double* qg = A.c.q + (int64_t)i * DIM * m;
-        for (int o = warp; o < DIM * m; o += nwarps) {
-            const int ax = o / m, cc = o - ax * m;
-            double u = 0.0, v = 0.0;
-            for (int t = lane; t < n_p; t += 32) {
-                const double pt = sP[t * m + cc];
-                u += sSumIn[ax * n_p + t] * pt;
-                v += (rho_o * sSumIn[(DIM + ax) * n_p + t]) * pt;
+        if (loop) {
+            // one pass over all threads: (output, 7-sample chunk) partial products into the (idle) reduction
+            // buffer, then one thread per output adds the chunks in order (the in-kernel loop's latency path)
+            constexpr int kQC = 15;
+            const int chunk = (n_p + kQC - 1) / kQC;
+            for (int w = tid; w < DIM * m * kQC; w += nthr) {
+                const int o = w / kQC, c = w - o * kQC, ax = o / m, cc = o - ax * m;
+                const int t0 = c * chunk, t1 = min(t0 + chunk, n_p);
+                double u = 0.0, v = 0.0;
+                for (int t = t0; t < t1; ++t) {
+                    const double pt = sP[t * m + cc];
+                    u = fma(sSumIn[ax * n_p + t], pt, u);
+                    v = fma(rho_o * sSumIn[(DIM + ax) * n_p + t], pt, v);
+                }
+                sRed[2 * w] = u;
+                sRed[2 * w + 1] = v;
             }
-            u = warp_sum(u);
-            v = warp_sum(v);
-            if (lane == 0) sQlin[o] = ((loop ? sBq[DIM * kMaxNk + o] : qg[o]) + u) - v;
+            __syncthreads();
+            for (int o = tid; o < DIM * m; o += nthr) {
+                double u = 0.0, v = 0.0;
+                for (int c = 0; c < kQC; ++c) {
+                    u += sRed[2 * (o * kQC + c)];
+                    v += sRed[2 * (o * kQC + c) + 1];
+                }
+                sQlin[o] = (sBq[DIM * kMaxNk + o] + u) - v;
+            }
+        } else {
+            for (int o = warp; o < DIM * m; o += nwarps) {
+                const int ax = o / m, cc = o - ax * m;
+                double u = 0.0, v = 0.0;
+                for (int t = lane; t < n_p; t += 32) {
+                    const double pt = sP[t * m + cc];
+                    u += sSumIn[ax * n_p + t] * pt;
+                    v += (rho_o * sSumIn[(DIM + ax) * n_p + t]) * pt;
+                }
+                u = warp_sum(u);
+                v = warp_sum(v);
+                if (lane == 0) sQlin[o] = (qg[o] + u) - v;
+            }
         }
         if (loop && tid == 0) sKLevel = level;  // the staged K^-1 rows' level (read again after the next sync)
         __syncthreads();
+        TRO_PHASE(2)
         // xi = K^-1 [-q_lin ; b]  (first m rows of the saddle solution, qpcore.py:141-143)
         const double* Kl = A.c.kinv + (int64_t)level * nk * nk;
         const double* bg = A.c.bvals + (int64_t)i * DIM * ne;
@@ -376,6 +421,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
             }
         }
         __syncthreads();
+        TRO_PHASE(3)
         for (int k = tid; k < DIM * n_p; k += nthr) {
             const int ax = k / n_p, t = k - ax * n_p;
             double acc = 0.0;
@@ -384,6 +430,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
             A.s.pos[(int64_t)i * DIM * n_p + k] = acc;  // previous positions already staged
         }
         __syncthreads();
+        TRO_PHASE(4)
     }
 
     // ---------------- fused element pass
@@ -526,6 +573,7 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         sWarp[32 + warp] = mx;
     }
     __syncthreads();
+    TRO_PHASE(5)
     double* sg = A.s.sums + (int64_t)i * 2 * DIM * n_p;
     for (int k = tid; k < 2 * DIM * n_p; k += nthr) {
         double acc = 0.0;
@@ -533,17 +581,20 @@ __global__ void __launch_bounds__(kMaxThreads, TRO_MIN_BLOCKS) alg1_kernel(Alg1A
         sg[k] = acc;
         if constexpr (loop) sSumIn[k] = acc;  // the next iteration's position step reads them from here
     }
-    if (tid == 0) {
-        double ss = 0.0, mm = 0.0;
-        for (int w = 0; w < nwarps; ++w) {
-            ss += sWarp[w];
-            mm = fmax(mm, sWarp[32 + w]);
-        }
+    if (warp == 0) {
+        // the per-warp partials reduced by warp 0 (shuffle tree), then lane 0 runs the schedule
+        double ss = lane < nwarps ? sWarp[lane] : 0.0;
+        double mm = lane < nwarps ? sWarp[32 + lane] : 0.0;
+        ss = warp_sum(ss);
+        mm = warp_max(mm);
+        if (lane == 0) {
         if (ss != ss) mm = ss;  // np.max propagates NaN
         const double nrm = sqrt(ss);
         A.s.res_norm[i] = nrm;
         A.s.res_max[i] = mm;
         if constexpr (!prime) alg1_schedule(A, i, status0, level, rho, rho_o, nrm, mm, loop ? &sS : nullptr);
+        TRO_PHASE(6)
+        }
     }
     }  // rep_
     if constexpr (loop) {
@@ -816,3 +867,9 @@ extern "C" int tro_alg1_linear_terms(int64_t n_members, int32_t n_p, int32_t m, 
         n_members, n_p, m, dim, n_eq, P, frac, bvals, desired, -2.0 * w_track, q);
     return (int)cudaGetLastError();
 }
+
+#ifdef TRO_PHASE_PROF
+extern "C" int tro_debug_phase(long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, tro::g_phase, sizeof(long long) * (n < 8192 ? n : 8192));
+}
+#endif

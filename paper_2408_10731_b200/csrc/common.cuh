@@ -46,21 +46,28 @@ __device__ __forceinline__ double warp_max(double v) {
 // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)), then the n % 8 tail in order; then / n.
 // (The stall windows here are <= 32, so the recursive n > 128 branch never applies.)
 __device__ __forceinline__ double np_mean_ring(const double* ring, int start, int w, int w2) {
+    // ring index of window element k: (start + k) mod w2, one division for the whole window
+    int i0 = start % w2;
+    auto at = [&](int k) {
+        int idx = i0 + k;
+        if (idx >= w2) idx -= w2;
+        return ring[idx];
+    };
     double res;
     if (w < 8) {
         res = 0.0;
-        for (int k = 0; k < w; ++k) res += ring[(start + k) % w2];
+        for (int k = 0; k < w; ++k) res += at(k);
     } else {
         double r[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = ring[(start + j) % w2];
+        for (int j = 0; j < 8; ++j) r[j] = at(j);
         int k = 8;
         for (; k < w - (w % 8); k += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] += ring[(start + k + j) % w2];
+            for (int j = 0; j < 8; ++j) r[j] += at(k + j);
         }
         res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-        for (; k < w; ++k) res += ring[(start + k) % w2];
+        for (; k < w; ++k) res += at(k);
     }
     return res / (double)w;
 }
