@@ -221,7 +221,7 @@ def run_c4(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_c4()
-        line["cpu_baseline"] = {"value": v, "unit": "sample-inner-it/s", "cores": info["cores"], "kind": "port",
+        line["cpu_baseline"] = {"value": v, "unit": "sample-inner-it/s", "cores": info["cores"], "kind": "port", "cpu_model": _cpu_model(),
                                 "sample": info["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -377,7 +377,7 @@ def run_c2alt(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_c2alt()
-        line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port",
+        line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port", "cpu_model": _cpu_model(),
                                 "sample": info["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -476,7 +476,7 @@ def run_val(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_val()
-        line["cpu_baseline"] = {"value": v, "unit": "traj/s", "cores": 1, "kind": "port", "sample": info}
+        line["cpu_baseline"] = {"value": v, "unit": "traj/s", "cores": 1, "kind": "port", "cpu_model": _cpu_model(), "sample": info}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -627,7 +627,7 @@ def run_mpc(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_mpc()
-        line["cpu_baseline"] = {"value": v, "unit": "robot-steps/s", "cores": 1, "kind": "port",
+        line["cpu_baseline"] = {"value": v, "unit": "robot-steps/s", "cores": 1, "kind": "port", "cpu_model": _cpu_model(),
                                 "sample": info}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -776,7 +776,7 @@ def run_c3(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, info = cpu_reference_c3()
-        line["cpu_baseline"] = {"value": v, "unit": "problem-it/s", "cores": info["cores"], "kind": "port",
+        line["cpu_baseline"] = {"value": v, "unit": "problem-it/s", "cores": info["cores"], "kind": "port", "cpu_model": _cpu_model(),
                                 "sample": info["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -879,6 +879,20 @@ def traffic_for(cfg: str):
     with open(path) as fh:
         d = json.load(fh)
     return d.get(cfg, {}).get("dram_bytes_per_launch")
+
+
+def _cpu_model() -> str:
+    """The host CPU the baseline ran on (BASELINE.md §3 asks for it), from /proc/cpuinfo."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def measured_peaks():
@@ -1240,7 +1254,7 @@ def run_b200(args):
         # bounded sample: ~40 member-solves per host core (C5 ~0.45 s each -> ~20 s of CPU work)
         sample = 40 * (os.cpu_count() or 1) if args.config != "c1" else 2 * (os.cpu_count() or 1)
         v, info = cpu_reference(args.config, sample)
-        line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port",
+        line["cpu_baseline"] = {"value": v, "unit": "traj-it/s", "cores": info["cores"], "kind": "port", "cpu_model": _cpu_model(),
                                 "sample": f"{sample} members x {info['iterations']} AM its of the same recipe, "
                                           f"oracle port of solver_single (1 BLAS thread/process), "
                                           f"wall {info['wall_s']:.1f}s"}
@@ -1267,7 +1281,7 @@ def run_reference(args):
                           "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                           "dtype": "f64", "data": "synthetic", "config": {"workload": CONFIGS["c3"][3]},
                           "cpu_baseline": {"value": value, "unit": "problem-it/s", "cores": info["cores"],
-                                           "kind": "port", "sample": info["sample"]},
+                                           "kind": "port", "cpu_model": _cpu_model(), "sample": info["sample"]},
                           "e2e": {"value": value, "unit": "problem-it/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}), flush=True)
         return
@@ -1283,7 +1297,7 @@ def run_reference(args):
                           "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                           "dtype": "f64", "data": "synthetic", "config": {"workload": CONFIGS["c2alt"][3]},
                           "cpu_baseline": {"value": value, "unit": "traj-it/s", "cores": info["cores"],
-                                           "kind": "port", "sample": info["sample"]},
+                                           "kind": "port", "cpu_model": _cpu_model(), "sample": info["sample"]},
                           "e2e": {"value": value, "unit": "traj-it/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}), flush=True)
         return
@@ -1303,7 +1317,7 @@ def run_reference(args):
                           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
                           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                           "config": {"workload": CONFIGS[args.config][3]},
-                          "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "port", "sample": info},
+                          "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "port", "cpu_model": _cpu_model(), "sample": info},
                           "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
               flush=True)
         return
@@ -1319,7 +1333,7 @@ def run_reference(args):
                           "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                           "dtype": "f64", "data": "synthetic", "config": {"workload": CONFIGS["c4"][3]},
                           "cpu_baseline": {"value": value, "unit": "sample-inner-it/s", "cores": info["cores"],
-                                           "kind": "port", "sample": info["sample"]},
+                                           "kind": "port", "cpu_model": _cpu_model(), "sample": info["sample"]},
                           "e2e": {"value": value, "unit": "sample-inner-it/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}), flush=True)
         return
@@ -1348,7 +1362,7 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic (seeded scenario recipe, SURVEY.md §8(d))",
         "config": {"workload": desc, "members": members_total, "n_obs": n_o, "n_p": 100, "am_iters": n_iter},
-        "cpu_baseline": {"value": value, "unit": "traj-it/s", "cores": procs, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "traj-it/s", "cores": procs, "kind": "port", "cpu_model": _cpu_model(),
                          "sample": f"{sample} members x {n_iter} AM its per step (bounded sample of the workload)"},
         "e2e": {"value": value, "unit": "traj-it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

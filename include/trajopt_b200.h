@@ -275,6 +275,11 @@ typedef struct tro_ma_consts {
     const double* statics;   /* B x n_static x 3 sphere centres (NULL if n_static == 0) */
     const double* line_u;    /* m: straight-line init coefficients (see tro_alg1_consts) */
     const double* line_v;
+    const double* bnd;       /* optional 6 x m boundary rows of one agent (basis.boundary_matrix) and, after them, */
+                             /* its m x 6 pseudo-inverse A'(AA')^-1: after each QP step every agent's coefficients */
+                             /* are projected onto A c = b_eq (c -= A+ (A c - b_eq)), so the boundary conditions */
+                             /* hold to rounding although the explicit K^-1 (cond ~1e12) leaves ~1e-8 there; the */
+                             /* projection only removes error (orthogonal onto the constraint set).  NULL: off */
 } tro_ma_consts;
 
 typedef struct tro_ma_state {

@@ -168,7 +168,7 @@ class MaDims(ctypes.Structure):
 
 class MaConsts(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in ("P", "kinv", "level_rho", "pair_i", "pair_j", "pair_s", "pair_a", "pair_b",
-                                        "inc_ptr", "inc_pair", "b_eq", "statics", "line_u", "line_v")]
+                                        "inc_ptr", "inc_pair", "b_eq", "statics", "line_u", "line_v", "bnd")]
 
 
 class MaState(ctypes.Structure):

@@ -177,6 +177,32 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
         }
     }
     __syncthreads();
+    if (mode == 0 && A.c.bnd) {
+        // project every agent's new coefficients onto its boundary conditions, c -= A+ (A c - b) (the explicit
+        // K^-1's ~1e-8 there; the reference's LU solve holds them to ~1e-13): one thread per (axis, agent)
+        const double* Ab = A.c.bnd;           // 6 x m
+        const double* Ap = A.c.bnd + 6 * m;   // m x 6
+        for (int k = tid; k < 3 * n_a; k += blockDim.x) {
+            const int ax = k / n_a, a = k - ax * n_a;
+            double* c = sXi + ax * nv + a * m;
+            const double* bv = bg + ax * neq + 6 * a;
+            double r[6];
+#pragma unroll
+            for (int e = 0; e < 6; ++e) {
+                double acc = -bv[e];
+                for (int cc = 0; cc < m; ++cc) acc = fma(Ab[e * m + cc], c[cc], acc);
+                r[e] = acc;
+            }
+            for (int cc = 0; cc < m; ++cc) {
+                double acc = c[cc];
+#pragma unroll
+                for (int e = 0; e < 6; ++e) acc = fma(-Ap[cc * 6 + e], r[e], acc);
+                c[cc] = acc;
+                xg[ax * nv + a * m + cc] = acc;
+            }
+        }
+        __syncthreads();
+    }
     for (int k = tid; k < n_p * n_a; k += blockDim.x) {  // one (t, agent) per thread: 3 axes share the P row
         const int t = k / n_a, a = k - t * n_a;
         double p0 = 0.0, p1 = 0.0, p2 = 0.0;

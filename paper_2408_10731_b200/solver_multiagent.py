@@ -216,6 +216,9 @@ class MaEngine:
                         if struct.n_static else None)
         u, v = line_basis_vectors(struct.basis)
         self.line_u, self.line_v = torch.as_tensor(u, **f64), torch.as_tensor(v, **f64)
+        # one agent's boundary rows and their pseudo-inverse: the boundary projection after each QP step
+        Ab = boundary_matrix(struct.basis)
+        self.bnd = torch.as_tensor(np.concatenate([Ab.ravel(), np.linalg.pinv(Ab).ravel()]), **f64)
         self.state = torch.zeros((B, n_p, 3, npairs), **f64)
         self.xi = torch.zeros((B, 3, n_a * m), **f64)
         self.sums = torch.zeros((B, 2, n_a, 3, m), **f64)
@@ -237,7 +240,7 @@ class MaEngine:
         self._consts = _lib.MaConsts(p(self.P), p(self.kinv), p(self.level_rho), p(self.pair_i), p(self.pair_j),
                                      p(self.pair_s), p(self.pair_a), p(self.pair_b), p(self.inc_ptr),
                                      p(self.inc_pair), p(self.b_eq), p(self.statics), p(self.line_u),
-                                     p(self.line_v))
+                                     p(self.line_v), p(self.bnd))
         self._state = _lib.MaState(p(self.state), p(self.xi), p(self.sums), p(self.ring), p(self.res_norm),
                                    p(self.res_max), p(self.hist), p(self.level), p(self.iteration),
                                    p(self.last_change), p(self.n_hist), p(self.status), p(self.export_d),

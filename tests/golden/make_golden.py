@@ -690,7 +690,51 @@ def _c5_member(args):
     return row
 
 
-def make_c5_dist(n_members=512, n_o=100):
+def make_c2_dist():
+    """The same fixture for the C2 recipe (n_o 50)."""
+    make_c5_dist(512, 50, "c2_dist.npz")
+
+
+def make_ma_dist(n_problems=128):
+    """Tier-3 end-state fixture of the C3 recipe (16 agents, square-antipodal seeds 0..n-1, agent (0.3, 0.45),
+    JointParams(max_iter=200, rho_final=1e3)): per problem the reference's final residual norm / max,
+    convergence, iterations, final level, min pair distance and the boundary-condition error."""
+    import multiprocessing as mp
+
+    with mp.get_context("fork").Pool(os.cpu_count()) as pool:
+        rows = pool.map(_ma_problem, list(range(n_problems)), chunksize=2)
+    out = {"seeds": np.arange(n_problems), "scal": np.array(rows, dtype=float),
+           "scal_names": np.array(["res_norm", "res_max", "converged", "iterations", "rho", "min_pair_distance",
+                                   "boundary_err"])}
+    np.savez_compressed(os.path.join(OUT, "ma_dist.npz"), **out)
+    sc = out["scal"]
+    print("ma_dist: converged", sc[:, 2].mean(), "median res_norm", np.median(sc[:, 0]), "median min dist",
+          np.median(sc[:, 5]))
+
+
+def _ma_problem(seed):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from trajopt import solver_multiagent as MA
+    from trajopt.bench.runner import multiagent_problem_from_scenario
+    from trajopt.geometry import EllipsoidShape
+
+    basis = build_basis(0.0, 10.0, 100, 10)
+    sc = gen_scenario("square-antipodal", {"n_agents": 16, "agent_radius": 0.3, "side": 8.0}, seed=seed)
+    prob = multiagent_problem_from_scenario(sc, basis)
+    prob.agent_shape = EllipsoidShape(0.3, 0.45)
+    sol = MA.solve_joint(prob, MA.JointParams(max_iter=200, rho_final=1e3))
+    xi = sol.state.xi  # (3, n_a m)
+    m = basis.P.shape[1]
+    bc = 0.0
+    for a, b in enumerate(prob.boundaries):
+        for k in range(3):
+            c = xi[k, a * m:(a + 1) * m]
+            bc = max(bc, abs(basis.P[0] @ c - b[k].p0), abs(basis.P[-1] @ c - b[k].p1))
+    return [sol.residual_norm, sol.residual_max, int(sol.converged), sol.iterations, sol.residual_history[-1]["rho"],
+            sol.min_pair_distance, bc]
+
+
+def make_c5_dist(n_members=512, n_o=100, name="c5_dist.npz"):
     """Tier-3 end-state distribution fixture: members 0..n-1 of the C5 recipe."""
     import multiprocessing as mp
 
@@ -702,9 +746,9 @@ def make_c5_dist(n_members=512, n_o=100):
         out[f"{tag}_scal"] = np.array([r[k][1:] for r in rows], dtype=float)
     out["scal_names"] = np.array(["res_norm", "res_max", "rho_o", "iterations", "converged", "n_factorizations",
                                   "worst_violation", "boundary_err"])
-    np.savez_compressed(os.path.join(OUT, "c5_dist.npz"), **out)
+    np.savez_compressed(os.path.join(OUT, name), **out)
     f, c = out["fixed_scal"], out["conv_scal"]
-    print("c5_dist: fixed median max|r|", np.median(f[:, 1]), "collision-free", np.mean(f[:, 6] <= 0),
+    print(name, ": fixed median max|r|", np.median(f[:, 1]), "collision-free", np.mean(f[:, 6] <= 0),
           "| converged", np.mean(c[:, 4]), "iters median", np.median(c[:, 3]))
 
 

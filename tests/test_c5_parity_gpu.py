@@ -103,17 +103,17 @@ def test_c5_teacher_forced_fp32(golden, member, k, layout):
 
 
 # ------------------------------------------------------------------ tier 3: end-state distributions
-def _device_dist(tag):
+def _device_dist(tag, n_o=100, name="c5_dist.npz"):
     from paper_2408_10731_b200 import metrics, scenarios
 
-    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c5_dist.npz"))
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name))
     members = g["members"]
     basis = build_basis(0.0, 10.0, 100, 10)
-    batch = scenarios.flow3d_batch(100, members, basis=basis)
+    batch = scenarios.flow3d_batch(n_o, members, basis=basis)
     params = SingleParams(max_iter=200, tol=0.0) if tag == "fixed" else SingleParams()
     sol = solve_single_batch(batch, params, layout="half")
     res = sol.numpy()
-    sc = scenarios.flow3d_scenario(100, 0)
+    sc = scenarios.flow3d_scenario(n_o, 0)
     val = metrics.validate_batch(sc, basis.grid.timestamps, xi=res.xi, basis=basis)
     pos = np.einsum("tc,bkc->btk", basis.P, res.xi)
     bc = np.maximum(np.abs(pos[:, 0] - batch.bvals[:, :, 0]).max(1), np.abs(pos[:, -1] - batch.bvals[:, :, 3]).max(1))
@@ -138,9 +138,10 @@ def _bootstrap_quantile_ok(dev, ref, q, rng, n_boot=2000):
     return lo <= 0.0 <= hi
 
 
-@pytest.mark.parametrize("tag", ["fixed", "conv"])
-def test_c5_end_state_distribution(tag):
-    g, res, val, bc = _device_dist(tag)
+@pytest.mark.parametrize("tag,n_o,name", [("fixed", 100, "c5_dist.npz"), ("conv", 100, "c5_dist.npz"),
+                                          ("fixed", 50, "c2_dist.npz"), ("conv", 50, "c2_dist.npz")])
+def test_c5_end_state_distribution(tag, n_o, name):
+    g, res, val, bc = _device_dist(tag, n_o, name)
     names = list(g["scal_names"])
     ref = g[f"{tag}_scal"]
     n = ref.shape[0]
@@ -233,3 +234,47 @@ def test_device_window_mean_is_numpy_mean_bitwise():
     np.testing.assert_array_equal(got, ref)
     seq = np.array([sum(x[k, : int(w[k])]) / w[k] for k in range(n)])
     assert (seq != ref).sum() > 100  # the test discriminates numpy's order from a sequential sum
+
+
+def test_multiagent_end_state_distribution():
+    """Tier 3 for the C3 recipe (16 agents, square-antipodal seeds 0..127, chaotic per SURVEY A.3): the device
+    batch against the reference's own runs (tests/golden/ma_dist.npz): final residual norm quantiles, final
+    penalty-level mix, minimum pair distance quantiles, converged fraction, boundary conditions."""
+    from paper_2408_10731_b200 import scenarios as S
+    from paper_2408_10731_b200 import solver_multiagent as MA
+    from paper_2408_10731_b200.basis import AxisBoundary
+    from paper_2408_10731_b200.geometry import EllipsoidShape
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ma_dist.npz"))
+    names = list(g["scal_names"])
+    ref = g["scal"]
+    col = lambda name: ref[:, names.index(name)]  # noqa: E731
+    b = build_basis(0.0, 10.0, 100, 10)
+    probs = []
+    for s in g["seeds"]:
+        starts, goals = S.square_antipodal(16, 8.0, 0.3, seed=int(s))
+        bnds = [tuple(AxisBoundary(p0=float(starts[i, k]), p1=float(goals[i, k])) for k in range(3))
+                for i in range(16)]
+        probs.append(MA.MultiAgentProblem(basis=b, boundaries=bnds, agent_shape=EllipsoidShape(0.3, 0.45)))
+    params = MA.JointParams(max_iter=200, rho_final=1e3)
+    eng = MA.solve_joint_batch(probs, params, history=True)
+    n = len(probs)
+    xi = eng.xi.cpu().numpy()  # (B, 3, 16 m)
+    m = b.P.shape[1]
+    pos = np.einsum("tc,bkac->batk", b.P, xi.reshape(n, 3, 16, m))  # (B, agent, t, axis)
+    dmin = np.array([min(float(np.linalg.norm(pos[q, i] - pos[q, j], axis=1).min())
+                         for i in range(16) for j in range(i + 1, 16)) for q in range(n)])
+    bc = np.array([max(max(abs(pos[q, a, 0, k] - probs[q].boundaries[a][k].p0),
+                           abs(pos[q, a, -1, k] - probs[q].boundaries[a][k].p1)) for a in range(16) for k in range(3))
+                   for q in range(n)])
+    res_norm = eng.res_norm.cpu().numpy()
+    conv = (eng.status.cpu().numpy() & 1) != 0
+    rho = eng.level_rho.cpu().numpy()[eng.level.cpu().numpy()]
+    rng = np.random.default_rng(1)
+    assert _binom_ok(float(conv.mean()), float(col("converged").mean()), n)
+    for q in (0.1, 0.25, 0.5, 0.75, 0.9):
+        assert _bootstrap_quantile_ok(np.log10(res_norm), np.log10(col("res_norm")), q, rng), ("res", q)
+        assert _bootstrap_quantile_ok(dmin, col("min_pair_distance"), q, rng), ("dmin", q)
+    # the staged level schedule ends at the same penalty for (almost) every problem
+    assert abs(float(np.mean(rho == rho.max())) - float(np.mean(col("rho") == col("rho").max()))) <= 0.1
+    assert float(bc.max()) <= 1e-8 and float(col("boundary_err").max()) <= 1e-8
