@@ -15,10 +15,10 @@
 // large) and the boundary columns [nv, nk) (against b_eq, O(1)); one exponent over both would bound the error
 // by max|A_r| max|R_c|, which the saddle inverse's structure makes ~1e4 x larger than the result.
 //
-// Kernel: one CTA per (128-row m-tile, 32-column n-tile); warp 0 = TMA producer (2-D tensor maps over
+// Kernel: persistent, one CTA per SM over (128-row m-tile, 32-column n-tile) tiles; warp 0 = TMA producer (2-D tensor maps over
 // the pre-tiled int8 slices: every (slice, tile, k-step) operand is one 4 KB / 1 KB box already in the
 // canonical no-swizzle K-major core-matrix layout), warp 1 = TMEM allocator + MMA issuer (one elected lane:
-// S(S+1)/2 MMAs of 128x32x32 per k-step into 2 x S int32 accumulators of 32 TMEM columns each), warps 4-7 =
+// S(S+1)/2 MMAs of 128x32x32 per k-step into 2 x S int32 accumulators of 32 TMEM columns each), warps 4-11 =
 // epilogue (tcgen05.ld 32x32b, Horner in fp64, exact power-of-two scaling, coalesced xi stores).  Columns of
 // problems at different rho levels: one pass per level present in the tile (A slices are per level; the
 // B slices carry each column's own rho).
@@ -98,6 +98,12 @@ struct OzArgs {
     double* xi;            // B x 3 x nv
 };
 
+// 2^e as a double, built from the exponent field (e within the normal range)
+__device__ __forceinline__ double pow2(int e) {
+    e = max(-1022, min(1023, e));
+    return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
 // ---------------------------------------------------------------- B slices: R columns -> int8 slices
 // one warp per column c = 3 p + ax: R[k][c] = rho_L sums_B - sums_C (k < nv: the primal K block),
 // b_eq (nv <= k < nk: the boundary K block); per block a column exponent (max |R| < 2^eb) and S truncated
@@ -152,13 +158,14 @@ __global__ void __launch_bounds__(256) ozaki_split_b_kernel(tro_ma_dims d, tro_m
         int e = 0;
         if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
         if (lane == 0) bexp[blk * N + col] = e;
+        const double sc = pow2(-e);
 #pragma unroll
         for (int u = 0; u < kMaxG; ++u) {
             const int g = lane + 32 * u;
             if (4 * g >= kpb) break;
             double x[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[q] = ldexp(v[u][q], -e);  // |x| < 1, exact
+            for (int q = 0; q < 4; ++q) x[q] = v[u][q] * sc;  // |x| < 1, exact
             const int k0 = 4 * g, kst = k0 / BK;
             const int off = canon_off(n, k0 - kst * BK);
 #pragma unroll
@@ -179,8 +186,21 @@ __global__ void __launch_bounds__(256) ozaki_split_b_kernel(tro_ma_dims d, tro_m
 }
 
 // ---------------------------------------------------------------- the int8 GEMM + fp64 epilogue
+// rho levels present among the active problems of columns [c0, c0 + BN): one GEMM pass each
+__device__ __forceinline__ uint32_t tile_levels(const OzArgs& a, int c0) {
+    uint32_t mask = 0;
+    const int p0 = c0 / 3, p1 = min((c0 + BN - 1) / 3, a.n_problems - 1);
+    for (int p = p0; p <= p1; ++p)
+        if (!(a.status[p] & TRO_CONVERGED)) mask |= 1u << a.level[p];
+    return mask;
+}
+
+// Persistent: one CTA per SM walks the tiles t = blockIdx.x, += gridDim.x (m-tile fastest, so the CTAs in
+// flight share the level's A slices in L2).  The producer runs ahead across tiles (the stage ring never
+// drains), the MMA warp starts a tile's MMAs as soon as the epilogue has emptied TMEM, and the epilogue of
+// one tile overlaps the TMA loads of the next.
 template <int S>
-__global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(384, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                             const __grid_constant__ CUtensorMap tmB, OzArgs a) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     constexpr int kStageBytes = S * (kABytes + kBBytes);
@@ -190,13 +210,11 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 1;
     uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 1);
-    uint32_t* lvmask = tbase + 1;
-    int32_t* sColLv = reinterpret_cast<int32_t*>(lvmask + 1);  // [BN] the column's level, -1: skip
-    int32_t* sColE = sColLv + BN;                               // [2][BN] column exponents per K block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nt = blockIdx.x, mt = blockIdx.y;
-    const int c0 = nt * BN;
+    const int n_tiles = a.nt * a.mt;
+    const int ks = a.ks0 + a.ks1;
+    static_assert(BN == 32, "the epilogue maps one column per lane");
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -204,22 +222,8 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
             mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
-        mbar_init(tempty, 128);
+        mbar_init(tempty, 256);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        // rho levels present among this tile's active problems (one GEMM pass each)
-        uint32_t mask = 0;
-        const int p0 = c0 / 3, p1 = min((c0 + BN - 1) / 3, a.n_problems - 1);
-        for (int p = p0; p <= p1; ++p)
-            if (!(a.status[p] & TRO_CONVERGED)) mask |= 1u << a.level[p];
-        *lvmask = mask;
-    }
-    if (threadIdx.x < BN) {
-        const int col = c0 + threadIdx.x, p = col / 3;
-        int lv = -1;
-        if (p < a.n_problems && !(a.status[p] & TRO_CONVERGED)) lv = a.level[p];
-        sColLv[threadIdx.x] = lv;
-        sColE[threadIdx.x] = a.b_exp[col];
-        sColE[BN + threadIdx.x] = a.b_exp[a.nt * BN + col];
     }
     if (warp == 1) {  // TMEM: 2 K blocks x S accumulators x 32 columns (512 allocated)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tbase)));
@@ -229,30 +233,30 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tbase;
-    const uint32_t mask = *lvmask;
 
     if (warp == 0) {
         // ======================= TMA producer
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (uint32_t lm = mask; lm; lm &= lm - 1) {
-                const int L = __ffs(lm) - 1;
-                for (int kst = 0; kst < a.ks0 + a.ks1; ++kst) {
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    unsigned char* st = stages + s * kStageBytes;
-                    mbar_expect_tx(&full[s], kStageBytes);
-                    for (int i = 0; i < S; ++i) {
-                        const int blk = (((L * S + i) * a.mt + mt) * (a.ks0 + a.ks1) + kst);
-                        tma_2d(st + i * kABytes, &tmA, 0, blk * (kABytes / 256), &full[s]);
-                    }
-                    for (int j = 0; j < S; ++j) {
-                        const int blk = ((j * a.nt + nt) * (a.ks0 + a.ks1) + kst);
-                        tma_2d(st + S * kABytes + j * kBBytes, &tmB, 0, blk * (kBBytes / 256), &full[s]);
-                    }
-                    if (++s == kStages) {
-                        s = 0;
-                        ph ^= 1u;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const int mt = tile % a.mt, nt = tile / a.mt;
+                for (uint32_t lm = tile_levels(a, nt * BN); lm; lm &= lm - 1) {
+                    const int L = __ffs(lm) - 1;
+                    for (int kst = 0; kst < ks; ++kst) {
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        unsigned char* st = stages + s * kStageBytes;
+                        mbar_expect_tx(&full[s], kStageBytes);
+                        for (int i = 0; i < S; ++i)
+                            tma_2d(st + i * kABytes, &tmA, 0, (((L * S + i) * a.mt + mt) * ks + kst) * (kABytes / 256),
+                                   &full[s]);
+                        for (int j = 0; j < S; ++j)
+                            tma_2d(st + S * kABytes + j * kBBytes, &tmB, 0, ((j * a.nt + nt) * ks + kst) * (kBBytes / 256),
+                                   &full[s]);
+                        if (++s == kStages) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
                     }
                 }
             }
@@ -262,72 +266,89 @@ __global__ void __launch_bounds__(256, 1) ozaki_gemm_kernel(const __grid_constan
         int s = 0;
         uint32_t ph = 0;
         int pass = 0;
-        for (uint32_t lm = mask; lm; lm &= lm - 1, ++pass) {
-            if (pass > 0) mbar_wait(tempty, (uint32_t)((pass - 1) & 1));  // the epilogue drained TMEM
-            tc_fence_after();
-            for (int kst = 0; kst < a.ks0 + a.ks1; ++kst) {
-                mbar_wait(&full[s], ph);
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            const int nt = tile / a.mt;
+            for (uint32_t lm = tile_levels(a, nt * BN); lm; lm &= lm - 1, ++pass) {
+                if (pass > 0) mbar_wait(tempty, (uint32_t)((pass - 1) & 1));  // the epilogue drained TMEM
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t sa = smem_u32(stages + s * kStageBytes);
-                    const uint32_t sb = sa + S * kABytes;
-                    const int blk = kst < a.ks0 ? 0 : 1;
-                    const bool first = kst == 0 || kst == a.ks0;  // first k-step of this K block
-                    const uint32_t tb = tmem + blk * S * BN;
+                for (int kst = 0; kst < ks; ++kst) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t sa = smem_u32(stages + s * kStageBytes);
+                        const uint32_t sb = sa + S * kABytes;
+                        const int blk = kst < a.ks0 ? 0 : 1;
+                        const bool first = kst == 0 || kst == a.ks0;  // first k-step of this K block
+                        const uint32_t tb = tmem + blk * S * BN;
 #pragma unroll
-                    for (int dd = 0; dd < S; ++dd)
+                        for (int dd = 0; dd < S; ++dd)
 #pragma unroll
-                        for (int i = 0; i <= dd; ++i)
-                            umma_i8(tb + dd * BN, sdesc(sa + i * kABytes), sdesc(sb + (dd - i) * kBBytes),
-                                    (!first || i > 0) ? 1u : 0u);
-                    umma_commit(&empty[s]);  // frees the stage when these MMAs have read it
+                            for (int i = 0; i <= dd; ++i)
+                                umma_i8(tb + dd * BN, sdesc(sa + i * kABytes), sdesc(sb + (dd - i) * kBBytes),
+                                        (!first || i > 0) ? 1u : 0u);
+                        umma_commit(&empty[s]);  // frees the stage when these MMAs have read it
+                    }
+                    __syncwarp();
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
                 }
+                if (lane == 0) umma_commit(tfull);  // accumulators complete
                 __syncwarp();
-                if (++s == kStages) {
-                    s = 0;
-                    ph ^= 1u;
-                }
             }
-            if (lane == 0) umma_commit(tfull);  // accumulators complete
-            __syncwarp();
         }
     } else if (warp >= 4) {
-        // ======================= epilogue: TMEM -> fp64 -> xi
-        const int q = warp & 3;                 // TMEM lane quarter of this warp
-        const int row = mt * BM + 32 * q + lane;  // output row of K^-1
+        // ======================= epilogue: TMEM -> fp64 -> xi (8 warps: two per TMEM lane quarter, each
+        // draining half of the tile's columns, so the single TMEM buffer is back to the MMA warp sooner)
+        const int q = warp & 3;            // TMEM lane quarter of this warp
+        const int half = (warp - 4) >> 2;  // which 16 columns
         const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
         int pass = 0;
-        for (uint32_t lm = mask; lm; lm &= lm - 1, ++pass) {
-            const int L = __ffs(lm) - 1;
-            mbar_wait(tfull, (uint32_t)(pass & 1));
-            tc_fence_after();
-            const int ea0 = a.a_exp[(L * 2 + 0) * a.mt * BM + row];
-            const int ea1 = a.a_exp[(L * 2 + 1) * a.mt * BM + row];
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            const int mt = tile % a.mt, nt = tile / a.mt, c0 = nt * BN;
+            const int row = mt * BM + 32 * q + lane;  // output row of K^-1
+            // lane l holds column c0 + l's level and power-of-two scales (read while the MMAs run)
+            const int my_col = c0 + lane;
+            const int my_p = my_col / 3;
+            int my_lv = -1;
+            if (my_p < a.n_problems && !(a.status[my_p] & TRO_CONVERGED)) my_lv = a.level[my_p];
+            const double my_s0 = pow2(a.b_exp[my_col] - 14), my_s1 = pow2(a.b_exp[a.nt * BN + my_col] - 14);
+            for (uint32_t lm = tile_levels(a, c0); lm; lm &= lm - 1, ++pass) {
+                const int L = __ffs(lm) - 1;
+                const double sa0 = row < a.nv ? pow2(a.a_exp[(L * 2 + 0) * a.mt * BM + row]) : 0.0;
+                const double sa1 = row < a.nv ? pow2(a.a_exp[(L * 2 + 1) * a.mt * BM + row]) : 0.0;
+                mbar_wait(tfull, (uint32_t)(pass & 1));
+                tc_fence_after();
 #pragma unroll 1
-            for (int cc = 0; cc < BN; cc += 8) {
-                int32_t P[2][S][8];
+                for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 8) {
+                    int32_t P[2][S][8];
 #pragma unroll
-                for (int bl = 0; bl < 2; ++bl)
+                    for (int bl = 0; bl < 2; ++bl)
 #pragma unroll
-                    for (int dd = 0; dd < S; ++dd) tmem_ld8(tq + (bl * S + dd) * BN + cc, P[bl][dd]);
-                tmem_wait_ld();
+                        for (int dd = 0; dd < S; ++dd) tmem_ld8(tq + (bl * S + dd) * BN + cc, P[bl][dd]);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int cl = cc + jj, col = c0 + cl;
-                    if (row >= a.nv || sColLv[cl] != L) continue;
-                    const int p = col / 3, ax = col - 3 * p;
-                    double v0 = (double)P[0][S - 1][jj], v1 = (double)P[1][S - 1][jj];  // Horner over 128^-d
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const int cl = cc + jj, col = c0 + cl;
+                        const int lv = __shfl_sync(0xffffffffu, my_lv, cl);
+                        const double s0 = __shfl_sync(0xffffffffu, my_s0, cl);
+                        const double s1 = __shfl_sync(0xffffffffu, my_s1, cl);
+                        if (row >= a.nv || lv != L) continue;
+                        const int p = col / 3, ax = col - 3 * p;
+                        double v0 = (double)P[0][S - 1][jj], v1 = (double)P[1][S - 1][jj];  // Horner over 128^-d
 #pragma unroll
-                    for (int dd = S - 2; dd >= 0; --dd) {
-                        v0 = fma(v0, 0.0078125, (double)P[0][dd][jj]);
-                        v1 = fma(v1, 0.0078125, (double)P[1][dd][jj]);
+                        for (int dd = S - 2; dd >= 0; --dd) {
+                            v0 = fma(v0, 0.0078125, (double)P[0][dd][jj]);
+                            v1 = fma(v1, 0.0078125, (double)P[1][dd][jj]);
+                        }
+                        // exact power-of-two scalings (no under/overflow at these magnitudes), one rounding each
+                        a.xi[(int64_t)p * 3 * a.nv + ax * a.nv + row] = (v0 * s0) * sa0 + (v1 * s1) * sa1;
                     }
-                    a.xi[(int64_t)p * 3 * a.nv + ax * a.nv + row] =
-                        ldexp(v0, ea0 + sColE[cl] - 14) + ldexp(v1, ea1 + sColE[BN + cl] - 14);
                 }
+                tc_fence_before();
+                mbar_arrive(tempty);
             }
-            tc_fence_before();
-            mbar_arrive(tempty);
         }
     }
     tc_fence_before();
@@ -409,7 +430,10 @@ static int run(const tro_ma_dims* d, const tro_ma_consts* c, const tro_ma_state*
         cudaFuncSetAttribute(ozaki_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr[dev] = true;
     }
-    ozaki_gemm_kernel<S><<<dim3(nt, mt), 256, smem, st>>>(mA, mB, a);
+    static int n_sm = 0;
+    if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = nt * mt;
+    ozaki_gemm_kernel<S><<<tiles < n_sm ? tiles : n_sm, 384, smem, st>>>(mA, mB, a);
     return (int)cudaGetLastError();
 }
 

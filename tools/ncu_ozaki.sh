@@ -10,7 +10,7 @@ import csv
 rows = list(csv.reader(open("gpurun_out/ncu_ozaki_raw.csv")))
 h, v = rows[0], rows[2]
 for k, x in zip(h, v):
-    if any(t in k for t in ("pipe_tensor", "pipe_tc", "tmem", "uma", "gpu__time_duration.sum", "dram__bytes")):
+    if any(t in k for t in ("pipe_tensor", "pipe_tc", "tmem", "uma", "gpu__time_duration.sum", "dram__bytes", "lts__t_bytes.sum", "issue_stalled", "sm__cycles_active.avg", "smsp__cycles_active.avg")):
         print(f"{k:80s} {x}")
 PY
 rm -f gpurun_out/ncu_ozaki.ncu-rep
