@@ -26,9 +26,19 @@ namespace tro {
 #ifndef MA_MINB
 #define MA_MINB 2  // resident CTAs per SM the element kernel is compiled for (128 registers)
 #endif
-constexpr int kMaWarps = 8;
+constexpr int kMaWarps = 10;  // 100 samples = 10 rounds of 10 (C3); 2 CTAs x 10 warps per SM
 constexpr int kMaMaxAgents = 32;
 constexpr int kMaMaxRing = 64;
+
+// one bulk L2 prefetch of [p, p + bytes) (16-B aligned, bytes a multiple of 16): the lambda rows of the
+// rounds ahead, so the per-lane one-element-ahead loads hit L2 instead of waiting on HBM
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+#ifndef MA_AHEAD
+#define MA_AHEAD 2
+#endif
+constexpr int kMaAhead = MA_AHEAD;  // rounds of lambda rows prefetched into L2 ahead of the element pass
 
 struct MaArgs {
     tro_ma_dims d;
@@ -38,26 +48,26 @@ struct MaArgs {
 };
 
 struct MaSmem {
-    int P, pos, scratch, red, sumin, rhs, xi, warp, pair, ints, total;  // doubles
+    int P, xi, pos, scratch, sumin, rhs, V, warp, pair, ints, total;  // doubles
 };
 constexpr int kPairW = 9;  // per pair: a, b, 1/a, 1/b, a^2, b^2, static centre (3)
+// scatter scratch, one record per pair: recon + static (x y z), lambda (x y z), one pad double.  The odd
+// 56-byte stride keeps the element pass's per-lane record writes conflict-free, and the scatter reads a
+// record's three components at immediate offsets from one address.
+constexpr int kScrW = 7;
 __host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs, int n_eq, int n_inc) {
     MaSmem L;
     int off = 0;
-    L.P = off;       off += n_p * m;
-    L.pos = off;     off += n_p * n_a * 3;               // positions [t][agent][axis]
-    L.scratch = off; off += kMaWarps * n_pairs * 6;      // per warp: (recon+static, lambda) per pair
-    // the prologue's buffers (sums in, RHS, xi) are dead before the element pass: they alias the scratch
-    const int pro = 2 * n_a * 3 * m + 3 * (n_a * m + n_eq) + 3 * n_a * m;
-    if (pro > kMaWarps * n_pairs * 6) off += pro - kMaWarps * n_pairs * 6;
+    L.P = off;       off += n_p * ((m + 1) & ~1);        // basis rows padded to an even stride (16-B rows)
+    L.xi = off;      off += 3 * n_a * m;                 // this launch's coefficients [axis][agent][c]
+    L.pos = off;     off += kMaWarps * n_a * 3;          // per warp: its sample's positions [agent][axis]
+    L.scratch = off; off += kMaWarps * n_pairs * kScrW;  // per warp: (recon+static, lambda) per pair
+    // the fused prologue's buffers (sums in, RHS) are dead before the element pass: they alias the scratch
+    const int pro = 2 * n_a * 3 * m + 3 * (n_a * m + n_eq);
+    if (pro > kMaWarps * n_pairs * kScrW) off += pro - kMaWarps * n_pairs * kScrW;
     L.sumin = L.scratch;
     L.rhs = L.sumin + 2 * n_a * 3 * m;
-    L.xi = L.rhs + 3 * (n_a * m + n_eq);
-    // cross-warp reduction of the contracted sums reuses pos + scratch
-    const int red_need = kMaWarps * 2 * n_a * 3 * m;
-    const int have = off - L.pos;
-    L.red = L.pos;
-    if (red_need > have) off += red_need - have;
+    L.V = off;       off += 2 * kMaWarps * 2 * n_a * 3;  // per round, per warp: the scattered agent sums (x2 buffers)
     L.warp = off;    off += 2 * kMaWarps;
     L.pair = off;    off += kPairW * n_pairs;            // SoA [field][pair]
     L.ints = off;    off += (2 * n_pairs + n_a + 1 + n_inc + 1) / 2 + 1;  // pair_i, pair_j, inc_ptr, inc_pair
@@ -88,19 +98,29 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     int* sPairJ = sPairI + np_;
     int* sIncPtr = sPairJ + np_;
     int* sInc = sIncPtr + n_a + 1;
-    double* sPos = smem + L.pos;
-    double* sScr = smem + L.scratch + warp * np_ * 6;
-    double* sRed = smem + L.red;
+    double* sPos = smem + L.pos + warp * n_a * 3;
+    double* sScr = smem + L.scratch + warp * np_ * kScrW;
+    double* sV = smem + L.V;
     double* sSumIn = smem + L.sumin;
     double* sRhs = smem + L.rhs;
     double* sXi = smem + L.xi;
     double* sWarp = smem + L.warp;
 
+    bool uni;  // every pair shares (a, b) and has an agent partner
     const int status0 = A.s.status[i];
     if (mode == 0 && (status0 & TRO_CONVERGED)) return;
+    if (mode == 0 && lane == 0 && ((3 * np_ * 8) & 15) == 0)  // this warp's first kMaAhead rounds of lambda rows
+        for (int r = 0; r < kMaAhead; ++r) {
+            const int t = r * kMaWarps + warp;
+            if (t < n_p) prefetch_l2(A.s.state + ((int64_t)i * n_p + t) * 3 * np_, 3 * np_ * 8);
+        }
     const int level = A.s.level[i];
     const double rho = A.c.level_rho[level];
-    for (int k = tid; k < n_p * m; k += blockDim.x) sP[k] = ld_const(A.c.P + k);
+    const int mp = (m + 1) & ~1;
+    for (int k = tid; k < n_p * mp; k += blockDim.x) {
+        const int t = k / mp, c = k - t * mp;
+        sP[k] = c < m ? ld_const(A.c.P + t * m + c) : 0.0;
+    }
     {
         // per-pair constants (no divisions in the element pass) and the incidence lists
         const double* statics_i = A.c.statics ? A.c.statics + (int64_t)i * A.d.n_static * 3 : nullptr;
@@ -119,7 +139,16 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
             sPairJ[p] = pj;
         }
         for (int k = tid; k <= n_a; k += blockDim.x) sIncPtr[k] = A.c.inc_ptr[k];
-        for (int k = tid; k < n_inc; k += blockDim.x) sInc[k] = A.c.inc_pair[k];
+        // one (a, b) for every pair and no statics (identical agents): the constants live in registers
+        bool same = true;
+        for (int p = tid; p < np_; p += blockDim.x)
+            same = same && A.c.pair_j[p] >= 0 && A.c.pair_a[p] == A.c.pair_a[0] && A.c.pair_b[p] == A.c.pair_b[0];
+        uni = __syncthreads_and(same) != 0;
+        // incidence entries as scratch byte offsets of the pair's record, bit 0 = negative sign
+        for (int k = tid; k < n_inc; k += blockDim.x) {
+            const int pe = A.c.inc_pair[k];
+            sInc[k] = pe >= 0 ? pe * (kScrW * 8) : (-pe - 1) * (kScrW * 8) + 1;
+        }
     }
     double* xg = A.s.xi + (int64_t)i * 3 * nv;
     const double* bg = A.c.b_eq + (int64_t)i * 3 * neq;
@@ -203,169 +232,217 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
         }
         __syncthreads();
     }
-    for (int k = tid; k < n_p * n_a; k += blockDim.x) {  // one (t, agent) per thread: 3 axes share the P row
-        const int t = k / n_a, a = k - t * n_a;
-        double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-        for (int cc = 0; cc < m; ++cc) {
-            const double pv = sP[t * m + cc];
-            p0 = fma(pv, sXi[a * m + cc], p0);
-            p1 = fma(pv, sXi[nv + a * m + cc], p1);
-            p2 = fma(pv, sXi[2 * nv + a * m + cc], p2);
-        }
-        double* o = sPos + k * 3;
-        o[0] = p0;
-        o[1] = p1;
-        o[2] = p2;
-    }
-    __syncthreads();
-
-    // ---------------- element pass: warps over t, lanes over pairs
-    constexpr int MA = M ? M : 1;
-    double acc[3 * MA];  // per-lane contracted sums of one (agent, B|C) task  (M > 0)
+    {
+        // coefficients to [c][agent][axis]: the per-round position products read consecutive words
+        constexpr int kPer = (3 * 16 * 11 + kMaWarps * 32 - 1) / (kMaWarps * 32);  // n_a <= 16, m <= 11
+        double tv[kPer];
 #pragma unroll
-    for (int c = 0; c < 3 * MA; ++c) acc[c] = 0.0;
+        for (int j = 0; j < kPer; ++j) {
+            const int k = tid + j * kMaWarps * 32;
+            tv[j] = k < 3 * nv ? sXi[k] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int k = tid + j * kMaWarps * 32;
+            if (k < 3 * nv) {
+                const int ax = k / nv, r = k - ax * nv, a = r / m, cc = r - a * m;
+                sXi[cc * 3 * n_a + a * 3 + ax] = tv[j];
+            }
+        }
+        __syncthreads();
+    }
+    // ---------------- element pass in rounds of kMaWarps samples: warp w takes t = r kMaWarps + w, lanes
+    // over pairs; the warp then scatters its pairs' recon / lambda to the agents (fixed incidence order)
+    // into V[round parity][w], and after one barrier the CTA contracts the round's V rows with P[t][:]
+    // (thread = (agent-sum row, 4 basis columns), samples in ascending t): no per-lane accumulator bank.
     const int tasks = 2 * n_a;
+    const int rows = tasks * 3;  // [which][agent][axis]
+    const int ng = (m + 3) >> 2;
+    const int crow = tid / ng, cg = (tid - crow * ng) * 4;
+    const bool owner = crow < rows;
+    double cacc[4] = {0.0, 0.0, 0.0, 0.0};
     double sumsq = 0.0, mx = 0.0;
-    const int64_t rowW = 3 * (int64_t)np_;  // state[i][t][w][p], W = 3
+    const int rowW = 3 * np_;  // state[i][t][w][p], W = 3 (a problem's block stays far below 2^31 doubles)
     double* st = A.s.state + (int64_t)i * n_p * rowW;
-    const double* statics = A.c.statics ? A.c.statics + (int64_t)i * A.d.n_static * 3 : nullptr;
     const int64_t nplane = (int64_t)A.d.n_problems * n_p * np_;
 
     const double ir = 1.0 / rho;
     // lambda of this lane's next element, loaded one element ahead (two HBM loads in flight per lane)
     double nlx = 0.0, nly = 0.0, nlz = 0.0;
     if (mode == 0 && warp < n_p && lane < np_) {
-        const double* r0 = st + warp * rowW;
-        nlx = ld_stream(r0 + lane);
-        nly = ld_stream(r0 + np_ + lane);
-        nlz = ld_stream(r0 + 2 * np_ + lane);
+        const double* r0 = st + warp * rowW + lane;
+        nlx = ld_stream(r0);
+        nly = ld_stream(r0 + np_);
+        nlz = ld_stream(r0 + 2 * np_);
     }
-    for (int t = warp; t < n_p; t += kMaWarps) {
-        const double* pt = sPos + t * n_a * 3;
-        double* srow = st + t * rowW;
-        for (int p = lane; p < np_; p += 32) {
-            double clx = 0.0, cly = 0.0, clz = 0.0;
-            if (mode == 0) {
-                clx = nlx, cly = nly, clz = nlz;
-                int p2 = p + 32, t2 = t;
-                if (p2 >= np_) p2 = lane, t2 = t + kMaWarps;
-                if (t2 < n_p) {
-                    const double* r2 = st + t2 * rowW;
-                    nlx = ld_stream(r2 + p2);
-                    nly = ld_stream(r2 + np_ + p2);
-                    nlz = ld_stream(r2 + 2 * np_ + p2);
+    const double u_pa = sPair[0], u_pb = sPair[np_], u_ipa = sPair[2 * np_], u_ipb = sPair[3 * np_];
+    const double u_pa2 = sPair[4 * np_], u_pb2 = sPair[5 * np_];
+    const int n_rounds = (n_p + kMaWarps - 1) / kMaWarps;
+    const bool pf = mode == 0 && lane == 0 && ((rowW * 8) & 15) == 0;
+    for (int rd = 0; rd < n_rounds; ++rd) {
+        const int t = rd * kMaWarps + warp;
+        if (pf && t + kMaAhead * kMaWarps < n_p) prefetch_l2(st + (t + kMaAhead * kMaWarps) * rowW, rowW * 8);
+        double* sVr = sV + (rd & 1) * kMaWarps * rows;
+        if (t < n_p) {
+            // this sample's positions (one (agent, axis) per lane slot; same FMA order as the basis product)
+            {
+                // slots k0 = lane, k1 = lane + 32 (3 n_a <= 48); lanes past the last slot compute a discarded
+                // value from in-bounds shared memory, so the loop is branch-free
+                const int xs = 3 * n_a;
+                const double* xp = sXi + lane;
+                const double* prow = sP + t * mp;
+                double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+                for (int cc = 0; cc < m; ++cc) {
+                    const double pv = prow[cc];
+                    p0 = fma(pv, xp[0], p0);
+                    p1 = fma(pv, xp[32], p1);
+                    xp += xs;
                 }
+                if (lane < xs) sPos[lane] = p0;
+                if (lane + 32 < xs) sPos[lane + 32] = p1;
             }
-            const int pi = sPairI[p], pj = sPairJ[p];
-            const double pa = sPair[p], pb = sPair[np_ + p];
-            double cen[3];
-            if (pj >= 0) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) cen[k] = pt[pj * 3 + k];
-            } else {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) cen[k] = sPair[(6 + k) * np_ + p];
-            }
-            const double dx = pt[pi * 3 + 0] - cen[0], dy = pt[pi * 3 + 1] - cen[1], dz = pt[pi * 3 + 2] - cen[2];
-            // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) as unit vectors (:280-282)
-            double ca, sa, cb, sb;
-            const int64_t ex_i = ((int64_t)i * n_p + t) * np_ + p;
-            if (prime) {  // the given state's angles
-                sincos(A.s.export_ab[ex_i], &sa, &ca);
-                sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
-            } else {
-                const double h2 = fma(dx, dx, dy * dy);
-                double planar;
-                if (h2 > 0.0) {
-                    const double r = rsqrt_fast(h2);
-                    ca = dx * r;
-                    sa = dy * r;
-                    planar = h2 * r * sPair[2 * np_ + p];  // hypot(dx, dy) / pa
-                } else {
-                    ca = flip_sign(1.0, sign_bit(dx));
-                    sa = flip_sign(0.0, sign_bit(dy));
-                    planar = 0.0;
-                }
-                unit2(dz * sPair[3 * np_ + p], planar, &cb, &sb);
-            }
-            double lx, ly, lz, d;
-            if (prime) {
-                lx = srow[p];
-                ly = srow[np_ + p];
-                lz = srow[2 * np_ + p];
-                d = A.s.export_d[ex_i];
-            } else if (init) {
-                lx = ly = lz = 0.0;
-                d = 1.0;
-            } else {
-                lx = clx;
-                ly = cly;
-                lz = clz;
-                // multiplier-shifted single-variable quadratic in d, clamped at [1, 1e6] (:285-293)
-                const double num = pa * sb * (ca * fma(lx, ir, dx) + sa * fma(ly, ir, dy)) + pb * cb * fma(lz, ir, dz);
-                const double den = sPair[4 * np_ + p] * (sb * sb) + sPair[5 * np_ + p] * (cb * cb);
-                const double q = num * rcp_fast(den);
-                d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
-            }
-            const double rx = pa * d * sb * ca, ry = pa * d * sb * sa, rz = pb * d * cb;
-            if (prime) {
-            } else if (!init) {
-                const double ex = dx - rx, ey = dy - ry, ez = dz - rz;  // residual (:203-208)
-                sumsq = fma(ex, ex, fma(ey, ey, fma(ez, ez, sumsq)));
-                const double ae = fabs(ex) > fabs(ey) ? fabs(ex) : fabs(ey);
-                const double am = ae > fabs(ez) ? ae : fabs(ez);
-                mx = am > mx ? am : mx;
-                lx = fma(rho, ex, lx);  // lambda += rho * res (:296)
-                ly = fma(rho, ey, ly);
-                lz = fma(rho, ez, lz);
-                st_stream(srow + p, lx);
-                st_stream(srow + np_ + p, ly);
-                st_stream(srow + 2 * np_ + p, lz);
-            } else {
-                srow[p] = 0.0;
-                srow[np_ + p] = 0.0;
-                srow[2 * np_ + p] = 0.0;
-            }
-            if (!prime && A.s.export_d) {  // runtime: batch and single solves share one code path
-                const int64_t e = ex_i;
-                A.s.export_d[e] = d;
-                A.s.export_ab[e] = atan2(sa, ca);           // the reference's stored angles
-                A.s.export_ab[nplane + e] = atan2(sb, cb);
-            }
-            // next RHS: recon (+ static centre) and lambda, scattered to the pair's agents below
-            // planes [recon x y z | lambda x y z] x pairs: lanes write consecutive pairs (no bank conflicts)
-            double* sc = sScr + p;
-            sc[0] = rx + (pj < 0 ? cen[0] : 0.0);
-            sc[np_] = ry + (pj < 0 ? cen[1] : 0.0);
-            sc[2 * np_] = rz + (pj < 0 ? cen[2] : 0.0);
-            sc[3 * np_] = lx;
-            sc[4 * np_] = ly;
-            sc[5 * np_] = lz;
-        }
-        __syncwarp();
-        // per-agent signed incidence sums (fixed order), contracted with P[t][:]
-        for (int task = lane; task < tasks; task += 32) {
-            const int a = task % n_a, which = task / n_a;  // which 0: B (recon), 1: C (lambda)
-            double v[3] = {0.0, 0.0, 0.0};
-            for (int q = sIncPtr[a]; q < sIncPtr[a + 1]; ++q) {
-                const int pe = sInc[q];
-                const double sgn = pe >= 0 ? 1.0 : -1.0;
-                const double* sc = sScr + (pe >= 0 ? pe : -pe - 1) + 3 * which * np_;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) v[k] = fma(sgn, sc[k * np_], v[k]);
-            }
-            if constexpr (M > 0) {
-                if (task < 32) {  // M > 0 path keeps one task per lane (tasks <= 32)
-#pragma unroll
-                    for (int cc = 0; cc < M; ++cc) {
-                        const double pv = sP[t * M + cc];
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) acc[k * M + cc] = fma(pv, v[k], acc[k * M + cc]);
+            __syncwarp();
+            const double* pt = sPos;
+            double* srow = st + t * rowW;
+            for (int p = lane; p < np_; p += 32) {
+                double clx = 0.0, cly = 0.0, clz = 0.0;
+                if (mode == 0) {
+                    clx = nlx, cly = nly, clz = nlz;
+                    const int nxt = p + 32 < np_ ? t * rowW + p + 32 : (t + kMaWarps) * rowW + lane;
+                    if (nxt < n_p * rowW) {
+                        const double* r2 = st + nxt;
+                        nlx = ld_stream(r2);
+                        nly = ld_stream(r2 + np_);
+                        nlz = ld_stream(r2 + 2 * np_);
                     }
                 }
+                const int pi = sPairI[p], pj = sPairJ[p];
+                double pa, pb, ipa, ipb, pa2, pb2;
+                if (uni) {
+                    pa = u_pa, pb = u_pb, ipa = u_ipa, ipb = u_ipb, pa2 = u_pa2, pb2 = u_pb2;
+                } else {
+                    pa = sPair[p], pb = sPair[np_ + p], ipa = sPair[2 * np_ + p], ipb = sPair[3 * np_ + p];
+                    pa2 = sPair[4 * np_ + p], pb2 = sPair[5 * np_ + p];
+                }
+                double cen[3];
+                if (uni || pj >= 0) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) cen[k] = pt[pj * 3 + k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) cen[k] = sPair[(6 + k) * np_ + p];
+                }
+                const double dx = pt[pi * 3 + 0] - cen[0], dy = pt[pi * 3 + 1] - cen[1], dz = pt[pi * 3 + 2] - cen[2];
+                // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) as unit vectors (:280-282)
+                double ca, sa, cb, sb;
+                const int64_t ex_i = ((int64_t)i * n_p + t) * np_ + p;
+                if (prime) {  // the given state's angles
+                    sincos(A.s.export_ab[ex_i], &sa, &ca);
+                    sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
+                } else {
+                    const double h2 = fma(dx, dx, dy * dy);
+                    double planar;
+                    if (h2 > 0.0) {
+                        const double r = rsqrt_fast(h2);
+                        ca = dx * r;
+                        sa = dy * r;
+                        planar = h2 * r * ipa;  // hypot(dx, dy) / pa
+                    } else {
+                        ca = flip_sign(1.0, sign_bit(dx));
+                        sa = flip_sign(0.0, sign_bit(dy));
+                        planar = 0.0;
+                    }
+                    unit2(dz * ipb, planar, &cb, &sb);
+                }
+                double lx, ly, lz, d;
+                if (prime) {
+                    lx = srow[p];
+                    ly = srow[np_ + p];
+                    lz = srow[2 * np_ + p];
+                    d = A.s.export_d[ex_i];
+                } else if (init) {
+                    lx = ly = lz = 0.0;
+                    d = 1.0;
+                } else {
+                    lx = clx;
+                    ly = cly;
+                    lz = clz;
+                    // multiplier-shifted single-variable quadratic in d, clamped at [1, 1e6] (:285-293)
+                    const double num = pa * sb * (ca * fma(lx, ir, dx) + sa * fma(ly, ir, dy)) + pb * cb * fma(lz, ir, dz);
+                    const double den = pa2 * (sb * sb) + pb2 * (cb * cb);
+                    const double q = num * rcp_fast(den);
+                    d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
+                }
+                const double rx = pa * d * sb * ca, ry = pa * d * sb * sa, rz = pb * d * cb;
+                if (prime) {
+                } else if (!init) {
+                    const double ex = dx - rx, ey = dy - ry, ez = dz - rz;  // residual (:203-208)
+                    sumsq = fma(ex, ex, fma(ey, ey, fma(ez, ez, sumsq)));
+                    const double ae = fabs(ex) > fabs(ey) ? fabs(ex) : fabs(ey);
+                    const double am = ae > fabs(ez) ? ae : fabs(ez);
+                    mx = am > mx ? am : mx;
+                    lx = fma(rho, ex, lx);  // lambda += rho * res (:296)
+                    ly = fma(rho, ey, ly);
+                    lz = fma(rho, ez, lz);
+                    st_stream(srow + p, lx);
+                    st_stream(srow + np_ + p, ly);
+                    st_stream(srow + 2 * np_ + p, lz);
+                } else {
+                    srow[p] = 0.0;
+                    srow[np_ + p] = 0.0;
+                    srow[2 * np_ + p] = 0.0;
+                }
+                if (!prime && A.s.export_d) {  // runtime: batch and single solves share one code path
+                    const int64_t e = ex_i;
+                    A.s.export_d[e] = d;
+                    A.s.export_ab[e] = atan2(sa, ca);           // the reference's stored angles
+                    A.s.export_ab[nplane + e] = atan2(sb, cb);
+                }
+                // next RHS: recon (+ static centre) and lambda, scattered to the pair's agents below
+                double* sc = sScr + p * kScrW;
+                sc[0] = rx + (pj < 0 ? cen[0] : 0.0);
+                sc[1] = ry + (pj < 0 ? cen[1] : 0.0);
+                sc[2] = rz + (pj < 0 ? cen[2] : 0.0);
+                sc[3] = lx;
+                sc[4] = ly;
+                sc[5] = lz;
+            }
+            __syncwarp();
+            // per-agent signed incidence sums (fixed order) -> V[w][which][agent][axis]
+            for (int task = lane; task < tasks; task += 32) {
+                const int a = task % n_a, which = task / n_a;  // which 0: B (recon), 1: C (lambda)
+                double v[3] = {0.0, 0.0, 0.0};
+                const char* base = reinterpret_cast<const char*>(sScr + 3 * which);
+                for (int q = sIncPtr[a]; q < sIncPtr[a + 1]; ++q) {
+                    const int w = sInc[q];
+                    const double sgn = (w & 1) ? -1.0 : 1.0;
+                    const double* sc = reinterpret_cast<const double*>(base + (w & ~7));
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) v[k] = fma(sgn, sc[k], v[k]);
+                }
+                double* vo = sVr + warp * rows + task * 3;
+                vo[0] = v[0];
+                vo[1] = v[1];
+                vo[2] = v[2];
             }
         }
-        __syncwarp();
+        __syncthreads();
+        // contraction of this round's samples, ascending t
+        if (owner) {
+            const int tn = min(kMaWarps, n_p - rd * kMaWarps);
+#pragma unroll 5
+            for (int w = 0; w < tn; ++w) {
+                const double vv = sVr[w * rows + crow];
+                const double2* pr = reinterpret_cast<const double2*>(sP + (rd * kMaWarps + w) * mp + cg);
+                const double2 q0 = pr[0], q1 = pr[1];  // columns past m: padding / next row, never written
+                cacc[0] = fma(q0.x, vv, cacc[0]);
+                cacc[1] = fma(q0.y, vv, cacc[1]);
+                cacc[2] = fma(q1.x, vv, cacc[2]);
+                cacc[3] = fma(q1.y, vv, cacc[3]);
+            }
+        }
     }
 
     // ---------------- reductions
@@ -375,24 +452,13 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
         sWarp[warp] = sumsq;
         sWarp[kMaWarps + warp] = mx;
     }
-    __syncthreads();  // positions / scratch are dead from here: reuse them as the reduction buffer
-    const int per_task = 3 * m;
-    if constexpr (M > 0) {
-        if (lane < tasks) {
-            double* r = sRed + (warp * tasks + lane) * per_task;
+    double* sg = A.s.sums + (int64_t)i * 2 * n_a * 3 * m;  // [which][a][k][c] = [row][c]
+    if (owner) {
 #pragma unroll
-            for (int c = 0; c < 3 * M; ++c) r[c] = acc[c];  // [k][c]
-        }
+        for (int c = 0; c < 4; ++c)
+            if (cg + c < m) sg[crow * m + cg + c] = cacc[c];
     }
     __syncthreads();
-    double* sg = A.s.sums + (int64_t)i * 2 * n_a * 3 * m;  // [which][a][k][c]
-    for (int o = tid; o < tasks * per_task; o += blockDim.x) {
-        const int task = o / per_task, r = o - task * per_task;
-        double v = 0.0;
-        for (int w = 0; w < kMaWarps; ++w) v += sRed[(w * tasks + task) * per_task + r];
-        const int a = task % n_a, which = task / n_a, k = r / m, cc = r - k * m;
-        sg[(int64_t)which * n_a * 3 * m + (a * 3 + k) * m + cc] = v;
-    }
     if (tid == 0 && mode == 0) {
         double ss = 0.0, mm = 0.0;
         for (int w = 0; w < kMaWarps; ++w) {

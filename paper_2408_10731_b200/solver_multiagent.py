@@ -117,6 +117,27 @@ def inflate_radius(radius: float, typical_residual: float, factor: float) -> flo
     return radius + factor * typical_residual
 
 
+def _colour_order(n_a: int, pi, pj, ps) -> np.ndarray:
+    """Reference pair indices in colour-major order: the agent pairs by the circle method (n_a - 1 perfect
+    matchings for even n_a, n_a near-perfect ones for odd), then one colour per static sphere."""
+    index = {(i, j): p for p, (i, j) in enumerate(zip(pi, pj)) if j >= 0}
+    order = []
+    n = n_a + (n_a & 1)  # a dummy agent for odd n_a
+    ring = list(range(n))
+    for _ in range(n - 1):
+        rnd = []
+        for k in range(n // 2):
+            a, b = ring[k], ring[n - 1 - k]
+            if a < n_a and b < n_a:
+                rnd.append(index[(min(a, b), max(a, b))])
+        order.extend(sorted(rnd, key=lambda p: pi[p]))
+        ring = [ring[0]] + [ring[-1]] + ring[1:-1]
+    statics = sorted((p for p in range(len(pi)) if pj[p] < 0), key=lambda p: (ps[p], pi[p]))
+    order.extend(statics)
+    assert sorted(order) == list(range(len(pi)))
+    return np.asarray(order, np.int64)
+
+
 class _Structure:
     """Pairs, A_fo, and the level factorizations (solver_multiagent.py:100-165)."""
 
@@ -157,13 +178,20 @@ class _Structure:
             self.rho_levels = [params.rho_start]
             self.factors = [qpcore.factorize(Q, self.A_eq)]
         self.n_factorizations = len(self.factors)
-        # CSR incidence: per agent, the pairs it is first (+) / second (-) member of, in pair order
+        # Device pair order: colour-major (a proper edge colouring, round-robin for the agent pairs, one colour
+        # per static sphere), so that at step q of the per-agent scatter every agent reads a pair of colour q,
+        # and the pairs of one colour sit in consecutive scratch records (conflict-free shared-memory reads).
+        # dev_perm[d] = the reference index of device pair d; the engine's pair planes use the device order.
+        self.dev_perm = _colour_order(n_a, pi, pj, ps)
+        dpi, dpj = self.pair_i[self.dev_perm], self.pair_j[self.dev_perm]
+        # CSR incidence over device pairs: per agent, the pairs it is first (+) / second (-) member of, in
+        # device (= colour) order
         inc_ptr, inc = [0], []
         for a in range(n_a):
             for p in range(self.n_pairs):
-                if pi[p] == a:
+                if dpi[p] == a:
                     inc.append(p)
-                elif pj[p] == a:
+                elif dpj[p] == a:
                     inc.append(-p - 1)
             inc_ptr.append(len(inc))
         self.inc_ptr, self.inc_pair = np.array(inc_ptr, np.int32), np.array(inc, np.int32)
@@ -204,11 +232,14 @@ class MaEngine:
         self.kinv = torch.as_tensor(np.stack([f.kinv for f in struct.factors]), **f64).contiguous()
         assert self.kinv.shape[1] == nk
         self.level_rho = torch.as_tensor(np.asarray(struct.rho_levels), **f64)
-        self.pair_i = torch.as_tensor(struct.pair_i.astype(np.int32), **i32)
-        self.pair_j = torch.as_tensor(struct.pair_j.astype(np.int32), **i32)
-        self.pair_s = torch.as_tensor(struct.pair_s.astype(np.int32), **i32)
-        self.pair_a = torch.as_tensor(struct.pa, **f64)
-        self.pair_b = torch.as_tensor(struct.pb, **f64)
+        perm = struct.dev_perm  # device pair d = reference pair perm[d]
+        self._perm = torch.as_tensor(perm, dtype=torch.long, device=self.device)
+        self._inv = torch.as_tensor(np.argsort(perm), dtype=torch.long, device=self.device)
+        self.pair_i = torch.as_tensor(struct.pair_i[perm].astype(np.int32), **i32)
+        self.pair_j = torch.as_tensor(struct.pair_j[perm].astype(np.int32), **i32)
+        self.pair_s = torch.as_tensor(struct.pair_s[perm].astype(np.int32), **i32)
+        self.pair_a = torch.as_tensor(struct.pa[perm], **f64)
+        self.pair_b = torch.as_tensor(struct.pb[perm], **f64)
         self.inc_ptr = torch.as_tensor(struct.inc_ptr, **i32)
         self.inc_pair = torch.as_tensor(struct.inc_pair, **i32)
         self.b_eq = torch.as_tensor(np.ascontiguousarray(b_eq), **f64)
@@ -279,15 +310,25 @@ class MaEngine:
                                      ctypes.c_void_p(_lib.stream_handle()))
         _lib.check(rc, "tro_ma_run")
 
+    def lam_ref(self, b: int = 0) -> np.ndarray:
+        """Problem b's multipliers in the reference layout (3, n_pairs, n_p) and pair order."""
+        return self.state[b].permute(1, 2, 0)[:, self._inv].cpu().numpy()
+
+    def export_ref(self, b: int = 0):
+        """Problem b's exported d, alpha, beta as (n_pairs, n_p) arrays in the reference pair order."""
+        return tuple(x.T[self._inv].cpu().numpy() for x in (self.export_d[b], self.export_ab[0, b],
+                                                              self.export_ab[1, b]))
+
     def load_state(self, xi, lam, d, alpha, beta, level, iteration):
         """Warm state per problem (host arrays, leading batch axis): xi (B, 3, n_a m), lam (B, 3, n_pairs,
         n_p), d / alpha / beta (B, n_pairs, n_p); then prime() computes the first RHS sums."""
         dev = self.device
         self.xi.copy_(torch.as_tensor(np.asarray(xi, float)).reshape(self.xi.shape))
-        self.state.copy_(torch.as_tensor(np.asarray(lam, float)).permute(0, 3, 1, 2))
-        self.export_d.copy_(torch.as_tensor(np.asarray(d, float)).permute(0, 2, 1))
-        self.export_ab[0].copy_(torch.as_tensor(np.asarray(alpha, float)).permute(0, 2, 1))
-        self.export_ab[1].copy_(torch.as_tensor(np.asarray(beta, float)).permute(0, 2, 1))
+        pc = self._perm.cpu()  # reference pair order -> device pair order
+        self.state.copy_(torch.as_tensor(np.asarray(lam, float))[:, :, pc].permute(0, 3, 1, 2))
+        self.export_d.copy_(torch.as_tensor(np.asarray(d, float))[:, pc].permute(0, 2, 1))
+        self.export_ab[0].copy_(torch.as_tensor(np.asarray(alpha, float))[:, pc].permute(0, 2, 1))
+        self.export_ab[1].copy_(torch.as_tensor(np.asarray(beta, float))[:, pc].permute(0, 2, 1))
         self.level.copy_(torch.as_tensor(np.asarray(level).reshape(self.B).astype(np.int32)))
         self.iteration.copy_(torch.as_tensor(np.asarray(iteration).reshape(self.B).astype(np.int32)))
         del dev
@@ -406,9 +447,9 @@ def solve_joint(problem: MultiAgentProblem, params: JointParams | None = None) -
     nh = int(eng.n_hist[0].item())
     hist = eng.hist[0, :nh].cpu().numpy()
     xi = eng.xi[0].cpu().numpy()
-    lam = eng.state[0].permute(1, 2, 0).cpu().numpy()  # (3, n_pairs, n_p)
-    state = JointState(xi=xi, d=eng.export_d[0].T.cpu().numpy(), alpha=eng.export_ab[0, 0].T.cpu().numpy(),
-                       beta=eng.export_ab[1, 0].T.cpu().numpy(), lam=lam, level=int(eng.level[0].item()),
+    lam = eng.lam_ref(0)  # (3, n_pairs, n_p)
+    d, alpha, beta = eng.export_ref(0)
+    state = JointState(xi=xi, d=d, alpha=alpha, beta=beta, lam=lam, level=int(eng.level[0].item()),
                        iteration=int(eng.iteration[0].item()))
     basis = problem.basis
     trajs, positions = [], []

@@ -60,10 +60,11 @@ def test_teacher_forced_step(golden, k):
     eng.iterate()
     torch.cuda.synchronize()
     assert rel(eng.xi[0].cpu().numpy(), g[f"r6_k{k + 1}_xi"]) < 1e-10
-    np.testing.assert_allclose(eng.export_d[0].T.cpu().numpy(), g[f"r6_k{k + 1}_d"], atol=1e-9)
-    np.testing.assert_allclose(eng.export_ab[0, 0].T.cpu().numpy(), g[f"r6_k{k + 1}_alpha"], atol=1e-9)
-    np.testing.assert_allclose(eng.export_ab[1, 0].T.cpu().numpy(), g[f"r6_k{k + 1}_beta"], atol=1e-9)
-    lam = eng.state[0].permute(1, 2, 0).cpu().numpy()
+    d, alpha, beta = eng.export_ref(0)  # the engine's colour-major pair order mapped back
+    np.testing.assert_allclose(d, g[f"r6_k{k + 1}_d"], atol=1e-9)
+    np.testing.assert_allclose(alpha, g[f"r6_k{k + 1}_alpha"], atol=1e-9)
+    np.testing.assert_allclose(beta, g[f"r6_k{k + 1}_beta"], atol=1e-9)
+    lam = eng.lam_ref(0)
     ref = g[f"r6_k{k + 1}_lam"]
     assert np.max(np.abs(lam - ref)) <= 1e-8 * max(1.0, np.abs(ref).max())
 
