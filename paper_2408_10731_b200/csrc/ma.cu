@@ -17,6 +17,8 @@
 //              schedule (:313-335).
 // Deterministic: every reduction has a fixed order, so a problem's bits do not depend on
 // the batch or the GPU count.
+#include <type_traits>
+
 #include "common.cuh"
 #include "fastmath.cuh"
 #include "../../include/trajopt_b200.h"
@@ -40,6 +42,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 #endif
 constexpr int kMaAhead = MA_AHEAD;  // rounds of lambda rows prefetched into L2 ahead of the element pass
 
+// D(8x8) += A(8x4, row) B(4x8, col) in fp64 on the tensor cores (lane l: A[l/4][l%4], B[l%4][l/4],
+// D[l/4][2 (l%4) + {0, 1}])
+__device__ __forceinline__ void dmma884(double* d, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
 struct MaArgs {
     tro_ma_dims d;
     tro_ma_consts c;
@@ -50,7 +60,7 @@ struct MaArgs {
 struct MaSmem {
     int P, xi, pos, scratch, sumin, rhs, V, warp, pair, ints, total;  // doubles
 };
-constexpr int kPairW = 9;  // per pair: a, b, 1/a, 1/b, a^2, b^2, static centre (3)
+constexpr int kPairW = 7;  // per pair: a, b, 1/a, 1/b, static centre (3)
 // scatter scratch, one record per pair: recon + static (x y z), lambda (x y z), one pad double.  The odd
 // 56-byte stride keeps the element pass's per-lane record writes conflict-free, and the scatter reads a
 // record's three components at immediate offsets from one address.
@@ -131,10 +141,8 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
             sPair[1 * np_ + p] = pb;
             sPair[2 * np_ + p] = 1.0 / pa;
             sPair[3 * np_ + p] = 1.0 / pb;
-            sPair[4 * np_ + p] = pa * pa;
-            sPair[5 * np_ + p] = pb * pb;
             for (int k = 0; k < 3; ++k)
-                sPair[(6 + k) * np_ + p] = pj < 0 ? statics_i[A.c.pair_s[p] * 3 + k] : 0.0;
+                sPair[(4 + k) * np_ + p] = pj < 0 ? statics_i[A.c.pair_s[p] * 3 + k] : 0.0;
             sPairI[p] = A.c.pair_i[p];
             sPairJ[p] = pj;
         }
@@ -254,17 +262,19 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     }
     // ---------------- element pass in rounds of kMaWarps samples: warp w takes t = r kMaWarps + w, lanes
     // over pairs; the warp then scatters its pairs' recon / lambda to the agents (fixed incidence order)
-    // into V[round parity][w], and after one barrier the CTA contracts the round's V rows with P[t][:]
-    // (thread = (agent-sum row, 4 basis columns), samples in ascending t): no per-lane accumulator bank.
+    // into V[round parity][w], and after one barrier the CTA contracts the round's V rows with P[t][:] as
+    // 8x8x4 fp64 tensor-core tiles (accumulated across rounds in the owning warp's registers).
     const int tasks = 2 * n_a;
     const int rows = tasks * 3;  // [which][agent][axis]
-    const int ng = (m + 3) >> 2;
-    const int crow = tid / ng, cg = (tid - crow * ng) * 4;
-    const bool owner = crow < rows;
-    double cacc[4] = {0.0, 0.0, 0.0, 0.0};
+    // contraction tiles: D[rows x m] = V^T[rows x t] P[t x m] as 8x8 DMMA tiles, warp w owning tiles
+    // w, w + kMaWarps, ... (rows <= 96, m <= 11: at most 12 x 2 tiles, <= 3 per warp)
+    constexpr int kMaxTiles = 3;
+    const int n_mt = (rows + 7) >> 3, n_nt = (m + 7) >> 3;
+    double cacc[kMaxTiles][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     double sumsq = 0.0, mx = 0.0;
     const int rowW = 3 * np_;  // state[i][t][w][p], W = 3 (a problem's block stays far below 2^31 doubles)
-    double* st = A.s.state + (int64_t)i * n_p * rowW;
+    double* st;  // pinned in a register: rematerialising the 64-bit product per element cost ~20 instructions
+    asm volatile("mov.b64 %0, %1;" : "=l"(st) : "l"(A.s.state + (int64_t)i * n_p * rowW));
     const int64_t nplane = (int64_t)A.d.n_problems * n_p * np_;
 
     const double ir = 1.0 / rho;
@@ -277,7 +287,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
         nlz = ld_stream(r0 + 2 * np_);
     }
     const double u_pa = sPair[0], u_pb = sPair[np_], u_ipa = sPair[2 * np_], u_ipb = sPair[3 * np_];
-    const double u_pa2 = sPair[4 * np_], u_pb2 = sPair[5 * np_];
+    const double u_pa2 = u_pa * u_pa, u_pb2 = u_pb * u_pb;
     const int n_rounds = (n_p + kMaWarps - 1) / kMaWarps;
     const bool pf = mode == 0 && lane == 0 && ((rowW * 8) & 15) == 0;
     for (int rd = 0; rd < n_rounds; ++rd) {
@@ -306,109 +316,117 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
             __syncwarp();
             const double* pt = sPos;
             double* srow = st + t * rowW;
-            for (int p = lane; p < np_; p += 32) {
-                double clx = 0.0, cly = 0.0, clz = 0.0;
-                if (mode == 0) {
-                    clx = nlx, cly = nly, clz = nlz;
-                    const int nxt = p + 32 < np_ ? t * rowW + p + 32 : (t + kMaWarps) * rowW + lane;
-                    if (nxt < n_p * rowW) {
-                        const double* r2 = st + nxt;
-                        nlx = ld_stream(r2);
-                        nly = ld_stream(r2 + np_);
-                        nlz = ld_stream(r2 + 2 * np_);
+            // the pair pass, specialised on whether the pair constants are uniform (registers, no loads)
+            auto pair_pass = [&](auto uni_tag) {
+                constexpr bool UNI = decltype(uni_tag)::value;
+                for (int p = lane; p < np_; p += 32) {
+                    double clx = 0.0, cly = 0.0, clz = 0.0;
+                    if (mode == 0) {
+                        clx = nlx, cly = nly, clz = nlz;
+                        const int nxt = p + 32 < np_ ? t * rowW + p + 32 : (t + kMaWarps) * rowW + lane;
+                        if (nxt < n_p * rowW) {
+                            const double* r2 = st + nxt;
+                            nlx = ld_stream(r2);
+                            nly = ld_stream(r2 + np_);
+                            nlz = ld_stream(r2 + 2 * np_);
+                        }
                     }
-                }
-                const int pi = sPairI[p], pj = sPairJ[p];
-                double pa, pb, ipa, ipb, pa2, pb2;
-                if (uni) {
-                    pa = u_pa, pb = u_pb, ipa = u_ipa, ipb = u_ipb, pa2 = u_pa2, pb2 = u_pb2;
-                } else {
-                    pa = sPair[p], pb = sPair[np_ + p], ipa = sPair[2 * np_ + p], ipb = sPair[3 * np_ + p];
-                    pa2 = sPair[4 * np_ + p], pb2 = sPair[5 * np_ + p];
-                }
-                double cen[3];
-                if (uni || pj >= 0) {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) cen[k] = pt[pj * 3 + k];
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) cen[k] = sPair[(6 + k) * np_ + p];
-                }
-                const double dx = pt[pi * 3 + 0] - cen[0], dy = pt[pi * 3 + 1] - cen[1], dz = pt[pi * 3 + 2] - cen[2];
-                // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) as unit vectors (:280-282)
-                double ca, sa, cb, sb;
-                const int64_t ex_i = ((int64_t)i * n_p + t) * np_ + p;
-                if (prime) {  // the given state's angles
-                    sincos(A.s.export_ab[ex_i], &sa, &ca);
-                    sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
-                } else {
-                    const double h2 = fma(dx, dx, dy * dy);
-                    double planar;
-                    if (h2 > 0.0) {
-                        const double r = rsqrt_fast(h2);
-                        ca = dx * r;
-                        sa = dy * r;
-                        planar = h2 * r * ipa;  // hypot(dx, dy) / pa
+                    const int pi = sPairI[p], pj = sPairJ[p];
+                    double pa, pb, ipa, ipb, pa2, pb2;
+                    if constexpr (UNI) {
+                        pa = u_pa, pb = u_pb, ipa = u_ipa, ipb = u_ipb, pa2 = u_pa2, pb2 = u_pb2;
                     } else {
-                        ca = flip_sign(1.0, sign_bit(dx));
-                        sa = flip_sign(0.0, sign_bit(dy));
-                        planar = 0.0;
+                        pa = sPair[p], pb = sPair[np_ + p], ipa = sPair[2 * np_ + p], ipb = sPair[3 * np_ + p];
+                        pa2 = pa * pa, pb2 = pb * pb;
                     }
-                    unit2(dz * ipb, planar, &cb, &sb);
+                    double cen[3];
+                    if (UNI || pj >= 0) {
+    #pragma unroll
+                        for (int k = 0; k < 3; ++k) cen[k] = pt[pj * 3 + k];
+                    } else {
+    #pragma unroll
+                        for (int k = 0; k < 3; ++k) cen[k] = sPair[(4 + k) * np_ + p];
+                    }
+                    const double dx = pt[pi * 3 + 0] - cen[0], dy = pt[pi * 3 + 1] - cen[1], dz = pt[pi * 3 + 2] - cen[2];
+                    // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) as unit vectors (:280-282)
+                    double ca, sa, cb, sb;
+                    const int64_t ex_i = ((int64_t)i * n_p + t) * np_ + p;
+                    if (prime) {  // the given state's angles
+                        sincos(A.s.export_ab[ex_i], &sa, &ca);
+                        sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
+                    } else {
+                        const double h2 = fma(dx, dx, dy * dy);
+                        double planar;
+                        if (h2 > 0.0) {
+                            const double r = rsqrt_fast(h2);
+                            ca = dx * r;
+                            sa = dy * r;
+                            planar = h2 * r * ipa;  // hypot(dx, dy) / pa
+                        } else {
+                            ca = flip_sign(1.0, sign_bit(dx));
+                            sa = flip_sign(0.0, sign_bit(dy));
+                            planar = 0.0;
+                        }
+                        unit2(dz * ipb, planar, &cb, &sb);
+                    }
+                    double lx, ly, lz, d;
+                    if (prime) {
+                        lx = srow[p];
+                        ly = srow[np_ + p];
+                        lz = srow[2 * np_ + p];
+                        d = A.s.export_d[ex_i];
+                    } else if (init) {
+                        lx = ly = lz = 0.0;
+                        d = 1.0;
+                    } else {
+                        lx = clx;
+                        ly = cly;
+                        lz = clz;
+                        // multiplier-shifted single-variable quadratic in d, clamped at [1, 1e6] (:285-293)
+                        const double num = pa * sb * (ca * fma(lx, ir, dx) + sa * fma(ly, ir, dy)) + pb * cb * fma(lz, ir, dz);
+                        const double den = pa2 * (sb * sb) + pb2 * (cb * cb);
+                        const double q = num * rcp_fast(den);
+                        d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
+                    }
+                    const double rx = pa * d * sb * ca, ry = pa * d * sb * sa, rz = pb * d * cb;
+                    if (prime) {
+                    } else if (!init) {
+                        const double ex = dx - rx, ey = dy - ry, ez = dz - rz;  // residual (:203-208)
+                        sumsq = fma(ex, ex, fma(ey, ey, fma(ez, ez, sumsq)));
+                        const double ae = fabs(ex) > fabs(ey) ? fabs(ex) : fabs(ey);
+                        const double am = ae > fabs(ez) ? ae : fabs(ez);
+                        mx = am > mx ? am : mx;
+                        lx = fma(rho, ex, lx);  // lambda += rho * res (:296)
+                        ly = fma(rho, ey, ly);
+                        lz = fma(rho, ez, lz);
+                        st_stream(srow + p, lx);
+                        st_stream(srow + np_ + p, ly);
+                        st_stream(srow + 2 * np_ + p, lz);
+                    } else {
+                        srow[p] = 0.0;
+                        srow[np_ + p] = 0.0;
+                        srow[2 * np_ + p] = 0.0;
+                    }
+                    if (!prime && A.s.export_d) {  // runtime: batch and single solves share one code path
+                        const int64_t e = ex_i;
+                        A.s.export_d[e] = d;
+                        A.s.export_ab[e] = atan2(sa, ca);           // the reference's stored angles
+                        A.s.export_ab[nplane + e] = atan2(sb, cb);
+                    }
+                    // next RHS: recon (+ static centre) and lambda, scattered to the pair's agents below
+                    double* sc = sScr + p * kScrW;
+                    sc[0] = rx + (pj < 0 ? cen[0] : 0.0);
+                    sc[1] = ry + (pj < 0 ? cen[1] : 0.0);
+                    sc[2] = rz + (pj < 0 ? cen[2] : 0.0);
+                    sc[3] = lx;
+                    sc[4] = ly;
+                    sc[5] = lz;
                 }
-                double lx, ly, lz, d;
-                if (prime) {
-                    lx = srow[p];
-                    ly = srow[np_ + p];
-                    lz = srow[2 * np_ + p];
-                    d = A.s.export_d[ex_i];
-                } else if (init) {
-                    lx = ly = lz = 0.0;
-                    d = 1.0;
-                } else {
-                    lx = clx;
-                    ly = cly;
-                    lz = clz;
-                    // multiplier-shifted single-variable quadratic in d, clamped at [1, 1e6] (:285-293)
-                    const double num = pa * sb * (ca * fma(lx, ir, dx) + sa * fma(ly, ir, dy)) + pb * cb * fma(lz, ir, dz);
-                    const double den = pa2 * (sb * sb) + pb2 * (cb * cb);
-                    const double q = num * rcp_fast(den);
-                    d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
-                }
-                const double rx = pa * d * sb * ca, ry = pa * d * sb * sa, rz = pb * d * cb;
-                if (prime) {
-                } else if (!init) {
-                    const double ex = dx - rx, ey = dy - ry, ez = dz - rz;  // residual (:203-208)
-                    sumsq = fma(ex, ex, fma(ey, ey, fma(ez, ez, sumsq)));
-                    const double ae = fabs(ex) > fabs(ey) ? fabs(ex) : fabs(ey);
-                    const double am = ae > fabs(ez) ? ae : fabs(ez);
-                    mx = am > mx ? am : mx;
-                    lx = fma(rho, ex, lx);  // lambda += rho * res (:296)
-                    ly = fma(rho, ey, ly);
-                    lz = fma(rho, ez, lz);
-                    st_stream(srow + p, lx);
-                    st_stream(srow + np_ + p, ly);
-                    st_stream(srow + 2 * np_ + p, lz);
-                } else {
-                    srow[p] = 0.0;
-                    srow[np_ + p] = 0.0;
-                    srow[2 * np_ + p] = 0.0;
-                }
-                if (!prime && A.s.export_d) {  // runtime: batch and single solves share one code path
-                    const int64_t e = ex_i;
-                    A.s.export_d[e] = d;
-                    A.s.export_ab[e] = atan2(sa, ca);           // the reference's stored angles
-                    A.s.export_ab[nplane + e] = atan2(sb, cb);
-                }
-                // next RHS: recon (+ static centre) and lambda, scattered to the pair's agents below
-                double* sc = sScr + p * kScrW;
-                sc[0] = rx + (pj < 0 ? cen[0] : 0.0);
-                sc[1] = ry + (pj < 0 ? cen[1] : 0.0);
-                sc[2] = rz + (pj < 0 ? cen[2] : 0.0);
-                sc[3] = lx;
-                sc[4] = ly;
-                sc[5] = lz;
-            }
+            };
+            if (uni)
+                pair_pass(std::integral_constant<bool, true>{});
+            else
+                pair_pass(std::integral_constant<bool, false>{});
             __syncwarp();
             // per-agent signed incidence sums (fixed order) -> V[w][which][agent][axis]
             for (int task = lane; task < tasks; task += 32) {
@@ -429,18 +447,24 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
             }
         }
         __syncthreads();
-        // contraction of this round's samples, ascending t
-        if (owner) {
+        // contraction of this round's samples on the fp64 tensor cores (k = sample within the round)
+        {
             const int tn = min(kMaWarps, n_p - rd * kMaWarps);
-#pragma unroll 5
-            for (int w = 0; w < tn; ++w) {
-                const double vv = sVr[w * rows + crow];
-                const double2* pr = reinterpret_cast<const double2*>(sP + (rd * kMaWarps + w) * mp + cg);
-                const double2 q0 = pr[0], q1 = pr[1];  // columns past m: padding / next row, never written
-                cacc[0] = fma(q0.x, vv, cacc[0]);
-                cacc[1] = fma(q0.y, vv, cacc[1]);
-                cacc[2] = fma(q1.x, vv, cacc[2]);
-                cacc[3] = fma(q1.y, vv, cacc[3]);
+            const double* prd = sP + rd * kMaWarps * mp;
+#pragma unroll
+            for (int j = 0; j < kMaxTiles; ++j) {
+                const int tile = warp + j * kMaWarps;
+                if (tile < n_mt * n_nt) {
+                    const int mt = tile / n_nt, nt = tile - mt * n_nt;
+                    const int ar = mt * 8 + (lane >> 2), bc = nt * 8 + (lane >> 2);
+#pragma unroll
+                    for (int ks = 0; ks < (kMaWarps + 3) / 4; ++ks) {
+                        const int k = 4 * ks + (lane & 3);
+                        const double av = (k < tn && ar < rows) ? sVr[k * rows + ar] : 0.0;
+                        const double bv = (k < tn && bc < m) ? prd[k * mp + bc] : 0.0;
+                        dmma884(cacc[j], av, bv);
+                    }
+                }
             }
         }
     }
@@ -453,10 +477,17 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
         sWarp[kMaWarps + warp] = mx;
     }
     double* sg = A.s.sums + (int64_t)i * 2 * n_a * 3 * m;  // [which][a][k][c] = [row][c]
-    if (owner) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-            if (cg + c < m) sg[crow * m + cg + c] = cacc[c];
+    for (int j = 0; j < kMaxTiles; ++j) {
+        const int tile = warp + j * kMaWarps;
+        if (tile < n_mt * n_nt) {
+            const int mt = tile / n_nt, nt = tile - mt * n_nt;
+            const int r = mt * 8 + (lane >> 2), c0 = nt * 8 + 2 * (lane & 3);
+            if (r < rows) {
+                if (c0 < m) sg[r * m + c0] = cacc[j][0];
+                if (c0 + 1 < m) sg[r * m + c0 + 1] = cacc[j][1];
+            }
+        }
     }
     __syncthreads();
     if (tid == 0 && mode == 0) {
@@ -516,11 +547,6 @@ constexpr int kQpCols = 3 * kQpP;      // 48 RHS columns
 constexpr int kQpLd = kQpCols + 4;     // padded smem row (bank spread of the B fragments)
 constexpr int kQpMt = 3;               // m-tiles per warp (8 warps x 3 x 8 rows >= nv = 176)
 
-__device__ __forceinline__ void dmma884(double* d, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                 : "+d"(d[0]), "+d"(d[1])
-                 : "d"(a), "d"(b));
-}
 
 template <int M>
 __global__ void __launch_bounds__(256) ma_qp_kernel(MaArgs A) {

@@ -24,6 +24,6 @@ for r in rows:
                 vals.append(0.0)
         lines.append((vals, int(r[0]), r[1].strip()[:80]))
 print(cols)
-key = 0
+key = 1
 for vals, ln, src in sorted(lines, key=lambda x: -x[0][key])[:top]:
     print("  ".join(f"{v:12.0f}" for v in vals), f" L{ln:<4} {src}")
