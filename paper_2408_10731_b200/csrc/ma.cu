@@ -28,7 +28,10 @@ namespace tro {
 #ifndef MA_MINB
 #define MA_MINB 2  // resident CTAs per SM the element kernel is compiled for (128 registers)
 #endif
-constexpr int kMaWarps = 10;  // 100 samples = 10 rounds of 10 (C3); 2 CTAs x 10 warps per SM
+#ifndef MA_WARPS
+#define MA_WARPS 10
+#endif
+constexpr int kMaWarps = MA_WARPS;  // 100 samples = 10 rounds of 10 (C3); 2 CTAs x 10 warps per SM
 constexpr int kMaMaxAgents = 32;
 constexpr int kMaMaxRing = 64;
 
@@ -268,9 +271,11 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     const int rows = tasks * 3;  // [which][agent][axis]
     // contraction tiles: D[rows x m] = V^T[rows x t] P[t x m] as 8x8 DMMA tiles, warp w owning tiles
     // w, w + kMaWarps, ... (rows <= 96, m <= 11: at most 12 x 2 tiles, <= 3 per warp)
-    constexpr int kMaxTiles = 3;
+    constexpr int kMaxTiles = (24 + kMaWarps - 1) / kMaWarps;
     const int n_mt = (rows + 7) >> 3, n_nt = (m + 7) >> 3;
-    double cacc[kMaxTiles][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double cacc[kMaxTiles][2];
+#pragma unroll
+    for (int j = 0; j < kMaxTiles; ++j) cacc[j][0] = cacc[j][1] = 0.0;
     double sumsq = 0.0, mx = 0.0;
     const int rowW = 3 * np_;  // state[i][t][w][p], W = 3 (a problem's block stays far below 2^31 doubles)
     double* st;  // pinned in a register: rematerialising the 64-bit product per element cost ~20 instructions
