@@ -50,12 +50,16 @@ struct B2Args {
 };
 
 // per-sample shared arrays
+// The F'g rows reuse the geometry rows kX..kAY: a sample's thread reads its geometry into registers before
+// it writes that sample's F'g inputs, and no other thread reads them (18 rows instead of 26: the smaller
+// per-CTA footprint leaves L1 room for the shared obstacle tracks and basis rows at 7 CTAs / SM).
 enum {
     kX, kY, kC, kS, kVX, kVY, kAX, kAY, kTgt,                // geometry of the new xi
-    kGVX, kGVY, kGAX, kGAY, kGX, kGY, kGCX, kGCY,           // F'g inputs
     kRVX, kRVY, kRAX, kRAY, kRX, kRY, kRCX, kRCY, kDPsi,    // F'r / heading residual inputs
-    kNT
+    kNT,
+    kGVX = kX, kGVY, kGAX, kGAY, kGX, kGY, kGCX, kGCY,      // F'g inputs (aliasing the geometry rows)
 };
+static_assert(kGCY < kTgt, "the F'g rows must not overlap the heading targets");
 
 struct B2Smem {
     int T, xi, rhs, po, pn, rp, out, part, ab, ai, red, total;
