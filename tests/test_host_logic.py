@@ -166,3 +166,37 @@ def test_ozaki_row_split_is_exact():
         scale = np.maximum(np.abs(A).max(axis=2, keepdims=True), 1e-300)
         assert np.max(np.abs(R - A) / scale) <= tol
     assert ea[0, 5] == 0 and not sl[0, :, 0].reshape(S, -1)[:, :0].size
+
+
+@pytest.mark.parametrize("n_a,n_static", [(2, 0), (3, 1), (5, 2), (16, 0), (16, 3)])
+def test_multiagent_colour_order(n_a, n_static):
+    """The device pair order is a permutation in colour-major order: a proper edge colouring (every agent in at
+    most one pair per colour), each colour's pairs contiguous, so step q of every agent's incidence list reads
+    one contiguous block of scratch records (conflict-free shared-memory reads in the MA scatter)."""
+    from paper_2408_10731_b200.solver_multiagent import _colour_order
+
+    pi, pj, ps = [], [], []
+    for i in range(n_a):
+        for j in range(i + 1, n_a):
+            pi.append(i), pj.append(j), ps.append(-1)
+    for s in range(n_static):
+        for i in range(n_a):
+            pi.append(i), pj.append(-1), ps.append(s)
+    pi, pj, ps = np.array(pi), np.array(pj), np.array(ps)
+    order = _colour_order(n_a, pi, pj, ps)
+    assert sorted(order.tolist()) == list(range(len(pi)))
+    # split the order into colours: consecutive blocks where no agent repeats
+    colours, cur, seen = [], [], set()
+    for p in order:
+        members = {pi[p]} | ({pj[p]} if pj[p] >= 0 else set())
+        if members & seen:
+            colours.append(cur)
+            cur, seen = [], set()
+        cur.append(p)
+        seen |= members
+    colours.append(cur)
+    n_agent_colours = n_a - 1 + (n_a & 1) if n_a > 1 else 0
+    assert len(colours) == n_agent_colours + n_static
+    if n_a % 2 == 0:  # perfect matchings: every agent once per colour, so incidence steps stay aligned
+        for c in colours[:n_agent_colours]:
+            assert len(c) == n_a // 2
