@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "fastmath.cuh"
+#include "tma.cuh"
 #include "../../include/trajopt_b200.h"
 
 namespace tro {
@@ -122,6 +123,11 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     bool uni;  // every pair shares (a, b) and has an agent partner
     const int status0 = A.s.status[i];
     if (mode == 0 && (status0 & TRO_CONVERGED)) return;
+    __shared__ uint64_t sBar[4];  // V[0 / 1] published by every warp (full), read by every warp (empty)
+    if (tid == 0) {
+        for (int k = 0; k < 4; ++k) mbar_init(&sBar[k], kMaWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     if (mode == 0 && lane == 0 && ((3 * np_ * 8) & 15) == 0)  // this warp's first kMaAhead rounds of lambda rows
         for (int r = 0; r < kMaAhead; ++r) {
             const int t = r * kMaWarps + warp;
@@ -294,6 +300,32 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     const double u_pa = sPair[0], u_pb = sPair[np_], u_ipa = sPair[2 * np_], u_ipb = sPair[3 * np_];
     const double u_pa2 = u_pa * u_pa, u_pb2 = u_pb * u_pb;
     const int n_rounds = (n_p + kMaWarps - 1) / kMaWarps;
+    // contraction of round r's samples on the fp64 tensor cores (k = sample within the round), once every
+    // warp has published V[r & 1]; then this warp releases the buffer for round r + 2
+    auto contract = [&](int r) {
+        const int bb = r & 1;
+        mbar_wait(&sBar[bb], (uint32_t)((r >> 1) & 1));
+        const double* sVb = sV + bb * kMaWarps * rows;
+        const int tn = min(kMaWarps, n_p - r * kMaWarps);
+        const double* prd = sP + r * kMaWarps * mp;
+#pragma unroll
+        for (int j = 0; j < kMaxTiles; ++j) {
+            const int tile = warp + j * kMaWarps;
+            if (tile < n_mt * n_nt) {
+                const int mt = tile / n_nt, nt = tile - mt * n_nt;
+                const int ar = mt * 8 + (lane >> 2), bc = nt * 8 + (lane >> 2);
+#pragma unroll
+                for (int ks = 0; ks < (kMaWarps + 3) / 4; ++ks) {
+                    const int k = 4 * ks + (lane & 3);
+                    const double av = (k < tn && ar < rows) ? sVb[k * rows + ar] : 0.0;
+                    const double bv = (k < tn && bc < m) ? prd[k * mp + bc] : 0.0;
+                    dmma884(cacc[j], av, bv);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sBar[2 + bb]);
+    };
     const bool pf = mode == 0 && lane == 0 && ((rowW * 8) & 15) == 0;
     for (int rd = 0; rd < n_rounds; ++rd) {
         const int t = rd * kMaWarps + warp;
@@ -433,7 +465,9 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
             else
                 pair_pass(std::integral_constant<bool, false>{});
             __syncwarp();
-            // per-agent signed incidence sums (fixed order) -> V[w][which][agent][axis]
+            // per-agent signed incidence sums (fixed order) -> V[w][which][agent][axis]; V[rd & 1] was last
+            // read by round rd - 2's contraction
+            if (rd >= 2) mbar_wait(&sBar[2 + (rd & 1)], (uint32_t)(((rd - 2) >> 1) & 1));
             for (int task = lane; task < tasks; task += 32) {
                 const int a = task % n_a, which = task / n_a;  // which 0: B (recon), 1: C (lambda)
                 double v[3] = {0.0, 0.0, 0.0};
@@ -451,28 +485,13 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
                 vo[2] = v[2];
             }
         }
-        __syncthreads();
-        // contraction of this round's samples on the fp64 tensor cores (k = sample within the round)
-        {
-            const int tn = min(kMaWarps, n_p - rd * kMaWarps);
-            const double* prd = sP + rd * kMaWarps * mp;
-#pragma unroll
-            for (int j = 0; j < kMaxTiles; ++j) {
-                const int tile = warp + j * kMaWarps;
-                if (tile < n_mt * n_nt) {
-                    const int mt = tile / n_nt, nt = tile - mt * n_nt;
-                    const int ar = mt * 8 + (lane >> 2), bc = nt * 8 + (lane >> 2);
-#pragma unroll
-                    for (int ks = 0; ks < (kMaWarps + 3) / 4; ++ks) {
-                        const int k = 4 * ks + (lane & 3);
-                        const double av = (k < tn && ar < rows) ? sVr[k * rows + ar] : 0.0;
-                        const double bv = (k < tn && bc < m) ? prd[k * mp + bc] : 0.0;
-                        dmma884(cacc[j], av, bv);
-                    }
-                }
-            }
-        }
+        // V[b] complete for this warp: publish it, then contract the previous round (usually already
+        // published by every warp, so no CTA-wide barrier per round)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sBar[rd & 1]);
+        if (rd > 0) contract(rd - 1);
     }
+    contract(n_rounds - 1);
 
     // ---------------- reductions
     sumsq = warp_sum(sumsq);
