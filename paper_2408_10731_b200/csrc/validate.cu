@@ -5,9 +5,14 @@
 // sum |pos[t+1] - pos[t]|, the worst incursion max(1 + margin - dist) and the clearance lower bound
 // min((dist - 1) min(a, b)) with dist the ellipsoidal distance sqrt(dx^2/a^2 + dy^2/a^2 [+ dz^2/b^2])
 // to every obstacle's constant-velocity track (scenarios.py:118-127).  Here one warp owns one member:
-// lanes own samples, positions / accelerations come from the coefficients (P xi, Pddot xi) or from
-// given samples, obstacle centres are predicted on the fly (c + v (t - t0)), and every reduction runs
-// in a fixed order so a member's numbers do not depend on the batch.
+// positions / accelerations come from the coefficients (P xi, Pddot xi as 8x8x4 fp64 tensor-core tiles, the
+// member's coefficients held as the B fragments) or from given samples; the (sample, obstacle) distance
+// pass keeps up to 4 of a lane's samples in registers per broadcast obstacle record and spreads the < 32
+// tail samples over the lanes by obstacle; obstacle centres are predicted on the fly (c + v (t - t0)).
+// Every sum runs in a fixed order and the rest are exact minima, so a member's numbers do not depend on
+// the batch.
+#include <type_traits>
+
 #include "common.cuh"
 #include "fastmath.cuh"
 #include "../../include/trajopt_b200.h"
@@ -19,6 +24,13 @@ namespace tro {
 #endif
 constexpr int kValWarps = VAL_WARPS;  // members per CTA (fewer when the sample buffers would not fit)
 constexpr int kValRec = 9;     // doubles per obstacle record
+
+// D(8x8) += A(8x4, row) B(4x8, col), fp64 tensor cores (lane l: A[l/4][l%4], B[l%4][l/4], D[l/4][2 (l%4) + j])
+__device__ __forceinline__ void dmma884_v(double* d, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
 
 struct ValArgs {
     tro_val_dims d;
@@ -68,60 +80,112 @@ __global__ void __launch_bounds__(kValWarps * 32) validate_kernel(ValArgs A) {
     if (i >= A.d.n_members) return;
     double* pw = sPos + (int64_t)warp * n_p * DIM;
     const double* xi = coeffs ? A.io.xi + i * DIM * m : nullptr;
-    const double t0 = __ldg(A.c.t);
+    const double t0_time = __ldg(A.c.t);
     double smooth = 0.0, track = 0.0;
     double qmin = __longlong_as_double(0x7ff0000000000000LL), clear = qmin;
-    for (int t = lane; t < n_p; t += 32) {
-        double p[3] = {0, 0, 0}, ac[3] = {0, 0, 0};
-        if (coeffs) {
+    if (coeffs) {
+        // positions and accelerations on the fp64 tensor cores: [P | Pdd](t, c) x xi(c, axis) as 8x8x4 tiles
+        // (t = tile row, axis = tile column); the member's coefficients are the B fragments, loaded once
+        const int ksn = (m + 3) >> 2;  // m <= 16 (tro_validate_f64)
+        double bx[4];
 #pragma unroll
-            for (int k = 0; k < DIM; ++k) {
-                double ps = 0.0, as = 0.0;
-                for (int c = 0; c < m; ++c) {
-                    const double x = __ldg(xi + k * m + c);
-                    ps = fma(sP[t * m + c], x, ps);
-                    as = fma(sPdd[t * m + c], x, as);
+        for (int ks = 0; ks < 4; ++ks) {
+            const int c = 4 * ks + (lane & 3), ax = lane >> 2;
+            bx[ks] = (ks < ksn && c < m && ax < DIM) ? __ldg(xi + ax * m + c) : 0.0;
+        }
+        for (int mt = 0; mt < (n_p + 7) >> 3; ++mt) {
+            double dp[2] = {0.0, 0.0}, da[2] = {0.0, 0.0};
+            const int ta = mt * 8 + (lane >> 2);
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                if (ks < ksn) {
+                    const int c = 4 * ks + (lane & 3);
+                    const bool ok = ta < n_p && c < m;
+                    dmma884_v(dp, ok ? sP[ta * m + c] : 0.0, bx[ks]);
+                    dmma884_v(da, ok ? sPdd[ta * m + c] : 0.0, bx[ks]);
                 }
-                p[k] = ps;
-                ac[k] = as;
             }
-        } else {
+            const int td = mt * 8 + (lane >> 2), ax0 = 2 * (lane & 3);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                if (td < n_p && ax0 + j < DIM) {
+                    pw[td * DIM + ax0 + j] = dp[j];
+                    smooth = fma(da[j], da[j], smooth);
+                }
+            }
+        }
+    } else {
+        for (int t = lane; t < n_p; t += 32) {
 #pragma unroll
             for (int k = 0; k < DIM; ++k) {
-                p[k] = __ldg(A.io.pos + (i * n_p + t) * DIM + k);
-                ac[k] = __ldg(A.io.acc + (i * n_p + t) * DIM + k);
+                pw[t * DIM + k] = __ldg(A.io.pos + (i * n_p + t) * DIM + k);
+                const double ac = __ldg(A.io.acc + (i * n_p + t) * DIM + k);
+                smooth = fma(ac, ac, smooth);
             }
         }
-#pragma unroll
-        for (int k = 0; k < DIM; ++k) {
-            pw[t * DIM + k] = p[k];
-            smooth = fma(ac[k], ac[k], smooth);
-        }
-        if (A.c.desired) {
+    }
+    __syncwarp();
+    if (A.c.desired)
+        for (int t = lane; t < n_p; t += 32) {
             const double* dd = A.c.desired + (A.d.per_member_desired ? (i * n_p + t) * DIM : (int64_t)t * DIM);
 #pragma unroll
             for (int k = 0; k < DIM; ++k) {
-                const double e = p[k] - __ldg(dd + k);
+                const double e = pw[t * DIM + k] - __ldg(dd + k);
                 track = fma(e, e, track);
             }
         }
-        const double tau = __ldg(A.c.t + t) - t0;  // predict_obstacles: c + v (t_now + t - t0), t_now = 0
+    // obstacle distances: every (sample, obstacle) pair, all reductions are minima (exact, order-free), so lanes
+    // can take any partition.  Full groups of 32 samples: each lane keeps up to 4 of its samples in registers
+    // and reuses one broadcast obstacle record for all of them; the < 32 tail samples are spread over the
+    // lanes by obstacle instead (no idle lanes at n_p = 100).
+    const double* tt = A.c.t;
+    auto element = [&](const double* o, double p0, double p1, double p2, double tau) {
+        double q = 0.0;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            const double d = (k == 0 ? p0 : k == 1 ? p1 : p2) - fma(o[3 + k], tau, o[k]);
+            // metrics.py:63-65: the last axis uses b (z in 3-D, y in 2-D), the others a; multiplied by the
+            // reciprocal squares (<= 1 ulp per term from the reference's divisions)
+            q = fma(d * d, k == DIM - 1 ? o[7] : o[6], q);
+        }
+        qmin = q < qmin ? q : qmin;
+        if (!uniform) {
+            const double cl = (sqrt(q) - 1.0) * o[8];
+            clear = cl < clear ? cl : clear;
+        }
+    };
+    auto group = [&](auto ns_tag, int t0) {
+        constexpr int NS = decltype(ns_tag)::value;
+        double pp[NS][3], tau[NS];
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+            const int t = t0 + 32 * u + lane;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) pp[u][k] = k < DIM ? pw[t * DIM + k] : 0.0;
+            tau[u] = __ldg(tt + t) - t0_time;  // predict_obstacles: c + v (t_now + t - t0), t_now = 0
+        }
         for (int j = 0; j < n_o; ++j) {
             const double* o = sObs + kValRec * j;
-            double q = 0.0;
 #pragma unroll
-            for (int k = 0; k < DIM; ++k) {
-                const double d = p[k] - fma(o[3 + k], tau, o[k]);
-                // metrics.py:63-65: the last axis uses b (z in 3-D, y in 2-D), the others a; multiplied by the
-                // reciprocal squares (<= 1 ulp per term from the reference's divisions)
-                q = fma(d * d, k == DIM - 1 ? o[7] : o[6], q);
-            }
-            qmin = q < qmin ? q : qmin;
-            if (!uniform) {
-                const double cl = (sqrt(q) - 1.0) * o[8];
-                clear = cl < clear ? cl : clear;
-            }
+            for (int u = 0; u < NS; ++u) element(o, pp[u][0], pp[u][1], pp[u][2], tau[u]);
         }
+    };
+    const int n_full = n_p >> 5;
+    int g = 0;
+    for (; g + 4 <= n_full; g += 4) group(std::integral_constant<int, 4>{}, 32 * g);
+    switch (n_full - g) {
+        case 3: group(std::integral_constant<int, 3>{}, 32 * g); break;
+        case 2: group(std::integral_constant<int, 2>{}, 32 * g); break;
+        case 1: group(std::integral_constant<int, 1>{}, 32 * g); break;
+        default: break;
+    }
+    for (int t = 32 * n_full; t < n_p; ++t) {  // tail samples: lanes over obstacles
+        const double* pp = pw + t * DIM;
+        double pt[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) pt[k] = k < DIM ? pp[k] : 0.0;
+        const double tau = __ldg(tt + t) - t0_time;
+        for (int j = lane; j < n_o; j += 32) element(sObs + kValRec * j, pt[0], pt[1], pt[2], tau);
     }
     __syncwarp();
     // arc length over the warp's stored positions (metrics.py:39-40), fixed order: lanes own segments
@@ -162,7 +226,7 @@ __global__ void __launch_bounds__(kValWarps * 32) validate_kernel(ValArgs A) {
 extern "C" int tro_validate_f64(const tro_val_dims* d, const tro_val_consts* c, const tro_val_io* io, void* stream) {
     if (!d || !c || !io || !io->out || (d->dim != 2 && d->dim != 3) || d->n_p < 2 || d->n_obs < 0 || !c->t)
         return TRO_EINVAL;
-    if (io->xi ? (d->m < 1 || !c->P || !c->Pdd) : (!io->pos || !io->acc)) return TRO_EINVAL;
+    if (io->xi ? (d->m < 1 || d->m > 16 || !c->P || !c->Pdd) : (!io->pos || !io->acc)) return TRO_EINVAL;
     if (d->n_obs > 0 && (!c->centers || !c->velocities || !c->shape_a || !c->shape_b)) return TRO_EINVAL;
     if (d->n_members <= 0) return 0;
     tro::ValArgs A;
@@ -180,13 +244,14 @@ extern "C" int tro_validate_f64(const tro_val_dims* d, const tro_val_consts* c, 
     const size_t smem = smem_for(wpc);
     if (smem > 200 * 1024) return TRO_EINVAL;
     const unsigned blocks = (unsigned)((d->n_members + wpc - 1) / wpc);
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (d->dim == 3) {
+    if (d->dim == 3)
         cudaFuncSetAttribute(tro::validate_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        tro::validate_kernel<3><<<blocks, wpc * 32, smem, st>>>(A);
-    } else {
+    else
         cudaFuncSetAttribute(tro::validate_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (d->dim == 3)
+        tro::validate_kernel<3><<<blocks, wpc * 32, smem, st>>>(A);
+    else
         tro::validate_kernel<2><<<blocks, wpc * 32, smem, st>>>(A);
-    }
     return (int)cudaGetLastError();
 }
