@@ -265,21 +265,25 @@ __global__ void __launch_bounds__(kPrWarps * 32, PR_MINB) priest_project_kernel(
                     unsigned inside = 0;
 #pragma unroll
                     for (int u = 0; u < kB; ++u) {
-                        // 1 <= q2 <= 1e12 as one unsigned range test on the bit pattern (q2 >= 0, so
-                        // the patterns are monotone; NaN falls outside): integer pipe, not fp64
-                        const unsigned long long qb = (unsigned long long)__double_as_longlong(q2[u]);
-                        const bool out = qb - 0x3FF0000000000000ull <= 0x426D1A94A2000000ull - 0x3FF0000000000000ull;
-                        outside += out ? 1 : 0;
-                        inside |= out ? 0u : (1u << u);
+                        // 1 <= q2 < 2^40 (the high word below 1e12's) as one 32-bit unsigned range test on the
+                        // bit pattern (q2 >= 0, so the patterns are monotone; NaN and 0 fall outside): integer
+                        // pipe, two instructions; the sliver [hi(1e12), 1e12] is settled exactly below
+                        const unsigned hi = (unsigned)__double2hiint(q2[u]);
+                        inside |= (hi - 0x3FF00000u < 0x426D1A94u - 0x3FF00000u) ? 0u : (1u << u);
                     }
+                    outside += kB - __popc(inside);
                     if (inside) {  // per-lane (lanes of the remainder slot walk different obstacle groups)
 #pragma unroll
                         for (int u = 0; u < kB; ++u) {
                             if (inside & (1u << u)) {  // recompute the offsets (keeping kB live costs registers)
                                 double dl[3], cc[3];
                                 const double qq = q2_of(j + u * jstep, dl, cc);
-                                const double* o = sObs + 8 * (j + u * jstep);
-                                inside_target<DIM>(p, dl, cc, qq, o[5], o[6], S, rr);
+                                if (qq >= 1.0 && qq <= 1e12) {  // the exact test (reached only near 1e12)
+                                    ++outside;
+                                } else {
+                                    const double* o = sObs + 8 * (j + u * jstep);
+                                    inside_target<DIM>(p, dl, cc, qq, o[5], o[6], S, rr);
+                                }
                             }
                         }
                     }
