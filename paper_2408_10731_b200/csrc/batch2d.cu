@@ -27,6 +27,10 @@ __device__ __forceinline__ double clip(double x, double lo, double hi) { return 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
 constexpr int kB2Threads = 128;
+#ifndef B2_Q
+#define B2_Q 8  // t-chunks of the F' contraction (partials in shared memory)
+#endif
+constexpr int kB2Q = B2_Q;
 constexpr int kB2Warps = kB2Threads / 32;
 constexpr int kB2MaxRing = 64;
 constexpr int kB2MaxC = 8;
@@ -75,7 +79,7 @@ __host__ __device__ inline B2Smem b2_layout(int n_p, int m, int n_o) {
     L.pn = off;   off += m;
     L.rp = off;   off += m + 2;
     L.out = off;  off += 2 * nv + m;
-    L.part = off; off += 8 * (2 * nv + m);
+    L.part = off; off += kB2Q * (2 * nv + m);
     L.ab = off;   off += 5 * (n_o > 0 ? n_o : 1);  // per obstacle (a, b, a^2, b^2, 1/a)
     off = (off + 1) & ~1;
     L.ai = off;   off += 2 * (n_o > 0 ? n_o : 1);  // per obstacle (a^2, (1e6 a)^2), 16-byte aligned
@@ -701,7 +705,7 @@ __global__ void __launch_bounds__(kB2Threads, B2_MINB) b2_kernel(B2Args A) {
     // thread (k, q) keeps all columns of one basis row k over t-chunk q in registers (one basis
     // load per sample feeds every column), partials summed over q in a fixed order.
     {
-        constexpr int kQ = 8;
+        constexpr int kQ = kB2Q;
         const int chunk = (n_p + kQ - 1) / kQ;
         const int ncol = iter ? 17 : 8;
         for (int w = tid; w < m * kQ; w += kB2Threads) {
