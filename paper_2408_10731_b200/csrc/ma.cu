@@ -4,16 +4,18 @@
 // N_a per static sphere) for one iteration of solve_joint (solver_multiagent.py:252-335):
 //   prologue : the per-axis QP, xi = K_L^-1 [ rho A'B - A'C ; b_eq ], from the agent-
 //              contracted sums B (recon + statics) and C (lambda) the previous launch left
-//              behind (b_fo = recon - lambda/rho + statics, :266-268), then every agent's
-//              positions on the grid (shared memory);
-//   body     : warps walk the horizon, lanes the pairs (state[i][t][w][p], pairs fastest:
-//              coalesced).  Per (pair, t): alpha/beta of the new offsets in trig-free form
-//              (unit vectors), the multiplier-shifted d (:285-293), residual and multiplier
-//              ascent (:295-296).  Only the multipliers persist: alpha, beta come from the
-//              positions and d only feeds the next RHS, which is folded into the sums here.
-//   epilogue : each pair's recon and lambda are scattered to its two agents through an
-//              incidence list in a fixed order, contracted with P (per-lane accumulators),
-//              reduced across warps; residual norm / max; history; the staged level
+//              behind (b_fo = recon - lambda/rho + statics, :266-268) -- or, mode 4, the xi the
+//              batched tensor-core QP kernel (ma_qp_kernel) wrote; the boundary projection;
+//   body     : rounds of kMaWarps samples, warp w on t = r kMaWarps + w: the sample's positions,
+//              then lanes over pairs (state[i][t][w][p], pairs fastest: coalesced).  Per (pair, t):
+//              alpha/beta of the new offsets in trig-free form (unit vectors), the multiplier-shifted
+//              d (:285-293), residual and multiplier ascent (:295-296).  Only the multipliers persist:
+//              alpha, beta come from the positions and d only feeds the next RHS, folded into the sums;
+//              each pair's recon and lambda are scattered to its two agents through colour-ordered
+//              incidence lists (fixed order) into the round's V rows;
+//   contract : V (agent sums x samples) times P on the fp64 tensor cores (DMMA tiles owned by warps,
+//              accumulated across rounds; rounds handed over through mbarriers);
+//   epilogue : the sums B, C for the next launch; residual norm / max; history; the staged level
 //              schedule (:313-335).
 // Deterministic: every reduction has a fixed order, so a problem's bits do not depend on
 // the batch or the GPU count.
