@@ -102,3 +102,34 @@ def test_batch_equals_single_and_oracle_step():
         prob = OM.Problem(b_eq=MA._b_eq(probs[s]), statics=np.zeros((0, 3)))
         _, hist, _ = OM.solve(st, prob, b.P, max_iter=12, kinv=kinv)
         np.testing.assert_allclose(eng.hist[s, :4, 0].cpu().numpy(), hist[:4, 0], rtol=1e-9)
+
+
+@pytest.mark.parametrize("n_agents,n_static", [(5, 1), (7, 0)])
+def test_odd_roster_colour_order_matches_oracle(n_agents, n_static):
+    """Odd agent counts: the round-robin colouring leaves every agent one bye, so the incidence steps are not
+    aligned across lanes (conflicting, still correct) -- the device run must match the oracle step for step,
+    and the multipliers must come back in the reference pair order."""
+    from paper_2408_10731_b200.basis import build_basis
+
+    b = build_basis(0.0, 10.0, 100, 10)
+    starts, goals = scenarios.square_antipodal(n_agents, 6.0, 0.4, seed=3)
+    bnds = [tuple(AxisBoundary(p0=float(starts[i, k]), p1=float(goals[i, k])) for k in range(3))
+            for i in range(n_agents)]
+    statics = [MA.StaticSphere(center=np.array([0.3, -0.2, 1.0]), radius=0.5)][:n_static]
+    prob = MA.MultiAgentProblem(basis=b, boundaries=bnds, agent_shape=EllipsoidShape(0.3, 0.45),
+                                static_obstacles=statics)
+    params = MA.JointParams(max_iter=8, rho_final=1e3)
+    struct = MA._Structure(prob, params)
+    assert sorted(struct.dev_perm.tolist()) == list(range(struct.n_pairs))
+    assert not np.array_equal(struct.dev_perm, np.arange(struct.n_pairs))  # the order really is permuted
+    sol = MA.solve_joint(prob, params)
+    st = OM.make_structure(b.P, b.Pdot, b.Pddot, n_agents, 0.3, 0.45, n_static=n_static,
+                           static_radii=[s.radius for s in statics], rho_final=1e3)
+    oprob = OM.Problem(b_eq=MA._b_eq(prob), statics=np.array([s.center for s in statics]).reshape(-1, 3))
+    kinv = [f.kinv for f in struct.factors]
+    ostate, hist, _ = OM.solve(st, oprob, b.P, max_iter=8, kinv=kinv)
+    h = np.array([[x["norm"], x["max_abs"]] for x in sol.residual_history])
+    np.testing.assert_allclose(h[:4], hist[:4, :2], rtol=1e-9)
+    # multipliers in the reference pair order (lam_ref / JointState.lam): a wrong pair mapping would be O(1) off
+    assert sol.state.lam.shape == ostate.lam.shape
+    assert np.max(np.abs(sol.state.lam - ostate.lam)) <= 1e-6 * max(1.0, np.abs(ostate.lam).max())
