@@ -126,3 +126,31 @@ def test_pinned_host_input_pipelined_matches_one_launch(golden, per_member_desir
     got = np.stack([r["smoothness"], r["tracking"], r["arc_length"], r["worst"], r["min_clearance"]], axis=1)
     np.testing.assert_array_equal(got, ref)
     np.testing.assert_array_equal(r["success"], ref[:, 3] <= 0.0)
+
+
+@pytest.mark.parametrize("n_p", [20, 40, 64, 100, 131])
+@pytest.mark.parametrize("dim", [2, 3])
+def test_coefficient_mode_sample_counts(n_p, dim):
+    """Coefficient input across sample counts: no full 32-sample group (20), a group + tail (40, 100, 131),
+    groups only (64); positions / accelerations from the tensor-core products, the distance pass's register
+    groups and lane-spread tail -- all against the oracle metrics on P xi, Pddot xi."""
+    rng = np.random.default_rng(n_p + 10 * dim)
+    m, n_o, B = 11, 37, 96
+    t = np.linspace(0.0, 10.0, n_p)
+    P = rng.normal(size=(n_p, m))
+    Pdd = rng.normal(size=(n_p, m))
+    basis = BasisSet(grid=TimeGrid(0.0, 10.0, n_p, t), degree=m - 1, P=P, Pdot=np.zeros_like(P), Pddot=Pdd)
+    obs = [Obs(float(rng.uniform(0.3, 0.6)), float(rng.uniform(0.3, 0.6)), list(rng.uniform(-2, 2, dim)),
+               list(rng.uniform(-0.3, 0.3, dim))) for _ in range(n_o)]
+    sc = Scene(dim, obs)
+    xi = rng.normal(size=(B, dim, m)) * 0.5
+    des = rng.uniform(-2, 2, (n_p, dim))
+    r = MT.validate_batch(sc, t, xi=xi, basis=basis, desired=des, margin=0.05)
+    c = np.array([o.center for o in obs]); v = np.array([o.velocity for o in obs])
+    a = np.array([o.a for o in obs]); b = np.array([o.b for o in obs])
+    for i in range(0, B, 7):
+        pos = P @ xi[i].T
+        acc = Pdd @ xi[i].T
+        ref = OMT.metrics(pos, acc, t, c, v, a, b, dim, des, 0.05)
+        got = [r["smoothness"][i], r["tracking"][i], r["arc_length"][i], r["worst"][i], r["min_clearance"][i]]
+        assert rel(got, ref) <= 1e-12, (i, got, ref)
