@@ -133,3 +133,29 @@ def test_odd_roster_colour_order_matches_oracle(n_agents, n_static):
     # multipliers in the reference pair order (lam_ref / JointState.lam): a wrong pair mapping would be O(1) off
     assert sol.state.lam.shape == ostate.lam.shape
     assert np.max(np.abs(sol.state.lam - ostate.lam)) <= 1e-6 * max(1.0, np.abs(ostate.lam).max())
+
+
+@pytest.mark.parametrize("n_p,degree", [(37, 8), (10, 10), (131, 8), (37, 10), (100, 8), (40, 10), (100, 10)])
+def test_sample_rounds_and_basis_sizes_match_oracle(n_p, degree):
+    """The element pass runs in rounds of 10 samples: sample counts that leave a partial last round (37, 131)
+    or a single round (10), and both compiled basis sizes (m = 9, 11), step for step against the oracle."""
+    from paper_2408_10731_b200.basis import build_basis
+
+    b = build_basis(0.0, 10.0, n_p, degree)
+    n_agents = 6
+    # random endpoints: antipodal rosters put every agent at the layout centre at the middle sample of an
+    # odd grid (all pair offsets exactly zero, alpha = atan2 of rounding noise on either side)
+    rng = np.random.default_rng(5)
+    starts, goals = rng.uniform(-3.0, 3.0, (n_agents, 3)), rng.uniform(-3.0, 3.0, (n_agents, 3))
+    bnds = [tuple(AxisBoundary(p0=float(starts[i, k]), p1=float(goals[i, k])) for k in range(3))
+            for i in range(n_agents)]
+    prob = MA.MultiAgentProblem(basis=b, boundaries=bnds, agent_shape=EllipsoidShape(0.3, 0.45))
+    params = MA.JointParams(max_iter=6, rho_final=1e3)
+    struct = MA._Structure(prob, params)
+    sol = MA.solve_joint(prob, params)
+    st = OM.make_structure(b.P, b.Pdot, b.Pddot, n_agents, 0.3, 0.45, rho_final=1e3)
+    oprob = OM.Problem(b_eq=MA._b_eq(prob), statics=np.zeros((0, 3)))
+    ostate, hist, _ = OM.solve(st, oprob, b.P, max_iter=6, kinv=[f.kinv for f in struct.factors])
+    h = np.array([[x["norm"], x["max_abs"]] for x in sol.residual_history])
+    np.testing.assert_allclose(h[:4], hist[:4, :2], rtol=1e-9)
+    assert np.max(np.abs(sol.state.lam - ostate.lam)) <= 1e-6 * max(1.0, np.abs(ostate.lam).max())
