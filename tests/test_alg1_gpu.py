@@ -240,7 +240,8 @@ def test_batch_members_equal_single_solves(golden):
         np.testing.assert_array_equal(one.state.xi, xi[i])
 
 
-@pytest.mark.parametrize("n_p,layout", [(100, "angle"), (100, "unit"), (100, "half"), (60, "angle"), (60, "unit"), (60, "half")])
+@pytest.mark.parametrize("n_p,layout", [(100, "angle"), (100, "unit"), (100, "half"), (60, "angle"), (60, "unit"), (60, "half"),
+                                        (37, "half"), (130, "half")])
 def test_oracle_vs_device_step(golden, n_p, layout):
     """C5 shape (n_o 100) and a generic horizon (n_p 60, the non-specialised kernel): device one
     step == oracle one step from an oracle mid-run state."""
