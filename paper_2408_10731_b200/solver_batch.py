@@ -604,14 +604,15 @@ def _device_geometry(struct: _Structure, xi, psi, alpha=None) -> dict:
 
 
 # ------------------------------------------------------------------ reference API
-def init_state(problem: BatchProblem, samples: np.ndarray, params: BatchParams | None = None) -> BatchState:
+def init_state(problem: BatchProblem, samples: np.ndarray, params: BatchParams | None = None, *,
+               _struct: "_Structure | None" = None) -> BatchState:
     """State from position-coefficient samples (N_b, 2m): [xi_x | xi_y] (solver_batch.py:234-278).
 
     The heading is seeded from the desired-path direction; copies, angles and scales are made
     consistent with the sampled geometry (implied, materialised on the device when read);
     multipliers start at zero."""
     params = params or BatchParams()
-    struct = _structure_for(problem)
+    struct = _struct if _struct is not None else _structure_for(problem)  # solve_batch_opt passes its own
     basis, m = problem.basis, struct.m
     samples = np.asarray(samples, dtype=float)
     n_b = samples.shape[0]
@@ -816,7 +817,7 @@ def solve_batch_opt(
     if state is None:
         if samples is None:
             samples = _default_samples(problem, m, mean, covariance, seed)
-        state = init_state(problem, samples, params)
+        state = init_state(problem, samples, params, _struct=struct)  # one content fingerprint per call
         state._implied = (state._implied[0], state._implied[1], struct)
 
     eng, lv, given = _engine_for(state, problem, struct, params, max_hist=params.max_iter, cached=True)
