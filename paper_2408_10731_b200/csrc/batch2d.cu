@@ -36,7 +36,7 @@ constexpr int kB2MaxRing = 64;
 constexpr int kB2MaxC = 8;
 constexpr int kB2MaxM = 16;
 #ifndef B2_UNROLL_BASIS
-#define B2_UNROLL_BASIS 1
+#define B2_UNROLL_BASIS 4  // unroll count of the per-sample basis products (C2-alt: 1 -> 45.1, 2 -> 44.2, 4 -> 44.0, 8 -> 53.3, 16 -> 45.5 us/it)
 #endif
 #ifndef B2_OBS_BATCH
 #define B2_OBS_BATCH 5  // obstacles whose track loads are issued before the first use (element pass; 8 spilled more: 49.8 vs 47.0 us per C2-alt iteration)
@@ -44,7 +44,7 @@ constexpr int kB2MaxM = 16;
 #ifndef B2_MINB
 #define B2_MINB 7  // 7 CTAs / SM (72 registers, some spills): C2-alt's 1024 members in one wave; 6 % faster than 4 CTAs / 128 registers at 1024 and 8192 members (tools/tune_b2.sh)
 #endif
-constexpr int kB2UnrollM = B2_UNROLL_BASIS ? kB2MaxM : 1;
+constexpr int kB2UnrollM = B2_UNROLL_BASIS > 0 ? B2_UNROLL_BASIS : 1;
 
 struct B2Args {
     tro_b2_dims d;
