@@ -26,6 +26,9 @@ namespace tro {
 #define PR_WARPS 8
 #endif
 constexpr int kPrWarps = PR_WARPS;  // samples (warps) per CTA
+#ifndef PR_KB
+#define PR_KB 4  // obstacles per batch of scaled distances (C4: 2 / 3 / 4 / 6 / 8 -> 7.37 / 6.66 / 6.53 / 6.64 / 7.00 ms)
+#endif
 #ifndef PR_MINB
 #define PR_MINB 2  // 2 CTAs / SM at the 128-register cap (3 spills heavily)
 #endif
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(kPrWarps * 32, PR_MINB) priest_project_kernel(
                 const double* tr = A.c.tracks + t;
                 // the scaled distances of kB obstacles first (independent: ILP across obstacles), then the
                 // rare inside targets; ncu showed the one-obstacle-at-a-time chain stalled on fixed latency
-                constexpr int kB = 4;
+                constexpr int kB = PR_KB;
                 auto q2_of = [&](int j, double* dl, double* cc) -> double {
                     const double* o = sObs + 8 * j;
                     double ia2;
