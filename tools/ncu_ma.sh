@@ -14,7 +14,8 @@ rows = list(csv.reader(open("gpurun_out/ncu_ma_raw.csv")))
 h, v = rows[0], rows[2]
 for k, x in zip(h, v):
     if any(t in k for t in ("shared_op", "mem_shared", "bank", "l1tex__throughput", "lsu_mem", "l1tex__data_pipe_lsu",
-                            "sm__warps_active", "launch__occupancy_limit", "smsp__thread_inst_executed_per_inst")):
+                            "sm__warps_active", "launch__occupancy_limit", "smsp__thread_inst_executed_per_inst",
+                            "dmma", "pipe_tensor", "pipe_fp64")):
         print(f"{k:90s} {x}")
 PY
 rm -f gpurun_out/ncu_ma.ncu-rep gpurun_out/ncu_ma_raw.csv
