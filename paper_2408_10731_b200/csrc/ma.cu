@@ -31,6 +31,9 @@ namespace tro {
 #ifndef MA_MINB
 #define MA_MINB 2  // resident CTAs per SM the element kernel is compiled for (128 registers)
 #endif
+#ifndef MA_QP_PRE
+#define MA_QP_PRE 4  // k-steps of K^-1 fragments in flight in the DMMA QP kernel (2 / 3 / 4 / 6 / 8: 83 / 83 / 69 / 99 / 105 us)
+#endif
 #ifndef MA_PAIR_UNROLL
 #define MA_PAIR_UNROLL 1  // pair chunks per loop trip of the element pass (C3: 1 -> 0.945, 2 -> 1.05, 4 -> 1.40 ms)
 #endif
@@ -634,7 +637,7 @@ __global__ void __launch_bounds__(256) ma_qp_kernel(MaArgs A) {
 #pragma unroll
             for (int n = 0; n < kQpCols / 8; ++n) acc[t][n][0] = acc[t][n][1] = 0.0;
         // A fragments (K^-1 from L2) loaded kPre k-steps ahead: a k-step's 18 DMMA do not cover an L2 load
-        constexpr int kPre = 4;
+        constexpr int kPre = MA_QP_PRE;
         auto load_a = [&](int k0, double* af) {
             const int kk = k0 + acol;
 #pragma unroll
