@@ -110,6 +110,36 @@ def solve_single_batch_sharded(batch, params=None, *, group=None, gather_results
     return local, merged, full
 
 
+def solve_joint_batch_sharded(problems: list, params=None, *, group=None, gather_results: bool = False, **kw):
+    """solver_multiagent.solve_joint_batch over all ranks of `group`: rank r solves problems
+    [shard_range(B, r, world)) with no per-iteration communication (joint problems are independent,
+    solver_multiagent.py:300-368), then one all-gather of the per-shard summaries (max|r|, ||r||,
+    converged, in problem order).  gather_results=True also all-gathers xi, the residuals, the counters and
+    the levels for the bitwise shard-vs-single tests.  Returns (local engine, merged summary, full or None)."""
+    from . import _lib
+    from .solver_multiagent import solve_joint_batch
+
+    rank, world = _world(group)
+    if len(problems) < world:
+        raise ValueError("fewer problems than ranks")
+    lo, hi = shard_range(len(problems), rank, world)
+    eng = solve_joint_batch(list(problems[lo:hi]), params, **kw)
+    conv = (eng.status & _lib.TRO_CONVERGED) != 0
+    merged = gather_summaries(shard_summary(eng.res_max, eng.res_norm, conv, lo), group)
+    full = None
+    if gather_results:
+        local = {"xi": eng.xi.cpu().numpy(), "res_norm": eng.res_norm.cpu().numpy(),
+                 "res_max": eng.res_max.cpu().numpy(), "iteration": eng.iteration.cpu().numpy(),
+                 "level": eng.level.cpu().numpy(), "converged": conv.cpu().numpy()}
+        parts = [None] * world
+        if world > 1:
+            dist.all_gather_object(parts, local, group=group)
+        else:
+            parts = [local]
+        full = {k: np.concatenate([q[k] for q in parts]) for k in local}
+    return eng, merged, full
+
+
 # ------------------------------------------------------------------ Alg. 2 (batch-global rho)
 # solve_batch_opt's penalty rule is batch-global (solver_batch.py:454-461): each iteration needs the
 # best member (argmin of ||r||, first index; numpy returns the first NaN) and min_i max|r_i| over the
