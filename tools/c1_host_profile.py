@@ -15,4 +15,4 @@ pr.enable()
 for _ in range(20):
     solver_single.solve_single(prob, solver_single.SingleParams())
 pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)

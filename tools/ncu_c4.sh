@@ -5,4 +5,5 @@ ncu --set full --import-source on --clock-control none -k regex:priest_project -
     python bench.py --config c4 --steps 1 --warmup 3 > gpurun_out/ncu_c4.log 2>&1
 python tools/ncu_summary.py gpurun_out/ncu_c4.ncu-rep > gpurun_out/ncu_c4.txt 2>&1
 python tools/ncu_lines.py gpurun_out/ncu_c4.ncu-rep 40 > gpurun_out/ncu_c4_lines.txt 2>&1
+python tools/ncu_lines_smem.py gpurun_out/ncu_c4.ncu-rep 25 > gpurun_out/ncu_c4_smem.txt 2>&1
 rm -f gpurun_out/ncu_c4.ncu-rep
