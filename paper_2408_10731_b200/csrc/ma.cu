@@ -395,13 +395,9 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
                         for (int k = 0; k < 3; ++k) cen[k] = sPair[(4 + k) * np_ + p];
                     }
                     const double dx = pt[pi * 3 + 0] - cen[0], dy = pt[pi * 3 + 1] - cen[1], dz = pt[pi * 3 + 2] - cen[2];
-                    // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) as unit vectors (:280-282)
-                    double ca, sa, cb, sb;
+                    // alpha = atan2(dy, dx), beta = atan2(hypot(dx/pa, dy/pa), dz/pb) (:280-282)
                     const int64_t ex_i = ((int64_t)i * n_p + t) * np_ + p;
-                    if (prime) {  // the given state's angles
-                        sincos(A.s.export_ab[ex_i], &sa, &ca);
-                        sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
-                    } else {
+                    auto angles = [&](double& ca, double& sa, double& cb, double& sb) {  // as unit vectors
                         const double h2 = fma(dx, dx, dy * dy);
                         double planar;
                         if (h2 > 0.0) {
@@ -415,27 +411,56 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
                             planar = 0.0;
                         }
                         unit2(dz * ipb, planar, &cb, &sb);
-                    }
-                    double lx, ly, lz, d;
-                    if (prime) {
-                        lx = srow[p];
-                        ly = srow[np_ + p];
-                        lz = srow[2 * np_ + p];
-                        d = A.s.export_d[ex_i];
-                    } else if (init) {
-                        lx = ly = lz = 0.0;
-                        d = 1.0;
-                    } else {
+                    };
+                    double ca = 0.0, sa = 0.0, cb = 0.0, sb = 0.0;
+                    double lx, ly, lz, d, rx, ry, rz;
+                    if constexpr (!prime && !init) {
                         lx = clx;
                         ly = cly;
                         lz = clz;
-                        // multiplier-shifted single-variable quadratic in d, clamped at [1, 1e6] (:285-293)
-                        const double num = pa * sb * (ca * fma(lx, ir, dx) + sa * fma(ly, ir, dy)) + pb * cb * fma(lz, ir, dz);
-                        const double den = pa2 * (sb * sb) + pb2 * (cb * cb);
-                        const double q = num * rcp_fast(den);
-                        d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
+                        // The polar update collapsed: with the unit vectors of the offset delta, pa sb ca = dx / g,
+                        // pa sb sa = dy / g, pb cb = dz / g and pa^2 sb^2 + pb^2 cb^2 = |delta|^2 / g^2, where
+                        // g^2 = (dx^2 + dy^2) / pa^2 + dz^2 / pb^2.  So the multiplier-shifted quadratic (:285-293)
+                        // is q = g (delta . (delta + lambda / rho)) / |delta|^2 and the reconstruction is
+                        // (d / g) delta: no angle is formed (same quantities up to rounding)
+                        const double h2 = fma(dx, dx, dy * dy);
+                        const double g2 = fma(dz * dz, ipb * ipb, h2 * (ipa * ipa));
+                        if (g2 > 0.0) {
+                            const double rg = rsqrt_fast(g2);
+                            const double dot = fma(dz, fma(lz, ir, dz), fma(dy, fma(ly, ir, dy), dx * fma(lx, ir, dx)));
+                            const double q = dot * (g2 * rg) * rcp_fast(fma(dz, dz, h2));
+                            d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
+                            const double sc = d * rg;
+                            rx = sc * dx;
+                            ry = sc * dy;
+                            rz = sc * dz;
+                        } else {  // delta == 0: atan2's conventions (alpha = 0 / pi, beta = 0 / pi along z)
+                            angles(ca, sa, cb, sb);
+                            const double q = pb * cb * fma(lz, ir, dz) * rcp_fast(pb2);
+                            d = q < 1.0 ? 1.0 : (q > 1e6 ? 1e6 : q);
+                            rx = pa * d * sb * ca;
+                            ry = pa * d * sb * sa;
+                            rz = pb * d * cb;
+                        }
+                        if (A.s.export_d) angles(ca, sa, cb, sb);  // the exported angles
+                    } else {
+                        if (prime) {  // the given state's angles
+                            sincos(A.s.export_ab[ex_i], &sa, &ca);
+                            sincos(A.s.export_ab[nplane + ex_i], &sb, &cb);
+                            lx = srow[p];
+                            ly = srow[np_ + p];
+                            lz = srow[2 * np_ + p];
+                            d = A.s.export_d[ex_i];
+                        } else {  // init
+                            angles(ca, sa, cb, sb);
+                            lx = ly = lz = 0.0;
+                            d = 1.0;
+                        }
+                        rx = pa * d * sb * ca;
+                        ry = pa * d * sb * sa;
+                        rz = pb * d * cb;
                     }
-                    const double rx = pa * d * sb * ca, ry = pa * d * sb * sa, rz = pb * d * cb;
+                    (void)pa2;
                     if (prime) {
                     } else if (!init) {
                         const double ex = dx - rx, ey = dy - ry, ez = dz - rz;  // residual (:203-208)
