@@ -78,6 +78,9 @@ constexpr int kPairW = 7;  // per pair: a, b, 1/a, 1/b, static centre (3)
 // 56-byte stride keeps the element pass's per-lane record writes conflict-free, and the scatter reads a
 // record's three components at immediate offsets from one address.
 constexpr int kScrW = 7;
+// V row stride: 6 n_a agent sums padded to 4 (mod 16) doubles, so the 4 samples (k) of a DMMA A fragment land
+// 8 banks apart (rows of 96 put all four on one bank: 4-way conflicts)
+__host__ __device__ inline int ma_vstride(int n_a) { return 6 * n_a + ((4 - (6 * n_a) % 16) + 16) % 16; }
 __host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs, int n_eq, int n_inc) {
     MaSmem L;
     int off = 0;
@@ -90,7 +93,7 @@ __host__ __device__ inline MaSmem ma_layout(int n_p, int m, int n_a, int n_pairs
     if (pro > kMaWarps * n_pairs * kScrW) off += pro - kMaWarps * n_pairs * kScrW;
     L.sumin = L.scratch;
     L.rhs = L.sumin + 2 * n_a * 3 * m;
-    L.V = off;       off += 2 * kMaWarps * 2 * n_a * 3;  // per round, per warp: the scattered agent sums (x2 buffers)
+    L.V = off;       off += 2 * kMaWarps * ma_vstride(n_a);  // per round, per warp: the scattered agent sums (x2 buffers)
     L.warp = off;    off += 2 * kMaWarps;
     L.pair = off;    off += kPairW * n_pairs;            // SoA [field][pair]
     L.ints = off;    off += (2 * n_pairs + n_a + 1 + n_inc + 1) / 2 + 1;  // pair_i, pair_j, inc_ptr, inc_pair
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     // 8x8x4 fp64 tensor-core tiles (accumulated across rounds in the owning warp's registers).
     const int tasks = 2 * n_a;
     const int rows = tasks * 3;  // [which][agent][axis]
+    const int vs = ma_vstride(n_a);  // V row stride: the DMMA A-fragment reads hit 16 distinct bank pairs
     // contraction tiles: D[rows x m] = V^T[rows x t] P[t x m] as 8x8 DMMA tiles, warp w owning tiles
     // w, w + kMaWarps, ... (rows <= 96, m <= 11: at most 12 x 2 tiles, <= 3 per warp)
     constexpr int kMaxTiles = (24 + kMaWarps - 1) / kMaWarps;
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     auto contract = [&](int r) {
         const int bb = r & 1;
         mbar_wait(&sBar[bb], (uint32_t)((r >> 1) & 1));
-        const double* sVb = sV + bb * kMaWarps * rows;
+        const double* sVb = sV + bb * kMaWarps * vs;
         const int tn = min(kMaWarps, n_p - r * kMaWarps);
         const double* prd = sP + r * kMaWarps * mp;
 #pragma unroll
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
 #pragma unroll
                 for (int ks = 0; ks < (kMaWarps + 3) / 4; ++ks) {
                     const int k = 4 * ks + (lane & 3);
-                    const double av = (k < tn && ar < rows) ? sVb[k * rows + ar] : 0.0;
+                    const double av = (k < tn && ar < rows) ? sVb[k * vs + ar] : 0.0;
                     const double bv = (k < tn && bc < m) ? prd[k * mp + bc] : 0.0;
                     dmma884(cacc[j], av, bv);
                 }
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
     for (int rd = 0; rd < n_rounds; ++rd) {
         const int t = rd * kMaWarps + warp;
         if (pf && t + kMaAhead * kMaWarps < n_p) prefetch_l2(st + (t + kMaAhead * kMaWarps) * rowW, rowW * 8);
-        double* sVr = sV + (rd & 1) * kMaWarps * rows;
+        double* sVr = sV + (rd & 1) * kMaWarps * vs;
         if (t < n_p) {
             // this sample's positions (one (agent, axis) per lane slot; same FMA order as the basis product)
             {
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(kMaWarps * 32, MA_MINB) ma_kernel(MaArgs A) {
 #pragma unroll
                     for (int k = 0; k < 3; ++k) v[k] = fma(sgn, sc[k], v[k]);
                 }
-                double* vo = sVr + warp * rows + task * 3;
+                double* vo = sVr + warp * vs + task * 3;
                 vo[0] = v[0];
                 vo[1] = v[1];
                 vo[2] = v[2];
