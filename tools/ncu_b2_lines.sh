@@ -5,6 +5,7 @@ ncu --set full --import-source on --clock-control none -k regex:b2_kernel --laun
     -o gpurun_out/ncu_b2 -f python tools/b2_profile.py > gpurun_out/ncu_b2.log 2>&1
 python tools/ncu_summary.py gpurun_out/ncu_b2.ncu-rep > gpurun_out/ncu_b2.txt 2>&1
 python tools/ncu_lines.py gpurun_out/ncu_b2.ncu-rep 80 > gpurun_out/ncu_b2_lines.txt 2>&1
+python tools/ncu_lines_smem.py gpurun_out/ncu_b2.ncu-rep 12 > gpurun_out/ncu_b2_smem.txt 2>&1
 ncu -i gpurun_out/ncu_b2.ncu-rep --page raw --csv > gpurun_out/ncu_b2_raw.csv 2>&1
 python - >> gpurun_out/ncu_b2.txt <<'PY'
 import csv
